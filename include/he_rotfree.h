@@ -1,0 +1,210 @@
+/*
+ * he_rotfree.h -- C ABI of the B200 (sm_100a) server hot path of
+ * arXiv 2409.05205, "Efficient Homomorphically Encrypted Convolutional
+ * Neural Network Without Rotation" (Akherati & Zhang).
+ *
+ * The library evaluates, on the GPU, the server side of the paper's
+ * rotation-free Conv procedure (Algorithm 1: Line 14
+ * product c0 * fhat^(n), Lines 15-17 valid-slot extraction) and FC
+ * procedure (Algorithm 2, Line 13: c0 * w + b), plus the
+ * additive mask phi1 of the garbled-circuit bridge, in an
+ * RNS ring Z_Q[X]/(X^N+1), Q = q_0 ... q_{L-1}, each q_j prime, q_j < 2^50,
+ * q_j = 1 (mod 2N) (§II-A; BASELINE.json north_star).
+ *
+ * Conventions (all entry points):
+ *  - Every device buffer is allocated and owned by the caller.  The
+ *    library owns only the context tables (allocated in he_ctx_create) and
+ *    never allocates or synchronises in the hot path; all work is enqueued
+ *    on the caller's stream (`stream` is a cudaStream_t, NULL = legacy
+ *    default stream) and the call returns without waiting.
+ *  - Residue buffers are uint64_t, canonical (each value in [0, q_j)); the
+ *    library's outputs are always canonical.  Inputs that are not
+ *    canonical give unspecified (but memory-safe) results.
+ *  - Polynomials are stored coefficient-major: the innermost axis is the
+ *    N coefficients of one limb, the next axis the L limbs.
+ *  - Errors: argument / shape checks are synchronous and return a status
+ *    before anything is enqueued.  HE_ECUDA reports a launch error from
+ *    cudaGetLastError(); asynchronous faults surface at the caller's next
+ *    synchronisation.  he_status_str() names each status.
+ *  - Plaintext-scale values (image pixels, mask phi1, FC bias) are encoded
+ *    as enc_j(m) = round(Q * (m mod t) / t) mod q_j (BFV-style, DESIGN.md
+ *    reading R2; the paper's CKKS ⌈Δm⌋ of Eq. (1)).
+ */
+#ifndef HE_ROTFREE_H
+#define HE_ROTFREE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HE_OK = 0,
+    HE_EINVAL = 1,   /* null pointer, non-positive batch, bad argument      */
+    HE_ESHAPE = 2,   /* layer does not fit the ring / unsupported geometry  */
+    HE_EPARAM = 3,   /* ring parameters: q not prime, q >= 2^50, q != 1 mod
+                        2N, duplicate q, t even or t >= 2^32, N unsupported  */
+    HE_ECUDA = 4,    /* CUDA launch / allocation error                      */
+    HE_ENOMEM = 5    /* caller workspace too small                          */
+} he_status;
+
+const char* he_status_str(he_status s);
+
+/* ------------------------------------------------------------------ ring */
+/* Ring description.  log2N in [8, 15]; 1 <= L <= 64; q[L]
+ * host array (copied); t odd, 3 <= t < 2^32. */
+typedef struct {
+    uint32_t log2N;
+    uint32_t L;
+    const uint64_t* q;
+    uint64_t t;
+} he_ring_desc;
+
+typedef struct he_ctx he_ctx;
+
+/* Creates an immutable context on CUDA device `device`: validates the ring
+ * (HE_EPARAM), picks psi_j = the smallest primitive 2N-th root of unity mod
+ * q_j (reading R9), and uploads the twiddle tables (psi^{brv(k)} and its
+ * inverse with Shoup companions) and per-limb constants.  The context may
+ * be used concurrently from several streams. */
+he_status he_ctx_create(const he_ring_desc* r, int device, he_ctx** out);
+void he_ctx_destroy(he_ctx* ctx);
+/* psi_j used for limb j (host value). */
+uint64_t he_ctx_psi(const he_ctx* ctx, uint32_t j);
+
+/* ------------------------------------------------------------------ conv */
+/* Conv layer geometry in the paper's notation (§II-B):
+ * w_i = image rows, h_i = row length, f_w = filter rows, f_h = filter
+ * columns, stride s_w = s_h = stride, pad 1 = "same" (client zero-pads
+ * (f-1)/2 on each side), 0 = valid. */
+typedef struct {
+    int32_t c_i, c_o, w_i, h_i, f_w, f_h, stride, pad;
+} he_conv_desc;
+
+/* Packing plan (reading R11).  s = largest power of two with
+ * s * w_p * h_p <= N (the paper's spacing s = c_i of Eq. (5)-(7) when its
+ * preconditions hold); c_ib = min(c_i, s) input
+ * channels per input ciphertext (n_ib blocks), c_ob = min(c_o, s) output
+ * channels per output ciphertext (n_ob blocks); output channel n of a block
+ * sits at offset t_n = (n mod c_ob) * (s / c_ob) (Eq. (7) shift n c_i/c_o);
+ * n_valid = c_ob * w_o * h_o valid slots per output block. */
+typedef struct {
+    he_conv_desc d;
+    int32_t s, c_ib, n_ib, c_ob, n_ob, w_p, h_p, w_o, h_o, n_valid;
+} he_conv_plan;
+
+/* Host-only, deterministic.  s_override = 0 applies R11; otherwise it must
+ * be a power of two with s_override * w_p * h_p <= N (paper-literal layouts
+ * use s = c_i).  HE_ESHAPE if the padded image does not fit, if
+ * n_ib * s > 4096 (MAC accumulator headroom) or for c_i, c_o, sizes < 1. */
+he_status he_conv_plan_make(const he_ctx* ctx, const he_conv_desc* d,
+                            int s_override, he_conv_plan* out);
+
+/* a1, client side (Eq. (5); Alg. 1 Line 2).  Packs
+ * d_img int32 [B][c_i][w_i][h_i] into the input polynomials
+ *   i_beta(X) = sum_m sum_{k,l} Ip^{(beta c_ib + m)}_{k,l} X^{s((k-f_w)h_p+l)+m}
+ * (negacyclic sign on negative exponents) and encodes every coefficient
+ * with enc_j, giving d_pt uint64 [B][n_ib][L][N].  If d_ve is non-NULL
+ * (uint64 [B][n_ib][L][N], the caller's v*b + e0 residues of Eq. (1)) it
+ * is added mod q_j, so d_pt becomes the c0-only encryption of Alg. 1
+ * Line 9.  d_ve may alias d_pt. */
+he_status he_pack_input(const he_ctx* ctx, const he_conv_plan* p,
+                        const int32_t* d_img, int B, const uint64_t* d_ve,
+                        uint64_t* d_pt, void* stream);
+
+/* a2, server initialisation (Eq. (6)-(7); Alg. 1
+ * Line 4).  Packs d_w int32 [c_o][c_i][f_w][f_h] (weights, any sign, used
+ * unscaled: R3) into the filter polynomials, takes their forward NTT and
+ * stores them in the opaque NTT-domain layout d_fspec (he_filter_bytes()
+ * bytes) consumed by he_conv.  d_ws: workspace of
+ * he_pack_filters_workspace_bytes() bytes. */
+size_t he_filter_bytes(const he_ctx* ctx, const he_conv_plan* p);
+size_t he_pack_filters_workspace_bytes(const he_ctx* ctx,
+                                       const he_conv_plan* p);
+he_status he_pack_filters(const he_ctx* ctx, const he_conv_plan* p,
+                          const int32_t* d_w, uint64_t* d_fspec, void* d_ws,
+                          size_t ws_bytes, void* stream);
+
+/* a3-a7, the server hot path (Alg. 1 Lines 13-17; mask
+ * PAPER.md:280).  d_c0 uint64 [B][n_ib][L][N] (c0 of each input block);
+ * d_fspec from he_pack_filters; d_phi1 uint32 [B][n_ob][N] mask values in
+ * [0, t) or NULL (no mask).  Writes the full output polynomials
+ *   d_out[b][ob][j][s*k + t_n] = (sum_beta c0_beta * fhat_beta^{(n)})_{s*k+t_n}
+ * for every k < N/s and channel n of block ob, 0 at every other
+ * coefficient, then + enc_j(phi1[b][ob][i]) at every coefficient i.
+ * d_out uint64 [B][n_ob][L][N].  d_ws: he_conv_workspace_bytes(B) bytes
+ * (HE_ENOMEM if smaller). */
+size_t he_conv_workspace_bytes(const he_ctx* ctx, const he_conv_plan* p,
+                               int B);
+he_status he_conv(const he_ctx* ctx, const he_conv_plan* p,
+                  const uint64_t* d_c0, int B, const uint64_t* d_fspec,
+                  const uint32_t* d_phi1, uint64_t* d_out, void* d_ws,
+                  size_t ws_bytes, void* stream);
+
+/* a7-a8 ("invalid slots ... do not need to be sent").
+ * Gathers the n_valid valid slots of each output block, in increasing
+ * coefficient order (row K < w_o, column L < h_o, channel n of the block:
+ * i = s*(stride*K*h_p + stride*L) + t_n), from d_out uint64
+ * [B][n_ob][L][N] into d_compact uint64 [B][n_ob][L][n_valid].  If d_phi1
+ * is non-NULL the mask enc_j(phi1[b][ob][i]) is added to each gathered
+ * slot (for outputs produced by he_conv without a mask). */
+he_status he_mask_extract(const he_ctx* ctx, const he_conv_plan* p,
+                          const uint64_t* d_out, int B,
+                          const uint32_t* d_phi1, uint64_t* d_compact,
+                          void* stream);
+
+/* -------------------------------------------------------------------- FC */
+/* FC layer with n_i inputs, n_o outputs; requires
+ * n_i * n_o <= N and N <= 16384 (single-CTA inverse transform). */
+typedef struct {
+    int32_t n_i, n_o;
+} he_fc_desc;
+
+/* Eq. (9): i(X) = sum_l I_l X^{l n_o}, encoded with enc_j;
+ * d_in int32 [B][n_i] -> d_pt uint64 [B][L][N]; optional d_ve as in
+ * he_pack_input. */
+he_status he_pack_fc_input(const he_ctx* ctx, const he_fc_desc* f,
+                           const int32_t* d_in, int B, const uint64_t* d_ve,
+                           uint64_t* d_pt, void* stream);
+
+/* Server initialisation of Algorithm 2 (Lines 3-4):
+ * w(X) per Eq. (10), generalised to N >= n_i n_o (reading R17):
+ *   w(X) = sum_k W_{k,0} X^k - sum_{l>=1} sum_k W_{k,l} X^{N - l n_o + k},
+ * d_W int32 [n_o][n_i]; stored NTT-domain in d_wspec (he_fc_wspec_bytes()).
+ * d_bias int32 [n_o] (or NULL = 0) is encoded into d_bias_enc uint64
+ * [L][n_o].  d_ws: he_fc_workspace_bytes(ctx, f, 1) bytes. */
+size_t he_fc_wspec_bytes(const he_ctx* ctx, const he_fc_desc* f);
+he_status he_pack_fc_weights(const he_ctx* ctx, const he_fc_desc* f,
+                             const int32_t* d_W, const int32_t* d_bias,
+                             uint64_t* d_wspec, uint64_t* d_bias_enc,
+                             void* d_ws, size_t ws_bytes, void* stream);
+
+/* a9, Algorithm 2 Line 13, first n_o coefficients only
+ * (PAPER.md:267):  d_out[b][j][k] = (c0_b * w)_k + bias_enc[j][k]
+ *                                   + enc_j(phi1[b][k]),  k < n_o.
+ * d_c0 uint64 [B][L][N]; d_phi1 uint32 [B][n_o] or NULL; d_out uint64
+ * [B][L][n_o]; d_ws: he_fc_workspace_bytes(B) bytes. */
+size_t he_fc_workspace_bytes(const he_ctx* ctx, const he_fc_desc* f, int B);
+he_status he_fc(const he_ctx* ctx, const he_fc_desc* f, const uint64_t* d_c0,
+                int B, const uint64_t* d_wspec, const uint64_t* d_bias_enc,
+                const uint32_t* d_phi1, uint64_t* d_out, void* d_ws,
+                size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------ transforms */
+/* Batched negacyclic NTT over `batch` x L limbs stored [batch][L][N]
+ * (the primitive behind a2, a3, a9; PAPER.md:28 cites NTT as the standard
+ * polynomial-product speed-up).  In place.  Forward: canonical natural-
+ * order coefficients in, canonical evaluations out in bit-reversed order:
+ * out[p] = a(psi_j^{2 brv(p) + 1}).  Inverse: exactly undoes the forward
+ * (bit-reversed in, natural out, includes N^{-1}). */
+he_status he_ntt_forward(const he_ctx* ctx, uint64_t* d_data, int batch,
+                         void* stream);
+he_status he_ntt_inverse(const he_ctx* ctx, uint64_t* d_data, int batch,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HE_ROTFREE_H */

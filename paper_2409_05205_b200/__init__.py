@@ -1,0 +1,299 @@
+"""Thin Python binding of libhe_rotfree.so (include/he_rotfree.h).
+
+Argument marshalling only: every step of the path runs in the library's
+sm_100a kernels.  Torch is used for device memory and streams; residue
+tensors are torch.int64 (bit patterns of the uint64 residues), masks and
+integer data torch.int32.  There is no CPU fallback: importing this module
+raises if the CUDA library is missing, and every call checks that its
+tensors live on the context's CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhe_rotfree.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import "
+        f"__graft_entry__ as g; g.build()'` (nvcc, sm_100a). There is no CPU "
+        f"fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+HE_OK, HE_EINVAL, HE_ESHAPE, HE_EPARAM, HE_ECUDA, HE_ENOMEM = range(6)
+
+
+class HeError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {_lib.he_status_str(status).decode()}")
+
+
+class RingDesc(ctypes.Structure):
+    _fields_ = [("log2N", ctypes.c_uint32), ("L", ctypes.c_uint32),
+                ("q", ctypes.POINTER(ctypes.c_uint64)), ("t", ctypes.c_uint64)]
+
+
+class ConvDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("c_i", "c_o", "w_i", "h_i", "f_w", "f_h", "stride", "pad")]
+
+
+class ConvPlan(ctypes.Structure):
+    _fields_ = [("d", ConvDesc)] + [(n, ctypes.c_int32) for n in
+                                     ("s", "c_ib", "n_ib", "c_ob", "n_ob", "w_p",
+                                      "h_p", "w_o", "h_o", "n_valid")]
+
+    def __repr__(self):
+        return (f"ConvPlan(s={self.s}, c_ib={self.c_ib}, n_ib={self.n_ib}, "
+                f"c_ob={self.c_ob}, n_ob={self.n_ob}, w_o={self.w_o}, "
+                f"h_o={self.h_o}, n_valid={self.n_valid})")
+
+
+class FcDesc(ctypes.Structure):
+    _fields_ = [("n_i", ctypes.c_int32), ("n_o", ctypes.c_int32)]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_SZ = ctypes.c_size_t
+
+
+def _sig(name, args, res=ctypes.c_int):
+    f = getattr(_lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_lib.he_status_str.argtypes = [ctypes.c_int]
+_lib.he_status_str.restype = ctypes.c_char_p
+_sig("he_ctx_create", [ctypes.POINTER(RingDesc), _I, ctypes.POINTER(_P)])
+_sig("he_ctx_destroy", [_P], None)
+_sig("he_ctx_psi", [_P, ctypes.c_uint32], ctypes.c_uint64)
+_sig("he_conv_plan_make", [_P, ctypes.POINTER(ConvDesc), _I,
+                           ctypes.POINTER(ConvPlan)])
+_sig("he_pack_input", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _P])
+_sig("he_filter_bytes", [_P, ctypes.POINTER(ConvPlan)], _SZ)
+_sig("he_pack_filters_workspace_bytes", [_P, ctypes.POINTER(ConvPlan)], _SZ)
+_sig("he_pack_filters", [_P, ctypes.POINTER(ConvPlan), _P, _P, _P, _SZ, _P])
+_sig("he_conv_workspace_bytes", [_P, ctypes.POINTER(ConvPlan), _I], _SZ)
+_sig("he_conv", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _P, _P, _SZ,
+                 _P])
+_sig("he_mask_extract", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _P])
+_sig("he_pack_fc_input", [_P, ctypes.POINTER(FcDesc), _P, _I, _P, _P, _P])
+_sig("he_fc_wspec_bytes", [_P, ctypes.POINTER(FcDesc)], _SZ)
+_sig("he_fc_workspace_bytes", [_P, ctypes.POINTER(FcDesc), _I], _SZ)
+_sig("he_pack_fc_weights", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _P, _P,
+                            _SZ, _P])
+_sig("he_fc", [_P, ctypes.POINTER(FcDesc), _P, _I, _P, _P, _P, _P, _P, _SZ,
+               _P])
+_sig("he_ntt_forward", [_P, _P, _I, _P])
+_sig("he_ntt_inverse", [_P, _P, _I, _P])
+
+EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
+            "he_conv_plan_make", "he_pack_input", "he_filter_bytes",
+            "he_pack_filters_workspace_bytes", "he_pack_filters",
+            "he_conv_workspace_bytes", "he_conv", "he_mask_extract",
+            "he_pack_fc_input", "he_fc_wspec_bytes", "he_fc_workspace_bytes",
+            "he_pack_fc_weights", "he_fc", "he_ntt_forward", "he_ntt_inverse"]
+
+
+def _check(st: int, what: str):
+    if st != HE_OK:
+        raise HeError(st, what)
+
+
+def _stream(stream: Optional[torch.cuda.Stream]):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def conv_plan_make(ctx: Optional["Context"], c_i, c_o, w_i, h_i, f_w=3, f_h=3,
+                   stride=1, pad=1, s_override=0) -> ConvPlan:
+    d = ConvDesc(c_i, c_o, w_i, h_i, f_w, f_h, stride, pad)
+    p = ConvPlan()
+    _check(_lib.he_conv_plan_make(ctx._h, ctypes.byref(d), s_override,
+                                  ctypes.byref(p)), "he_conv_plan_make")
+    return p
+
+
+class Context:
+    """he_ctx: immutable ring context on one CUDA device."""
+
+    def __init__(self, primes: Sequence[int], log2N: int, t: int = 65537,
+                 device: int = 0):
+        self.primes = [int(q) for q in primes]
+        self.L = len(self.primes)
+        self.log2N = log2N
+        self.N = 1 << log2N
+        self.t = t
+        self.device = torch.device("cuda", device)
+        arr = (ctypes.c_uint64 * self.L)(*self.primes)
+        self._q = arr
+        r = RingDesc(log2N, self.L, ctypes.cast(arr, ctypes.POINTER(
+            ctypes.c_uint64)), t)
+        h = ctypes.c_void_p()
+        _check(_lib.he_ctx_create(ctypes.byref(r), device, ctypes.byref(h)),
+               "he_ctx_create")
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.he_ctx_destroy(h)
+        self._h = None
+
+    def psi(self, j: int) -> int:
+        return int(_lib.he_ctx_psi(self._h, j))
+
+    # -------------------------------------------------------------- helpers
+    def _dev(self, *ts):
+        for t in ts:
+            if t is not None and (not t.is_cuda or t.device != self.device
+                                  or not t.is_contiguous()):
+                raise ValueError("tensors must be contiguous on " +
+                                 str(self.device))
+
+    def empty_u64(self, *shape) -> torch.Tensor:
+        return torch.empty(shape, dtype=torch.int64, device=self.device)
+
+    @staticmethod
+    def _ptr(t: Optional[torch.Tensor]):
+        return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+    # ---------------------------------------------------------------- conv
+    def plan(self, c_i, c_o, w_i, h_i, f_w=3, f_h=3, stride=1, pad=1,
+             s_override=0) -> ConvPlan:
+        return conv_plan_make(self, c_i, c_o, w_i, h_i, f_w, f_h, stride, pad,
+                              s_override)
+
+    def pack_input(self, p: ConvPlan, img: torch.Tensor,
+                   ve: Optional[torch.Tensor] = None,
+                   out: Optional[torch.Tensor] = None, stream=None):
+        B = img.shape[0]
+        if out is None:
+            out = self.empty_u64(B, p.n_ib, self.L, self.N)
+        self._dev(img, ve, out)
+        _check(_lib.he_pack_input(self._h, ctypes.byref(p), self._ptr(img), B,
+                                  self._ptr(ve), self._ptr(out),
+                                  _stream(stream)), "he_pack_input")
+        return out
+
+    def pack_filters(self, p: ConvPlan, W: torch.Tensor, stream=None):
+        nb = _lib.he_filter_bytes(self._h, ctypes.byref(p))
+        fspec = self.empty_u64(nb // 8)
+        wsb = _lib.he_pack_filters_workspace_bytes(self._h, ctypes.byref(p))
+        ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        self._dev(W)
+        _check(_lib.he_pack_filters(self._h, ctypes.byref(p), self._ptr(W),
+                                    self._ptr(fspec), self._ptr(ws), wsb,
+                                    _stream(stream)), "he_pack_filters")
+        return fspec
+
+    def conv_workspace(self, p: ConvPlan, B: int) -> torch.Tensor:
+        nb = _lib.he_conv_workspace_bytes(self._h, ctypes.byref(p), B)
+        return torch.empty(nb, dtype=torch.uint8, device=self.device)
+
+    def conv(self, p: ConvPlan, c0: torch.Tensor, fspec: torch.Tensor,
+             phi1: Optional[torch.Tensor] = None,
+             out: Optional[torch.Tensor] = None,
+             ws: Optional[torch.Tensor] = None, stream=None):
+        B = c0.shape[0]
+        if out is None:
+            out = self.empty_u64(B, p.n_ob, self.L, self.N)
+        if ws is None:
+            ws = self.conv_workspace(p, B)
+        self._dev(c0, fspec, phi1, out, ws)
+        _check(_lib.he_conv(self._h, ctypes.byref(p), self._ptr(c0), B,
+                            self._ptr(fspec), self._ptr(phi1), self._ptr(out),
+                            self._ptr(ws), ws.numel() * ws.element_size(),
+                            _stream(stream)), "he_conv")
+        return out
+
+    def mask_extract(self, p: ConvPlan, out_full: torch.Tensor,
+                     phi1: Optional[torch.Tensor] = None,
+                     compact: Optional[torch.Tensor] = None, stream=None):
+        B = out_full.shape[0]
+        if compact is None:
+            compact = self.empty_u64(B, p.n_ob, self.L, p.n_valid)
+        self._dev(out_full, phi1, compact)
+        _check(_lib.he_mask_extract(self._h, ctypes.byref(p),
+                                    self._ptr(out_full), B, self._ptr(phi1),
+                                    self._ptr(compact), _stream(stream)),
+               "he_mask_extract")
+        return compact
+
+    # ------------------------------------------------------------------ FC
+    def fc_pack_input(self, n_i, n_o, inp: torch.Tensor,
+                      ve: Optional[torch.Tensor] = None,
+                      out: Optional[torch.Tensor] = None, stream=None):
+        f = FcDesc(n_i, n_o)
+        B = inp.shape[0]
+        if out is None:
+            out = self.empty_u64(B, self.L, self.N)
+        self._dev(inp, ve, out)
+        _check(_lib.he_pack_fc_input(self._h, ctypes.byref(f), self._ptr(inp),
+                                     B, self._ptr(ve), self._ptr(out),
+                                     _stream(stream)), "he_pack_fc_input")
+        return out
+
+    def fc_pack_weights(self, W: torch.Tensor,
+                        bias: Optional[torch.Tensor] = None, stream=None):
+        n_o, n_i = W.shape
+        f = FcDesc(n_i, n_o)
+        wspec = self.empty_u64(_lib.he_fc_wspec_bytes(self._h,
+                                                      ctypes.byref(f)) // 8)
+        benc = self.empty_u64(self.L, n_o)
+        wsb = _lib.he_fc_workspace_bytes(self._h, ctypes.byref(f), 1)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        self._dev(W, bias)
+        _check(_lib.he_pack_fc_weights(self._h, ctypes.byref(f), self._ptr(W),
+                                       self._ptr(bias), self._ptr(wspec),
+                                       self._ptr(benc), self._ptr(ws), wsb,
+                                       _stream(stream)), "he_pack_fc_weights")
+        return wspec, benc
+
+    def fc_workspace(self, n_i, n_o, B) -> torch.Tensor:
+        f = FcDesc(n_i, n_o)
+        nb = _lib.he_fc_workspace_bytes(self._h, ctypes.byref(f), B)
+        return torch.empty(nb, dtype=torch.uint8, device=self.device)
+
+    def fc(self, n_i, n_o, c0: torch.Tensor, wspec: torch.Tensor,
+           bias_enc: torch.Tensor, phi1: Optional[torch.Tensor] = None,
+           out: Optional[torch.Tensor] = None,
+           ws: Optional[torch.Tensor] = None, stream=None):
+        f = FcDesc(n_i, n_o)
+        B = c0.shape[0]
+        if out is None:
+            out = self.empty_u64(B, self.L, n_o)
+        if ws is None:
+            ws = self.fc_workspace(n_i, n_o, B)
+        self._dev(c0, wspec, bias_enc, phi1, out, ws)
+        _check(_lib.he_fc(self._h, ctypes.byref(f), self._ptr(c0), B,
+                          self._ptr(wspec), self._ptr(bias_enc),
+                          self._ptr(phi1), self._ptr(out), self._ptr(ws),
+                          ws.numel() * ws.element_size(), _stream(stream)),
+               "he_fc")
+        return out
+
+    # ---------------------------------------------------------- transforms
+    def ntt_forward(self, data: torch.Tensor, stream=None):
+        self._dev(data)
+        batch = data.numel() // (self.L * self.N)
+        _check(_lib.he_ntt_forward(self._h, self._ptr(data), batch,
+                                   _stream(stream)), "he_ntt_forward")
+        return data
+
+    def ntt_inverse(self, data: torch.Tensor, stream=None):
+        self._dev(data)
+        batch = data.numel() // (self.L * self.N)
+        _check(_lib.he_ntt_inverse(self._h, self._ptr(data), batch,
+                                   _stream(stream)), "he_ntt_inverse")
+        return data

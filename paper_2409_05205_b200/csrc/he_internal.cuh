@@ -1,0 +1,214 @@
+// he_internal.cuh -- context layout, 64-bit modular arithmetic and the
+// shared-memory NTT passes used by every kernel of the library.
+//
+// Arithmetic is integer only (no tensor cores: modular 64-bit products are
+// not a float contraction, BASELINE.json north_star).  Residues are < q <
+// 2^50.  Twiddle products use Shoup's precomputed-quotient multiplication;
+// butterflies are Harvey's lazy forms (values kept in [0, 4q) / [0, 2q)).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/he_rotfree.h"
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+// Per-limb constants (device copy in he_ctx::d_limb).
+struct he_limb {
+    u64 q;          // prime q_j
+    u64 q2;         // 2 q_j
+    u64 ninv, ninv_p;       // N^{-1} mod q and its Shoup companion
+    u64 delta, delta_p;     // Delta_t mod q (R2) and Shoup companion
+    u64 r25, r25_p;         // 2^25 mod q
+    u64 r50, r50_p;         // 2^50 mod q
+    u64 one_p;              // Shoup companion of 1  (floor(2^64 / q))
+};
+
+struct he_ctx {
+    int device;
+    uint32_t logN, N, L;
+    u64 t, r_t;             // plaintext modulus, r_t = Q mod t (R2)
+    u64 t_inv;              // floor(2^64 / t) (for floor(x / t))
+    u64* q_host;
+    u64* psi_host;
+    he_limb* limb_host;
+    he_limb* d_limb;        // [L]
+    ulonglong2* d_tw_fwd;   // [L][N]  {psi^{brv(k)}, Shoup}
+    ulonglong2* d_tw_inv;   // [L][N]  {psi^{-brv(k)}, Shoup}
+};
+
+// ------------------------------------------------------------ arithmetic
+// x * w mod q in [0, 2q) for any x < 2^64 (Shoup): wp = floor(w 2^64 / q).
+__device__ __forceinline__ u64 shoup_mul(u64 x, u64 w, u64 wp, u64 q) {
+    u64 qh = __umul64hi(x, wp);
+    return x * w - qh * q;
+}
+
+__device__ __forceinline__ u64 csub(u64 x, u64 m) { return x >= m ? x - m : x; }
+
+// Cooley-Tukey butterfly, inputs/outputs in [0, 4q).
+__device__ __forceinline__ void ct_bfly(u64& X, u64& Y, ulonglong2 w, u64 q,
+                                        u64 q2) {
+    u64 x = csub(X, q2);
+    u64 t = shoup_mul(Y, w.x, w.y, q);
+    X = x + t;
+    Y = x - t + q2;
+}
+
+// Gentleman-Sande butterfly, inputs/outputs in [0, 2q).
+__device__ __forceinline__ void gs_bfly(u64& X, u64& Y, ulonglong2 w, u64 q,
+                                        u64 q2) {
+    u64 x = X, y = Y;
+    X = csub(x + y, q2);
+    Y = shoup_mul(x - y + q2, w.x, w.y, q);
+}
+
+// floor(x / t) for x < 2^63 with t_inv = floor(2^64 / t).
+__device__ __forceinline__ u64 div_by_t(u64 x, u64 t, u64 t_inv) {
+    u64 d = __umul64hi(x, t_inv);
+    return (x - d * t >= t) ? d + 1 : d;
+}
+
+// enc_j(m) = (Delta_t mod q) m + floor((r_t m + floor(t/2)) / t)  mod q,
+// m in [0, t)  (R2; equals round(Q m / t) mod q_j).
+__device__ __forceinline__ u64 enc_plain(u64 m, const he_limb& L, u64 t,
+                                         u64 r_t, u64 t_inv) {
+    u64 a = shoup_mul(m, L.delta, L.delta_p, L.q);                  // [0, 2q)
+    u64 f = div_by_t(r_t * m + (t >> 1), t, t_inv);                 // < t
+    f = shoup_mul(f, 1, L.one_p, L.q);              // [0, 2q) even if t > q
+    return csub(csub(a + f, 2 * L.q), L.q);
+}
+
+__device__ __forceinline__ u64 addmod(u64 a, u64 b, u64 q) {
+    return csub(a + b, q);
+}
+
+// Canonical value -> "split25" word (hi25 << 32 | lo25) used by the MAC.
+__device__ __forceinline__ u64 to_split25(u64 v) {
+    return ((v >> 25) << 32) | (v & ((1ull << 25) - 1));
+}
+
+// ---------------------------------------------------- shared-memory NTT
+// Padding: one 8-byte word per 16 (kills bank conflicts for every stride).
+__device__ __forceinline__ int PAD(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded_words(int n) { return n + (n >> 4); }
+
+// One pass of K radix-2 Cooley-Tukey stages (forward NTT, bit-reversed
+// output), on a segment of NS words of an N-point transform held in shared
+// memory.  Stages st0 .. st0+K-1 (stage st has m = 2^st blocks, stride
+// t = N >> (st+1)).  `seg` / `split`: this CTA holds words
+// [seg*NS, (seg+1)*NS) of the transform (N = NS << split).
+template <int K>
+__device__ __forceinline__ void ct_pass(u64* sm, int logN, int NS, int st0,
+                                        int seg, int split,
+                                        const ulonglong2* __restrict__ tw,
+                                        u64 q, u64 q2) {
+    const int lt0 = logN - st0 - 1;        // log2 t0
+    const int ltk = lt0 - (K - 1);         // log2 tk
+    const int tk = 1 << ltk;
+    const int ngroups = NS >> K;
+    for (int g = threadIdx.x; g < ngroups; g += blockDim.x) {
+        const int blk = g >> ltk, off = g & (tk - 1);
+        const int base = (blk << (lt0 + 1)) + off;
+        u64 x[1 << K];
+#pragma unroll
+        for (int c = 0; c < (1 << K); ++c) x[c] = sm[PAD(base + (c << ltk))];
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+            const int half = 1 << (K - 1 - r);
+            const int twb = (1 << (st0 + r)) + (seg << (st0 + r - split)) +
+                            (blk << r);
+#pragma unroll
+            for (int c = 0; c < (1 << K); ++c) {
+                if (c & half) continue;
+                const ulonglong2 w = __ldg(&tw[twb + (c >> (K - r))]);
+                ct_bfly(x[c], x[c + half], w, q, q2);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < (1 << K); ++c) sm[PAD(base + (c << ltk))] = x[c];
+    }
+}
+
+// One pass of K radix-2 Gentleman-Sande stages (inverse NTT, bit-reversed
+// input, natural output) over `narr` independent M-point transforms stored
+// at sm + a * arr_stride.  Strides t = 2^lt0 .. 2^(lt0+K-1); the twiddle of
+// block i at stride t is tw_inv[M/(2t) + i] (the prefix of the N-point
+// table serves every M = N/s: brv_N(k) = s brv_M(k) for k < M).  `seg`:
+// offset of this segment's blocks when the M-point transform is one of
+// 2^split segments of a larger transform (logMS = log2 of the full size).
+template <int K>
+__device__ __forceinline__ void gs_pass(u64* sm, int arr_stride, int narr,
+                                        int logM, int lt0, int seg,
+                                        int logMfull,
+                                        const ulonglong2* __restrict__ tw,
+                                        u64 q, u64 q2) {
+    const int tk = 1 << lt0;
+    const int gper = 1 << (logM - K);
+    const int total = narr * gper;
+    for (int G = threadIdx.x; G < total; G += blockDim.x) {
+        const int a = G >> (logM - K), g = G & (gper - 1);
+        u64* s = sm + a * arr_stride;
+        const int blk = g >> lt0, off = g & (tk - 1);
+        const int base = (blk << (lt0 + K)) + off;
+        u64 x[1 << K];
+#pragma unroll
+        for (int c = 0; c < (1 << K); ++c) x[c] = s[PAD(base + (c << lt0))];
+#pragma unroll
+        for (int v = 0; v < K; ++v) {
+            const int half = 1 << v;
+            const int lt = lt0 + v;                       // log2 t
+            const int hh = 1 << (logMfull - lt - 1);      // full-size h
+            const int segoff = seg << (logM - lt - 1);
+#pragma unroll
+            for (int c = 0; c < (1 << K); ++c) {
+                if (c & half) continue;
+                const int ib = (blk << (K - 1 - v)) + (c >> (v + 1));
+                const ulonglong2 w = __ldg(&tw[hh + segoff + ib]);
+                gs_bfly(x[c], x[c + half], w, q, q2);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < (1 << K); ++c) s[PAD(base + (c << lt0))] = x[c];
+    }
+}
+
+// Full forward pass schedule on a segment: stages split .. logN-1 in passes
+// of up to 4 stages (the remainder first).
+__device__ __forceinline__ void ct_all(u64* sm, int logN, int NS, int seg,
+                                       int split, const ulonglong2* tw, u64 q,
+                                       u64 q2) {
+    int st = split;
+    int rem = (logN - split) & 3;
+    if (rem) {
+        if (rem == 1) ct_pass<1>(sm, logN, NS, st, seg, split, tw, q, q2);
+        else if (rem == 2) ct_pass<2>(sm, logN, NS, st, seg, split, tw, q, q2);
+        else ct_pass<3>(sm, logN, NS, st, seg, split, tw, q, q2);
+        st += rem;
+        __syncthreads();
+    }
+    for (; st < logN; st += 4) {
+        ct_pass<4>(sm, logN, NS, st, seg, split, tw, q, q2);
+        __syncthreads();
+    }
+}
+
+// Full inverse schedule on narr M-point arrays: strides 1 .. M/2.
+__device__ __forceinline__ void gs_all(u64* sm, int arr_stride, int narr,
+                                       int logM, int seg, int logMfull,
+                                       const ulonglong2* tw, u64 q, u64 q2) {
+    int lt = 0;
+    int rem = logM & 3;
+    for (; lt + 4 <= logM; lt += 4) {
+        gs_pass<4>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
+        __syncthreads();
+    }
+    if (rem) {
+        if (rem == 1) gs_pass<1>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
+        else if (rem == 2) gs_pass<2>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
+        else gs_pass<3>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
+        __syncthreads();
+    }
+}

@@ -1,0 +1,143 @@
+// u1_microbench.cu -- U1: register-resident throughput of the
+// integer operations the hot path is built from, measured on the B200 that
+// runs the bench.  These are the "alu" roofline denominators bench.py uses
+// (DESIGN.md "Roofline").  Not part of the product C-ABI (separate .so).
+//
+//   which 0: IMAD      (mad.lo.u32)                      -> IMAD / s
+//   which 1: IMAD.WIDE (mad.wide.u32, 64-bit addend)     -> IMAD.WIDE / s
+//   which 2: lazy modular MAC, 25-bit split (4 mad.wide) -> MAC / s
+//   which 3: Shoup Cooley-Tukey butterfly (ct_bfly)      -> butterflies / s
+//   which 4: Shoup Gentleman-Sande butterfly (gs_bfly)   -> butterflies / s
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "he_internal.cuh"
+
+__global__ void u1_imad(const u32* in, u32* out, int iters, long long* cyc) {
+    u32 a = in[0], b = in[1];
+    u32 x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+    long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[i]) : "r"(a), "r"(b));
+    }
+    long long c1 = clock64();
+    u32 s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s ^= x[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
+}
+
+__global__ void u1_imad_wide(const u32* in, u32* out, int iters, long long* cyc) {
+    u32 a = in[0] + threadIdx.x, b = in[1];
+    u64 acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = i;
+    long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc[i]) : "r"(a), "r"(b));
+    }
+    long long c1 = clock64();
+    u64 s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s ^= acc[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = (u32)(s ^ (s >> 32));
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
+}
+
+// 2 independent lazy MACs per iteration (acc0 += c0 f0; acc1 += c0 f1 + c1 f0;
+// acc2 += c1 f1), i.e. 8 mad.wide per iteration.
+__global__ void u1_mac(const u32* in, u32* out, int iters, long long* cyc) {
+    u32 c0 = in[0] + threadIdx.x, c1 = in[1], f0 = in[2], f1 = in[3];
+    u64 a[2][3] = {{0, 0, 0}, {1, 1, 1}};
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a[m][0]) : "r"(c0), "r"(f0));
+            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a[m][1]) : "r"(c0), "r"(f1));
+            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a[m][1]) : "r"(c1), "r"(f0));
+            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a[m][2]) : "r"(c1), "r"(f1));
+        }
+    }
+    long long t1 = clock64();
+    u64 s = a[0][0] ^ a[0][1] ^ a[0][2] ^ a[1][0] ^ a[1][1] ^ a[1][2];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = (u32)(s ^ (s >> 32));
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = t1 - t0;
+}
+
+template <bool GS>
+__global__ void u1_bfly(const u64* in, u32* out, int iters, long long* cyc) {
+    const u64 q = in[0], q2 = 2 * q;
+    const ulonglong2 w = make_ulonglong2(in[1], in[2]);
+    u64 X[8], Y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { X[i] = (threadIdx.x + i) % q; Y[i] = (threadIdx.x * 7 + i) % q; }
+    long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (GS) gs_bfly(X[i], Y[i], w, q, q2);
+            else ct_bfly(X[i], Y[i], w, q, q2);
+        }
+    }
+    long long c1 = clock64();
+    u64 s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s ^= X[i] ^ Y[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = (u32)(s ^ (s >> 32));
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
+}
+
+// Runs kernel `which` once (after one warm-up launch); returns the elapsed
+// milliseconds, the in-kernel cycle count of block 0 (SM clock estimate)
+// and the number of operations executed.  0 on success.
+extern "C" int u1_run(int which, int blocks, int threads, int iters, float* ms,
+                      long long* cycles, double* ops) {
+    u32* d_in = nullptr;
+    u32* d_out = nullptr;
+    long long* d_cyc = nullptr;
+    u64 h_in64[4] = {1125899906826241ull, 11286399139ull, 0, 0};
+    h_in64[2] = (u64)(((unsigned __int128)h_in64[1] << 64) / h_in64[0]);
+    if (cudaMalloc(&d_in, 64) || cudaMalloc(&d_out, sizeof(u32) * blocks * threads) ||
+        cudaMalloc(&d_cyc, sizeof(long long)))
+        return 1;
+    if (which >= 3) cudaMemcpy(d_in, h_in64, sizeof(h_in64), cudaMemcpyHostToDevice);
+    else {
+        u32 h[4] = {3u, 5u, 0x1ffffffu, 0x1234567u};
+        cudaMemcpy(d_in, h, sizeof(h), cudaMemcpyHostToDevice);
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double per_iter = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+        if (rep == 1) cudaEventRecord(e0);
+        switch (which) {
+            case 0: u1_imad<<<blocks, threads>>>(d_in, d_out, iters, d_cyc); per_iter = 8; break;
+            case 1: u1_imad_wide<<<blocks, threads>>>(d_in, d_out, iters, d_cyc); per_iter = 8; break;
+            case 2: u1_mac<<<blocks, threads>>>(d_in, d_out, iters, d_cyc); per_iter = 2; break;
+            case 3: u1_bfly<false><<<blocks, threads>>>((const u64*)d_in, d_out, iters, d_cyc); per_iter = 8; break;
+            case 4: u1_bfly<true><<<blocks, threads>>>((const u64*)d_in, d_out, iters, d_cyc); per_iter = 8; break;
+            default: return 2;
+        }
+        if (rep == 1) cudaEventRecord(e1);
+    }
+    cudaEventSynchronize(e1);
+    int rc = cudaGetLastError() != cudaSuccess ? 3 : 0;
+    cudaEventElapsedTime(ms, e0, e1);
+    cudaMemcpy(cycles, d_cyc, sizeof(long long), cudaMemcpyDeviceToHost);
+    *ops = (double)blocks * threads * iters * per_iter;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d_in);
+    cudaFree(d_out);
+    cudaFree(d_cyc);
+    return rc;
+}

@@ -1,0 +1,315 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bit-exact on every compared residue (integer work).  Sizes: small rings
+with several tiles and ragged batches, every BASELINE.json config (configs
+1-3 in full, configs 4-5 in the bench launch configuration with sampled
+images), plus edge cases (B = 0, valid padding, s_override, stride 2,
+n_ib / n_ob > 1, masks on/off, N = 256 .. 32768).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import ref as R
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(),
+                                 reason="needs a CUDA GPU")]
+
+
+@pytest.fixture(scope="module")
+def he():
+    import paper_2409_05205_b200 as he
+    return he
+
+
+def u64(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy().view(np.uint64)
+
+
+def dev(a: np.ndarray) -> torch.Tensor:
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint64:
+        a = a.view(np.int64)
+    if a.dtype == np.uint32:
+        a = a.view(np.int32)
+    return torch.from_numpy(a).cuda()
+
+
+def brv(x, bits):
+    return int(format(x, f"0{bits}b")[::-1], 2) if bits else 0
+
+
+_CTX = {}
+
+
+def ctx_for(he, N, primes, t=65537):
+    key = (N, tuple(primes), t)
+    if key not in _CTX:
+        _CTX[key] = he.Context(primes, N.bit_length() - 1, t)
+    return _CTX[key]
+
+
+RINGS = {
+    256: (7681, 12289, 40961),
+    1024: tuple(synth.PRIMES_CFG1) + (R.find_primes(1024, 50, 1)[0],),
+    8192: tuple(synth.PRIMES_N8192[:2]),
+    16384: tuple(synth.PRIMES_N16384[:2]),
+    32768: tuple(synth.PRIMES_N32768[:2]),
+}
+
+
+# ------------------------------------------------------------- transforms
+@pytest.mark.parametrize("N", sorted(RINGS))
+def test_ntt_forward_matches_definition(he, N):
+    primes = RINGS[N]
+    ctx = ctx_for(he, N, primes)
+    logN = N.bit_length() - 1
+    for j, q in enumerate(primes):
+        assert ctx.psi(j) == R.min_psi(q, N)          # R9, independently
+    batch = 3
+    x = synth.uniform_residues((batch, len(primes), N), primes, 1, "misc", N)
+    d = dev(x)
+    ctx.ntt_forward(d)
+    got = u64(d)
+    rng = np.random.default_rng(N)
+    pos = np.arange(N) if N <= 1024 else np.unique(
+        np.concatenate([[0, 1, N - 1], rng.integers(0, N, 40)]))
+    for b in (0, batch - 1):
+        for j, q in enumerate(primes):
+            ks = np.array([brv(int(p), logN) for p in pos], np.int32)
+            want = R.ntt_def(x[b, j], q, ctx.psi(j), ks)
+            assert np.array_equal(got[b, j, pos], want)
+
+
+@pytest.mark.parametrize("N", sorted(RINGS))
+def test_ntt_roundtrip(he, N):
+    primes = RINGS[N]
+    ctx = ctx_for(he, N, primes)
+    x = synth.uniform_residues((5, len(primes), N), primes, 2, "misc", N)
+    d = dev(x)
+    ctx.ntt_forward(d)
+    assert not np.array_equal(u64(d), x)
+    ctx.ntt_inverse(d)
+    assert np.array_equal(u64(d), x)
+
+
+def test_ntt_inverse_matches_definition(he):
+    N, primes = 256, RINGS[256]
+    ctx = ctx_for(he, N, primes)
+    X = synth.uniform_residues((1, 3, N), primes, 3, "misc")
+    d = dev(X)
+    ctx.ntt_inverse(d)
+    got = u64(d)
+    for j, q in enumerate(primes):
+        nat = np.empty(N, np.uint64)         # bit-reversed -> natural order
+        for p in range(N):
+            nat[brv(p, 8)] = X[0, j, p]
+        assert np.array_equal(got[0, j], R.intt_def(nat, q, ctx.psi(j)))
+
+
+# -------------------------------------------------------------- conv path
+def run_conv(he, ctx, ring, Ly, B, seed, mask=True, s_override=0,
+             ve=False, check_b=None):
+    """GPU: pack_input -> pack_filters -> conv -> mask_extract; oracle: the
+    same on the sampled images.  Returns the plan."""
+    N = ring.N
+    plan_o = R.plan_conv(Ly, N, s_override)
+    p = ctx.plan(Ly.c_i, Ly.c_o, Ly.w_i, Ly.h_i, Ly.f_w, Ly.f_h, Ly.stride,
+                 Ly.pad, s_override)
+    assert (p.s, p.c_ib, p.n_ib, p.c_ob, p.n_ob, p.w_o, p.h_o, p.n_valid) == \
+        (plan_o.s, plan_o.c_ib, plan_o.n_ib, plan_o.c_ob, plan_o.n_ob,
+         plan_o.w_o, plan_o.h_o, plan_o.n_valid)
+    rng = np.random.default_rng(seed)
+    W = rng.integers(-8, 8, (Ly.c_o, Ly.c_i, Ly.f_w, Ly.f_h)).astype(np.int32)
+    c0 = synth.uniform_residues((B, p.n_ib, ring.L, N), ring.primes, seed)
+    phi = synth.phi1((B, p.n_ob, N), ring.t, seed) if mask else None
+    fspec = ctx.pack_filters(p, dev(W))
+    out = ctx.conv(p, dev(c0), fspec, dev(phi) if mask else None)
+    comp = ctx.mask_extract(p, out)
+    torch.cuda.synchronize()
+    g_out, g_comp = u64(out), u64(comp)
+    bs = list(range(B)) if check_b is None else check_b
+    ref = R.conv_server(c0[bs], W, plan_o, ring,
+                        phi[bs] if mask else None)
+    assert np.array_equal(g_out[bs], ref)
+    assert np.array_equal(g_comp[bs], R.compact(ref, plan_o))
+    return p
+
+
+SMALL = [
+    (synth.ConvLayer(1, 2, 4, 4), 256, 0, 3),
+    (synth.ConvLayer(3, 4, 4, 4), 256, 0, 2),
+    (synth.ConvLayer(4, 4, 4, 4, stride=2), 256, 0, 5),
+    (synth.ConvLayer(8, 2, 3, 3), 256, 0, 1),
+    (synth.ConvLayer(8, 8, 4, 4, stride=2), 256, 0, 17),
+    (synth.ConvLayer(4, 2, 2, 2, f_w=2, f_h=1, pad=0), 256, 4, 2),
+    (synth.ConvLayer(2, 3, 5, 3, f_w=3, f_h=1), 1024, 0, 33),
+    (synth.ConvLayer(5, 7, 6, 5), 1024, 0, 19),
+    (synth.ConvLayer(40, 70, 4, 4), 1024, 0, 35),   # n_ib = 3, n_ob = 5
+    (synth.ConvLayer(16, 16, 6, 6), 1024, 16, 7),   # s_override
+    (synth.ConvLayer(3, 5, 14, 14, f_w=5, f_h=5), 1024, 0, 9),  # fills ring
+]
+
+
+@pytest.mark.parametrize("case", SMALL, ids=lambda c: f"{c[0]}-N{c[1]}")
+@pytest.mark.parametrize("mask", [True, False])
+def test_conv_small(he, case, mask):
+    Ly, N, so, B = case
+    primes = RINGS[N]
+    ctx = ctx_for(he, N, primes)
+    ring = R.Ring(N, primes, 65537)
+    run_conv(he, ctx, ring, Ly, B, seed=B * 7 + N, mask=mask, s_override=so)
+
+
+@pytest.mark.parametrize("cfg_idx", [1, 2, 3])
+def test_conv_configs_full(he, cfg_idx):
+    cfg = synth.CONFIGS[cfg_idx]
+    ctx = ctx_for(he, cfg.N, cfg.primes, cfg.t)
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    run_conv(he, ctx, ring, cfg.conv[0], cfg.B, seed=cfg.seed)
+
+
+def _distinct_layers(cfg):
+    seen, out = set(), []
+    for i, Ly in enumerate(cfg.conv):
+        if Ly not in seen:
+            seen.add(Ly)
+            out.append((i, Ly))
+    return out
+
+
+@pytest.mark.parametrize("li", [i for i, _ in _distinct_layers(synth.CONFIGS[4])])
+def test_conv_config4_layers(he, li):
+    """Config 4 at the bench batch (B = 32), sampled images compared."""
+    cfg = synth.CONFIGS[4]
+    ctx = ctx_for(he, cfg.N, cfg.primes, cfg.t)
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    run_conv(he, ctx, ring, cfg.conv[li], cfg.B, seed=cfg.seed + li,
+             check_b=[0, cfg.B - 1])
+
+
+def test_conv_config5_sampled(he):
+    """Config 5 (N = 32768, L = 12, B = 256): sampled images."""
+    cfg = synth.CONFIGS[5]
+    ctx = ctx_for(he, cfg.N, cfg.primes, cfg.t)
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    run_conv(he, ctx, ring, cfg.conv[0], cfg.B, seed=cfg.seed,
+             check_b=[0, 131, 255])
+
+
+def test_conv_config5_paper_literal_s(he):
+    """Config 5 with s = c_i = 64 (the paper's own layout)."""
+    cfg = synth.CONFIGS[5]
+    ctx = ctx_for(he, cfg.N, cfg.primes, cfg.t)
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    run_conv(he, ctx, ring, cfg.conv[0], 8, seed=5, s_override=64,
+             check_b=[0, 7])
+
+
+# ------------------------------------------------------------ packing a1
+@pytest.mark.parametrize("cfg_idx", [1, 2, 3, 4])
+def test_pack_input(he, cfg_idx):
+    cfg = synth.CONFIGS[cfg_idx]
+    ctx = ctx_for(he, cfg.N, cfg.primes, cfg.t)
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    Ly = cfg.conv[-1]
+    plan = R.plan_conv(Ly, cfg.N)
+    p = ctx.plan(Ly.c_i, Ly.c_o, Ly.w_i, Ly.h_i, Ly.f_w, Ly.f_h, Ly.stride,
+                 Ly.pad)
+    B = 2
+    img = synth.images(cfg, len(cfg.conv) - 1, B)
+    ve = synth.uniform_residues((B, p.n_ib, ring.L, cfg.N), cfg.primes, 4, "ve")
+    got = u64(ctx.pack_input(p, dev(img)))
+    got_ve = u64(ctx.pack_input(p, dev(img), ve=dev(ve)))
+    for b in range(B):
+        ip = R.pack_input_int(img[b], plan)
+        for beta in range(plan.n_ib):
+            enc = R.encode(np.mod(ip[beta], cfg.t).astype(np.uint32), ring)
+            assert np.array_equal(got[b, beta], enc)
+            want = (enc.astype(object) + ve[b, beta].astype(object)) % \
+                ring.q_arr.astype(object)[:, None]
+            assert np.array_equal(got_ve[b, beta], want.astype(np.uint64))
+
+
+def test_protocol_config1_gpu_server(he):
+    """Client (oracle) -> GPU server -> client decrypt == conv mod t."""
+    cfg = synth.CONFIGS[1]
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    ctx = ctx_for(he, cfg.N, cfg.primes, cfg.t)
+    Ly = cfg.conv[0]
+    plan = R.plan_conv(Ly, cfg.N)
+    p = ctx.plan(Ly.c_i, Ly.c_o, Ly.w_i, Ly.h_i)
+    s_key = synth.secret_key(cfg.N, cfg.h, cfg.seed)
+    a = synth.uniform_residues((1, cfg.N), cfg.primes, cfg.seed, "a")
+    b_pk = R.keygen(ring, s_key, a, synth.gauss_poly(cfg.N, 3.2, cfg.seed, "e0", 9))
+    img = synth.images(cfg, 0)
+    W = synth.weights(cfg, 0)
+    v = synth.v_poly(cfg.N, cfg.seed, 0, 0)
+    e0 = synth.gauss_poly(cfg.N, 3.2, cfg.seed, "e0", 0, 0)
+    # c0 = v b + e0 + enc(i): the GPU packs/encodes i and adds v b + e0
+    vbe = R.encrypt_c0(ring, np.zeros(cfg.N, np.int64), b_pk, v, e0)
+    c0 = ctx.pack_input(p, dev(img), ve=dev(vbe[None, None]))
+    assert np.array_equal(u64(c0)[0, 0], R.encrypt_c0(
+        ring, R.pack_input_int(img[0], plan)[0], b_pk, v, e0))
+    phi = synth.phi1((1, p.n_ob, cfg.N), cfg.t, cfg.seed)
+    out = ctx.conv(p, c0, ctx.pack_filters(p, dev(W)), dev(phi))
+    ef = {(n, 0): synth.gauss_poly(cfg.N, 3.2, cfg.seed, "ef", n, 0)
+          for n in range(Ly.c_o)}
+    dec = R.conv_protocol_decrypt(ring, plan, W, u64(out)[0], s_key, a, [v],
+                                  ef, phi[0])
+    assert np.array_equal(dec, R.centered_mod_t(R.conv2d_ref(img[0], W, plan),
+                                                cfg.t))
+
+
+# ----------------------------------------------------------------- FC a9
+@pytest.mark.parametrize("N,n_i,n_o,B", [(256, 6, 5, 3), (1024, 10, 100, 2),
+                                         (16384, 64, 100, 32)])
+def test_fc(he, N, n_i, n_o, B):
+    primes = synth.PRIMES_N16384 if N == 16384 else RINGS[N]
+    ctx = ctx_for(he, N, primes)
+    ring = R.Ring(N, tuple(primes), 65537)
+    rng = np.random.default_rng(N + n_o)
+    W = rng.integers(-8, 8, (n_o, n_i)).astype(np.int32)
+    bias = rng.integers(-8, 8, n_o).astype(np.int32)
+    inp = rng.integers(0, 256, (B, n_i)).astype(np.int32)
+    c0 = synth.uniform_residues((B, ring.L, N), primes, N)
+    phi = synth.phi1((B, n_o), 65537, N)
+    wspec, benc = ctx.fc_pack_weights(dev(W), dev(bias))
+    out = u64(ctx.fc(n_i, n_o, dev(c0), wspec, benc, dev(phi)))
+    bs = [0, B - 1]
+    assert np.array_equal(out[bs], R.fc_server(c0[bs], W, bias, ring, phi[bs]))
+    # packed input: enc(Eq. 9)
+    pk = u64(ctx.fc_pack_input(n_i, n_o, dev(inp)))
+    for b in bs:
+        enc = R.encode(np.mod(R.fc_input_int(inp[b], n_o, N), 65537)
+                       .astype(np.uint32), ring)
+        assert np.array_equal(pk[b], enc)
+
+
+# --------------------------------------------------------------- errors
+def test_errors(he):
+    with pytest.raises(he.HeError) as e:
+        he.Context([7681, 7681], 8)
+    assert e.value.status == he.HE_EPARAM
+    with pytest.raises(he.HeError):
+        he.Context([7683], 8)                      # not prime
+    with pytest.raises(he.HeError):
+        he.Context([(1 << 50) + 1], 8)
+    ctx = ctx_for(he, 256, RINGS[256])
+    with pytest.raises(he.HeError) as e:
+        ctx.plan(1, 1, 17, 17)                     # 19*19 > 256
+    assert e.value.status == he.HE_ESHAPE
+    with pytest.raises(he.HeError):
+        ctx.plan(1, 1, 4, 4, s_override=3)
+    p = ctx.plan(2, 2, 4, 4)
+    c0 = ctx.empty_u64(2, p.n_ib, 3, 256)
+    fspec = ctx.pack_filters(p, torch.zeros(2, 2, 3, 3, dtype=torch.int32,
+                                            device="cuda"))
+    small_ws = torch.empty(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(he.HeError) as e:
+        ctx.conv(p, c0, fspec, ws=small_ws)
+    assert e.value.status == he.HE_ENOMEM
+    # B = 0 is a no-op
+    ctx.conv(p, ctx.empty_u64(0, p.n_ib, 3, 256), fspec)
