@@ -1,0 +1,516 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the rotation-free HE Conv/FC server hot path.
+
+Workload (default, BASELINE.json configs[3]): the full plain-20 stack
+(19 Conv layers + FC 64->100), ring N = 16384, L = 6 primes of 50 bits,
+B = 32 images per GPU (weak scaling: every rank serves its own batch, no
+data-path collective).  One step = the server evaluation of
+every layer for the batch: he_conv (forward NTT of c0, folded NTT-domain
+MAC, inverse NTT + slot scatter + enc(phi1) mask) and he_mask_extract
+(valid-slot payload) for each Conv layer, then he_fc.  Inputs are seeded
+synthetic residues (synth/); the per-layer filter spectra (server init,
+Alg. 1 Line 4) are prepared before the timed region and timed separately.
+
+Metric: ct x pt evals / s (one eval = one c0_beta x fhat_beta^{(n)} product
+with its extraction; B*c_o*n_ib per Conv layer, B per FC) plus ms per
+plain-20 image and NTT limbs / s against the roofline.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload plain20|cfg5|cfg3]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK_GBS = 6650.0           # B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["plain20", "cfg5", "cfg3"],
+                    default="plain20")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="short run for ncu: no e2e / cpu baseline / clocks")
+    return ap.parse_args()
+
+
+WORKLOADS = {"plain20": 4, "cfg5": 5, "cfg3": 3}
+
+
+def peaks():
+    try:
+        d = json.load(open(MEASURED))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------- workload def
+class LayerWork:
+    def __init__(self, idx, Ly, plan, N, L, B):
+        self.idx, self.Ly, self.p = idx, Ly, plan
+        M = N // plan.s
+        nlimb = B * plan.n_ib * L
+        self.evals = B * Ly.c_o * plan.n_ib
+        self.ntt_bfly = nlimb * (N // 2) * (N.bit_length() - 1)
+        self.ntt_bytes = nlimb * N * 16
+        self.macs = L * N * plan.n_ib * B * Ly.c_o
+        self.mac_bytes = 8 * (nlimb * N + Ly.c_o * plan.n_ib * L * N +
+                              L * M * B * Ly.c_o)
+        logM = M.bit_length() - 1
+        self.intt_bfly = B * plan.n_ob * plan.c_ob * L * (M // 2) * logM
+        self.intt_bytes = 8 * (L * M * B * Ly.c_o + B * plan.n_ob * L * N) + \
+            4 * B * plan.n_ob * N
+        self.c0_bytes = nlimb * N * 8
+        self.comp_bytes = B * plan.n_ob * L * plan.n_valid * 8
+        self.phi_bytes = B * plan.n_ob * N * 4
+
+
+def u1_peaks(device_index=0):
+    """Run the U1 register-resident microbenchmarks (libhe_u1.so) on this
+    GPU: returns rates per second and the in-kernel SM clock."""
+    import ctypes
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_2409_05205_b200",
+                                   "libhe_u1.so"))
+    lib.u1_run.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p] * 3
+    out = {}
+    names = ["imad", "imad_wide", "modmac", "ct_bfly", "gs_bfly"]
+    iters = {0: 20000, 1: 20000, 2: 20000, 3: 2000, 4: 2000}
+    for w, name in enumerate(names):
+        ms, cyc, ops = ctypes.c_float(), ctypes.c_longlong(), ctypes.c_double()
+        rc = lib.u1_run(w, 148 * 8, 256, iters[w], ctypes.byref(ms),
+                        ctypes.byref(cyc), ctypes.byref(ops))
+        if rc:
+            raise RuntimeError(f"u1 {name} rc={rc}")
+        rate = ops.value / (ms.value * 1e-3)
+        mhz = cyc.value / (ms.value * 1e3)
+        out[name] = {"per_s": rate, "sm_mhz_in_kernel": round(mhz, 1),
+                     "per_clk_per_sm": rate / (mhz * 1e6) / 148}
+    return out
+
+
+class ClockSampler:
+    def __init__(self, idx):
+        self.idx = idx
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for r in self.rows:
+            for n, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ reference
+def run_reference(args, cfg, rank):
+    """--impl reference: the CPU oracle as it stands (test infrastructure),
+    rank 0 only, one image through the whole stack per step."""
+    if rank != 0:
+        return
+    from oracle import ref as R
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    plans = [R.plan_conv(Ly, cfg.N) for Ly in cfg.conv]
+    Ws = [synth.weights(cfg, i) for i in range(len(cfg.conv))]
+    c0s = [synth.uniform_residues((1, p.n_ib, ring.L, cfg.N), cfg.primes,
+                                  cfg.seed, "c0", i) for i, p in enumerate(plans)]
+    phis = [synth.phi1((1, p.n_ob, cfg.N), cfg.t, cfg.seed, i)
+            for i, p in enumerate(plans)]
+    fc = None
+    if cfg.fc is not None:
+        fc = (synth.fc_weights(cfg), synth.fc_bias(cfg),
+              synth.uniform_residues((1, ring.L, cfg.N), cfg.primes, cfg.seed,
+                                     "c0", 99),
+              synth.phi1((1, cfg.fc.n_o), cfg.t, cfg.seed, 99))
+    evals = sum(Ly.c_o * p.n_ib for Ly, p in zip(cfg.conv, plans)) + \
+        (1 if fc else 0)
+
+    def step():
+        for p, W, c0, ph in zip(plans, Ws, c0s, phis):
+            R.compact(R.conv_server(c0, W, p, ring, ph), p)
+        if fc:
+            R.fc_server(fc[2], fc[0], fc[1], ring, fc[3])
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    v = evals / dt
+    line = {"metric": "Conv+FC layer ct×pt evals/sec", "value": v,
+            "unit": "ct×pt evals/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic",
+            "config": {"workload": f"cfg{cfg.idx} {cfg.name}", "N": cfg.N,
+                       "L": cfg.L, "images_per_step": 1},
+            "ms_per_plain20_image": dt * 1e3,
+            "cpu_baseline": {"value": v, "unit": "ct×pt evals/s",
+                             "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": f"1 image x {len(plans)} conv"
+                                       f"{' + FC' if fc else ''} layers per step"},
+            "e2e": {"value": v, "unit": "ct×pt evals/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours
+def main():
+    args = parse()
+    cfg = synth.CONFIGS[WORKLOADS[args.workload]]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2409_05205_b200 as he
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    B, N, L = cfg.B, cfg.N, cfg.L
+    ctx = he.Context(cfg.primes, cfg.log2N, cfg.t, local)
+    stream = torch.cuda.current_stream()
+
+    def d(a):
+        a = np.ascontiguousarray(a)
+        if a.dtype == np.uint64:
+            a = a.view(np.int64)
+        elif a.dtype == np.uint32:
+            a = a.view(np.int32)
+        return torch.from_numpy(a).to(dev)
+
+    # ---- server init (Alg. 1 Line 4 / Alg. 2 Lines 3-4), timed separately
+    layers, fspecs, c0_h, c0_d, phi_d, phi_h, outs, comps = [], [], [], [], [], [], [], []
+    t_init0 = time.perf_counter()
+    init_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    init_ev[0].record()
+    for i, Ly in enumerate(cfg.conv):
+        p = ctx.plan(Ly.c_i, Ly.c_o, Ly.w_i, Ly.h_i, Ly.f_w, Ly.f_h, Ly.stride,
+                     Ly.pad)
+        layers.append(LayerWork(i, Ly, p, N, L, B))
+        fspecs.append(ctx.pack_filters(p, d(synth.weights(cfg, i))))
+    init_ev[1].record()
+    torch.cuda.synchronize()
+    init_ms = init_ev[0].elapsed_time(init_ev[1])
+    for lw in layers:
+        p = lw.p
+        c0 = synth.uniform_residues((B, p.n_ib, L, N), cfg.primes,
+                                    cfg.seed + 1000 * rank, "c0", lw.idx)
+        ph = synth.phi1((B, p.n_ob, N), cfg.t, cfg.seed + 1000 * rank, lw.idx)
+        c0_h.append(torch.from_numpy(c0.view(np.int64)).pin_memory())
+        phi_h.append(torch.from_numpy(ph.view(np.int32)).pin_memory())
+        c0_d.append(c0_h[-1].to(dev))
+        phi_d.append(phi_h[-1].to(dev))
+        outs.append(ctx.empty_u64(B, p.n_ob, L, N))
+        comps.append(ctx.empty_u64(B, p.n_ob, L, p.n_valid))
+    ws = torch.empty(max(ctx.conv_workspace(p, B).numel() for p in
+                         [lw.p for lw in layers]), dtype=torch.uint8, device=dev)
+    fc = None
+    if cfg.fc is not None:
+        n_i, n_o = cfg.fc.n_i, cfg.fc.n_o
+        wspec, benc = ctx.fc_pack_weights(d(synth.fc_weights(cfg)),
+                                          d(synth.fc_bias(cfg)))
+        fc_c0 = synth.uniform_residues((B, L, N), cfg.primes,
+                                       cfg.seed + 1000 * rank, "c0", 99)
+        fc_ph = synth.phi1((B, n_o), cfg.t, cfg.seed + 1000 * rank, 99)
+        fc = dict(n_i=n_i, n_o=n_o, wspec=wspec, benc=benc,
+                  c0_h=torch.from_numpy(fc_c0.view(np.int64)).pin_memory(),
+                  ph_h=torch.from_numpy(fc_ph.view(np.int32)).pin_memory())
+        fc["c0_d"] = fc["c0_h"].to(dev)
+        fc["ph_d"] = fc["ph_h"].to(dev)
+        fc["out"] = ctx.empty_u64(B, L, n_o)
+        fc["ws"] = ctx.fc_workspace(n_i, n_o, B)
+        fc["out_h"] = torch.empty((B, L, n_o), dtype=torch.int64).pin_memory()
+    comp_h = [torch.empty(c.shape, dtype=torch.int64).pin_memory() for c in comps]
+    torch.cuda.synchronize()
+
+    evals_step = sum(lw.evals for lw in layers) + (B if fc else 0)
+    launches_step = 4 * len(layers) + (2 if fc else 0)
+
+    def step(evs=None):
+        for i, lw in enumerate(layers):
+            ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], outs[i], ws,
+                     events=None if evs is None else evs[i])
+            ctx.mask_extract(lw.p, outs[i], None, comps[i])
+        if fc:
+            ctx.fc(fc["n_i"], fc["n_o"], fc["c0_d"], fc["wspec"], fc["benc"],
+                   fc["ph_d"], fc["out"], fc["ws"],
+                   events=None if evs is None else evs[len(layers)])
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    # per-step stage events (he_conv_ex / he_fc_ex)
+    mk = lambda: torch.cuda.Event(enable_timing=True)
+    evs = [[[mk() for _ in range(4)] for _ in layers] + ([[mk() for _ in range(3)]] if fc else [])
+           for _ in range(args.steps)]
+    e0, e1 = mk(), mk()
+    barrier()
+    sampler = ClockSampler(local)
+    with (sampler if not args.profile else _Null()):
+        e0.record()
+        for k in range(args.steps):
+            step(evs[k])
+        e1.record()
+        barrier()
+    ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    # stage sums (ms per step, averaged over the timed steps)
+    st = {"ntt_fwd": 0.0, "mac_fold": 0.0, "intt_scatter": 0.0,
+          "mask_extract+gaps": 0.0, "fc_ntt_fwd": 0.0, "fc_inv": 0.0}
+    for k in range(args.steps):
+        E = evs[k]
+        for i in range(len(layers)):
+            a = E[i]
+            st["ntt_fwd"] += a[0].elapsed_time(a[1])
+            st["mac_fold"] += a[1].elapsed_time(a[2])
+            st["intt_scatter"] += a[2].elapsed_time(a[3])
+            nxt = E[i + 1][0] if i + 1 < len(E) else None
+            if nxt is not None:
+                st["mask_extract+gaps"] += a[3].elapsed_time(nxt)
+        if fc:
+            f = E[len(layers)]
+            st["fc_ntt_fwd"] += f[0].elapsed_time(f[1])
+            st["fc_inv"] += f[1].elapsed_time(f[2])
+    st = {k: v / args.steps for k, v in st.items()}
+
+    # ---- algorithmic work per step
+    W_ntt_bfly = sum(lw.ntt_bfly for lw in layers)
+    W_ntt_bytes = sum(lw.ntt_bytes for lw in layers)
+    W_macs = sum(lw.macs for lw in layers)
+    W_mac_bytes = sum(lw.mac_bytes for lw in layers)
+    W_intt_bfly = sum(lw.intt_bfly for lw in layers)
+    W_intt_bytes = sum(lw.intt_bytes for lw in layers)
+
+    hbm_gbs, hbm_src = peaks()
+    u1 = u1_peaks(local)
+    # U1 rates were measured at the in-kernel clock; they are the alu roofs.
+    kern = {
+        "ntt_fwd": (st["ntt_fwd"], W_ntt_bfly, u1["ct_bfly"]["per_s"], "Gbutterfly/s",
+                    W_ntt_bytes),
+        "mac_fold": (st["mac_fold"], W_macs, u1["modmac"]["per_s"], "Gmodmac/s",
+                     W_mac_bytes),
+        "intt_scatter": (st["intt_scatter"], W_intt_bfly, u1["gs_bfly"]["per_s"],
+                         "Gbutterfly/s", W_intt_bytes),
+    }
+    rl = {}
+    for name, (ms, ops, alu_peak, unit, byts) in kern.items():
+        t = ms * 1e-3
+        t_alu, t_hbm = ops / alu_peak, byts / (hbm_gbs * 1e9)
+        bound = "alu" if t_alu >= t_hbm else "hbm"
+        if bound == "alu":
+            rl[name] = {"bound": "alu", "achieved": ops / t / 1e9,
+                        "peak": alu_peak / 1e9, "unit": unit,
+                        "frac": (ops / t) / alu_peak, "traffic": None,
+                        "share_of_step": ms / ms_step,
+                        "hbm_frac": byts / t / 1e9 / hbm_gbs}
+        else:
+            rl[name] = {"bound": "hbm", "achieved": byts / t / 1e9,
+                        "peak": hbm_gbs, "unit": "GB/s",
+                        "frac": byts / t / 1e9 / hbm_gbs, "traffic": None,
+                        "share_of_step": ms / ms_step,
+                        "alu_frac": (ops / t) / alu_peak}
+    dom = max(kern, key=lambda k: kern[k][0])
+    roofline = dict(rl[dom])
+    roofline["kernel"] = dom
+    roofline["peak_source"] = ("U1 register-resident microbenchmark on this GPU"
+                               if roofline["bound"] == "alu" else hbm_src)
+    roofline["traffic_note"] = "per-launch DRAM bytes: see profiles/ ncu summary"
+
+    # ---- NTT limbs/s (he_ntt_forward alone, 1024 limbs > L2)
+    nl = 1024 // L * L
+    buf = torch.from_numpy(synth.uniform_residues(
+        (nl // L, L, N), cfg.primes, 7, "misc").view(np.int64)).to(dev)
+    for _ in range(3):
+        ctx.ntt_forward(buf)
+    a, b = mk(), mk()
+    a.record()
+    for _ in range(10):
+        ctx.ntt_forward(buf)
+    b.record()
+    torch.cuda.synchronize()
+    t_ntt = a.elapsed_time(b) / 10 * 1e-3
+    logN = N.bit_length() - 1
+    ntt = {"N": N, "limbs_per_launch": nl, "limbs_per_s": nl / t_ntt,
+           "alu_roof_limbs_per_s": u1["ct_bfly"]["per_s"] / (N // 2 * logN),
+           "hbm_roof_limbs_per_s": hbm_gbs * 1e9 / (16 * N)}
+    ntt["roof_limbs_per_s"] = min(ntt["alu_roof_limbs_per_s"], ntt["hbm_roof_limbs_per_s"])
+    ntt["frac"] = ntt["limbs_per_s"] / ntt["roof_limbs_per_s"]
+    del buf
+
+    # ---- e2e: host c0 (+phi1) -> device -> he_conv/he_mask_extract/he_fc -> host
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        h2d = sum(lw.c0_bytes + lw.phi_bytes for lw in layers)
+        d2h = sum(lw.comp_bytes for lw in layers)
+        if fc:
+            h2d += fc["c0_h"].numel() * 8 + fc["ph_h"].numel() * 4
+            d2h += fc["out"].numel() * 8
+
+        def e2e_step():
+            for i, lw in enumerate(layers):
+                c0_d[i].copy_(c0_h[i], non_blocking=True)
+                phi_d[i].copy_(phi_h[i], non_blocking=True)
+                ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], outs[i], ws)
+                ctx.mask_extract(lw.p, outs[i], None, comps[i])
+                comp_h[i].copy_(comps[i], non_blocking=True)
+            if fc:
+                fc["c0_d"].copy_(fc["c0_h"], non_blocking=True)
+                fc["ph_d"].copy_(fc["ph_h"], non_blocking=True)
+                ctx.fc(fc["n_i"], fc["n_o"], fc["c0_d"], fc["wspec"], fc["benc"],
+                       fc["ph_d"], fc["out"], fc["ws"])
+                fc["out_h"].copy_(fc["out"], non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        x0, x1 = mk(), mk()
+        x0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        x1.record()
+        barrier()
+        ms_e2e = max_over_ranks(x0.elapsed_time(x1) / args.steps)
+        e2e = {"value": evals_step * world / (ms_e2e * 1e-3), "unit": "ct×pt evals/s",
+               "ms_per_step": ms_e2e, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    # ---- CPU baseline: the oracle as it stands, rank 0, bounded sample
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and not args.profile:
+        from oracle import ref as R
+        ring = R.Ring(N, cfg.primes, cfg.t)
+        nimg = 4 if cfg.idx == 4 else 1
+        c0n = [t[:nimg].numpy().view(np.uint64) for t in c0_h]
+        phn = [t[:nimg].numpy().view(np.uint32) for t in phi_h]
+        oplans = [R.plan_conv(lw.Ly, N) for lw in layers]
+        Ws = [synth.weights(cfg, i) for i in range(len(layers))]
+        t0 = time.perf_counter()
+        for i in range(len(layers)):
+            R.compact(R.conv_server(c0n[i], Ws[i], oplans[i], ring, phn[i]), oplans[i])
+        if fc:
+            R.fc_server(fc["c0_h"][:nimg].numpy().view(np.uint64), synth.fc_weights(cfg),
+                        synth.fc_bias(cfg), ring, fc["ph_h"][:nimg].numpy().view(np.uint32))
+        dt = time.perf_counter() - t0
+        ev = nimg * (sum(lw.evals // B for lw in layers) + (1 if fc else 0))
+        cpu = {"value": ev / dt, "unit": "ct×pt evals/s", "cores": os.cpu_count(),
+               "kind": "oracle",
+               "sample": f"{nimg} image(s) x all {len(layers)} conv"
+                         f"{' + FC' if fc else ''} layers ({dt:.1f} s wall)"}
+
+    clocks = sampler.summary() if not args.profile else None
+    if rank == 0:
+        value = evals_step * world / (ms_step * 1e-3)
+        line = {
+            "metric": "Conv+FC layer ct×pt evals/sec", "value": value,
+            "unit": "ct×pt evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"cfg{cfg.idx} {cfg.name}: "
+                                   f"{len(layers)} conv{' + FC' if fc else ''}, "
+                                   f"N={N}, L={L}, B={B}/GPU",
+                       "global_batch": B * world, "N": N, "L": L,
+                       "parallelism": f"dp{world} (batch-sharded, no collective)",
+                       "l2": "inputs larger than L2 (>1 GB touched per step)"},
+            "ms_per_plain20_image": ms_step / B if cfg.idx == 4 else None,
+            "ntt": ntt, "stages_ms_per_step": st, "roofline": roofline,
+            "roofline_all": rl, "u1": u1, "init_ms": init_ms,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches_step * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+    def summary(self):
+        return None
+
+
+if __name__ == "__main__":
+    main()

@@ -143,6 +143,15 @@ he_status he_conv(const he_ctx* ctx, const he_conv_plan* p,
                   const uint32_t* d_phi1, uint64_t* d_out, void* d_ws,
                   size_t ws_bytes, void* stream);
 
+/* he_conv with stage events (measurement): if `events` is non-NULL it
+ * holds 4 cudaEvent_t handles, recorded on `stream` before K1 (forward NTT
+ * of c0), before K3 (folded MAC), before K4 (inverse NTT + scatter + mask)
+ * and after K4.  Results are identical to he_conv. */
+he_status he_conv_ex(const he_ctx* ctx, const he_conv_plan* p,
+                     const uint64_t* d_c0, int B, const uint64_t* d_fspec,
+                     const uint32_t* d_phi1, uint64_t* d_out, void* d_ws,
+                     size_t ws_bytes, void* stream, void* const* events);
+
 /* a7-a8 ("invalid slots ... do not need to be sent").
  * Gathers the n_valid valid slots of each output block, in increasing
  * coefficient order (row K < w_o, column L < h_o, channel n of the block:
@@ -191,6 +200,14 @@ he_status he_fc(const he_ctx* ctx, const he_fc_desc* f, const uint64_t* d_c0,
                 int B, const uint64_t* d_wspec, const uint64_t* d_bias_enc,
                 const uint32_t* d_phi1, uint64_t* d_out, void* d_ws,
                 size_t ws_bytes, void* stream);
+
+/* he_fc with stage events: 3 cudaEvent_t (before the forward NTT, before
+ * the pointwise-product + inverse-NTT kernel, after it) or NULL. */
+he_status he_fc_ex(const he_ctx* ctx, const he_fc_desc* f,
+                   const uint64_t* d_c0, int B, const uint64_t* d_wspec,
+                   const uint64_t* d_bias_enc, const uint32_t* d_phi1,
+                   uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream,
+                   void* const* events);
 
 /* ------------------------------------------------------------ transforms */
 /* Batched negacyclic NTT over `batch` x L limbs stored [batch][L][N]

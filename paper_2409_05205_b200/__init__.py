@@ -86,6 +86,10 @@ _sig("he_pack_filters", [_P, ctypes.POINTER(ConvPlan), _P, _P, _P, _SZ, _P])
 _sig("he_conv_workspace_bytes", [_P, ctypes.POINTER(ConvPlan), _I], _SZ)
 _sig("he_conv", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _P, _P, _SZ,
                  _P])
+_sig("he_conv_ex", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _P, _P,
+                    _SZ, _P, _P])
+_sig("he_fc_ex", [_P, ctypes.POINTER(FcDesc), _P, _I, _P, _P, _P, _P, _P, _SZ,
+                  _P, _P])
 _sig("he_mask_extract", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _P])
 _sig("he_pack_fc_input", [_P, ctypes.POINTER(FcDesc), _P, _I, _P, _P, _P])
 _sig("he_fc_wspec_bytes", [_P, ctypes.POINTER(FcDesc)], _SZ)
@@ -100,9 +104,18 @@ _sig("he_ntt_inverse", [_P, _P, _I, _P])
 EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_conv_plan_make", "he_pack_input", "he_filter_bytes",
             "he_pack_filters_workspace_bytes", "he_pack_filters",
-            "he_conv_workspace_bytes", "he_conv", "he_mask_extract",
+            "he_conv_workspace_bytes", "he_conv", "he_conv_ex", "he_mask_extract",
             "he_pack_fc_input", "he_fc_wspec_bytes", "he_fc_workspace_bytes",
-            "he_pack_fc_weights", "he_fc", "he_ntt_forward", "he_ntt_inverse"]
+            "he_pack_fc_weights", "he_fc", "he_fc_ex", "he_ntt_forward",
+            "he_ntt_inverse"]
+
+
+def _events(events):
+    """list of torch.cuda.Event -> void*[] of cudaEvent_t (or None)."""
+    if events is None:
+        return None
+    arr = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
+    return arr
 
 
 def _check(st: int, what: str):
@@ -204,17 +217,22 @@ class Context:
     def conv(self, p: ConvPlan, c0: torch.Tensor, fspec: torch.Tensor,
              phi1: Optional[torch.Tensor] = None,
              out: Optional[torch.Tensor] = None,
-             ws: Optional[torch.Tensor] = None, stream=None):
+             ws: Optional[torch.Tensor] = None, stream=None, events=None):
+        """he_conv (he_conv_ex when `events` = 4 torch.cuda.Event with
+        enable_timing, recorded at the K1/K3/K4 stage boundaries)."""
         B = c0.shape[0]
         if out is None:
             out = self.empty_u64(B, p.n_ob, self.L, self.N)
         if ws is None:
             ws = self.conv_workspace(p, B)
         self._dev(c0, fspec, phi1, out, ws)
-        _check(_lib.he_conv(self._h, ctypes.byref(p), self._ptr(c0), B,
-                            self._ptr(fspec), self._ptr(phi1), self._ptr(out),
-                            self._ptr(ws), ws.numel() * ws.element_size(),
-                            _stream(stream)), "he_conv")
+        args = (self._h, ctypes.byref(p), self._ptr(c0), B, self._ptr(fspec),
+                self._ptr(phi1), self._ptr(out), self._ptr(ws),
+                ws.numel() * ws.element_size(), _stream(stream))
+        if events is None:
+            _check(_lib.he_conv(*args), "he_conv")
+        else:
+            _check(_lib.he_conv_ex(*args, _events(events)), "he_conv_ex")
         return out
 
     def mask_extract(self, p: ConvPlan, out_full: torch.Tensor,
@@ -268,7 +286,7 @@ class Context:
     def fc(self, n_i, n_o, c0: torch.Tensor, wspec: torch.Tensor,
            bias_enc: torch.Tensor, phi1: Optional[torch.Tensor] = None,
            out: Optional[torch.Tensor] = None,
-           ws: Optional[torch.Tensor] = None, stream=None):
+           ws: Optional[torch.Tensor] = None, stream=None, events=None):
         f = FcDesc(n_i, n_o)
         B = c0.shape[0]
         if out is None:
@@ -276,11 +294,13 @@ class Context:
         if ws is None:
             ws = self.fc_workspace(n_i, n_o, B)
         self._dev(c0, wspec, bias_enc, phi1, out, ws)
-        _check(_lib.he_fc(self._h, ctypes.byref(f), self._ptr(c0), B,
-                          self._ptr(wspec), self._ptr(bias_enc),
-                          self._ptr(phi1), self._ptr(out), self._ptr(ws),
-                          ws.numel() * ws.element_size(), _stream(stream)),
-               "he_fc")
+        args = (self._h, ctypes.byref(f), self._ptr(c0), B, self._ptr(wspec),
+                self._ptr(bias_enc), self._ptr(phi1), self._ptr(out),
+                self._ptr(ws), ws.numel() * ws.element_size(), _stream(stream))
+        if events is None:
+            _check(_lib.he_fc(*args), "he_fc")
+        else:
+            _check(_lib.he_fc_ex(*args, _events(events)), "he_fc_ex")
         return out
 
     # ---------------------------------------------------------- transforms

@@ -577,9 +577,20 @@ extern "C" size_t he_conv_workspace_bytes(const he_ctx* c, const he_conv_plan* p
     return sizeof(u64) * (spec + fold) + 256;
 }
 
+static inline void rec(void* const* ev, int i, cudaStream_t st) {
+    if (ev && ev[i]) cudaEventRecord((cudaEvent_t)ev[i], st);
+}
+
 extern "C" he_status he_conv(const he_ctx* c, const he_conv_plan* p, const uint64_t* d_c0,
                              int B, const uint64_t* d_fspec, const uint32_t* d_phi1,
                              uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream) {
+    return he_conv_ex(c, p, d_c0, B, d_fspec, d_phi1, d_out, d_ws, ws_bytes, stream, nullptr);
+}
+
+extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const uint64_t* d_c0,
+                                int B, const uint64_t* d_fspec, const uint32_t* d_phi1,
+                                uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream,
+                                void* const* ev) {
     if (!c || !p || B < 0) return HE_EINVAL;
     if (!plan_ok(c, p)) return HE_ESHAPE;
     if (B == 0) return HE_OK;
@@ -589,8 +600,10 @@ extern "C" he_status he_conv(const he_ctx* c, const he_conv_plan* p, const uint6
     const PlanDev P = plan_dev(p);
     u64* spec = (u64*)d_ws;
     u64* fold = spec + (size_t)B * P.n_ib * c->L * c->N;
+    rec(ev, 0, st);
     he_status s = launch_ntt_fwd(c, (const u64*)d_c0, spec, (long)B * P.n_ib * c->L, 1, st);
     if (s != HE_OK) return s;
+    rec(ev, 1, st);
     launch_mac(spec, (const u64*)d_fspec, fold, B, P.n_ib, c->L, c->logN, P.logs, P.c_o,
                c->d_limb, st);
     HE_CHECK_LAUNCH();
@@ -599,10 +612,12 @@ extern "C" he_status he_conv(const he_ctx* c, const he_conv_plan* p, const uint6
     int cc = std::max(1, std::min(P.c_ob, max_words / padded_words(M)));
     const size_t smem = sizeof(u64) * (size_t)cc * padded_words(M);
     if (!set_smem(k_intt_scatter, smem)) return HE_ECUDA;
+    rec(ev, 2, st);
     k_intt_scatter<<<(unsigned)(B * P.n_ob * c->L), 512, smem, st>>>(
         fold, d_phi1, (u64*)d_out, P, B, c->L, c->logN, cc, c->d_limb, c->d_tw_inv, c->t,
         c->r_t, c->t_inv);
     HE_CHECK_LAUNCH();
+    rec(ev, 3, st);
     return HE_OK;
 }
 
@@ -794,20 +809,31 @@ extern "C" he_status he_fc(const he_ctx* c, const he_fc_desc* f, const uint64_t*
                            const uint64_t* d_wspec, const uint64_t* d_bias_enc,
                            const uint32_t* d_phi1, uint64_t* d_out, void* d_ws,
                            size_t ws_bytes, void* stream) {
-    if (!c || !f || !d_c0 || !d_wspec || !d_bias_enc || !d_out || B < 0) return HE_EINVAL;
+    return he_fc_ex(c, f, d_c0, B, d_wspec, d_bias_enc, d_phi1, d_out, d_ws, ws_bytes, stream,
+                    nullptr);
+}
+
+extern "C" he_status he_fc_ex(const he_ctx* c, const he_fc_desc* f, const uint64_t* d_c0,
+                              int B, const uint64_t* d_wspec, const uint64_t* d_bias_enc,
+                              const uint32_t* d_phi1, uint64_t* d_out, void* d_ws,
+                              size_t ws_bytes, void* stream, void* const* ev) {
+    if (!c || !f || B < 0) return HE_EINVAL;
     if (!fc_ok(c, f)) return HE_ESHAPE;
     if (B == 0) return HE_OK;
-    if (!d_ws) return HE_EINVAL;
+    if (!d_c0 || !d_wspec || !d_bias_enc || !d_out || !d_ws) return HE_EINVAL;
     if (ws_bytes < he_fc_workspace_bytes(c, f, B)) return HE_ENOMEM;
     cudaStream_t st = STREAM(stream);
     u64* spec = (u64*)d_ws;
+    rec(ev, 0, st);
     he_status s = launch_ntt_fwd(c, (const u64*)d_c0, spec, (long)B * c->L, 0, st);
     if (s != HE_OK) return s;
     const size_t smem = sizeof(u64) * padded_words(c->N);
     if (!set_smem(k_fc_inv, smem)) return HE_ECUDA;
+    rec(ev, 1, st);
     k_fc_inv<<<(unsigned)(B * c->L), ntt_threads(c->N), smem, st>>>(
         spec, (const ulonglong2*)d_wspec, (const u64*)d_bias_enc, d_phi1, (u64*)d_out, f->n_o,
         c->L, c->logN, c->d_limb, c->d_tw_inv, c->t, c->r_t, c->t_inv);
     HE_CHECK_LAUNCH();
+    rec(ev, 2, st);
     return HE_OK;
 }
