@@ -322,6 +322,10 @@ def main():
     mk = lambda: torch.cuda.Event(enable_timing=True)
     evs = [[[mk() for _ in range(4)] for _ in layers] + ([[mk() for _ in range(3)]] if fc else [])
            for _ in range(args.steps)]
+    for E in evs:                    # torch creates the cudaEvent_t lazily
+        for grp in E:
+            for ev in grp:
+                ev.record()
     e0, e1 = mk(), mk()
     barrier()
     sampler = ClockSampler(local)

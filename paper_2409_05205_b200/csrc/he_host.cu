@@ -155,6 +155,8 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
         Lm.r25_p = h_shoup(Lm.r25, q);
         Lm.r50 = (1ull << 50) % q;
         Lm.r50_p = h_shoup(Lm.r50, q);
+        Lm.r64 = (u64)(((u128)1 << 64) % q);
+        Lm.r64_p = h_shoup(Lm.r64, q);
         Lm.one_p = h_shoup(1, q);
     }
     int prev = 0;

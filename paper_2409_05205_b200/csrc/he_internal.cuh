@@ -23,6 +23,7 @@ struct he_limb {
     u64 delta, delta_p;     // Delta_t mod q (R2) and Shoup companion
     u64 r25, r25_p;         // 2^25 mod q
     u64 r50, r50_p;         // 2^50 mod q
+    u64 r64, r64_p;         // 2^64 mod q
     u64 one_p;              // Shoup companion of 1  (floor(2^64 / q))
 };
 
@@ -79,6 +80,12 @@ __device__ __forceinline__ u64 enc_plain(u64 m, const he_limb& L, u64 t,
     u64 f = div_by_t(r_t * m + (t >> 1), t, t_inv);                 // < t
     f = shoup_mul(f, 1, L.one_p, L.q);              // [0, 2q) even if t > q
     return csub(csub(a + f, 2 * L.q), L.q);
+}
+
+// acc += a * b (32 x 32 -> 64, 64-bit accumulate): one IMAD.WIDE.U32.
+// (Plain C `acc += (u64)a * b` makes nvcc add the zero high words too.)
+__device__ __forceinline__ void madw(u64& acc, u32 a, u32 b) {
+    asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
 }
 
 __device__ __forceinline__ u64 addmod(u64 a, u64 b, u64 q) {
@@ -176,12 +183,13 @@ __device__ __forceinline__ void gs_pass(u64* sm, int arr_stride, int narr,
 }
 
 // Full forward pass schedule on a segment: stages split .. logN-1 in passes
-// of up to 4 stages (the remainder first).
+// of up to RMAX stages (the remainder first).
+template <int RMAX>
 __device__ __forceinline__ void ct_all(u64* sm, int logN, int NS, int seg,
                                        int split, const ulonglong2* tw, u64 q,
                                        u64 q2) {
     int st = split;
-    int rem = (logN - split) & 3;
+    const int rem = (logN - split) % RMAX;
     if (rem) {
         if (rem == 1) ct_pass<1>(sm, logN, NS, st, seg, split, tw, q, q2);
         else if (rem == 2) ct_pass<2>(sm, logN, NS, st, seg, split, tw, q, q2);
@@ -189,20 +197,21 @@ __device__ __forceinline__ void ct_all(u64* sm, int logN, int NS, int seg,
         st += rem;
         __syncthreads();
     }
-    for (; st < logN; st += 4) {
-        ct_pass<4>(sm, logN, NS, st, seg, split, tw, q, q2);
+    for (; st < logN; st += RMAX) {
+        ct_pass<RMAX>(sm, logN, NS, st, seg, split, tw, q, q2);
         __syncthreads();
     }
 }
 
 // Full inverse schedule on narr M-point arrays: strides 1 .. M/2.
+template <int RMAX>
 __device__ __forceinline__ void gs_all(u64* sm, int arr_stride, int narr,
                                        int logM, int seg, int logMfull,
                                        const ulonglong2* tw, u64 q, u64 q2) {
     int lt = 0;
-    int rem = logM & 3;
-    for (; lt + 4 <= logM; lt += 4) {
-        gs_pass<4>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
+    const int rem = logM % RMAX;
+    for (; lt + RMAX <= logM; lt += RMAX) {
+        gs_pass<RMAX>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
         __syncthreads();
     }
     if (rem) {

@@ -42,60 +42,55 @@ static bool set_smem(F* f, size_t bytes) {
 static inline int ntt_threads(int NS) { return std::min(512, std::max(16, NS / 16)); }
 
 // ===================================================================== K1
-// Forward negacyclic NTT, one CTA per limb (N <= 16384; the N = 32768
-// variant is k_ntt_fwd_split below).  Smem-staged radix-2^4 passes,
-// Shoup twiddles from L1/L2, 16-byte coalesced global loads and stores.
-// OUT_FMT 0: canonical, 1: split25 words for the MAC.
-template <int OUT_FMT>
-__global__ void __launch_bounds__(512)
-k_ntt_fwd_body(const u64* in, u64* out, int logN, int L,
-               const he_limb* __restrict__ limbs,
-               const ulonglong2* __restrict__ tw_all) {
+// Forward negacyclic NTT (natural in, bit-reversed out) of one limb by a
+// cluster of 2^S CTAs (S = 0 for N <= 8192, 1 for 16384, 2 for 32768), so
+// every CTA holds NS = N >> S <= 8192 words (69.6 KB of shared memory) and
+// two 512-thread CTAs fit on an SM.  Each CTA reads the 2^S words
+// x[i + r NS] of its output index i, applies the first S stages to them and
+// keeps the value of its own segment; the remaining stages run in shared
+// memory as radix-8 passes (ct_pass) with Shoup twiddles from L1/L2.  The
+// cluster barrier after the loads makes in-place use safe.  16-byte
+// coalesced global loads and stores.  OUT_FMT 0: canonical, 1: split25.
+template <int S, int OUT_FMT>
+__device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int logN, int L,
+                                                const he_limb* __restrict__ limbs,
+                                                const ulonglong2* __restrict__ tw_all) {
     extern __shared__ u64 sm[];
-    const int N = 1 << logN;
-    const int li = blockIdx.x, l = li % L;
-    const u64 q = limbs[l].q, q2 = 2 * q;
-    const ulonglong2* tw = tw_all + (size_t)l * N;
-    const u64* src = in + (size_t)li * N;
-    for (int i = 2 * threadIdx.x; i < N; i += 2 * blockDim.x) {
-        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src + i);
-        sm[PAD(i)] = v.x;
-        sm[PAD(i + 1)] = v.y;
-    }
-    __syncthreads();
-    ct_all(sm, logN, N, 0, 0, tw, q, q2);
-    u64* dst = out + (size_t)li * N;
-    for (int i = 2 * threadIdx.x; i < N; i += 2 * blockDim.x) {
-        u64 x = csub(csub(sm[PAD(i)], q2), q), y = csub(csub(sm[PAD(i + 1)], q2), q);
-        if (OUT_FMT == 1) { x = to_split25(x); y = to_split25(y); }
-        *reinterpret_cast<ulonglong2*>(dst + i) = make_ulonglong2(x, y);
-    }
-}
-
-// N = 32768: a 2-CTA cluster per limb; both CTAs read the whole limb, apply
-// stage 0 and keep their half (the cluster barrier makes in-place use safe).
-template <int OUT_FMT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512)
-k_ntt_fwd_split(const u64* in, u64* out, int logN,
-                int L, const he_limb* __restrict__ limbs,
-                const ulonglong2* __restrict__ tw_all) {
-    extern __shared__ u64 sm[];
-    const int N = 1 << logN, NS = N >> 1;
-    const int li = blockIdx.x >> 1, seg = blockIdx.x & 1;
+    const int N = 1 << logN, NS = N >> S;
+    const int li = blockIdx.x >> S, seg = blockIdx.x & ((1 << S) - 1);
     const int l = li % L;
     const u64 q = limbs[l].q, q2 = 2 * q;
     const ulonglong2* tw = tw_all + (size_t)l * N;
     const u64* src = in + (size_t)li * N;
-    const ulonglong2 w = tw[1];
     for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
-        const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(src + i);
-        const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(src + i + NS);
-        const u64 t0 = shoup_mul(b.x, w.x, w.y, q), t1 = shoup_mul(b.y, w.x, w.y, q);
-        sm[PAD(i)] = seg ? a.x - t0 + q2 : a.x + t0;
-        sm[PAD(i + 1)] = seg ? a.y - t1 + q2 : a.y + t1;
+        u64 vx[1 << S], vy[1 << S];
+#pragma unroll
+        for (int r = 0; r < (1 << S); ++r) {
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src + i + r * NS);
+            vx[r] = v.x;
+            vy[r] = v.y;
+        }
+#pragma unroll
+        for (int st = 0; st < S; ++st) {
+            const int half = 1 << (S - 1 - st);
+#pragma unroll
+            for (int r = 0; r < (1 << S); ++r) {
+                if (r & half) continue;
+                const ulonglong2 w = __ldg(&tw[(1 << st) + (r >> (S - st))]);
+                ct_bfly(vx[r], vx[r + half], w, q, q2);
+                ct_bfly(vy[r], vy[r + half], w, q, q2);
+            }
+        }
+        u64 ox = vx[0], oy = vy[0];
+#pragma unroll
+        for (int r = 1; r < (1 << S); ++r)
+            if (r == seg) { ox = vx[r]; oy = vy[r]; }
+        sm[PAD(i)] = ox;
+        sm[PAD(i + 1)] = oy;
     }
-    cg::this_cluster().sync();          // both halves read before any write
-    ct_all(sm, logN, NS, seg, 1, tw, q, q2);
+    if (S) cg::this_cluster().sync();
+    else __syncthreads();
+    ct_all<3>(sm, logN, NS, seg, S, tw, q, q2);
     u64* dst = out + (size_t)li * N + (size_t)seg * NS;
     for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
         u64 x = csub(csub(sm[PAD(i)], q2), q), y = csub(csub(sm[PAD(i + 1)], q2), q);
@@ -104,27 +99,44 @@ k_ntt_fwd_split(const u64* in, u64* out, int logN,
     }
 }
 
+template <int OUT_FMT>
+__global__ void __launch_bounds__(512, 2)
+k_ntt_fwd_s0(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
+             const ulonglong2* __restrict__ tw_all) {
+    ntt_fwd_segment<0, OUT_FMT>(in, out, logN, L, limbs, tw_all);
+}
+
+template <int OUT_FMT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 2)
+k_ntt_fwd_s1(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
+             const ulonglong2* __restrict__ tw_all) {
+    ntt_fwd_segment<1, OUT_FMT>(in, out, logN, L, limbs, tw_all);
+}
+
+template <int OUT_FMT>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 2)
+k_ntt_fwd_s2(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
+             const ulonglong2* __restrict__ tw_all) {
+    ntt_fwd_segment<2, OUT_FMT>(in, out, logN, L, limbs, tw_all);
+}
+
 // Launch the forward NTT over nlimbs = batch * L limbs.
 static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
                                 long nlimbs, int out_fmt, cudaStream_t st) {
     if (nlimbs <= 0) return HE_OK;
-    const int logN = c->logN, N = c->N;
-    if (logN <= 14) {
-        const int threads = ntt_threads(N);
-        const size_t smem = sizeof(u64) * padded_words(N);
-        auto k = out_fmt ? k_ntt_fwd_body<1> : k_ntt_fwd_body<0>;
-        if (!set_smem(k, smem)) return HE_ECUDA;
-        k<<<(unsigned)nlimbs, threads, smem, st>>>(in, out, logN, c->L, c->d_limb,
-                                                   c->d_tw_fwd);
-    } else {
-        const int NS = N / 2;
-        const int threads = ntt_threads(NS);
-        const size_t smem = sizeof(u64) * padded_words(NS);
-        auto k = out_fmt ? k_ntt_fwd_split<1> : k_ntt_fwd_split<0>;
-        if (!set_smem(k, smem)) return HE_ECUDA;
-        k<<<(unsigned)(2 * nlimbs), threads, smem, st>>>(in, out, logN, c->L,
-                                                         c->d_limb, c->d_tw_fwd);
-    }
+    const int logN = c->logN;
+    const int S = logN <= 13 ? 0 : logN - 13;
+    const int NS = c->N >> S;
+    const int threads = std::min(512, std::max(32, NS / 16));
+    const size_t smem = sizeof(u64) * padded_words(NS);
+    typedef void (*kfn)(const u64*, u64*, int, int, const he_limb*, const ulonglong2*);
+    kfn k;
+    if (S == 0) k = out_fmt ? k_ntt_fwd_s0<1> : k_ntt_fwd_s0<0>;
+    else if (S == 1) k = out_fmt ? k_ntt_fwd_s1<1> : k_ntt_fwd_s1<0>;
+    else k = out_fmt ? k_ntt_fwd_s2<1> : k_ntt_fwd_s2<0>;
+    if (!set_smem(k, smem)) return HE_ECUDA;
+    k<<<(unsigned)(nlimbs << S), threads, smem, st>>>(in, out, logN, c->L, c->d_limb,
+                                                      c->d_tw_fwd);
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
@@ -146,7 +158,7 @@ k_ntt_inv(const u64* in, u64* out, int logN, int L,
         sm[PAD(i + 1)] = v.y;
     }
     __syncthreads();
-    gs_all(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
+    gs_all<4>(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
     u64* dst = out + (size_t)li * N;
     const u64 ni = Lm.ninv, nip = Lm.ninv_p;
     for (int i = 2 * threadIdx.x; i < N; i += 2 * blockDim.x) {
@@ -175,7 +187,7 @@ k_ntt_inv_split(const u64* in, u64* out, int logN,
         sm[PAD(i + 1)] = v.y;
     }
     __syncthreads();
-    gs_all(sm, 0, 1, logN - 1, seg, logN, twi, q, q2);
+    gs_all<4>(sm, 0, 1, logN - 1, seg, logN, twi, q, q2);
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
     const u64* lo = seg ? cl.map_shared_rank(sm, 0) : sm;
@@ -407,165 +419,250 @@ extern "C" he_status he_pack_filters(const he_ctx* c, const he_conv_plan* p,
 // ===================================================================== K3
 // Folded NTT-domain MAC: for each (l, g), the modular GEMM
 //   out[l][g][b][n] = sum_{k < K} C[b][beta][l][g s + u] * F[l][g][k][n] mod q
-// (k = beta s + u).  Operands are split25 words: v = hi * 2^25 + lo, so each
-// term is 4 IMAD.WIDE.U32 into three 64-bit accumulators (acc0: lo*lo,
-// acc1: cross, acc2: hi*hi), reduced once per output.  K <= 4096 keeps the
-// accumulators below 2^64.
+// (k = beta s + u, K = n_ib s).  Operands are split25 words v = hi 2^25 + lo,
+// so each term is 4 IMAD.WIDE.U32 into three 64-bit accumulators (acc0:
+// lo*lo, acc1: cross terms, acc2: hi*hi), reduced once per output.
+// K <= 4096 keeps every accumulator below 2^63.
+//
+// CTA = 8 warps over GC consecutive groups g of one limb, a 32-image tile
+// and a TNT-channel tile; warp (gl, nt) owns a 32 x 8 output tile of group
+// gl, lane (ty, tx) = (lane / 4, lane % 4) the 4 x 2 outputs
+// b = ty + 8 i, n = 8 nt + tx + 4 j.  C and F chunks of KC = 16 k-values
+// are staged in shared memory ([k][row] layout: broadcast-free, conflict-free
+// reads).
 __device__ __forceinline__ u64 mac_reduce(u64 a0, u64 a1, u64 a2, const he_limb& Lm) {
+    // V = a0 + a1 2^25 + a2 2^50 as a 128-bit (hi, lo), then
+    // V mod q = (hi * (2^64 mod q) + lo) mod q via two Shoup products.
     const u64 q = Lm.q;
-    u64 r = shoup_mul(a0, 1, Lm.one_p, q) + shoup_mul(a1, Lm.r25, Lm.r25_p, q) +
-            shoup_mul(a2, Lm.r50, Lm.r50_p, q);          // < 6q
-    r = csub(r, 4 * q);
+    u64 lo = a0 + (a1 << 25);
+    u64 hi = (a1 >> 39) + (lo < a0);
+    const u64 t = lo + (a2 << 50);
+    hi += (a2 >> 14) + (t < lo);
+    lo = t;
+    u64 r = shoup_mul(hi, Lm.r64, Lm.r64_p, q) + shoup_mul(lo, 1, Lm.one_p, q);  // < 4q
     r = csub(r, 2 * q);
     return csub(r, q);
 }
 
-template <int TM, int TN>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc),
+                 "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int NW>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NW)); }
+
+template <int TNT>
+struct MacTile {
+    static constexpr int WPG = TNT / 8;   // warps per group
+    static constexpr int GC = 8 / WPG;    // groups per CTA iteration
+    static constexpr int KC = 16;         // k per chunk
+    static constexpr int CW = KC + 1;     // padded sC row (conflict-free reads)
+    static constexpr int C_WORDS = GC * 32 * CW;
+    static constexpr int F_WORDS = GC * KC * TNT;
+    static constexpr size_t SMEM = 2 * sizeof(u64) * (C_WORDS + F_WORDS);
+};
+
+template <int TNT>
+__global__ void __launch_bounds__(256, 2)
 k_mac_fold(const u64* __restrict__ C, const u64* __restrict__ F, u64* __restrict__ out,
-           int B, int n_ib, int L, int logN, int logs, int c_o, int GC,
+           int B, int n_ib, int L, int logN, int logs, int c_o, int GI,
            const he_limb* __restrict__ limbs) {
-    constexpr int TBc = 16 * TM, TNc = 16 * TN, KC = 32;
-    __shared__ u64 sC[KC][TBc + 1];
-    __shared__ u64 sF[KC][TNc];
-    const int N = 1 << logN, s = 1 << logs, M = N >> logs, K = n_ib * s;
-    const int nG = (M + GC - 1) / GC;
-    const int l = blockIdx.x / nG, g0 = (blockIdx.x % nG) * GC;
-    const int b0 = blockIdx.y * TBc, n0 = blockIdx.z * TNc;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    typedef MacTile<TNT> T;
+    constexpr int GC = T::GC, KC = T::KC, CW = T::CW, WPG = T::WPG;
+    extern __shared__ u64 smem[];
+    u64* sCb = smem;                       // [2][GC][32][CW]
+    u64* sFb = smem + 2 * T::C_WORDS;      // [2][GC][KC][TNT]
+    const int N = 1 << logN, s = 1 << logs, M = N >> logs, K = n_ib << logs;
+    const int nG = (M + GC * GI - 1) / (GC * GI);
+    const int l = blockIdx.x / nG, g0 = (blockIdx.x - l * nG) * GC * GI;
+    const int b0 = blockIdx.y * 32, n0 = blockIdx.z * TNT;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gl = warp / WPG, nt = warp - gl * WPG;
+    const int ty = lane >> 2, tx = lane & 3;
+    const int nK = (K + KC - 1) / KC, nchunks = GI * nK;
+
+    auto issue = [&](int c, int buf) {
+        const int it = c / nK, k0 = (c - it * nK) * KC;
+        const int gb = g0 + it * GC;
+        u64* sC = sCb + buf * T::C_WORDS;
+        u64* sF = sFb + buf * T::F_WORDS;
+        for (int e = threadIdx.x; e < GC * 32 * KC; e += 256) {
+            const int kk = e & (KC - 1), r = e >> 4;
+            const int gg = r & (GC - 1), bl = r / GC;
+            const int k = k0 + kk, b = b0 + bl, gq = gb + gg;
+            const bool ok = k < K && b < B && gq < M;
+            const u64* src = ok ? C + (((size_t)b * n_ib + (k >> logs)) * L + l) * N +
+                                      ((size_t)gq << logs) + (k & (s - 1))
+                                : C;
+            cp_async8(sC + (gg * 32 + bl) * CW + kk, src, ok);
+        }
+        for (int e = threadIdx.x; e < GC * KC * TNT; e += 256) {
+            const int nl = e & (TNT - 1), r = e / TNT;
+            const int kk = r & (KC - 1), gg = r >> 4;
+            const int k = k0 + kk, n = n0 + nl, gq = gb + gg;
+            const bool ok = k < K && n < c_o && gq < M;
+            const u64* src = ok ? F + (((size_t)l * M + gq) * K + k) * c_o + n : F;
+            cp_async8(sF + (gg * KC + kk) * TNT + nl, src, ok);
+        }
+        cp_async_commit();
+    };
+
+    u64 a0[4][2], a1[4][2], a2[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) a0[i][j] = a1[i][j] = a2[i][j] = 0;
     const he_limb Lm = limbs[l];
-    for (int g = g0; g < min(g0 + GC, M); ++g) {
-        u64 a0[TM][TN], a1[TM][TN], a2[TM][TN];
+    issue(0, 0);
+    for (int c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) {
+            issue(c + 1, (c + 1) & 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int it = c / nK, k0 = (c - it * nK) * KC;
+        const int kc = min(KC, K - k0);
+        const u64* sC = sCb + (c & 1) * T::C_WORDS + gl * 32 * CW;
+        const u64* sF = sFb + (c & 1) * T::F_WORDS + gl * KC * TNT;
+#pragma unroll 4
+        for (int kk = 0; kk < kc; ++kk) {
+            u32 c0[4], c1[4], f0[2], f1[2];
 #pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) a0[i][j] = a1[i][j] = a2[i][j] = 0;
-        const u64* Fg = F + ((size_t)l * M + g) * K * c_o;
-        for (int k0 = 0; k0 < K; k0 += KC) {
-            const int kc = min(KC, K - k0);
-            for (int idx = threadIdx.x; idx < TBc * kc; idx += 256) {
-                const int bl = idx / kc, kk = idx - bl * kc;
-                const int b = b0 + bl, k = k0 + kk;
-                u64 v = 0;
-                if (b < B)
-                    v = C[(((size_t)b * n_ib + (k >> logs)) * L + l) * N +
-                          ((size_t)g << logs) + (k & (s - 1))];
-                sC[kk][bl] = v;
+            for (int i = 0; i < 4; ++i) {
+                const u64 v = sC[(ty + 8 * i) * CW + kk];
+                c0[i] = (u32)v;
+                c1[i] = (u32)(v >> 32);
             }
-            for (int idx = threadIdx.x; idx < kc * TNc; idx += 256) {
-                const int kk = idx / TNc, nl = idx - kk * TNc;
-                const int n = n0 + nl;
-                sF[kk][nl] = n < c_o ? Fg[(size_t)(k0 + kk) * c_o + n] : 0;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const u64 v = sF[kk * TNT + nt * 8 + tx + 4 * j];
+                f0[j] = (u32)v;
+                f1[j] = (u32)(v >> 32);
             }
-            __syncthreads();
-            for (int kk = 0; kk < kc; ++kk) {
-                u32 c0[TM], c1[TM], f0[TN], f1[TN];
 #pragma unroll
-                for (int i = 0; i < TM; ++i) {
-                    const u64 v = sC[kk][ty + 16 * i];
-                    c0[i] = (u32)v;
-                    c1[i] = (u32)(v >> 32);
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    madw(a0[i][j], c0[i], f0[j]);
+                    madw(a1[i][j], c0[i], f1[j]);
+                    madw(a1[i][j], c1[i], f0[j]);
+                    madw(a2[i][j], c1[i], f1[j]);
                 }
+        }
+        if (k0 + KC >= K) {                      // last chunk of this iteration
+            const int g = g0 + it * GC + gl;
+            if (g < M) {
+                u64* og = out + ((size_t)l * M + g) * B * c_o;
 #pragma unroll
-                for (int j = 0; j < TN; ++j) {
-                    const u64 v = sF[kk][tx + 16 * j];
-                    f0[j] = (u32)v;
-                    f1[j] = (u32)(v >> 32);
-                }
+                for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int i = 0; i < TM; ++i)
-#pragma unroll
-                    for (int j = 0; j < TN; ++j) {
-                        a0[i][j] += (u64)c0[i] * f0[j];
-                        a1[i][j] += (u64)c0[i] * f1[j];
-                        a1[i][j] += (u64)c1[i] * f0[j];
-                        a2[i][j] += (u64)c1[i] * f1[j];
+                    for (int j = 0; j < 2; ++j) {
+                        const int b = b0 + ty + 8 * i, n = n0 + nt * 8 + tx + 4 * j;
+                        if (b < B && n < c_o)
+                            og[(size_t)b * c_o + n] = mac_reduce(a0[i][j], a1[i][j], a2[i][j], Lm);
                     }
             }
-            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) a0[i][j] = a1[i][j] = a2[i][j] = 0;
         }
-        u64* og = out + ((size_t)l * M + g) * B * c_o;
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) {
-                const int b = b0 + ty + 16 * i, n = n0 + tx + 16 * j;
-                if (b < B && n < c_o)
-                    og[(size_t)b * c_o + n] = mac_reduce(a0[i][j], a1[i][j], a2[i][j], Lm);
-            }
+        __syncthreads();
     }
 }
 
-template <int TM, int TN>
-static void launch_mac_t(const u64* C, const u64* F, u64* out, int B, int n_ib, int L,
-                         int logN, int logs, int c_o, const he_limb* limbs,
-                         cudaStream_t st) {
-    const int M = (1 << logN) >> logs, K = n_ib << logs;
-    int GC = std::max(1, 256 / K);
-    GC = std::min(GC, M);
-    const int nG = (M + GC - 1) / GC;
-    dim3 grid(L * nG, (B + 16 * TM - 1) / (16 * TM), (c_o + 16 * TN - 1) / (16 * TN));
-    k_mac_fold<TM, TN><<<grid, 256, 0, st>>>(C, F, out, B, n_ib, L, logN, logs, c_o, GC,
-                                             limbs);
+template <int TNT>
+static he_status launch_mac_t(const u64* C, const u64* F, u64* out, int B, int n_ib, int L,
+                              int logN, int logs, int c_o, const he_limb* limbs,
+                              cudaStream_t st) {
+    typedef MacTile<TNT> T;
+    const int M = (1 << logN) >> logs;
+    const int btiles = (B + 31) / 32, ntiles = (c_o + TNT - 1) / TNT;
+    const long work = (long)L * ((M + T::GC - 1) / T::GC) * btiles * ntiles;
+    int GI = (int)std::max(1L, std::min(16L, work / (148 * 8)));
+    GI = std::min(GI, (M + T::GC - 1) / T::GC);
+    const int nG = (M + T::GC * GI - 1) / (T::GC * GI);
+    if (!set_smem(k_mac_fold<TNT>, T::SMEM)) return HE_ECUDA;
+    dim3 grid(L * nG, btiles, ntiles);
+    k_mac_fold<TNT><<<grid, 256, T::SMEM, st>>>(C, F, out, B, n_ib, L, logN, logs, c_o, GI,
+                                                 limbs);
+    return HE_OK;
 }
 
-static void launch_mac(const u64* C, const u64* F, u64* out, int B, int n_ib, int L,
-                       int logN, int logs, int c_o, const he_limb* limbs, cudaStream_t st) {
-    const int tm = B > 32 ? 4 : (B > 16 ? 2 : 1);
-    const int tn = c_o > 32 ? 4 : (c_o > 16 ? 2 : 1);
-#define MAC_CASE(A, Bt) \
-    if (tm == A && tn == Bt) { launch_mac_t<A, Bt>(C, F, out, B, n_ib, L, logN, logs, c_o, limbs, st); return; }
-    MAC_CASE(1, 1) MAC_CASE(1, 2) MAC_CASE(1, 4)
-    MAC_CASE(2, 1) MAC_CASE(2, 2) MAC_CASE(2, 4)
-    MAC_CASE(4, 1) MAC_CASE(4, 2) MAC_CASE(4, 4)
-#undef MAC_CASE
+static he_status launch_mac(const u64* C, const u64* F, u64* out, int B, int n_ib, int L,
+                            int logN, int logs, int c_o, const he_limb* limbs,
+                            cudaStream_t st) {
+    if (c_o <= 16) return launch_mac_t<16>(C, F, out, B, n_ib, L, logN, logs, c_o, limbs, st);
+    if (c_o <= 32) return launch_mac_t<32>(C, F, out, B, n_ib, L, logN, logs, c_o, limbs, st);
+    return launch_mac_t<64>(C, F, out, B, n_ib, L, logN, logs, c_o, limbs, st);
 }
 
 // ===================================================================== K4
-// Per (b, ob, l): (N/s)-point inverse NTTs (root psi^s, no scaling: N^{-1}
-// is in the filter spectra) of the folded products of the block's channels,
-// then the full output row: slot s*j + t_n <- result_n[j] (Alg. 1 Lines
-// 15-17; Eq. (7) shift as offset t_n), other slots 0, + enc(phi1) at every
-// coefficient.  Channels are processed in chunks of `cc`
-// that fit shared memory; a slot owned by no channel is written with the
-// first chunk.
-__global__ void __launch_bounds__(512)
+// One CTA per (b, ob, l, channel chunk): (N/s)-point inverse NTTs (root
+// psi^s, no scaling: N^{-1} is in the filter spectra) of the folded products
+// of `cc` channels of block ob, then the output slots of those channels
+// (Alg. 1 Lines 15-17; Eq. (7) shift realised as the offset t_n):
+//   out[b][ob][l][s j + u] for j < N/s and u in [u0, u1),
+//   u0 = ch0 * step, u1 = (last chunk ? s : (ch0 + cc) * step),
+// value result_{u/step}[j] when step | u, else 0, then + enc(phi1) at every
+// coefficient.  The chunks tile [0, s), so every coefficient
+// of the row is written exactly once, in contiguous runs of u1 - u0 words.
+// Channel arrays sit in shared memory at an odd word stride (conflict-free).
+__global__ void __launch_bounds__(256, 3)
 k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                u64* __restrict__ out, PlanDev P, int B, int L, int logN, int cc,
-               const he_limb* __restrict__ limbs, const ulonglong2* __restrict__ twi_all,
-               u64 t, u64 r_t, u64 t_inv) {
+               int nchunk, int stride, const he_limb* __restrict__ limbs,
+               const ulonglong2* __restrict__ twi_all, u64 t, u64 r_t, u64 t_inv) {
     extern __shared__ u64 sm[];
     const int N = 1 << logN, M = N >> P.logs, logM = logN - P.logs;
-    const int stride = padded_words(M);
-    const int l = blockIdx.x % L;
-    const int bo = blockIdx.x / L, ob = bo % P.n_ob, b = bo / P.n_ob;
+    int r = blockIdx.x;
+    const int ch = r % nchunk;
+    r /= nchunk;
+    const int l = r % L;
+    r /= L;
+    const int ob = r % P.n_ob, b = r / P.n_ob;
     const he_limb Lm = limbs[l];
     const u64 q = Lm.q, q2 = 2 * q;
     const ulonglong2* twi = twi_all + (size_t)l * N;
+    const int ch0 = ch * cc, ncc = min(cc, P.c_ob - ch0);
+    const u64* fb = fold + (size_t)b * P.c_o + ob * P.c_ob + ch0;
+    for (int idx = threadIdx.x; idx < ncc * M; idx += blockDim.x) {
+        const int g = idx / ncc, a = idx - g * ncc;
+        const int n = ob * P.c_ob + ch0 + a;
+        sm[a * stride + PAD(g)] = n < P.c_o ? fb[((size_t)l * M + g) * B * P.c_o + a] : 0;
+    }
+    __syncthreads();
+    gs_all<3>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
+    const int u0 = ch0 * P.step;
+    const int u1 = (ch == nchunk - 1) ? P.s : (ch0 + ncc) * P.step;
+    const int w = u1 - u0;
     const u32* ph = phi1 ? phi1 + ((size_t)b * P.n_ob + ob) * N : nullptr;
     u64* orow = out + (((size_t)b * P.n_ob + ob) * L + l) * N;
-    for (int ch0 = 0; ch0 < P.c_ob; ch0 += cc) {
-        const int ncc = min(cc, P.c_ob - ch0);
-        for (int idx = threadIdx.x; idx < ncc * M; idx += blockDim.x) {
-            const int g = idx / ncc, a = idx - g * ncc;
-            const int n = ob * P.c_ob + ch0 + a;
-            sm[a * stride + PAD(g)] =
-                n < P.c_o ? fold[(((size_t)l * M + g) * B + b) * P.c_o + n] : 0;
+    int lw = 0, ls = 0;                   // log2 w, log2 step (if powers of 2)
+    while ((1 << lw) < w) ++lw;
+    while ((1 << ls) < P.step) ++ls;
+    const bool pow2 = (1 << lw) == w && (1 << ls) == P.step;
+    for (int idx = threadIdx.x; idx < M * w; idx += blockDim.x) {
+        int j, u, nl;
+        if (pow2) {
+            j = idx >> lw;
+            u = u0 + (idx & (w - 1));
+            nl = u >> ls;
+        } else {
+            j = idx / w;
+            u = u0 + (idx - j * w);
+            nl = u / P.step;
         }
-        __syncthreads();
-        gs_all(sm, stride, ncc, logM, 0, logM, twi, q, q2);
-        for (int i = threadIdx.x; i < N; i += blockDim.x) {
-            const int u = i & (P.s - 1), j = i >> P.logs;
-            const int nl = u / P.step;
-            const bool owned = (u - nl * P.step == 0) && nl < P.c_ob;
-            u64 v;
-            if (owned && nl >= ch0 && nl < ch0 + ncc) v = csub(sm[(nl - ch0) * stride + PAD(j)], q);
-            else if (!owned && ch0 == 0) v = 0;
-            else continue;
-            if (ph) v = addmod(v, enc_plain(ph[i], Lm, t, r_t, t_inv), q);
-            orow[i] = v;
-        }
-        __syncthreads();
+        const int i = (j << P.logs) + u;
+        u64 v = 0;
+        if (u == nl * P.step && nl < ch0 + ncc)
+            v = csub(sm[(nl - ch0) * stride + PAD(j)], q);
+        if (ph) v = addmod(v, enc_plain(ph[i], Lm, t, r_t, t_inv), q);
+        orow[i] = v;
     }
 }
 
@@ -604,18 +701,21 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     he_status s = launch_ntt_fwd(c, (const u64*)d_c0, spec, (long)B * P.n_ib * c->L, 1, st);
     if (s != HE_OK) return s;
     rec(ev, 1, st);
-    launch_mac(spec, (const u64*)d_fspec, fold, B, P.n_ib, c->L, c->logN, P.logs, P.c_o,
-               c->d_limb, st);
+    s = launch_mac(spec, (const u64*)d_fspec, fold, B, P.n_ib, c->L, c->logN, P.logs, P.c_o,
+                   c->d_limb, st);
+    if (s != HE_OK) return s;
     HE_CHECK_LAUNCH();
     const int M = c->N >> P.logs;
-    const int max_words = 16384;                  // 128 KB of shared memory
-    int cc = std::max(1, std::min(P.c_ob, max_words / padded_words(M)));
-    const size_t smem = sizeof(u64) * (size_t)cc * padded_words(M);
+    const int stride = padded_words(M) | 1;          // odd: conflict-free
+    int cc = std::max(1, std::min(P.c_ob, 6144 / stride));   // <= 48 KB smem
+    while (cc & (cc - 1)) cc &= cc - 1;                       // power of two
+    const int nchunk = (P.c_ob + cc - 1) / cc;
+    const size_t smem = sizeof(u64) * (size_t)cc * stride;
     if (!set_smem(k_intt_scatter, smem)) return HE_ECUDA;
     rec(ev, 2, st);
-    k_intt_scatter<<<(unsigned)(B * P.n_ob * c->L), 512, smem, st>>>(
-        fold, d_phi1, (u64*)d_out, P, B, c->L, c->logN, cc, c->d_limb, c->d_tw_inv, c->t,
-        c->r_t, c->t_inv);
+    k_intt_scatter<<<(unsigned)(B * P.n_ob * c->L * nchunk), 256, smem, st>>>(
+        fold, d_phi1, (u64*)d_out, P, B, c->L, c->logN, cc, nchunk, stride, c->d_limb,
+        c->d_tw_inv, c->t, c->r_t, c->t_inv);
     HE_CHECK_LAUNCH();
     rec(ev, 3, st);
     return HE_OK;
@@ -796,7 +896,7 @@ k_fc_inv(const u64* __restrict__ spec, const ulonglong2* __restrict__ wspec,
         sm[PAD(i)] = shoup_mul(src[i], w.x, w.y, q);      // [0, 2q)
     }
     __syncthreads();
-    gs_all(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
+    gs_all<4>(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
     for (int k = threadIdx.x; k < n_o; k += blockDim.x) {
         u64 v = csub(sm[PAD(k)], q);
         v = addmod(v, bias_enc[(size_t)l * n_o + k], q);

@@ -5,7 +5,8 @@
 //
 //   which 0: IMAD      (mad.lo.u32)                      -> IMAD / s
 //   which 1: IMAD.WIDE (mad.wide.u32, 64-bit addend)     -> IMAD.WIDE / s
-//   which 2: lazy modular MAC, 25-bit split (4 mad.wide) -> MAC / s
+//   which 2: lazy modular MAC, 25-bit split (4 mad.wide + 2 LOP3 for the
+//            loop-carried operands)                   -> MAC / s
 //   which 3: Shoup Cooley-Tukey butterfly (ct_bfly)      -> butterflies / s
 //   which 4: Shoup Gentleman-Sande butterfly (gs_bfly)   -> butterflies / s
 #include <cuda_runtime.h>
@@ -40,8 +41,8 @@ __global__ void u1_imad_wide(const u32* in, u32* out, int iters, long long* cyc)
     long long c0 = clock64();
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc[i]) : "r"(a), "r"(b));
+        for (int i = 0; i < 8; ++i)   // multiplier is loop-carried: not hoistable
+            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc[i]) : "r"((u32)acc[i]), "r"(b));
     }
     long long c1 = clock64();
     u64 s = 0;
@@ -60,10 +61,13 @@ __global__ void u1_mac(const u32* in, u32* out, int iters, long long* cyc) {
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
-            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a[m][0]) : "r"(c0), "r"(f0));
-            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a[m][1]) : "r"(c0), "r"(f1));
-            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a[m][1]) : "r"(c1), "r"(f0));
-            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a[m][2]) : "r"(c1), "r"(f1));
+            // operands change every iteration (as the C spectrum words do in
+            // k_mac_fold), so ptxas cannot hoist the products out of the loop
+            const u32 x0 = c0 ^ (u32)a[m][2], x1 = c1 ^ (u32)a[m][0];
+            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a[m][0]) : "r"(x0), "r"(f0));
+            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a[m][1]) : "r"(x0), "r"(f1));
+            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a[m][1]) : "r"(x1), "r"(f0));
+            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(a[m][2]) : "r"(x1), "r"(f1));
         }
     }
     long long t1 = clock64();
