@@ -94,8 +94,9 @@ def u1_peaks(device_index=0):
                                    "libhe_u1.so"))
     lib.u1_run.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p] * 3
     out = {}
-    names = ["imad", "imad_wide", "modmac", "ct_bfly", "gs_bfly"]
-    iters = {0: 20000, 1: 20000, 2: 20000, 3: 2000, 4: 2000}
+    names = ["imad", "imad_wide", "modmac", "ct_bfly", "gs_bfly", "imma_u8",
+             "dfma"]
+    iters = {0: 20000, 1: 20000, 2: 20000, 3: 2000, 4: 2000, 5: 2000, 6: 20000}
     for w, name in enumerate(names):
         ms, cyc, ops = ctypes.c_float(), ctypes.c_longlong(), ctypes.c_double()
         rc = lib.u1_run(w, 148 * 8, 256, iters[w], ctypes.byref(ms),
@@ -369,8 +370,12 @@ def main():
     kern = {
         "ntt_fwd": (st["ntt_fwd"], W_ntt_bfly, u1["ct_bfly"]["per_s"], "Gbutterfly/s",
                     W_ntt_bytes),
-        "mac_fold": (st["mac_fold"], W_macs, u1["modmac"]["per_s"], "Gmodmac/s",
-                     W_mac_bytes),
+        # int8 tensor-core MAC: 49 u8 x u8 products per 50-bit modMAC, so its
+        # alu roof is the measured mma.sync int8 rate / 49 (HE_MAC=imad runs
+        # the IMAD kernel, whose roof is U1 "modmac").
+        "mac_fold": (st["mac_fold"], W_macs,
+                     u1["modmac"]["per_s"] if os.environ.get("HE_MAC", "")[:1] == "i"
+                     else u1["imma_u8"]["per_s"] / 49, "Gmodmac/s", W_mac_bytes),
         "intt_scatter": (st["intt_scatter"], W_intt_bfly, u1["gs_bfly"]["per_s"],
                          "Gbutterfly/s", W_intt_bytes),
     }

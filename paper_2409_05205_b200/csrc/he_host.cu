@@ -111,6 +111,10 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
     }
     he_ctx* c = (he_ctx*)calloc(1, sizeof(he_ctx));
     c->device = device;
+    {
+        const char* m = getenv("HE_MAC");
+        c->mac_mode = (m && m[0] == 'i') ? 1 : 0;     // HE_MAC=imad forces the IMAD MAC
+    }
     c->logN = r->log2N;
     c->N = N;
     c->L = L;
@@ -155,6 +159,10 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
         Lm.r25_p = h_shoup(Lm.r25, q);
         Lm.r50 = (1ull << 50) % q;
         Lm.r50_p = h_shoup(Lm.r50, q);
+        Lm.r40 = (u64)(((u128)1 << 40) % q);
+        Lm.r40_p = h_shoup(Lm.r40, q);
+        Lm.r80 = h_mulmod(Lm.r40, Lm.r40, q);
+        Lm.r80_p = h_shoup(Lm.r80, q);
         Lm.r64 = (u64)(((u128)1 << 64) % q);
         Lm.r64_p = h_shoup(Lm.r64, q);
         Lm.one_p = h_shoup(1, q);

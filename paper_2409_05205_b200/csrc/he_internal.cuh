@@ -24,11 +24,14 @@ struct he_limb {
     u64 r25, r25_p;         // 2^25 mod q
     u64 r50, r50_p;         // 2^50 mod q
     u64 r64, r64_p;         // 2^64 mod q
+    u64 r40, r40_p;         // 2^40 mod q   (byte-split MAC recombination)
+    u64 r80, r80_p;         // 2^80 mod q
     u64 one_p;              // Shoup companion of 1  (floor(2^64 / q))
 };
 
 struct he_ctx {
     int device;
+    int mac_mode;           // 0: auto (int8 tensor-core MAC when s >= 4), 1: IMAD MAC
     uint32_t logN, N, L;
     u64 t, r_t;             // plaintext modulus, r_t = Q mod t (R2)
     u64 t_inv;              // floor(2^64 / t) (for floor(x / t))
@@ -95,6 +98,18 @@ __device__ __forceinline__ u64 addmod(u64 a, u64 b, u64 q) {
 // Canonical value -> "split25" word (hi25 << 32 | lo25) used by the MAC.
 __device__ __forceinline__ u64 to_split25(u64 v) {
     return ((v >> 25) << 32) | (v & ((1ull << 25) - 1));
+}
+
+// 4 x 4 byte transpose: p_i = byte_i(a) | byte_i(b) << 8 | byte_i(c) << 16 |
+// byte_i(d) << 24  (8 PRMT).
+__device__ __forceinline__ void byte_transpose4(u32 a, u32 b, u32 c, u32 d, u32& p0,
+                                                u32& p1, u32& p2, u32& p3) {
+    const u32 t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+    const u32 t2 = __byte_perm(c, d, 0x5140), t3 = __byte_perm(c, d, 0x7362);
+    p0 = __byte_perm(t0, t2, 0x5410);
+    p1 = __byte_perm(t0, t2, 0x7632);
+    p2 = __byte_perm(t1, t3, 0x5410);
+    p3 = __byte_perm(t1, t3, 0x7632);
 }
 
 // ---------------------------------------------------- shared-memory NTT

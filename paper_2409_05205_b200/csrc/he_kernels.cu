@@ -50,7 +50,8 @@ static inline int ntt_threads(int NS) { return std::min(512, std::max(16, NS / 1
 // keeps the value of its own segment; the remaining stages run in shared
 // memory as radix-8 passes (ct_pass) with Shoup twiddles from L1/L2.  The
 // cluster barrier after the loads makes in-place use safe.  16-byte
-// coalesced global loads and stores.  OUT_FMT 0: canonical, 1: split25.
+// coalesced global loads and stores.  OUT_FMT 0: canonical, 1: split25,
+// 2: byte planes (int8 tensor-core MAC operand).
 template <int S, int OUT_FMT>
 __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int logN, int L,
                                                 const he_limb* __restrict__ limbs,
@@ -91,6 +92,26 @@ __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int log
     if (S) cg::this_cluster().sync();
     else __syncthreads();
     ct_all<3>(sm, logN, NS, seg, S, tw, q, q2);
+    if (OUT_FMT == 2) {
+        // byte planes for the int8 tensor-core MAC: plane j (j < 7) of limb li
+        // holds byte j of every coefficient, at byte offset li*8N + j*N.
+        unsigned char* base = reinterpret_cast<unsigned char*>(out + (size_t)li * N);
+        for (int i = 4 * threadIdx.x; i < NS; i += 4 * blockDim.x) {
+            u64 x[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] = csub(csub(sm[PAD(i + e)], q2), q);
+            u32 pl[8];
+            byte_transpose4((u32)x[0], (u32)x[1], (u32)x[2], (u32)x[3], pl[0], pl[1], pl[2],
+                            pl[3]);
+            byte_transpose4((u32)(x[0] >> 32), (u32)(x[1] >> 32), (u32)(x[2] >> 32),
+                            (u32)(x[3] >> 32), pl[4], pl[5], pl[6], pl[7]);
+            const int pos = seg * NS + i;
+#pragma unroll
+            for (int j = 0; j < 7; ++j)
+                *reinterpret_cast<u32*>(base + (size_t)j * N + pos) = pl[j];
+        }
+        return;
+    }
     u64* dst = out + (size_t)li * N + (size_t)seg * NS;
     for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
         u64 x = csub(csub(sm[PAD(i)], q2), q), y = csub(csub(sm[PAD(i + 1)], q2), q);
@@ -131,9 +152,11 @@ static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
     const size_t smem = sizeof(u64) * padded_words(NS);
     typedef void (*kfn)(const u64*, u64*, int, int, const he_limb*, const ulonglong2*);
     kfn k;
-    if (S == 0) k = out_fmt ? k_ntt_fwd_s0<1> : k_ntt_fwd_s0<0>;
-    else if (S == 1) k = out_fmt ? k_ntt_fwd_s1<1> : k_ntt_fwd_s1<0>;
-    else k = out_fmt ? k_ntt_fwd_s2<1> : k_ntt_fwd_s2<0>;
+    static kfn const tab[3][3] = {
+        {k_ntt_fwd_s0<0>, k_ntt_fwd_s0<1>, k_ntt_fwd_s0<2>},
+        {k_ntt_fwd_s1<0>, k_ntt_fwd_s1<1>, k_ntt_fwd_s1<2>},
+        {k_ntt_fwd_s2<0>, k_ntt_fwd_s2<1>, k_ntt_fwd_s2<2>}};
+    k = tab[S][out_fmt];
     if (!set_smem(k, smem)) return HE_ECUDA;
     k<<<(unsigned)(nlimbs << S), threads, smem, st>>>(in, out, logN, c->L, c->d_limb,
                                                       c->d_tw_fwd);
@@ -385,9 +408,49 @@ __global__ void k_filter_to_mac(const u64* __restrict__ spec, u64* __restrict__ 
     }
 }
 
+// Which MAC kernel a plan uses (deterministic; he_pack_filters and he_conv
+// agree): the int8 tensor-core MAC for s >= 4 (its operand staging moves
+// whole s-byte runs), else the IMAD MAC.  HE_MAC=imad forces the IMAD MAC.
+static bool use_imma(const he_ctx* c, const PlanDev& P) {
+    return c->mac_mode == 0 && P.s >= 4;
+}
+static inline int imma_kp(int K) { return (K + 15) & ~15; }
+static inline int imma_sw(int Kp) { return Kp / 4 + ((4 - Kp / 4) & 7); }   // = 4 mod 8
+
+// spectra [c_o][n_ib][L][N] -> byte planes Fpl[l][g][7][c_o][Kp] of
+// spec * N^{-1} (k = beta s + u < K; zero for K <= k < Kp).
+__global__ void k_filter_to_imma(const u64* __restrict__ spec, unsigned char* __restrict__ F,
+                                 PlanDev P, int L, int logN, int Kp,
+                                 const he_limb* __restrict__ limbs) {
+    const long N = 1L << logN;
+    const int K = P.n_ib * P.s, M = (int)(N >> P.logs);
+    const long total = (long)L * M * P.c_o * Kp;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const int k = (int)(idx % Kp);
+        long r = idx / Kp;
+        const int n = (int)(r % P.c_o);
+        r /= P.c_o;
+        const int g = (int)(r % M), l = (int)(r / M);
+        u64 v = 0;
+        if (k < K) {
+            const he_limb& Lm = limbs[l];
+            const int beta = k >> P.logs, u = k & (P.s - 1);
+            v = spec[(((long)n * P.n_ib + beta) * L + l) * N + ((long)g << P.logs) + u];
+            v = csub(shoup_mul(v, Lm.ninv, Lm.ninv_p, Lm.q), Lm.q);
+        }
+        unsigned char* dst = F + (((long)l * M + g) * 7 * P.c_o + n) * Kp + k;
+#pragma unroll
+        for (int j = 0; j < 7; ++j) dst[(long)j * P.c_o * Kp] = (unsigned char)(v >> (8 * j));
+    }
+}
+
 extern "C" size_t he_filter_bytes(const he_ctx* c, const he_conv_plan* p) {
     if (!c || !p) return 0;
-    return sizeof(u64) * (size_t)p->d.c_o * p->n_ib * c->L * c->N;
+    const size_t split = sizeof(u64) * (size_t)p->d.c_o * p->n_ib * c->L * c->N;
+    const size_t M = c->N / p->s;
+    const size_t planes = (size_t)c->L * M * 7 * p->d.c_o * imma_kp(p->n_ib * p->s);
+    return std::max(split, (planes + 15) & ~(size_t)15);
 }
 
 extern "C" size_t he_pack_filters_workspace_bytes(const he_ctx* c,
@@ -410,8 +473,15 @@ extern "C" he_status he_pack_filters(const he_ctx* c, const he_conv_plan* p,
     HE_CHECK_LAUNCH();
     he_status s = launch_ntt_fwd(c, ws, ws, (long)P.c_o * P.n_ib * c->L, 0, st);
     if (s != HE_OK) return s;
-    k_filter_to_mac<<<grid_for(total, 256), 256, 0, st>>>(ws, (u64*)d_fspec, P, c->L,
-                                                           c->logN, c->d_limb);
+    if (use_imma(c, P)) {
+        const int Kp = imma_kp(P.n_ib * P.s);
+        const long tot = (long)c->L * (c->N >> P.logs) * P.c_o * Kp;
+        k_filter_to_imma<<<grid_for(tot, 256), 256, 0, st>>>(ws, (unsigned char*)d_fspec, P,
+                                                              c->L, c->logN, Kp, c->d_limb);
+    } else {
+        k_filter_to_mac<<<grid_for(total, 256), 256, 0, st>>>(ws, (u64*)d_fspec, P, c->L,
+                                                               c->logN, c->d_limb);
+    }
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
@@ -601,6 +671,190 @@ static he_status launch_mac(const u64* C, const u64* F, u64* out, int B, int n_i
     return launch_mac_t<64>(C, F, out, B, n_ib, L, logN, logs, c_o, limbs, st);
 }
 
+// ============================================================ K3 (int8)
+// Folded MAC on the tensor cores, exact: with C = sum_i c_i 2^{8i} and
+// F = sum_j f_j 2^{8j} (bytes, i, j < 7; C, F < q < 2^50),
+//   sum_k C F = sum_{d=0}^{12} 2^{8d} S_d,   S_d = sum_{i+j=d} sum_k c_i f_j,
+// so each (l, g) GEMM [B x K] x [K x c_o] becomes 49 u8 x u8 -> s32 MMAs
+// (mma.sync m16n8k32 / m16n8k16) accumulated into 13 diagonal fragments
+// (S_d < 7 K 255^2 < 2^31 for K <= 4096), then one modular recombination per
+// output.  A operand: byte planes written by the forward NTT (OUT_FMT 2);
+// B operand: byte planes packed by he_pack_filters.  One CTA per (l, g,
+// 32-image tile); each warp owns 16 x 8 output tiles.
+__device__ __forceinline__ void mma_k32(int (&d)[4], u32 a0, u32 a1, u32 a2, u32 a3, u32 b0,
+                                        u32 b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_k16(int (&d)[4], u32 a0, u32 a1, u32 b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a0), "r"(a1), "r"(b0));
+}
+
+// V = sum_d S_d 2^{8d} mod q = lo + mid 2^40 + top 2^80 (mod q).
+__device__ __forceinline__ u64 reduce13(const int (&acc)[13][4], int e, const he_limb& Lm) {
+    u64 lo = 0, mid = 0, top = 0;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) lo += (u64)(u32)acc[d][e] << (8 * d);
+#pragma unroll
+    for (int d = 5; d < 10; ++d) mid += (u64)(u32)acc[d][e] << (8 * (d - 5));
+#pragma unroll
+    for (int d = 10; d < 13; ++d) top += (u64)(u32)acc[d][e] << (8 * (d - 10));
+    const u64 q = Lm.q;
+    u64 r = shoup_mul(lo, 1, Lm.one_p, q) + shoup_mul(mid, Lm.r40, Lm.r40_p, q) +
+            shoup_mul(top, Lm.r80, Lm.r80_p, q);                 // < 6q
+    r = csub(r, 4 * q);
+    r = csub(r, 2 * q);
+    return csub(r, q);
+}
+
+template <int CHUNK>
+__device__ __forceinline__ void cp_async_n(void* smem_dst, const void* gsrc, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    if (CHUNK == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc),
+                     "r"(valid ? 16 : 0));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(gsrc),
+                     "n"(CHUNK), "r"(valid ? CHUNK : 0));
+}
+
+template <int CHUNK>
+__device__ __forceinline__ void stage_a(u32* sA, const unsigned char* Cpl, int B, int b0,
+                                        int n_ib, int L, int l, int N, int g, int logs,
+                                        int sw) {
+    const int s = 1 << logs, per = s / CHUNK;
+    const int total = 32 * 7 * n_ib * per;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        const int c = e % per;
+        int r = e / per;
+        const int beta = r % n_ib;
+        r /= n_ib;
+        const int j = r % 7, b = r / 7;
+        const bool ok = b0 + b < B;
+        const unsigned char* src =
+            ok ? Cpl + ((((size_t)(b0 + b) * n_ib + beta) * L + l) * 8 + j) * (size_t)N +
+                     ((size_t)g << logs) + c * CHUNK
+               : Cpl;
+        cp_async_n<CHUNK>(reinterpret_cast<unsigned char*>(sA + (j * 32 + b) * sw) +
+                              beta * s + c * CHUNK,
+                          src, ok);
+    }
+}
+
+__global__ void __launch_bounds__(256, 2)
+k_mac_imma(const unsigned char* __restrict__ Cpl, const unsigned char* __restrict__ Fpl,
+           u64* __restrict__ out, int B, int n_ib, int L, int logN, int logs, int c_o, int Kp,
+           int sw, const he_limb* __restrict__ limbs) {
+    extern __shared__ u32 sm32[];
+    const int N = 1 << logN, M = N >> logs, K = n_ib << logs;
+    const int nrow = (c_o + 7) & ~7;
+    u32* sA = sm32;                       // [7][32][sw]
+    u32* sB = sm32 + 7 * 32 * sw;         // [7][nrow][sw]
+    const int l = blockIdx.x / M, g = blockIdx.x - l * M;
+    const int b0 = blockIdx.y * 32;
+    const int Kw = Kp >> 2, Kw0 = K >> 2;
+    // zero what the copies do not cover: A columns K..Kp, B rows c_o..nrow
+    for (int e = threadIdx.x; e < 7 * 32 * (Kw - Kw0); e += blockDim.x) {
+        const int w = Kw0 + e % (Kw - Kw0), row = e / (Kw - Kw0);
+        sA[row * sw + w] = 0;
+    }
+    for (int e = threadIdx.x; e < 7 * (nrow - c_o) * Kw; e += blockDim.x) {
+        const int w = e % Kw, r = e / Kw;
+        const int j = r / (nrow - c_o), n = c_o + r % (nrow - c_o);
+        sB[(j * nrow + n) * sw + w] = 0;
+    }
+    // stage A (C spectrum byte planes of the 32-image tile, group g)
+    const int s = 1 << logs;
+    if (s >= 16) stage_a<16>(sA, Cpl, B, b0, n_ib, L, l, N, g, logs, sw);
+    else if (s == 8) stage_a<8>(sA, Cpl, B, b0, n_ib, L, l, N, g, logs, sw);
+    else stage_a<4>(sA, Cpl, B, b0, n_ib, L, l, N, g, logs, sw);
+    // stage B (filter byte planes of group g), 16-byte chunks
+    {
+        const unsigned char* fg = Fpl + ((size_t)l * M + g) * 7 * c_o * Kp;
+        const int per = Kp / 16, total = 7 * c_o * per;
+        for (int e = threadIdx.x; e < total; e += blockDim.x) {
+            const int c = e % per, r = e / per;            // r = j * c_o + n
+            const int j = r / c_o, n = r - j * c_o;
+            cp_async_n<16>(reinterpret_cast<unsigned char*>(sB + (j * nrow + n) * sw) + c * 16,
+                           fg + (size_t)r * Kp + c * 16, true);
+        }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int nnt = nrow >> 3, items = 2 * nnt;
+    const he_limb Lm = limbs[l];
+    for (int it = warp; it < items; it += 8) {
+        const int bt = it / nnt, nt = it - bt * nnt;
+        int acc[13][4];
+#pragma unroll
+        for (int d = 0; d < 13; ++d)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[d][e] = 0;
+        const u32* ab = sA + (bt * 16 + gq) * sw + tq;
+        const u32* bb = sB + (nt * 8 + gq) * sw + tq;
+        int kw = 0;
+        for (; kw + 8 <= Kw; kw += 8) {
+            u32 bf0[7], bf1[7];
+#pragma unroll
+            for (int j = 0; j < 7; ++j) {
+                bf0[j] = bb[j * nrow * sw + kw];
+                bf1[j] = bb[j * nrow * sw + kw + 4];
+            }
+#pragma unroll
+            for (int i = 0; i < 7; ++i) {
+                const u32* ap = ab + i * 32 * sw + kw;
+                const u32 a0 = ap[0], a1 = ap[8 * sw], a2 = ap[4], a3 = ap[8 * sw + 4];
+#pragma unroll
+                for (int j = 0; j < 7; ++j) mma_k32(acc[i + j], a0, a1, a2, a3, bf0[j], bf1[j]);
+            }
+        }
+        if (kw < Kw) {                                   // one k16 step
+            u32 bf0[7];
+#pragma unroll
+            for (int j = 0; j < 7; ++j) bf0[j] = bb[j * nrow * sw + kw];
+#pragma unroll
+            for (int i = 0; i < 7; ++i) {
+                const u32* ap = ab + i * 32 * sw + kw;
+                const u32 a0 = ap[0], a1 = ap[8 * sw];
+#pragma unroll
+                for (int j = 0; j < 7; ++j) mma_k16(acc[i + j], a0, a1, bf0[j]);
+            }
+        }
+        u64* og = out + ((size_t)l * M + g) * B * c_o;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int b = b0 + bt * 16 + gq + 8 * (e >> 1), n = nt * 8 + 2 * tq + (e & 1);
+            if (b < B && n < c_o) og[(size_t)b * c_o + n] = reduce13(acc, e, Lm);
+        }
+    }
+}
+
+static he_status launch_mac_imma(const unsigned char* Cpl, const unsigned char* Fpl, u64* out,
+                                 int B, int n_ib, int L, int logN, int logs, int c_o,
+                                 const he_limb* limbs, cudaStream_t st) {
+    const int M = (1 << logN) >> logs, K = n_ib << logs;
+    const int Kp = imma_kp(K), sw = imma_sw(Kp);
+    const int nrow = (c_o + 7) & ~7;
+    const size_t smem = sizeof(u32) * (size_t)(7 * 32 + 7 * nrow) * sw;
+    if (smem > 227 * 1024) return HE_ESHAPE;
+    if (!set_smem(k_mac_imma, smem)) return HE_ECUDA;
+    dim3 grid(L * M, (B + 31) / 32);
+    k_mac_imma<<<grid, 256, smem, st>>>(Cpl, Fpl, out, B, n_ib, L, logN, logs, c_o, Kp, sw,
+                                        limbs);
+    return HE_OK;
+}
+
 // ===================================================================== K4
 // One CTA per (b, ob, l, channel chunk): (N/s)-point inverse NTTs (root
 // psi^s, no scaling: N^{-1} is in the filter spectra) of the folded products
@@ -697,12 +951,18 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     const PlanDev P = plan_dev(p);
     u64* spec = (u64*)d_ws;
     u64* fold = spec + (size_t)B * P.n_ib * c->L * c->N;
+    const bool imma = use_imma(c, P);
     rec(ev, 0, st);
-    he_status s = launch_ntt_fwd(c, (const u64*)d_c0, spec, (long)B * P.n_ib * c->L, 1, st);
+    he_status s = launch_ntt_fwd(c, (const u64*)d_c0, spec, (long)B * P.n_ib * c->L,
+                                 imma ? 2 : 1, st);
     if (s != HE_OK) return s;
     rec(ev, 1, st);
-    s = launch_mac(spec, (const u64*)d_fspec, fold, B, P.n_ib, c->L, c->logN, P.logs, P.c_o,
-                   c->d_limb, st);
+    if (imma)
+        s = launch_mac_imma((const unsigned char*)spec, (const unsigned char*)d_fspec, fold, B,
+                            P.n_ib, c->L, c->logN, P.logs, P.c_o, c->d_limb, st);
+    else
+        s = launch_mac(spec, (const u64*)d_fspec, fold, B, P.n_ib, c->L, c->logN, P.logs,
+                       P.c_o, c->d_limb, st);
     if (s != HE_OK) return s;
     HE_CHECK_LAUNCH();
     const int M = c->N >> P.logs;

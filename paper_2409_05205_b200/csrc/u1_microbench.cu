@@ -34,7 +34,7 @@ __global__ void u1_imad(const u32* in, u32* out, int iters, long long* cyc) {
 }
 
 __global__ void u1_imad_wide(const u32* in, u32* out, int iters, long long* cyc) {
-    u32 a = in[0] + threadIdx.x, b = in[1];
+    u32 b = in[1];
     u64 acc[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = i;
@@ -99,6 +99,50 @@ __global__ void u1_bfly(const u64* in, u32* out, int iters, long long* cyc) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
 }
 
+// which 5: legacy int8 tensor-core MMA (mma.sync m16n8k32 u8 x u8 -> s32),
+// 4 independent accumulators per warp -> int8 MACs / s (per lane-thread
+// count converted by the host: 4096 MACs per warp-instruction).
+__global__ void u1_imma(const u32* in, u32* out, int iters, long long* cyc) {
+    u32 a0 = in[0] + threadIdx.x, a1 = in[1], a2 = in[2], a3 = in[3];
+    u32 b0 = in[1] ^ threadIdx.x, b1 = in[2];
+    int acc[4][4] = {};
+    long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+            asm volatile(
+                "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+                "{%8,%9}, {%0,%1,%2,%3};"
+                : "+r"(acc[m][0]), "+r"(acc[m][1]), "+r"(acc[m][2]), "+r"(acc[m][3])
+                : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    }
+    long long c1 = clock64();
+    int s = 0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) s ^= acc[m][0] ^ acc[m][1] ^ acc[m][2] ^ acc[m][3];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = (u32)s;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
+}
+
+// which 6: FP64 DFMA chains.
+__global__ void u1_dfma(const u32* in, u32* out, int iters, long long* cyc) {
+    double a = 1.0 + in[0] * 1e-9, b = 1e-7 * in[1];
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+    long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+    }
+    long long c1 = clock64();
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = (u32)(long long)s;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
+}
+
 // Runs kernel `which` once (after one warm-up launch); returns the elapsed
 // milliseconds, the in-kernel cycle count of block 0 (SM clock estimate)
 // and the number of operations executed.  0 on success.
@@ -129,6 +173,8 @@ extern "C" int u1_run(int which, int blocks, int threads, int iters, float* ms,
             case 2: u1_mac<<<blocks, threads>>>(d_in, d_out, iters, d_cyc); per_iter = 2; break;
             case 3: u1_bfly<false><<<blocks, threads>>>((const u64*)d_in, d_out, iters, d_cyc); per_iter = 8; break;
             case 4: u1_bfly<true><<<blocks, threads>>>((const u64*)d_in, d_out, iters, d_cyc); per_iter = 8; break;
+            case 5: u1_imma<<<blocks, threads>>>(d_in, d_out, iters, d_cyc); per_iter = 4 * 4096.0 / 32; break;
+            case 6: u1_dfma<<<blocks, threads>>>(d_in, d_out, iters, d_cyc); per_iter = 8; break;
             default: return 2;
         }
         if (rep == 1) cudaEventRecord(e1);

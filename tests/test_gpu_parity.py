@@ -313,3 +313,15 @@ def test_errors(he):
     assert e.value.status == he.HE_ENOMEM
     # B = 0 is a no-op
     ctx.conv(p, ctx.empty_u64(0, p.n_ib, 3, 256), fspec)
+
+
+def test_conv_imad_mac_path(he, monkeypatch):
+    """HE_MAC=imad selects the IMAD (25-bit split) MAC kernel instead of the
+    int8 tensor-core MAC; both must be bit-exact."""
+    monkeypatch.setenv("HE_MAC", "imad")
+    for cfg_idx, li, B in [(3, 0, 64), (4, 1, 32), (4, 14, 32)]:
+        cfg = synth.CONFIGS[cfg_idx]
+        ctx = he.Context(cfg.primes, cfg.log2N, cfg.t)      # fresh: reads HE_MAC
+        ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+        run_conv(he, ctx, ring, cfg.conv[li], B, seed=cfg.seed + 7 * li,
+                 check_b=[0, B - 1])
