@@ -355,6 +355,18 @@ def main():
             st["fc_ntt_fwd"] += f[0].elapsed_time(f[1])
             st["fc_inv"] += f[1].elapsed_time(f[2])
     st = {k: v / args.steps for k, v in st.items()}
+    per_layer = []
+    for i, lw in enumerate(layers):
+        t = [0.0, 0.0, 0.0]
+        for k in range(args.steps):
+            a = evs[k][i]
+            t[0] += a[0].elapsed_time(a[1])
+            t[1] += a[1].elapsed_time(a[2])
+            t[2] += a[2].elapsed_time(a[3])
+        p = lw.p
+        per_layer.append({"layer": i, "s": p.s, "n_ib": p.n_ib, "n_ob": p.n_ob,
+                          "c_o": lw.Ly.c_o, "ntt_ms": t[0] / args.steps,
+                          "mac_ms": t[1] / args.steps, "intt_ms": t[2] / args.steps})
 
     # ---- algorithmic work per step
     W_ntt_bfly = sum(lw.ntt_bfly for lw in layers)
@@ -500,7 +512,8 @@ def main():
                        "parallelism": f"dp{world} (batch-sharded, no collective)",
                        "l2": "inputs larger than L2 (>1 GB touched per step)"},
             "ms_per_plain20_image": ms_step / B if cfg.idx == 4 else None,
-            "ntt": ntt, "stages_ms_per_step": st, "roofline": roofline,
+            "ntt": ntt, "stages_ms_per_step": st, "per_layer": per_layer,
+            "roofline": roofline,
             "roofline_all": rl, "u1": u1, "init_ms": init_ms,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_step * args.steps,

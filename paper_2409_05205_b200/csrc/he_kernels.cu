@@ -52,10 +52,22 @@ static inline int ntt_threads(int NS) { return std::min(512, std::max(16, NS / 1
 // cluster barrier after the loads makes in-place use safe.  16-byte
 // coalesced global loads and stores.  OUT_FMT 0: canonical, 1: split25,
 // 2: byte planes (int8 tensor-core MAC operand).
+// MAC-tile layout of the forward spectra (OUT_FMT 2): byte j (j < 7) of the
+// coefficient at position g s + u of limb (b, beta, l), g = gb Gt + gi, is
+//   A[((((l (M/Gt) + gb) 7 + j) B + b) Gt + gi) Kp + beta s + u]   (bytes),
+// with zeros in [K, Kp) of every row: a (plane, image) row holds Gt
+// consecutive groups, so a limb writes runs of Gt*s bytes (n_ib = 1) and the
+// int8 MAC stages each operand tile as contiguous blocks.
+struct TileLay {
+    int B, n_ib, logs, Kp, Gt;
+};
+static inline int tile_gt(int M) { return M < 16 ? M : 16; }
+
 template <int S, int OUT_FMT>
 __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int logN, int L,
                                                 const he_limb* __restrict__ limbs,
-                                                const ulonglong2* __restrict__ tw_all) {
+                                                const ulonglong2* __restrict__ tw_all,
+                                                TileLay T) {
     extern __shared__ u64 sm[];
     const int N = 1 << logN, NS = N >> S;
     const int li = blockIdx.x >> S, seg = blockIdx.x & ((1 << S) - 1);
@@ -93,9 +105,9 @@ __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int log
     else __syncthreads();
     ct_all<3>(sm, logN, NS, seg, S, tw, q, q2);
     if (OUT_FMT == 2) {
-        // byte planes for the int8 tensor-core MAC: plane j (j < 7) of limb li
-        // holds byte j of every coefficient, at byte offset li*8N + j*N.
-        unsigned char* base = reinterpret_cast<unsigned char*>(out + (size_t)li * N);
+        unsigned char* A = reinterpret_cast<unsigned char*>(out);
+        const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
+        const int s = 1 << T.logs, M = N >> T.logs, K = T.n_ib << T.logs;
         for (int i = 4 * threadIdx.x; i < NS; i += 4 * blockDim.x) {
             u64 x[4];
 #pragma unroll
@@ -106,9 +118,20 @@ __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int log
             byte_transpose4((u32)(x[0] >> 32), (u32)(x[1] >> 32), (u32)(x[2] >> 32),
                             (u32)(x[3] >> 32), pl[4], pl[5], pl[6], pl[7]);
             const int pos = seg * NS + i;
+            const int g = pos >> T.logs, u = pos & (s - 1);
+            const int gb = g / T.Gt, gi = g - gb * T.Gt;
+            unsigned char* row =
+                A + (((((size_t)l * (M / T.Gt) + gb) * 7) * T.B + b) * T.Gt + gi) * T.Kp +
+                beta * s + u;
+            const size_t pstride = (size_t)T.B * T.Gt * T.Kp;
+            const bool tail = (beta == T.n_ib - 1) && (u + 4 == s) && (T.Kp > K);
 #pragma unroll
-            for (int j = 0; j < 7; ++j)
-                *reinterpret_cast<u32*>(base + (size_t)j * N + pos) = pl[j];
+            for (int j = 0; j < 7; ++j) {
+                *reinterpret_cast<u32*>(row + j * pstride) = pl[j];
+                if (tail)
+                    for (int z = 4; z < T.Kp - K + 4; z += 4)
+                        *reinterpret_cast<u32*>(row + j * pstride + z) = 0u;
+            }
         }
         return;
     }
@@ -123,34 +146,35 @@ __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int log
 template <int OUT_FMT>
 __global__ void __launch_bounds__(512, 2)
 k_ntt_fwd_s0(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
-             const ulonglong2* __restrict__ tw_all) {
-    ntt_fwd_segment<0, OUT_FMT>(in, out, logN, L, limbs, tw_all);
+             const ulonglong2* __restrict__ tw_all, TileLay T) {
+    ntt_fwd_segment<0, OUT_FMT>(in, out, logN, L, limbs, tw_all, T);
 }
 
 template <int OUT_FMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 2)
 k_ntt_fwd_s1(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
-             const ulonglong2* __restrict__ tw_all) {
-    ntt_fwd_segment<1, OUT_FMT>(in, out, logN, L, limbs, tw_all);
+             const ulonglong2* __restrict__ tw_all, TileLay T) {
+    ntt_fwd_segment<1, OUT_FMT>(in, out, logN, L, limbs, tw_all, T);
 }
 
 template <int OUT_FMT>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 2)
 k_ntt_fwd_s2(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
-             const ulonglong2* __restrict__ tw_all) {
-    ntt_fwd_segment<2, OUT_FMT>(in, out, logN, L, limbs, tw_all);
+             const ulonglong2* __restrict__ tw_all, TileLay T) {
+    ntt_fwd_segment<2, OUT_FMT>(in, out, logN, L, limbs, tw_all, T);
 }
 
 // Launch the forward NTT over nlimbs = batch * L limbs.
 static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
-                                long nlimbs, int out_fmt, cudaStream_t st) {
+                                long nlimbs, int out_fmt, cudaStream_t st,
+                                TileLay T = TileLay{1, 1, 0, 16, 1}) {
     if (nlimbs <= 0) return HE_OK;
     const int logN = c->logN;
     const int S = logN <= 13 ? 0 : logN - 13;
     const int NS = c->N >> S;
     const int threads = std::min(512, std::max(32, NS / 16));
     const size_t smem = sizeof(u64) * padded_words(NS);
-    typedef void (*kfn)(const u64*, u64*, int, int, const he_limb*, const ulonglong2*);
+    typedef void (*kfn)(const u64*, u64*, int, int, const he_limb*, const ulonglong2*, TileLay);
     kfn k;
     static kfn const tab[3][3] = {
         {k_ntt_fwd_s0<0>, k_ntt_fwd_s0<1>, k_ntt_fwd_s0<2>},
@@ -159,7 +183,7 @@ static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
     k = tab[S][out_fmt];
     if (!set_smem(k, smem)) return HE_ECUDA;
     k<<<(unsigned)(nlimbs << S), threads, smem, st>>>(in, out, logN, c->L, c->d_limb,
-                                                      c->d_tw_fwd);
+                                                      c->d_tw_fwd, T);
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
@@ -416,6 +440,7 @@ static bool use_imma(const he_ctx* c, const PlanDev& P) {
 }
 static inline int imma_kp(int K) { return (K + 15) & ~15; }
 static inline int imma_sw(int Kp) { return Kp / 4 + ((4 - Kp / 4) & 7); }   // = 4 mod 8
+__device__ __forceinline__ int imma_sw_dev(int Kp) { return Kp / 4 + ((4 - Kp / 4) & 7); }
 
 // spectra [c_o][n_ib][L][N] -> byte planes Fpl[l][g][7][c_o][Kp] of
 // spec * N^{-1} (k = beta s + u < K; zero for K <= k < Kp).
@@ -626,14 +651,14 @@ k_mac_fold(const u64* __restrict__ C, const u64* __restrict__ F, u64* __restrict
         if (k0 + KC >= K) {                      // last chunk of this iteration
             const int g = g0 + it * GC + gl;
             if (g < M) {
-                u64* og = out + ((size_t)l * M + g) * B * c_o;
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
                         const int b = b0 + ty + 8 * i, n = n0 + nt * 8 + tx + 4 * j;
                         if (b < B && n < c_o)
-                            og[(size_t)b * c_o + n] = mac_reduce(a0[i][j], a1[i][j], a2[i][j], Lm);
+                            out[(((size_t)l * B + b) * c_o + n) * M + g] =
+                                mac_reduce(a0[i][j], a1[i][j], a2[i][j], Lm);
                     }
             }
 #pragma unroll
@@ -714,6 +739,18 @@ __device__ __forceinline__ u64 reduce13(const int (&acc)[13][4], int e, const he
     return csub(r, q);
 }
 
+// x / d for 0 <= x < 2^31 with d fixed per kernel: a shift when d is a power
+// of two, otherwise a plain division.
+struct FastDiv {
+    int d, sh;
+    bool p2;
+    __device__ __forceinline__ explicit FastDiv(int dd) : d(dd), sh(0),
+                                                         p2((dd & (dd - 1)) == 0) {
+        while ((1 << sh) < dd) ++sh;
+    }
+    __device__ __forceinline__ int div(int x) const { return p2 ? (x >> sh) : (x / d); }
+};
+
 template <int CHUNK>
 __device__ __forceinline__ void cp_async_n(void* smem_dst, const void* gsrc, bool valid) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -725,133 +762,176 @@ __device__ __forceinline__ void cp_async_n(void* smem_dst, const void* gsrc, boo
                      "n"(CHUNK), "r"(valid ? CHUNK : 0));
 }
 
-template <int CHUNK>
-__device__ __forceinline__ void stage_a(u32* sA, const unsigned char* Cpl, int B, int b0,
-                                        int n_ib, int L, int l, int N, int g, int logs,
-                                        int sw) {
-    const int s = 1 << logs, per = s / CHUNK;
-    const int total = 32 * 7 * n_ib * per;
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-        const int c = e % per;
-        int r = e / per;
-        const int beta = r % n_ib;
-        r /= n_ib;
-        const int j = r % 7, b = r / 7;
-        const bool ok = b0 + b < B;
-        const unsigned char* src =
-            ok ? Cpl + ((((size_t)(b0 + b) * n_ib + beta) * L + l) * 8 + j) * (size_t)N +
-                     ((size_t)g << logs) + c * CHUNK
-               : Cpl;
-        cp_async_n<CHUNK>(reinterpret_cast<unsigned char*>(sA + (j * 32 + b) * sw) +
-                              beta * s + c * CHUNK,
-                          src, ok);
-    }
-}
-
-__global__ void __launch_bounds__(256, 2)
-k_mac_imma(const unsigned char* __restrict__ Cpl, const unsigned char* __restrict__ Fpl,
-           u64* __restrict__ out, int B, int n_ib, int L, int logN, int logs, int c_o, int Kp,
-           int sw, const he_limb* __restrict__ limbs) {
+// CTA = (limb l, G consecutive groups, 16*TB16-image tile); one warp per
+// 16 x 8 output tile (bt, nt).  Work proceeds in "units" (GS groups x a
+// KC-byte k-chunk): for small K a unit is all G groups with the whole K, for
+// large K one group and a 64-byte k-chunk.  Each unit's A tile (7 planes x
+// rows x KC bytes per group, MAC-tile layout) and F tile (7 x c_o x KC) are
+// contiguous in global memory and are copied with 16-byte cp.async into
+// padded shared rows (stride = 4 mod 8 words: conflict-free fragments).
+// Reduced outputs go straight to the transposed fold out[l][b][n][g].
+template <int TB16>
+__global__ void __launch_bounds__(512)
+k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
+           u64* __restrict__ out, int B, int L, int M, int c_o, int Kp, int G, int GS,
+           int KC, int Gt, const he_limb* __restrict__ limbs) {
     extern __shared__ u32 sm32[];
-    const int N = 1 << logN, M = N >> logs, K = n_ib << logs;
-    const int nrow = (c_o + 7) & ~7;
-    u32* sA = sm32;                       // [7][32][sw]
-    u32* sB = sm32 + 7 * 32 * sw;         // [7][nrow][sw]
-    const int l = blockIdx.x / M, g = blockIdx.x - l * M;
-    const int b0 = blockIdx.y * 32;
-    const int Kw = Kp >> 2, Kw0 = K >> 2;
-    // zero what the copies do not cover: A columns K..Kp, B rows c_o..nrow
-    for (int e = threadIdx.x; e < 7 * 32 * (Kw - Kw0); e += blockDim.x) {
-        const int w = Kw0 + e % (Kw - Kw0), row = e / (Kw - Kw0);
-        sA[row * sw + w] = 0;
+    constexpr int rows = 16 * TB16;
+    const int nrow = (c_o + 7) & ~7, nnt = nrow >> 3;
+    const int swc = imma_sw_dev(KC);
+    const int rw = imma_sw_dev(GS * KC);                  // A row: GS groups x KC bytes
+    const int gb = 7 * nrow * swc;                        // B words per group
+    u32* sA = sm32;                                       // [7][rows][rw]
+    u32* sB = sm32 + 7 * rows * rw;                       // [GS][7][nrow][swc]
+    const int nGc = (M + G - 1) / G;
+    const int l = blockIdx.x / nGc, g0 = (blockIdx.x - l * nGc) * G;
+    const int b0 = blockIdx.y * rows;
+    const int gcnt = min(G, M - g0);
+    const int nkc = Kp / KC;
+    // padded B rows (n >= c_o) stay zero for the whole kernel
+    for (int e = threadIdx.x; e < GS * 7 * (nrow - c_o) * swc; e += blockDim.x) {
+        const int w = e % swc, r = e / swc;
+        const int n = c_o + r % (nrow - c_o), gj = r / (nrow - c_o);
+        sB[(gj * nrow + n) * swc + w] = 0;
     }
-    for (int e = threadIdx.x; e < 7 * (nrow - c_o) * Kw; e += blockDim.x) {
-        const int w = e % Kw, r = e / Kw;
-        const int j = r / (nrow - c_o), n = c_o + r % (nrow - c_o);
-        sB[(j * nrow + n) * sw + w] = 0;
-    }
-    // stage A (C spectrum byte planes of the 32-image tile, group g)
-    const int s = 1 << logs;
-    if (s >= 16) stage_a<16>(sA, Cpl, B, b0, n_ib, L, l, N, g, logs, sw);
-    else if (s == 8) stage_a<8>(sA, Cpl, B, b0, n_ib, L, l, N, g, logs, sw);
-    else stage_a<4>(sA, Cpl, B, b0, n_ib, L, l, N, g, logs, sw);
-    // stage B (filter byte planes of group g), 16-byte chunks
-    {
-        const unsigned char* fg = Fpl + ((size_t)l * M + g) * 7 * c_o * Kp;
-        const int per = Kp / 16, total = 7 * c_o * per;
-        for (int e = threadIdx.x; e < total; e += blockDim.x) {
-            const int c = e % per, r = e / per;            // r = j * c_o + n
-            const int j = r / c_o, n = r - j * c_o;
-            cp_async_n<16>(reinterpret_cast<unsigned char*>(sB + (j * nrow + n) * sw) + c * 16,
-                           fg + (size_t)r * Kp + c * 16, true);
-        }
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gq = lane >> 2, tq = lane & 3;
-    const int nnt = nrow >> 3, items = 2 * nnt;
+    const int bt = warp / nnt, nt = warp - bt * nnt;
     const he_limb Lm = limbs[l];
-    for (int it = warp; it < items; it += 8) {
-        const int bt = it / nnt, nt = it - bt * nnt;
-        int acc[13][4];
+    int acc[13][4];
+    for (int gu = 0; gu < gcnt; gu += GS) {
+        const int gsn = min(GS, gcnt - gu);
+        for (int kc = 0; kc < nkc; ++kc) {
+            const int k0 = kc * KC;
+            // ---- stage A: per (plane, image) the unit's gsn groups x KC bytes
+            //      are contiguous (KC = Kp, or gsn = 1): rows of rcpr 16-byte chunks
+            {
+                const int gbk = (g0 + gu) / Gt, gi0 = (g0 + gu) - gbk * Gt;
+                const int rcpr = (gsn * KC) >> 4;
+                const FastDiv drc(rcpr);
+                const int per = rows * rcpr;
+                const size_t plane_stride = (size_t)B * Gt * Kp;
+                const unsigned char* a0 =
+                    A + ((((size_t)l * (M / Gt) + gbk) * 7) * B + b0) * Gt * Kp +
+                    (size_t)gi0 * Kp + k0;
+                for (int e = threadIdx.x; e < per; e += blockDim.x) {
+                    const int bl = drc.div(e), c = e - bl * rcpr;
+                    const bool ok = b0 + bl < B;
+                    const unsigned char* src = a0 + (size_t)bl * Gt * Kp + c * 16;
+                    unsigned char* dst =
+                        reinterpret_cast<unsigned char*>(sA + (size_t)bl * rw) + c * 16;
 #pragma unroll
-        for (int d = 0; d < 13; ++d)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) acc[d][e] = 0;
-        const u32* ab = sA + (bt * 16 + gq) * sw + tq;
-        const u32* bb = sB + (nt * 8 + gq) * sw + tq;
-        int kw = 0;
-        for (; kw + 8 <= Kw; kw += 8) {
-            u32 bf0[7], bf1[7];
-#pragma unroll
-            for (int j = 0; j < 7; ++j) {
-                bf0[j] = bb[j * nrow * sw + kw];
-                bf1[j] = bb[j * nrow * sw + kw + 4];
+                    for (int j = 0; j < 7; ++j)
+                        cp_async_n<16>(dst + (size_t)j * rows * rw * 4,
+                                       ok ? src + j * plane_stride : A, ok);
+                }
             }
+            // ---- stage B: per (group, plane) a contiguous c_o x KC block
+            {
+                const int cpr2 = KC >> 4;
+                const FastDiv dc(cpr2), dn(c_o * cpr2);
+                const int per = c_o * cpr2, total = gsn * per;
+                const unsigned char* f0 = Fpl + (((size_t)l * M + g0 + gu) * 7) * c_o * Kp + k0;
+                for (int e = threadIdx.x; e < total; e += blockDim.x) {
+                    const int gi = dn.div(e), rem = e - gi * per;
+                    const int n = dc.div(rem), c = rem - n * cpr2;
+                    const unsigned char* src = f0 + ((size_t)gi * 7 * c_o + n) * Kp + c * 16;
+                    unsigned char* dst = reinterpret_cast<unsigned char*>(
+                                             sB + ((size_t)gi * 7 * nrow + n) * swc) + c * 16;
 #pragma unroll
-            for (int i = 0; i < 7; ++i) {
-                const u32* ap = ab + i * 32 * sw + kw;
-                const u32 a0 = ap[0], a1 = ap[8 * sw], a2 = ap[4], a3 = ap[8 * sw + 4];
-#pragma unroll
-                for (int j = 0; j < 7; ++j) mma_k32(acc[i + j], a0, a1, a2, a3, bf0[j], bf1[j]);
+                    for (int j = 0; j < 7; ++j)
+                        cp_async_n<16>(dst + (size_t)j * nrow * swc * 4,
+                                       src + (size_t)j * c_o * Kp, true);
+                }
             }
-        }
-        if (kw < Kw) {                                   // one k16 step
-            u32 bf0[7];
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncthreads();
+            for (int gi = 0; gi < gsn; ++gi) {
+                if (kc == 0) {
 #pragma unroll
-            for (int j = 0; j < 7; ++j) bf0[j] = bb[j * nrow * sw + kw];
+                    for (int d = 0; d < 13; ++d)
 #pragma unroll
-            for (int i = 0; i < 7; ++i) {
-                const u32* ap = ab + i * 32 * sw + kw;
-                const u32 a0 = ap[0], a1 = ap[8 * sw];
+                        for (int e = 0; e < 4; ++e) acc[d][e] = 0;
+                }
+                const u32* ab = sA + (bt * 16 + gq) * rw + gi * (KC >> 2) + tq;
+                const u32* bb = sB + (size_t)gi * gb + (nt * 8 + gq) * swc + tq;
+                const int Kw = KC >> 2;
+                int kw = 0;
+                for (; kw + 8 <= Kw; kw += 8) {
+                    u32 bf0[7], bf1[7];
 #pragma unroll
-                for (int j = 0; j < 7; ++j) mma_k16(acc[i + j], a0, a1, bf0[j]);
+                    for (int j = 0; j < 7; ++j) {
+                        bf0[j] = bb[j * nrow * swc + kw];
+                        bf1[j] = bb[j * nrow * swc + kw + 4];
+                    }
+#pragma unroll
+                    for (int i = 0; i < 7; ++i) {
+                        const u32* ap = ab + i * rows * rw + kw;
+                        const u32 a0 = ap[0], a1 = ap[8 * rw], a2 = ap[4], a3 = ap[8 * rw + 4];
+#pragma unroll
+                        for (int j = 0; j < 7; ++j)
+                            mma_k32(acc[i + j], a0, a1, a2, a3, bf0[j], bf1[j]);
+                    }
+                }
+                if (kw < Kw) {                               // one k16 step
+                    u32 bf0[7];
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) bf0[j] = bb[j * nrow * swc + kw];
+#pragma unroll
+                    for (int i = 0; i < 7; ++i) {
+                        const u32* ap = ab + i * rows * rw + kw;
+                        const u32 a0 = ap[0], a1 = ap[8 * rw];
+#pragma unroll
+                        for (int j = 0; j < 7; ++j) mma_k16(acc[i + j], a0, a1, bf0[j]);
+                    }
+                }
+                if (kc == nkc - 1) {
+                    const int g = g0 + gu + gi;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int b = b0 + bt * 16 + gq + 8 * (e >> 1);
+                        const int n = nt * 8 + 2 * tq + (e & 1);
+                        if (b < B && n < c_o)
+                            out[(((size_t)l * B + b) * c_o + n) * M + g] = reduce13(acc, e, Lm);
+                    }
+                }
             }
-        }
-        u64* og = out + ((size_t)l * M + g) * B * c_o;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int b = b0 + bt * 16 + gq + 8 * (e >> 1), n = nt * 8 + 2 * tq + (e & 1);
-            if (b < B && n < c_o) og[(size_t)b * c_o + n] = reduce13(acc, e, Lm);
+            __syncthreads();
         }
     }
 }
 
-static he_status launch_mac_imma(const unsigned char* Cpl, const unsigned char* Fpl, u64* out,
+static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fpl, u64* out,
                                  int B, int n_ib, int L, int logN, int logs, int c_o,
                                  const he_limb* limbs, cudaStream_t st) {
     const int M = (1 << logN) >> logs, K = n_ib << logs;
-    const int Kp = imma_kp(K), sw = imma_sw(Kp);
-    const int nrow = (c_o + 7) & ~7;
-    const size_t smem = sizeof(u32) * (size_t)(7 * 32 + 7 * nrow) * sw;
+    const int Kp = imma_kp(K);
+    const int nrow = (c_o + 7) & ~7, nnt = nrow / 8;
+    if (nnt > 32) return HE_ESHAPE;                       // c_o <= 256
+    const int TB16 = (nnt <= 8 && B > 16) ? 2 : 1;
+    const int rows = 16 * TB16, warps = TB16 * nnt;
+    const size_t budget = 48 * 1024;                      // several CTAs per SM
+    // one unit = GS groups x KC bytes of k
+    const int Gt = tile_gt(M);
+    auto unit_bytes = [&](int gs, int kc) {
+        return sizeof(u32) * 7 * ((size_t)rows * imma_sw(gs * kc) + (size_t)gs * nrow * imma_sw(kc));
+    };
+    int KC = Kp, GS = 1, G = 1;
+    if (unit_bytes(1, Kp) <= budget) {
+        GS = 1;
+        while (GS < Gt && unit_bytes(GS * 2, Kp) <= budget) GS *= 2;
+        G = GS;
+    } else {
+        KC = (Kp % 64 == 0) ? 64 : ((Kp % 32 == 0) ? 32 : 16);
+        GS = G = 1;
+    }
+    const size_t smem = unit_bytes(GS, KC);
     if (smem > 227 * 1024) return HE_ESHAPE;
-    if (!set_smem(k_mac_imma, smem)) return HE_ECUDA;
-    dim3 grid(L * M, (B + 31) / 32);
-    k_mac_imma<<<grid, 256, smem, st>>>(Cpl, Fpl, out, B, n_ib, L, logN, logs, c_o, Kp, sw,
-                                        limbs);
+    auto k = TB16 == 2 ? k_mac_imma<2> : k_mac_imma<1>;
+    if (!set_smem(k, smem)) return HE_ECUDA;
+    dim3 grid(L * ((M + G - 1) / G), (B + rows - 1) / rows);
+    k<<<grid, 32 * warps, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, G, GS, KC, Gt, limbs);
     return HE_OK;
 }
 
@@ -883,11 +963,12 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     const u64 q = Lm.q, q2 = 2 * q;
     const ulonglong2* twi = twi_all + (size_t)l * N;
     const int ch0 = ch * cc, ncc = min(cc, P.c_ob - ch0);
-    const u64* fb = fold + (size_t)b * P.c_o + ob * P.c_ob + ch0;
+    // fold layout [l][b][n][g]: the chunk's channel rows are contiguous in g
+    const u64* fb = fold + (((size_t)l * B + b) * P.c_o + ob * P.c_ob + ch0) * M;
     for (int idx = threadIdx.x; idx < ncc * M; idx += blockDim.x) {
-        const int g = idx / ncc, a = idx - g * ncc;
+        const int a = idx >> logM, g = idx & (M - 1);
         const int n = ob * P.c_ob + ch0 + a;
-        sm[a * stride + PAD(g)] = n < P.c_o ? fb[((size_t)l * M + g) * B * P.c_o + a] : 0;
+        sm[a * stride + PAD(g)] = n < P.c_o ? fb[idx] : 0;
     }
     __syncthreads();
     gs_all<3>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
@@ -920,12 +1001,20 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     }
 }
 
+// Workspace of he_conv: forward spectra (split25 words, or the MAC-tile
+// byte layout, whichever is larger) followed by the folded products.
+static size_t spec_words(const he_ctx* c, const he_conv_plan* p, int B) {
+    const size_t M = (size_t)c->N / p->s;
+    const size_t split = (size_t)B * p->n_ib * c->L * c->N;
+    const size_t tile = ((size_t)c->L * M * 7 * B * imma_kp(p->n_ib * p->s) + 7) / 8;
+    return std::max(split, tile);
+}
+
 extern "C" size_t he_conv_workspace_bytes(const he_ctx* c, const he_conv_plan* p, int B) {
     if (!c || !p || B < 0) return 0;
     const size_t M = (size_t)c->N / p->s;
-    const size_t spec = (size_t)B * p->n_ib * c->L * c->N;
     const size_t fold = (size_t)c->L * M * B * p->d.c_o;
-    return sizeof(u64) * (spec + fold) + 256;
+    return sizeof(u64) * (spec_words(c, p, B) + fold) + 256;
 }
 
 static inline void rec(void* const* ev, int i, cudaStream_t st) {
@@ -950,11 +1039,13 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     cudaStream_t st = STREAM(stream);
     const PlanDev P = plan_dev(p);
     u64* spec = (u64*)d_ws;
-    u64* fold = spec + (size_t)B * P.n_ib * c->L * c->N;
+    u64* fold = spec + spec_words(c, p, B);
     const bool imma = use_imma(c, P);
     rec(ev, 0, st);
     he_status s = launch_ntt_fwd(c, (const u64*)d_c0, spec, (long)B * P.n_ib * c->L,
-                                 imma ? 2 : 1, st);
+                                 imma ? 2 : 1, st,
+                                 TileLay{B, P.n_ib, P.logs, imma_kp(P.n_ib * P.s),
+                                         tile_gt(c->N >> P.logs)});
     if (s != HE_OK) return s;
     rec(ev, 1, st);
     if (imma)
@@ -966,9 +1057,13 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     if (s != HE_OK) return s;
     HE_CHECK_LAUNCH();
     const int M = c->N >> P.logs;
-    const int stride = padded_words(M) | 1;          // odd: conflict-free
-    int cc = std::max(1, std::min(P.c_ob, 6144 / stride));   // <= 48 KB smem
+    int cc = std::max(1, std::min(P.c_ob, 6144 / (padded_words(M) + 16)));  // <= 48 KB
     while (cc & (cc - 1)) cc &= cc - 1;                       // power of two
+    // array stride (words) = 16/cc (mod 16) for cc < 16, odd otherwise: the
+    // row writer reads (channel-fastest) 16 consecutive threads conflict-free
+    int stride = padded_words(M);
+    const int want = cc < 16 ? (16 / cc) & 15 : 1;
+    while ((stride & 15) != want && !(cc >= 16 && (stride & 1))) ++stride;
     const int nchunk = (P.c_ob + cc - 1) / cc;
     const size_t smem = sizeof(u64) * (size_t)cc * stride;
     if (!set_smem(k_intt_scatter, smem)) return HE_ECUDA;
