@@ -445,19 +445,45 @@ def main():
             h2d += fc["c0_h"].numel() * 8 + fc["ph_h"].numel() * 4
             d2h += fc["out"].numel() * 8
 
+        # copies overlap compute: layer i+1's c0/phi1 upload (H2D stream) and
+        # layer i-1's payload download (D2H stream) run while layer i computes
+        h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        nl = len(layers) + (1 if fc else 0)
+        up_done = [torch.cuda.Event() for _ in range(nl)]
+        comp_done = [torch.cuda.Event() for _ in range(nl)]
+        for e in comp_done:
+            e.record(stream)
+
         def e2e_step():
             for i, lw in enumerate(layers):
-                c0_d[i].copy_(c0_h[i], non_blocking=True)
-                phi_d[i].copy_(phi_h[i], non_blocking=True)
+                with torch.cuda.stream(h2d_s):
+                    h2d_s.wait_event(comp_done[i])          # WAR vs previous step
+                    c0_d[i].copy_(c0_h[i], non_blocking=True)
+                    phi_d[i].copy_(phi_h[i], non_blocking=True)
+                    up_done[i].record(h2d_s)
+                stream.wait_event(up_done[i])
                 ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], outs[i], ws)
                 ctx.mask_extract(lw.p, outs[i], None, comps[i])
-                comp_h[i].copy_(comps[i], non_blocking=True)
+                comp_done[i].record(stream)
+                with torch.cuda.stream(d2h_s):
+                    d2h_s.wait_event(comp_done[i])
+                    comp_h[i].copy_(comps[i], non_blocking=True)
             if fc:
-                fc["c0_d"].copy_(fc["c0_h"], non_blocking=True)
-                fc["ph_d"].copy_(fc["ph_h"], non_blocking=True)
+                i = len(layers)
+                with torch.cuda.stream(h2d_s):
+                    h2d_s.wait_event(comp_done[i])
+                    fc["c0_d"].copy_(fc["c0_h"], non_blocking=True)
+                    fc["ph_d"].copy_(fc["ph_h"], non_blocking=True)
+                    up_done[i].record(h2d_s)
+                stream.wait_event(up_done[i])
                 ctx.fc(fc["n_i"], fc["n_o"], fc["c0_d"], fc["wspec"], fc["benc"],
                        fc["ph_d"], fc["out"], fc["ws"])
-                fc["out_h"].copy_(fc["out"], non_blocking=True)
+                comp_done[i].record(stream)
+                with torch.cuda.stream(d2h_s):
+                    d2h_s.wait_event(comp_done[i])
+                    fc["out_h"].copy_(fc["out"], non_blocking=True)
+            # the step ends when its last payload is on the host
+            stream.wait_stream(d2h_s)
 
         for _ in range(2):
             e2e_step()
