@@ -436,52 +436,72 @@ def main():
     ntt["frac"] = ntt["limbs_per_s"] / ntt["roof_limbs_per_s"]
     del buf
 
-    # ---- e2e: host c0 (+phi1) -> device -> he_conv/he_mask_extract/he_fc -> host
+    # ---- e2e: the server loop through the public API with host buffers.
+    # c0 arrives in the 50-bit wire format (he_residues_unpack50), the
+    # server draws its mask phi1 on the device (he_phi1_generate), and the
+    # valid-slot payload leaves in the wire format (he_residues_pack50).
+    # Copies overlap compute: layer i+1's upload (H2D stream) and layer
+    # i-1's download (D2H stream) run while layer i computes.
     e2e = None
     if not args.no_e2e and not args.profile:
-        h2d = sum(lw.c0_bytes + lw.phi_bytes for lw in layers)
-        d2h = sum(lw.comp_bytes for lw in layers)
+        c0_pk_h, c0_pk_d, comp_pk_d, comp_pk_h = [], [], [], []
+        for i in range(len(layers)):
+            pk = ctx.pack50(c0_d[i])
+            c0_pk_d.append(pk)
+            c0_pk_h.append(pk.cpu().pin_memory())
+            comp_pk_d.append(torch.empty(ctx.packed_bytes(comps[i].numel()),
+                                         dtype=torch.uint8, device=dev))
+            comp_pk_h.append(torch.empty(comp_pk_d[-1].shape, dtype=torch.uint8).pin_memory())
         if fc:
-            h2d += fc["c0_h"].numel() * 8 + fc["ph_h"].numel() * 4
-            d2h += fc["out"].numel() * 8
-
-        # copies overlap compute: layer i+1's c0/phi1 upload (H2D stream) and
-        # layer i-1's payload download (D2H stream) run while layer i computes
+            fc["c0_pk_d"] = ctx.pack50(fc["c0_d"])
+            fc["c0_pk_h"] = fc["c0_pk_d"].cpu().pin_memory()
+            fc["out_pk_d"] = torch.empty(ctx.packed_bytes(fc["out"].numel()),
+                                         dtype=torch.uint8, device=dev)
+            fc["out_pk_h"] = torch.empty(fc["out_pk_d"].shape, dtype=torch.uint8).pin_memory()
+        torch.cuda.synchronize()
+        h2d = sum(t.numel() for t in c0_pk_h) + (fc["c0_pk_h"].numel() if fc else 0)
+        d2h = sum(t.numel() for t in comp_pk_h) + (fc["out_pk_h"].numel() if fc else 0)
         h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         nl = len(layers) + (1 if fc else 0)
         up_done = [torch.cuda.Event() for _ in range(nl)]
         comp_done = [torch.cuda.Event() for _ in range(nl)]
         for e in comp_done:
             e.record(stream)
+        mask_seed = [0]
 
         def e2e_step():
+            mask_seed[0] += 1
             for i, lw in enumerate(layers):
                 with torch.cuda.stream(h2d_s):
                     h2d_s.wait_event(comp_done[i])          # WAR vs previous step
-                    c0_d[i].copy_(c0_h[i], non_blocking=True)
-                    phi_d[i].copy_(phi_h[i], non_blocking=True)
+                    c0_pk_d[i].copy_(c0_pk_h[i], non_blocking=True)
                     up_done[i].record(h2d_s)
                 stream.wait_event(up_done[i])
+                ctx.unpack50(c0_pk_d[i], c0_d[i])
+                ctx.phi1_generate((mask_seed[0] << 8) + i, phi_d[i])
                 ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], outs[i], ws)
                 ctx.mask_extract(lw.p, outs[i], None, comps[i])
+                ctx.pack50(comps[i], comp_pk_d[i])
                 comp_done[i].record(stream)
                 with torch.cuda.stream(d2h_s):
                     d2h_s.wait_event(comp_done[i])
-                    comp_h[i].copy_(comps[i], non_blocking=True)
+                    comp_pk_h[i].copy_(comp_pk_d[i], non_blocking=True)
             if fc:
                 i = len(layers)
                 with torch.cuda.stream(h2d_s):
                     h2d_s.wait_event(comp_done[i])
-                    fc["c0_d"].copy_(fc["c0_h"], non_blocking=True)
-                    fc["ph_d"].copy_(fc["ph_h"], non_blocking=True)
+                    fc["c0_pk_d"].copy_(fc["c0_pk_h"], non_blocking=True)
                     up_done[i].record(h2d_s)
                 stream.wait_event(up_done[i])
+                ctx.unpack50(fc["c0_pk_d"], fc["c0_d"])
+                ctx.phi1_generate((mask_seed[0] << 8) + i, fc["ph_d"])
                 ctx.fc(fc["n_i"], fc["n_o"], fc["c0_d"], fc["wspec"], fc["benc"],
                        fc["ph_d"], fc["out"], fc["ws"])
+                ctx.pack50(fc["out"], fc["out_pk_d"])
                 comp_done[i].record(stream)
                 with torch.cuda.stream(d2h_s):
                     d2h_s.wait_event(comp_done[i])
-                    fc["out_h"].copy_(fc["out"], non_blocking=True)
+                    fc["out_pk_h"].copy_(fc["out_pk_d"], non_blocking=True)
             # the step ends when its last payload is on the host
             stream.wait_stream(d2h_s)
 
@@ -497,14 +517,16 @@ def main():
         ms_e2e = max_over_ranks(x0.elapsed_time(x1) / args.steps)
         e2e = {"value": evals_step * world / (ms_e2e * 1e-3), "unit": "ct×pt evals/s",
                "ms_per_step": ms_e2e, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h}
+               "d2h_bytes_per_step": d2h,
+               "wire": "50-bit packed residues (he_residues_pack50/unpack50); "
+                       "phi1 drawn on device (he_phi1_generate)"}
 
     # ---- CPU baseline: the oracle as it stands, rank 0, bounded sample
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
         from oracle import ref as R
         ring = R.Ring(N, cfg.primes, cfg.t)
-        nimg = 4 if cfg.idx == 4 else 1
+        nimg = 16 if cfg.idx == 4 else 1
         c0n = [t[:nimg].numpy().view(np.uint64) for t in c0_h]
         phn = [t[:nimg].numpy().view(np.uint32) for t in phi_h]
         oplans = [R.plan_conv(lw.Ly, N) for lw in layers]

@@ -209,6 +209,27 @@ he_status he_fc_ex(const he_ctx* ctx, const he_fc_desc* f,
                    uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream,
                    void* const* events);
 
+/* ------------------------------------------------------------ wire format */
+/* Residue wire format.  The paper counts ceil(log2 Q) bits per transmitted
+ * coefficient (Table II); here every residue (< 2^50) is
+ * bit-packed at 50 bits, little-endian: element i occupies bits
+ * [50 i, 50 i + 50) of the byte stream.  n must be a multiple of 32 (the
+ * stream is 50 n / 8 bytes, a multiple of 8); d_packed 8-byte aligned.
+ * Used for c0 arriving at the server (Alg. 1 Line 10) and the payload
+ * leaving it (Line 18).  Elements >= 2^50 give unspecified results. */
+he_status he_residues_pack50(const uint64_t* d_in, size_t n, uint8_t* d_packed,
+                             void* stream);
+he_status he_residues_unpack50(const uint8_t* d_packed, size_t n,
+                               uint64_t* d_out, void* stream);
+
+/* Server-side mask phi1 ("two random polynomials ... are
+ * generated"; reading R15): d_phi1[i] = SplitMix64(seed, i) mod t for
+ * i < n, a counter-based stream (z = seed + (i + 1) 0x9E3779B97F4A7C15,
+ * then the SplitMix64 finaliser), reproducible on any device and in the
+ * oracle. */
+he_status he_phi1_generate(const he_ctx* ctx, uint64_t seed, size_t n,
+                           uint32_t* d_phi1, void* stream);
+
 /* ------------------------------------------------------------ transforms */
 /* Batched negacyclic NTT over `batch` x L limbs stored [batch][L][N]
  * (the primitive behind a2, a3, a9; PAPER.md:28 cites NTT as the standard

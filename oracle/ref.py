@@ -703,3 +703,30 @@ def fc_protocol_decrypt(ring: Ring, W: np.ndarray, out_b: np.ndarray,
     if phi1_b is not None:
         m = (m - phi1_b.astype(np.int64)) % ring.t
     return np.where(m > ring.t // 2, m - ring.t, m)
+
+
+# ---------------------------------------------------------------------------
+# Server mask stream (R15): phi1[i] = SplitMix64(seed, i) mod t.
+# ---------------------------------------------------------------------------
+_SM_G = 0x9E3779B97F4A7C15
+_M64 = (1 << 64) - 1
+
+
+def splitmix64_py(seed: int, i: int) -> int:
+    """Definition with Python integers (Vigna's SplitMix64 finaliser applied
+    to the counter state seed + (i+1) * gamma)."""
+    z = (seed + (i + 1) * _SM_G) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def phi1_stream(seed: int, n: int, t: int) -> np.ndarray:
+    """Vectorised SplitMix64 (uint64 wrap-around arithmetic) mod t."""
+    with np.errstate(over="ignore"):
+        i = np.arange(1, n + 1, dtype=np.uint64)
+        z = np.uint64(seed & _M64) + i * np.uint64(_SM_G)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z % np.uint64(t)).astype(np.uint32)

@@ -98,6 +98,9 @@ _sig("he_pack_fc_weights", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _P, _P,
                             _SZ, _P])
 _sig("he_fc", [_P, ctypes.POINTER(FcDesc), _P, _I, _P, _P, _P, _P, _P, _SZ,
                _P])
+_sig("he_residues_pack50", [_P, _SZ, _P, _P])
+_sig("he_residues_unpack50", [_P, _SZ, _P, _P])
+_sig("he_phi1_generate", [_P, ctypes.c_uint64, _SZ, _P, _P])
 _sig("he_ntt_forward", [_P, _P, _I, _P])
 _sig("he_ntt_inverse", [_P, _P, _I, _P])
 
@@ -106,7 +109,8 @@ EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_pack_filters_workspace_bytes", "he_pack_filters",
             "he_conv_workspace_bytes", "he_conv", "he_conv_ex", "he_mask_extract",
             "he_pack_fc_input", "he_fc_wspec_bytes", "he_fc_workspace_bytes",
-            "he_pack_fc_weights", "he_fc", "he_fc_ex", "he_ntt_forward",
+            "he_pack_fc_weights", "he_fc", "he_fc_ex", "he_residues_pack50",
+            "he_residues_unpack50", "he_phi1_generate", "he_ntt_forward",
             "he_ntt_inverse"]
 
 
@@ -301,6 +305,39 @@ class Context:
             _check(_lib.he_fc(*args), "he_fc")
         else:
             _check(_lib.he_fc_ex(*args, _events(events)), "he_fc_ex")
+        return out
+
+    # --------------------------------------------------------- wire format
+    @staticmethod
+    def packed_bytes(n: int) -> int:
+        return n * 50 // 8
+
+    def pack50(self, x: torch.Tensor, out: Optional[torch.Tensor] = None,
+               stream=None) -> torch.Tensor:
+        """Residues (any shape, int64 view of u64 < 2^50) -> uint8 wire bytes."""
+        n = x.numel()
+        if out is None:
+            out = torch.empty(self.packed_bytes(n), dtype=torch.uint8,
+                              device=self.device)
+        self._dev(x, out)
+        _check(_lib.he_residues_pack50(self._ptr(x), n, self._ptr(out),
+                                       _stream(stream)), "he_residues_pack50")
+        return out
+
+    def unpack50(self, packed: torch.Tensor, out: torch.Tensor,
+                 stream=None) -> torch.Tensor:
+        self._dev(packed, out)
+        _check(_lib.he_residues_unpack50(self._ptr(packed), out.numel(),
+                                         self._ptr(out), _stream(stream)),
+               "he_residues_unpack50")
+        return out
+
+    def phi1_generate(self, seed: int, out: torch.Tensor, stream=None):
+        """out (int32 view of uint32) <- SplitMix64(seed, i) mod t."""
+        self._dev(out)
+        _check(_lib.he_phi1_generate(self._h, seed & (2 ** 64 - 1), out.numel(),
+                                     self._ptr(out), _stream(stream)),
+               "he_phi1_generate")
         return out
 
     # ---------------------------------------------------------- transforms

@@ -1292,3 +1292,94 @@ extern "C" he_status he_fc_ex(const he_ctx* c, const he_fc_desc* f, const uint64
     rec(ev, 2, st);
     return HE_OK;
 }
+
+// ============================================================ wire format
+// 50-bit packing, 4096 residues (3200 words) per CTA through shared memory:
+// coalesced word loads/stores, per-element shifts.
+static constexpr int PK_ELEMS = 4096, PK_WORDS = PK_ELEMS * 50 / 64;   // 3200
+static constexpr u64 MASK50 = (1ull << 50) - 1;
+
+__global__ void __launch_bounds__(256)
+k_unpack50(const u64* __restrict__ in, u64* __restrict__ out, size_t n) {
+    __shared__ u64 w[PK_WORDS + 1];
+    const size_t e0 = (size_t)blockIdx.x * PK_ELEMS;
+    const int ne = (int)min((size_t)PK_ELEMS, n - e0);
+    const int nw = ne * 50 / 64;                 // ne multiple of 32 -> exact
+    const u64* src = in + e0 / 64 * 50;
+    for (int i = threadIdx.x; i < nw; i += blockDim.x) w[i] = src[i];
+    if (threadIdx.x == 0) w[nw] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+        const int bit = 50 * i, wi = bit >> 6, sh = bit & 63;
+        u64 v = w[wi] >> sh;
+        if (sh > 14) v |= w[wi + 1] << (64 - sh);
+        out[e0 + i] = v & MASK50;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_pack50(const u64* __restrict__ in, u64* __restrict__ out, size_t n) {
+    __shared__ u64 x[PK_ELEMS + 2];
+    const size_t e0 = (size_t)blockIdx.x * PK_ELEMS;
+    const int ne = (int)min((size_t)PK_ELEMS, n - e0);
+    const int nw = ne * 50 / 64;
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) x[i] = in[e0 + i] & MASK50;
+    if (threadIdx.x < 2) x[ne + threadIdx.x] = 0;
+    __syncthreads();
+    u64* dst = out + e0 / 64 * 50;
+    for (int wi = threadIdx.x; wi < nw; wi += blockDim.x) {
+        const int lo = 64 * wi, i0 = lo / 50;
+        u64 v = 0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const int i = i0 + d, off = 50 * i - lo;      // bit of x_i's LSB in word
+            if (off >= 64) break;
+            v |= off >= 0 ? x[i] << off : x[i] >> (-off);
+        }
+        dst[wi] = v;
+    }
+}
+
+extern "C" he_status he_residues_pack50(const uint64_t* d_in, size_t n, uint8_t* d_packed,
+                                        void* stream) {
+    if (n % 32) return HE_EINVAL;
+    if (n == 0) return HE_OK;
+    if (!d_in || !d_packed || ((uintptr_t)d_packed & 7)) return HE_EINVAL;
+    k_pack50<<<(unsigned)((n + PK_ELEMS - 1) / PK_ELEMS), 256, 0, STREAM(stream)>>>(
+        (const u64*)d_in, (u64*)d_packed, n);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+extern "C" he_status he_residues_unpack50(const uint8_t* d_packed, size_t n, uint64_t* d_out,
+                                          void* stream) {
+    if (n % 32) return HE_EINVAL;
+    if (n == 0) return HE_OK;
+    if (!d_out || !d_packed || ((uintptr_t)d_packed & 7)) return HE_EINVAL;
+    k_unpack50<<<(unsigned)((n + PK_ELEMS - 1) / PK_ELEMS), 256, 0, STREAM(stream)>>>(
+        (const u64*)d_packed, (u64*)d_out, n);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+// ================================================================ phi1
+__global__ void k_phi1(u64 seed, size_t n, u32* __restrict__ out, u64 t) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        u64 z = seed + (i + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        out[i] = (u32)(z % t);
+    }
+}
+
+extern "C" he_status he_phi1_generate(const he_ctx* c, uint64_t seed, size_t n, uint32_t* d_phi1,
+                                      void* stream) {
+    if (!c) return HE_EINVAL;
+    if (n == 0) return HE_OK;
+    if (!d_phi1) return HE_EINVAL;
+    k_phi1<<<grid_for((long)n, 256), 256, 0, STREAM(stream)>>>(seed, n, d_phi1, c->t);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}

@@ -325,3 +325,42 @@ def test_conv_imad_mac_path(he, monkeypatch):
         ring = R.Ring(cfg.N, cfg.primes, cfg.t)
         run_conv(he, ctx, ring, cfg.conv[li], B, seed=cfg.seed + 7 * li,
                  check_b=[0, B - 1])
+
+
+# ------------------------------------------------------------ wire format
+def _pack50_ref(x: np.ndarray) -> np.ndarray:
+    """Bit-level definition of the 50-bit little-endian wire stream."""
+    acc, nbits, out = 0, 0, bytearray()
+    for v in x.tolist():
+        acc |= int(v) << nbits
+        nbits += 50
+        while nbits >= 8:
+            out.append(acc & 0xFF)
+            acc >>= 8
+            nbits -= 8
+    assert nbits == 0
+    return np.frombuffer(bytes(out), dtype=np.uint8)
+
+
+@pytest.mark.parametrize("n", [32, 4096, 4096 + 96, 3 * 4096 + 32])
+def test_pack50_roundtrip_and_layout(he, n):
+    ctx = ctx_for(he, 256, RINGS[256])
+    rng = np.random.default_rng(n)
+    x = rng.integers(0, 2 ** 50, n, dtype=np.uint64)
+    pk = ctx.pack50(dev(x))
+    got = pk.cpu().numpy()
+    assert got.size == n * 50 // 8
+    if n <= 4096 + 96:
+        assert np.array_equal(got, _pack50_ref(x))
+    back = torch.empty(n, dtype=torch.int64, device="cuda")
+    ctx.unpack50(pk, back)
+    assert np.array_equal(u64(back), x)
+
+
+def test_phi1_generate_matches_oracle(he):
+    ctx = ctx_for(he, 256, RINGS[256])
+    for seed, n in [(0, 1000), (2 ** 63 + 7, 65536 + 3)]:
+        out = torch.empty(n, dtype=torch.int32, device="cuda")
+        ctx.phi1_generate(seed, out)
+        assert np.array_equal(out.cpu().numpy().view(np.uint32),
+                              R.phi1_stream(seed, n, 65537))

@@ -121,3 +121,15 @@ def test_encode_decodes_exactly():
         enc = R.encode(m, ring)
         dec = R.crt_decode([enc[j] for j in range(ring.L)], ring)
         assert dec == [int(x) for x in m]
+
+
+def test_splitmix64_phi1_stream():
+    # SplitMix64 reference output for state 0 (Vigna's splitmix64.c): the
+    # first value is 0xe220a8397b1dcdaf; the vectorised stream must match the
+    # Python-int definition element by element.
+    assert R.splitmix64_py(0, 0) == 0xE220A8397B1DCDAF
+    for seed in (0, 1, 2 ** 63 + 12345, 2 ** 64 - 1):
+        v = R.phi1_stream(seed, 257, 65537)
+        assert [int(x) for x in v] == [R.splitmix64_py(seed, i) % 65537
+                                       for i in range(257)]
+        assert v.max() < 65537
