@@ -293,13 +293,12 @@ def main():
     torch.cuda.synchronize()
 
     evals_step = sum(lw.evals for lw in layers) + (B if fc else 0)
-    launches_step = 4 * len(layers) + (2 if fc else 0)
+    launches_step = 3 * len(layers) + (2 if fc else 0)
 
     def step(evs=None):
         for i, lw in enumerate(layers):
             ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], outs[i], ws,
-                     events=None if evs is None else evs[i])
-            ctx.mask_extract(lw.p, outs[i], None, comps[i])
+                     events=None if evs is None else evs[i], compact=comps[i])
         if fc:
             ctx.fc(fc["n_i"], fc["n_o"], fc["c0_d"], fc["wspec"], fc["benc"],
                    fc["ph_d"], fc["out"], fc["ws"],
@@ -339,7 +338,7 @@ def main():
     ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     # stage sums (ms per step, averaged over the timed steps)
     st = {"ntt_fwd": 0.0, "mac_fold": 0.0, "intt_scatter": 0.0,
-          "mask_extract+gaps": 0.0, "fc_ntt_fwd": 0.0, "fc_inv": 0.0}
+          "gaps": 0.0, "fc_ntt_fwd": 0.0, "fc_inv": 0.0}
     for k in range(args.steps):
         E = evs[k]
         for i in range(len(layers)):
@@ -349,7 +348,7 @@ def main():
             st["intt_scatter"] += a[2].elapsed_time(a[3])
             nxt = E[i + 1][0] if i + 1 < len(E) else None
             if nxt is not None:
-                st["mask_extract+gaps"] += a[3].elapsed_time(nxt)
+                st["gaps"] += a[3].elapsed_time(nxt)
         if fc:
             f = E[len(layers)]
             st["fc_ntt_fwd"] += f[0].elapsed_time(f[1])
@@ -479,8 +478,7 @@ def main():
                 stream.wait_event(up_done[i])
                 ctx.unpack50(c0_pk_d[i], c0_d[i])
                 ctx.phi1_generate((mask_seed[0] << 8) + i, phi_d[i])
-                ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], outs[i], ws)
-                ctx.mask_extract(lw.p, outs[i], None, comps[i])
+                ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], outs[i], ws, compact=comps[i])
                 ctx.pack50(comps[i], comp_pk_d[i])
                 comp_done[i].record(stream)
                 with torch.cuda.stream(d2h_s):

@@ -98,7 +98,8 @@ typedef struct {
 /* Host-only, deterministic.  s_override = 0 applies R11; otherwise it must
  * be a power of two with s_override * w_p * h_p <= N (paper-literal layouts
  * use s = c_i).  HE_ESHAPE if the padded image does not fit, if
- * n_ib * s > 4096 (MAC accumulator headroom) or for c_i, c_o, sizes < 1. */
+ * n_ib * s > 4096 (MAC accumulator headroom), for c_i, c_o, sizes < 1 or
+ * for a stride that is not a power of two. */
 he_status he_conv_plan_make(const he_ctx* ctx, const he_conv_desc* d,
                             int s_override, he_conv_plan* out);
 
@@ -143,14 +144,18 @@ he_status he_conv(const he_ctx* ctx, const he_conv_plan* p,
                   const uint32_t* d_phi1, uint64_t* d_out, void* d_ws,
                   size_t ws_bytes, void* stream);
 
-/* he_conv with stage events (measurement): if `events` is non-NULL it
- * holds 4 cudaEvent_t handles, recorded on `stream` before K1 (forward NTT
- * of c0), before K3 (folded MAC), before K4 (inverse NTT + scatter + mask)
- * and after K4.  Results are identical to he_conv. */
+/* he_conv with the payload fused in and stage events.  d_out (full
+ * output, as he_conv) and d_compact (uint64 [B][n_ob][L][n_valid], the
+ * masked valid slots exactly as he_mask_extract would gather them from
+ * d_out) are each nullable, not both.  If `events` is non-NULL it holds 4
+ * cudaEvent_t handles, recorded on `stream` before K1 (forward NTT of c0),
+ * before K3 (folded MAC), before K4 (inverse NTT + scatter + mask) and
+ * after K4 (measurement). */
 he_status he_conv_ex(const he_ctx* ctx, const he_conv_plan* p,
                      const uint64_t* d_c0, int B, const uint64_t* d_fspec,
-                     const uint32_t* d_phi1, uint64_t* d_out, void* d_ws,
-                     size_t ws_bytes, void* stream, void* const* events);
+                     const uint32_t* d_phi1, uint64_t* d_out,
+                     uint64_t* d_compact, void* d_ws, size_t ws_bytes,
+                     void* stream, void* const* events);
 
 /* a7-a8 ("invalid slots ... do not need to be sent").
  * Gathers the n_valid valid slots of each output block, in increasing

@@ -86,7 +86,7 @@ _sig("he_pack_filters", [_P, ctypes.POINTER(ConvPlan), _P, _P, _P, _SZ, _P])
 _sig("he_conv_workspace_bytes", [_P, ctypes.POINTER(ConvPlan), _I], _SZ)
 _sig("he_conv", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _P, _P, _SZ,
                  _P])
-_sig("he_conv_ex", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _P, _P,
+_sig("he_conv_ex", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _P, _P, _P,
                     _SZ, _P, _P])
 _sig("he_fc_ex", [_P, ctypes.POINTER(FcDesc), _P, _I, _P, _P, _P, _P, _P, _SZ,
                   _P, _P])
@@ -221,23 +221,32 @@ class Context:
     def conv(self, p: ConvPlan, c0: torch.Tensor, fspec: torch.Tensor,
              phi1: Optional[torch.Tensor] = None,
              out: Optional[torch.Tensor] = None,
-             ws: Optional[torch.Tensor] = None, stream=None, events=None):
-        """he_conv (he_conv_ex when `events` = 4 torch.cuda.Event with
-        enable_timing, recorded at the K1/K3/K4 stage boundaries)."""
+             ws: Optional[torch.Tensor] = None, stream=None, events=None,
+             compact: Optional[torch.Tensor] = None, full: bool = True):
+        """he_conv; he_conv_ex when `compact` (fused payload) or `events`
+        (4 torch.cuda.Event with enable_timing, recorded at the K1/K3/K4
+        stage boundaries) is given.  full=False skips the full output."""
         B = c0.shape[0]
-        if out is None:
+        if out is None and full:
             out = self.empty_u64(B, p.n_ob, self.L, self.N)
         if ws is None:
             ws = self.conv_workspace(p, B)
-        self._dev(c0, fspec, phi1, out, ws)
-        args = (self._h, ctypes.byref(p), self._ptr(c0), B, self._ptr(fspec),
-                self._ptr(phi1), self._ptr(out), self._ptr(ws),
-                ws.numel() * ws.element_size(), _stream(stream))
-        if events is None:
-            _check(_lib.he_conv(*args), "he_conv")
+        self._dev(c0, fspec, phi1, out, ws, compact)
+        if events is None and compact is None:
+            _check(_lib.he_conv(self._h, ctypes.byref(p), self._ptr(c0), B,
+                                self._ptr(fspec), self._ptr(phi1),
+                                self._ptr(out), self._ptr(ws),
+                                ws.numel() * ws.element_size(),
+                                _stream(stream)), "he_conv")
         else:
-            _check(_lib.he_conv_ex(*args, _events(events)), "he_conv_ex")
-        return out
+            _check(_lib.he_conv_ex(self._h, ctypes.byref(p), self._ptr(c0), B,
+                                   self._ptr(fspec), self._ptr(phi1),
+                                   self._ptr(out), self._ptr(compact),
+                                   self._ptr(ws),
+                                   ws.numel() * ws.element_size(),
+                                   _stream(stream), _events(events)),
+                   "he_conv_ex")
+        return out if full else compact
 
     def mask_extract(self, p: ConvPlan, out_full: torch.Tensor,
                      phi1: Optional[torch.Tensor] = None,

@@ -87,6 +87,7 @@ extern "C" void he_ctx_destroy(he_ctx* c) {
     cudaFree(c->d_limb);
     cudaFree(c->d_tw_fwd);
     cudaFree(c->d_tw_inv);
+    cudaFree(c->d_enc);
     cudaSetDevice(prev);
     free(c->q_host);
     free(c->psi_host);
@@ -179,6 +180,20 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
                          cudaMemcpyHostToDevice) == cudaSuccess &&
               cudaMemcpy(c->d_tw_inv, inv.data(), sizeof(ulonglong2) * L * N,
                          cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok && r->t <= (1u << 20)) {
+        // enc_j(m) = (Delta_t mod q_j) m + floor((r_t m + floor(t/2)) / t) mod q_j
+        const u64 t = r->t;
+        std::vector<u64> tab((size_t)L * t);
+        for (uint32_t j = 0; j < L; ++j) {
+            const u64 q = c->q_host[j], d = c->limb_host[j].delta;
+            for (u64 m = 0; m < t; ++m)
+                tab[(size_t)j * t + m] =
+                    (u64)(((u128)d * m + ((u128)rt * m + t / 2) / t) % q);
+        }
+        ok = cudaMalloc(&c->d_enc, sizeof(u64) * tab.size()) == cudaSuccess &&
+             cudaMemcpy(c->d_enc, tab.data(), sizeof(u64) * tab.size(),
+                        cudaMemcpyHostToDevice) == cudaSuccess;
+    }
     cudaSetDevice(prev);
     if (!ok) { cudaGetLastError(); he_ctx_destroy(c); return HE_ECUDA; }
     *out = c;
@@ -193,7 +208,8 @@ extern "C" he_status he_conv_plan_make(const he_ctx* c, const he_conv_desc* d,
                                        int s_override, he_conv_plan* out) {
     if (!c || !d || !out) return HE_EINVAL;
     if (d->c_i < 1 || d->c_o < 1 || d->w_i < 1 || d->h_i < 1 || d->f_w < 1 ||
-        d->f_h < 1 || d->stride < 1 || (d->pad != 0 && d->pad != 1))
+        d->f_h < 1 || d->stride < 1 || (d->stride & (d->stride - 1)) ||
+        (d->pad != 0 && d->pad != 1))
         return HE_ESHAPE;
     const long N = c->N;
     const int padw = d->pad ? (d->f_w - 1) / 2 : 0;

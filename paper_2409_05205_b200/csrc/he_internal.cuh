@@ -41,7 +41,12 @@ struct he_ctx {
     he_limb* d_limb;        // [L]
     ulonglong2* d_tw_fwd;   // [L][N]  {psi^{brv(k)}, Shoup}
     ulonglong2* d_tw_inv;   // [L][N]  {psi^{-brv(k)}, Shoup}
+    u64* d_enc;             // [L][t] enc_j(m) table (t <= 2^20), else nullptr
 };
+
+// enc_j(m) via the context table when present (one L2-resident load).
+__device__ __forceinline__ u64 enc_lookup(const u64* __restrict__ tab, int l, u64 t, u64 m,
+                                          const struct he_limb& L, u64 r_t, u64 t_inv);
 
 // ------------------------------------------------------------ arithmetic
 // x * w mod q in [0, 2q) for any x < 2^64 (Shoup): wp = floor(w 2^64 / q).
@@ -91,6 +96,11 @@ __device__ __forceinline__ void madw(u64& acc, u32 a, u32 b) {
     asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
 }
 
+__device__ __forceinline__ u64 enc_lookup(const u64* __restrict__ tab, int l, u64 t, u64 m,
+                                          const he_limb& L, u64 r_t, u64 t_inv) {
+    return tab ? __ldg(&tab[(size_t)l * t + m]) : enc_plain(m, L, t, r_t, t_inv);
+}
+
 __device__ __forceinline__ u64 addmod(u64 a, u64 b, u64 q) {
     return csub(a + b, q);
 }
@@ -134,19 +144,24 @@ __device__ __forceinline__ void ct_pass(u64* sm, int logN, int NS, int st0,
     for (int g = threadIdx.x; g < ngroups; g += blockDim.x) {
         const int blk = g >> ltk, off = g & (tk - 1);
         const int base = (blk << (lt0 + 1)) + off;
+        // all 2^K - 1 twiddles of the group first (independent loads in flight)
+        ulonglong2 tws[(1 << K) - 1];
+#pragma unroll
+        for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
+            const int twb = (1 << (st0 + r)) + (seg << (st0 + r - split)) + (blk << r);
+#pragma unroll
+            for (int z = 0; z < (1 << r); ++z) tws[o + z] = __ldg(&tw[twb + z]);
+        }
         u64 x[1 << K];
 #pragma unroll
         for (int c = 0; c < (1 << K); ++c) x[c] = sm[PAD(base + (c << ltk))];
 #pragma unroll
-        for (int r = 0; r < K; ++r) {
+        for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
             const int half = 1 << (K - 1 - r);
-            const int twb = (1 << (st0 + r)) + (seg << (st0 + r - split)) +
-                            (blk << r);
 #pragma unroll
             for (int c = 0; c < (1 << K); ++c) {
                 if (c & half) continue;
-                const ulonglong2 w = __ldg(&tw[twb + (c >> (K - r))]);
-                ct_bfly(x[c], x[c + half], w, q, q2);
+                ct_bfly(x[c], x[c + half], tws[o + (c >> (K - r))], q, q2);
             }
         }
 #pragma unroll
@@ -175,21 +190,26 @@ __device__ __forceinline__ void gs_pass(u64* sm, int arr_stride, int narr,
         u64* s = sm + a * arr_stride;
         const int blk = g >> lt0, off = g & (tk - 1);
         const int base = (blk << (lt0 + K)) + off;
+        // all 2^K - 1 twiddles of the group first (independent loads in flight)
+        ulonglong2 tws[(1 << K) - 1];
+#pragma unroll
+        for (int v = 0, o = 0; v < K; o += (1 << (K - 1 - v)), ++v) {
+            const int lt = lt0 + v;                       // log2 t
+            const int tb = (1 << (logMfull - lt - 1)) + (seg << (logM - lt - 1)) +
+                           (blk << (K - 1 - v));
+#pragma unroll
+            for (int z = 0; z < (1 << (K - 1 - v)); ++z) tws[o + z] = __ldg(&tw[tb + z]);
+        }
         u64 x[1 << K];
 #pragma unroll
         for (int c = 0; c < (1 << K); ++c) x[c] = s[PAD(base + (c << lt0))];
 #pragma unroll
-        for (int v = 0; v < K; ++v) {
+        for (int v = 0, o = 0; v < K; o += (1 << (K - 1 - v)), ++v) {
             const int half = 1 << v;
-            const int lt = lt0 + v;                       // log2 t
-            const int hh = 1 << (logMfull - lt - 1);      // full-size h
-            const int segoff = seg << (logM - lt - 1);
 #pragma unroll
             for (int c = 0; c < (1 << K); ++c) {
                 if (c & half) continue;
-                const int ib = (blk << (K - 1 - v)) + (c >> (v + 1));
-                const ulonglong2 w = __ldg(&tw[hh + segoff + ib]);
-                gs_bfly(x[c], x[c + half], w, q, q2);
+                gs_bfly(x[c], x[c + half], tws[o + (c >> (v + 1))], q, q2);
             }
         }
 #pragma unroll

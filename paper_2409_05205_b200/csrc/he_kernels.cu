@@ -948,9 +948,10 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
 // Channel arrays sit in shared memory at an odd word stride (conflict-free).
 __global__ void __launch_bounds__(256, 3)
 k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
-               u64* __restrict__ out, PlanDev P, int B, int L, int logN, int cc,
-               int nchunk, int stride, const he_limb* __restrict__ limbs,
-               const ulonglong2* __restrict__ twi_all, u64 t, u64 r_t, u64 t_inv) {
+               u64* __restrict__ out, u64* __restrict__ comp, PlanDev P, int B, int L,
+               int logN, int cc, int nchunk, int stride, const he_limb* __restrict__ limbs,
+               const ulonglong2* __restrict__ twi_all, const u64* __restrict__ enc_tab, u64 t,
+               u64 r_t, u64 t_inv) {
     extern __shared__ u64 sm[];
     const int N = 1 << logN, M = N >> P.logs, logM = logN - P.logs;
     int r = blockIdx.x;
@@ -965,10 +966,19 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     const int ch0 = ch * cc, ncc = min(cc, P.c_ob - ch0);
     // fold layout [l][b][n][g]: the chunk's channel rows are contiguous in g
     const u64* fb = fold + (((size_t)l * B + b) * P.c_o + ob * P.c_ob + ch0) * M;
-    for (int idx = threadIdx.x; idx < ncc * M; idx += blockDim.x) {
-        const int a = idx >> logM, g = idx & (M - 1);
-        const int n = ob * P.c_ob + ch0 + a;
-        sm[a * stride + PAD(g)] = n < P.c_o ? fb[idx] : 0;
+    const int tot = ncc * M, nvalid_a = min(ncc, P.c_o - (ob * P.c_ob + ch0));
+    for (int base = 0; base < tot; base += 8 * blockDim.x) {       // 8 loads in flight
+        u64 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int idx = base + e * blockDim.x + threadIdx.x;
+            v[e] = (idx < tot && (idx >> logM) < nvalid_a) ? fb[idx] : 0;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int idx = base + e * blockDim.x + threadIdx.x;
+            if (idx < tot) sm[(idx >> logM) * stride + PAD(idx & (M - 1))] = v[e];
+        }
     }
     __syncthreads();
     gs_all<3>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
@@ -976,28 +986,63 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     const int u1 = (ch == nchunk - 1) ? P.s : (ch0 + ncc) * P.step;
     const int w = u1 - u0;
     const u32* ph = phi1 ? phi1 + ((size_t)b * P.n_ob + ob) * N : nullptr;
-    u64* orow = out + (((size_t)b * P.n_ob + ob) * L + l) * N;
+    u64* orow = out ? out + (((size_t)b * P.n_ob + ob) * L + l) * N : nullptr;
+    u64* crow = comp ? comp + (((size_t)b * P.n_ob + ob) * L + l) * P.n_valid : nullptr;
+    const float inv_hp = 1.0f / (float)P.h_p;
+    int lstr = 0;                         // stride is a power of two (checked on host)
+    while ((1 << lstr) < P.stride) ++lstr;
     int lw = 0, ls = 0;                   // log2 w, log2 step (if powers of 2)
     while ((1 << lw) < w) ++lw;
     while ((1 << ls) < P.step) ++ls;
     const bool pow2 = (1 << lw) == w && (1 << ls) == P.step;
-    for (int idx = threadIdx.x; idx < M * w; idx += blockDim.x) {
-        int j, u, nl;
-        if (pow2) {
-            j = idx >> lw;
-            u = u0 + (idx & (w - 1));
-            nl = u >> ls;
-        } else {
-            j = idx / w;
-            u = u0 + (idx - j * w);
-            nl = u / P.step;
+    constexpr int EB = 4;                 // outputs per thread per batch
+    for (int base = 0; base < M * w; base += EB * blockDim.x) {
+        int ii[EB], vi[EB], sidx[EB];
+        bool go[EB];
+        u32 m[EB];
+#pragma unroll
+        for (int e = 0; e < EB; ++e) {
+            const int idx = base + e * blockDim.x + threadIdx.x;
+            int j, u, nl;
+            if (pow2) {
+                j = idx >> lw;
+                u = u0 + (idx & (w - 1));
+                nl = u >> ls;
+            } else {
+                j = idx / w;
+                u = u0 + (idx - j * w);
+                nl = u / P.step;
+            }
+            ii[e] = (j << P.logs) + u;
+            const bool owned = u == nl * P.step && nl < ch0 + ncc;
+            sidx[e] = owned ? (nl - ch0) * stride + PAD(j) : -1;
+            // valid slot (a8): j = stride*(K h_p + L), K < w_o, L < h_o
+            int vidx = -1;
+            if (crow && owned) {
+                int kr = (int)((float)j * inv_hp);
+                if (kr * P.h_p > j) --kr;
+                if ((kr + 1) * P.h_p <= j) ++kr;
+                const int lc = j - kr * P.h_p;
+                const int K_ = kr >> lstr, L_ = lc >> lstr;
+                if (((kr | lc) & (P.stride - 1)) == 0 && K_ < P.w_o && L_ < P.h_o)
+                    vidx = (K_ * P.h_o + L_) * P.c_ob + nl;
+            }
+            vi[e] = vidx;
+            go[e] = idx < M * w && (orow || vidx >= 0);
+            m[e] = (ph && go[e]) ? ph[ii[e]] : 0u;
         }
-        const int i = (j << P.logs) + u;
-        u64 v = 0;
-        if (u == nl * P.step && nl < ch0 + ncc)
-            v = csub(sm[(nl - ch0) * stride + PAD(j)], q);
-        if (ph) v = addmod(v, enc_plain(ph[i], Lm, t, r_t, t_inv), q);
-        orow[i] = v;
+        u64 en[EB];
+#pragma unroll
+        for (int e = 0; e < EB; ++e)
+            en[e] = (ph && go[e]) ? enc_lookup(enc_tab, l, t, m[e], Lm, r_t, t_inv) : 0;
+#pragma unroll
+        for (int e = 0; e < EB; ++e) {
+            if (!go[e]) continue;
+            u64 v = sidx[e] >= 0 ? csub(sm[sidx[e]], q) : 0;
+            v = addmod(v, en[e], q);
+            if (orow) orow[ii[e]] = v;
+            if (vi[e] >= 0) crow[vi[e]] = v;
+        }
     }
 }
 
@@ -1024,17 +1069,19 @@ static inline void rec(void* const* ev, int i, cudaStream_t st) {
 extern "C" he_status he_conv(const he_ctx* c, const he_conv_plan* p, const uint64_t* d_c0,
                              int B, const uint64_t* d_fspec, const uint32_t* d_phi1,
                              uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream) {
-    return he_conv_ex(c, p, d_c0, B, d_fspec, d_phi1, d_out, d_ws, ws_bytes, stream, nullptr);
+    if (!d_out && B > 0) return HE_EINVAL;
+    return he_conv_ex(c, p, d_c0, B, d_fspec, d_phi1, d_out, nullptr, d_ws, ws_bytes, stream,
+                      nullptr);
 }
 
 extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const uint64_t* d_c0,
                                 int B, const uint64_t* d_fspec, const uint32_t* d_phi1,
-                                uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream,
-                                void* const* ev) {
+                                uint64_t* d_out, uint64_t* d_compact, void* d_ws,
+                                size_t ws_bytes, void* stream, void* const* ev) {
     if (!c || !p || B < 0) return HE_EINVAL;
     if (!plan_ok(c, p)) return HE_ESHAPE;
     if (B == 0) return HE_OK;
-    if (!d_c0 || !d_fspec || !d_out || !d_ws) return HE_EINVAL;
+    if (!d_c0 || !d_fspec || (!d_out && !d_compact) || !d_ws) return HE_EINVAL;
     if (ws_bytes < he_conv_workspace_bytes(c, p, B)) return HE_ENOMEM;
     cudaStream_t st = STREAM(stream);
     const PlanDev P = plan_dev(p);
@@ -1069,8 +1116,8 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     if (!set_smem(k_intt_scatter, smem)) return HE_ECUDA;
     rec(ev, 2, st);
     k_intt_scatter<<<(unsigned)(B * P.n_ob * c->L * nchunk), 256, smem, st>>>(
-        fold, d_phi1, (u64*)d_out, P, B, c->L, c->logN, cc, nchunk, stride, c->d_limb,
-        c->d_tw_inv, c->t, c->r_t, c->t_inv);
+        fold, d_phi1, (u64*)d_out, (u64*)d_compact, P, B, c->L, c->logN, cc, nchunk, stride,
+        c->d_limb, c->d_tw_inv, c->d_enc, c->t, c->r_t, c->t_inv);
     HE_CHECK_LAUNCH();
     rec(ev, 3, st);
     return HE_OK;

@@ -126,15 +126,25 @@ def run_conv(he, ctx, ring, Ly, B, seed, mask=True, s_override=0,
     c0 = synth.uniform_residues((B, p.n_ib, ring.L, N), ring.primes, seed)
     phi = synth.phi1((B, p.n_ob, N), ring.t, seed) if mask else None
     fspec = ctx.pack_filters(p, dev(W))
-    out = ctx.conv(p, dev(c0), fspec, dev(phi) if mask else None)
+    d_c0, d_phi = dev(c0), (dev(phi) if mask else None)
+    out = ctx.conv(p, d_c0, fspec, d_phi)
     comp = ctx.mask_extract(p, out)
+    # fused payload (he_conv_ex): full + compact, and compact only
+    comp2 = ctx.empty_u64(B, p.n_ob, ring.L, p.n_valid)
+    out2 = ctx.conv(p, d_c0, fspec, d_phi, compact=comp2)
+    comp3 = ctx.empty_u64(B, p.n_ob, ring.L, p.n_valid)
+    ctx.conv(p, d_c0, fspec, d_phi, compact=comp3, full=False)
     torch.cuda.synchronize()
     g_out, g_comp = u64(out), u64(comp)
     bs = list(range(B)) if check_b is None else check_b
     ref = R.conv_server(c0[bs], W, plan_o, ring,
                         phi[bs] if mask else None)
+    ref_c = R.compact(ref, plan_o)
     assert np.array_equal(g_out[bs], ref)
-    assert np.array_equal(g_comp[bs], R.compact(ref, plan_o))
+    assert np.array_equal(g_comp[bs], ref_c)
+    assert np.array_equal(u64(out2)[bs], ref)
+    assert np.array_equal(u64(comp2)[bs], ref_c)
+    assert np.array_equal(u64(comp3)[bs], ref_c)
     return p
 
 
