@@ -66,6 +66,32 @@ __device__ __forceinline__ void ct_bfly(u64& X, u64& Y, ulonglong2 w, u64 q,
     Y = x - t + q2;
 }
 
+// Lazy Cooley-Tukey butterfly without the conditional subtraction: with
+// inputs < a q the outputs are < (a + 2) q (T = Shoup(Y) < 2q for any
+// 64-bit Y).  15 stages keep every value below 31 q < 2^55.
+__device__ __forceinline__ void ct_bfly_lazy(u64& X, u64& Y, ulonglong2 w, u64 q, u64 q2) {
+    const u64 x = X;
+    const u64 t = shoup_mul(Y, w.x, w.y, q);
+    X = x + t;
+    Y = x - t + q2;
+}
+
+// Lazy Gentleman-Sande butterfly for stage `lt` (t = 2^lt) of a transform
+// whose inputs are < 2q: inputs of stage lt are < 2^(lt+1) q, so
+// X - Y + 2^(lt+1) q >= 0; X' = X + Y grows, Y' = Shoup(.) < 2q.  Valid while
+// 2^(stages+1) q < 2^64 (<= 12 stages for q < 2^50).
+__device__ __forceinline__ void gs_bfly_lazy(u64& X, u64& Y, ulonglong2 w, u64 q, u64 off) {
+    const u64 x = X, y = Y;
+    X = x + y;
+    Y = shoup_mul(x - y + off, w.x, w.y, q);
+}
+
+// Full reduction of a lazy value v < 2^64 to [0, q).
+__device__ __forceinline__ u64 reduce_full(u64 v, u64 q, u64 one_p) {
+    const u64 r = v - __umul64hi(v, one_p) * q;     // [0, 2q)
+    return csub(r, q);
+}
+
 // Gentleman-Sande butterfly, inputs/outputs in [0, 2q).
 __device__ __forceinline__ void gs_bfly(u64& X, u64& Y, ulonglong2 w, u64 q,
                                         u64 q2) {
@@ -132,7 +158,7 @@ __host__ __device__ constexpr int padded_words(int n) { return n + (n >> 4); }
 // memory.  Stages st0 .. st0+K-1 (stage st has m = 2^st blocks, stride
 // t = N >> (st+1)).  `seg` / `split`: this CTA holds words
 // [seg*NS, (seg+1)*NS) of the transform (N = NS << split).
-template <int K>
+template <int K, bool LAZY = false>
 __device__ __forceinline__ void ct_pass(u64* sm, int logN, int NS, int st0,
                                         int seg, int split,
                                         const ulonglong2* __restrict__ tw,
@@ -161,7 +187,8 @@ __device__ __forceinline__ void ct_pass(u64* sm, int logN, int NS, int st0,
 #pragma unroll
             for (int c = 0; c < (1 << K); ++c) {
                 if (c & half) continue;
-                ct_bfly(x[c], x[c + half], tws[o + (c >> (K - r))], q, q2);
+                if (LAZY) ct_bfly_lazy(x[c], x[c + half], tws[o + (c >> (K - r))], q, q2);
+                else ct_bfly(x[c], x[c + half], tws[o + (c >> (K - r))], q, q2);
             }
         }
 #pragma unroll
@@ -176,7 +203,7 @@ __device__ __forceinline__ void ct_pass(u64* sm, int logN, int NS, int st0,
 // table serves every M = N/s: brv_N(k) = s brv_M(k) for k < M).  `seg`:
 // offset of this segment's blocks when the M-point transform is one of
 // 2^split segments of a larger transform (logMS = log2 of the full size).
-template <int K>
+template <int K, bool LAZY = false>
 __device__ __forceinline__ void gs_pass(u64* sm, int arr_stride, int narr,
                                         int logM, int lt0, int seg,
                                         int logMfull,
@@ -209,7 +236,9 @@ __device__ __forceinline__ void gs_pass(u64* sm, int arr_stride, int narr,
 #pragma unroll
             for (int c = 0; c < (1 << K); ++c) {
                 if (c & half) continue;
-                gs_bfly(x[c], x[c + half], tws[o + (c >> (v + 1))], q, q2);
+                if (LAZY) gs_bfly_lazy(x[c], x[c + half], tws[o + (c >> (v + 1))], q,
+                                       q << (lt0 + v + 1));
+                else gs_bfly(x[c], x[c + half], tws[o + (c >> (v + 1))], q, q2);
             }
         }
 #pragma unroll
@@ -219,40 +248,40 @@ __device__ __forceinline__ void gs_pass(u64* sm, int arr_stride, int narr,
 
 // Full forward pass schedule on a segment: stages split .. logN-1 in passes
 // of up to RMAX stages (the remainder first).
-template <int RMAX>
+template <int RMAX, bool LAZY = false>
 __device__ __forceinline__ void ct_all(u64* sm, int logN, int NS, int seg,
                                        int split, const ulonglong2* tw, u64 q,
                                        u64 q2) {
     int st = split;
     const int rem = (logN - split) % RMAX;
     if (rem) {
-        if (rem == 1) ct_pass<1>(sm, logN, NS, st, seg, split, tw, q, q2);
-        else if (rem == 2) ct_pass<2>(sm, logN, NS, st, seg, split, tw, q, q2);
-        else ct_pass<3>(sm, logN, NS, st, seg, split, tw, q, q2);
+        if (rem == 1) ct_pass<1, LAZY>(sm, logN, NS, st, seg, split, tw, q, q2);
+        else if (rem == 2) ct_pass<2, LAZY>(sm, logN, NS, st, seg, split, tw, q, q2);
+        else ct_pass<3, LAZY>(sm, logN, NS, st, seg, split, tw, q, q2);
         st += rem;
         __syncthreads();
     }
     for (; st < logN; st += RMAX) {
-        ct_pass<RMAX>(sm, logN, NS, st, seg, split, tw, q, q2);
+        ct_pass<RMAX, LAZY>(sm, logN, NS, st, seg, split, tw, q, q2);
         __syncthreads();
     }
 }
 
 // Full inverse schedule on narr M-point arrays: strides 1 .. M/2.
-template <int RMAX>
+template <int RMAX, bool LAZY = false>
 __device__ __forceinline__ void gs_all(u64* sm, int arr_stride, int narr,
                                        int logM, int seg, int logMfull,
                                        const ulonglong2* tw, u64 q, u64 q2) {
     int lt = 0;
     const int rem = logM % RMAX;
     for (; lt + RMAX <= logM; lt += RMAX) {
-        gs_pass<RMAX>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
+        gs_pass<RMAX, LAZY>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
         __syncthreads();
     }
     if (rem) {
-        if (rem == 1) gs_pass<1>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
-        else if (rem == 2) gs_pass<2>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
-        else gs_pass<3>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
+        if (rem == 1) gs_pass<1, LAZY>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
+        else if (rem == 2) gs_pass<2, LAZY>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
+        else gs_pass<3, LAZY>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, q2);
         __syncthreads();
     }
 }

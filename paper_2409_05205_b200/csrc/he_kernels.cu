@@ -103,7 +103,8 @@ __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int log
     }
     if (S) cg::this_cluster().sync();
     else __syncthreads();
-    ct_all<3>(sm, logN, NS, seg, S, tw, q, q2);
+    ct_all<3, true>(sm, logN, NS, seg, S, tw, q, q2);      // lazy: values < 31 q
+    const u64 one_p = limbs[l].one_p;
     if (OUT_FMT == 2) {
         unsigned char* A = reinterpret_cast<unsigned char*>(out);
         const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
@@ -111,7 +112,7 @@ __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int log
         for (int i = 4 * threadIdx.x; i < NS; i += 4 * blockDim.x) {
             u64 x[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) x[e] = csub(csub(sm[PAD(i + e)], q2), q);
+            for (int e = 0; e < 4; ++e) x[e] = reduce_full(sm[PAD(i + e)], q, one_p);
             u32 pl[8];
             byte_transpose4((u32)x[0], (u32)x[1], (u32)x[2], (u32)x[3], pl[0], pl[1], pl[2],
                             pl[3]);
@@ -137,7 +138,7 @@ __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int log
     }
     u64* dst = out + (size_t)li * N + (size_t)seg * NS;
     for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
-        u64 x = csub(csub(sm[PAD(i)], q2), q), y = csub(csub(sm[PAD(i + 1)], q2), q);
+        u64 x = reduce_full(sm[PAD(i)], q, one_p), y = reduce_full(sm[PAD(i + 1)], q, one_p);
         if (OUT_FMT == 1) { x = to_split25(x); y = to_split25(y); }
         *reinterpret_cast<ulonglong2*>(dst + i) = make_ulonglong2(x, y);
     }
@@ -981,7 +982,8 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         }
     }
     __syncthreads();
-    gs_all<3>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
+    if (logM <= 12) gs_all<3, true>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
+    else gs_all<3>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
     const int u0 = ch0 * P.step;
     const int u1 = (ch == nchunk - 1) ? P.s : (ch0 + ncc) * P.step;
     const int w = u1 - u0;
@@ -1038,7 +1040,7 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
 #pragma unroll
         for (int e = 0; e < EB; ++e) {
             if (!go[e]) continue;
-            u64 v = sidx[e] >= 0 ? csub(sm[sidx[e]], q) : 0;
+            u64 v = sidx[e] >= 0 ? reduce_full(sm[sidx[e]], q, Lm.one_p) : 0;
             v = addmod(v, en[e], q);
             if (orow) orow[ii[e]] = v;
             if (vi[e] >= 0) crow[vi[e]] = v;
