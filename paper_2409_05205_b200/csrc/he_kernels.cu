@@ -723,21 +723,25 @@ __device__ __forceinline__ void mma_k16(int (&d)[4], u32 a0, u32 a1, u32 b0) {
         : "r"(a0), "r"(a1), "r"(b0));
 }
 
-// V = sum_d S_d 2^{8d} mod q = lo + mid 2^40 + top 2^80 (mod q).
+// V = sum_{d<13} S_d 2^{8d} mod q, S_d < 2^31.  Exact 128-bit assembly from
+// 32-bit-aligned partial sums P_k = sum_{d = 4k..4k+3} S_d 2^{8(d-4k)}
+// (< 2^57, three mad.wide each): V = P0 + P1 2^32 + P2 2^64 + P3 2^96 =
+// lo + hi 2^64, then V mod q = lo + hi (2^64 mod q) with two Shoup products.
 __device__ __forceinline__ u64 reduce13(const int (&acc)[13][4], int e, const he_limb& Lm) {
-    u64 lo = 0, mid = 0, top = 0;
+    u64 P[4];
 #pragma unroll
-    for (int d = 0; d < 5; ++d) lo += (u64)(u32)acc[d][e] << (8 * d);
-#pragma unroll
-    for (int d = 5; d < 10; ++d) mid += (u64)(u32)acc[d][e] << (8 * (d - 5));
-#pragma unroll
-    for (int d = 10; d < 13; ++d) top += (u64)(u32)acc[d][e] << (8 * (d - 10));
+    for (int k = 0; k < 3; ++k) {
+        P[k] = (u64)(u32)acc[4 * k][e];
+        madw(P[k], (u32)acc[4 * k + 1][e], 1u << 8);
+        madw(P[k], (u32)acc[4 * k + 2][e], 1u << 16);
+        madw(P[k], (u32)acc[4 * k + 3][e], 1u << 24);
+    }
+    P[3] = (u64)(u32)acc[12][e];
+    const u64 lo = P[0] + (P[1] << 32);
+    const u64 hi = P[2] + (P[1] >> 32) + (P[3] << 32) + (lo < P[0] ? 1 : 0);
     const u64 q = Lm.q;
-    u64 r = shoup_mul(lo, 1, Lm.one_p, q) + shoup_mul(mid, Lm.r40, Lm.r40_p, q) +
-            shoup_mul(top, Lm.r80, Lm.r80_p, q);                 // < 6q
-    r = csub(r, 4 * q);
-    r = csub(r, 2 * q);
-    return csub(r, q);
+    const u64 r = shoup_mul(lo, 1, Lm.one_p, q) + shoup_mul(hi, Lm.r64, Lm.r64_p, q);  // < 4q
+    return csub(csub(r, 2 * q), q);
 }
 
 // x / d for 0 <= x < 2^31 with d fixed per kernel: a shift when d is a power

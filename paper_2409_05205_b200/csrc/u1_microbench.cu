@@ -87,8 +87,10 @@ __global__ void u1_bfly(const u64* in, u32* out, int iters, long long* cyc) {
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            if (GS) gs_bfly(X[i], Y[i], w, q, q2);
-            else ct_bfly(X[i], Y[i], w, q, q2);
+            // the lazy forms the kernels use (ct: no conditional subtraction;
+            // gs: offset q << (stage + 1), here a fixed 2^12 q)
+            if (GS) gs_bfly_lazy(X[i], Y[i], w, q, q << 12);
+            else ct_bfly_lazy(X[i], Y[i], w, q, q2);
         }
     }
     long long c1 = clock64();
