@@ -233,6 +233,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, cfg, rank)
+    if args.profile:
+        args.streams = 1            # profiling runs: one launch sequence per layer
 
     import torch
     import torch.distributed as dist
