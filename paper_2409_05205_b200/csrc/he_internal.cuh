@@ -66,24 +66,36 @@ __device__ __forceinline__ void ct_bfly(u64& X, u64& Y, ulonglong2 w, u64 q,
     Y = x - t + q2;
 }
 
+// Shoup product with an approximate quotient: Q' = x1 w1 + hi(x1 w0) +
+// hi(x0 w1) (32-bit halves; the x0 w0 term and the carries are dropped), so
+// Q - 2 <= Q' <= Q and the result x w - Q' q lies in [0, 4q) for any x < 2^64.
+__device__ __forceinline__ u64 shoup_mul4(u64 x, u64 w, u64 wp, u64 q) {
+    const u32 x0 = (u32)x, x1 = (u32)(x >> 32);
+    const u32 p0 = (u32)wp, p1 = (u32)(wp >> 32);
+    u64 qh = (u64)__umulhi(x0, p1) + __umulhi(x1, p0);
+    asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(qh) : "r"(x1), "r"(p1));
+    return x * w - qh * q;
+}
+
 // Lazy Cooley-Tukey butterfly without the conditional subtraction: with
-// inputs < a q the outputs are < (a + 2) q (T = Shoup(Y) < 2q for any
-// 64-bit Y).  15 stages keep every value below 31 q < 2^55.
+// inputs < a q the outputs are < (a + 4) q (T = Shoup4(Y) < 4q for any
+// 64-bit Y).  15 stages keep every value below 61 q < 2^56.
 __device__ __forceinline__ void ct_bfly_lazy(u64& X, u64& Y, ulonglong2 w, u64 q, u64 q2) {
     const u64 x = X;
-    const u64 t = shoup_mul(Y, w.x, w.y, q);
+    const u64 t = shoup_mul4(Y, w.x, w.y, q);
     X = x + t;
-    Y = x - t + q2;
+    Y = x - t + 2 * q2;
 }
 
 // Lazy Gentleman-Sande butterfly for stage `lt` (t = 2^lt) of a transform
-// whose inputs are < 2q: inputs of stage lt are < 2^(lt+1) q, so
-// X - Y + 2^(lt+1) q >= 0; X' = X + Y grows, Y' = Shoup(.) < 2q.  Valid while
-// 2^(stages+1) q < 2^64 (<= 12 stages for q < 2^50).
+// whose inputs are < 2q: inputs of stage lt are < 2^(lt+1) q (X' = X + Y
+// doubles the bound, Y' = Shoup4(.) < 4q <= 2^(lt+2) q), so
+// X - Y + 2^(lt+1) q >= 0.  Valid while 2^(stages+1) q < 2^64 (<= 12
+// stages for q < 2^50).
 __device__ __forceinline__ void gs_bfly_lazy(u64& X, u64& Y, ulonglong2 w, u64 q, u64 off) {
     const u64 x = X, y = Y;
     X = x + y;
-    Y = shoup_mul(x - y + off, w.x, w.y, q);
+    Y = shoup_mul4(x - y + off, w.x, w.y, q);      // < 4q <= offset of the next stage
 }
 
 // Full reduction of a lazy value v < 2^64 to [0, q).
