@@ -102,8 +102,9 @@ def u1_peaks(device_index=0):
     lib.u1_run.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p] * 3
     out = {}
     names = ["imad", "imad_wide", "modmac", "ct_bfly", "gs_bfly", "imma_u8",
-             "dfma"]
-    iters = {0: 20000, 1: 20000, 2: 20000, 3: 2000, 4: 2000, 5: 2000, 6: 20000}
+             "dfma", "dp_ct_bfly"]
+    iters = {0: 20000, 1: 20000, 2: 20000, 3: 2000, 4: 2000, 5: 2000, 6: 20000,
+             7: 2000}
     for w, name in enumerate(names):
         ms, cyc, ops = ctypes.c_float(), ctypes.c_longlong(), ctypes.c_double()
         rc = lib.u1_run(w, 148 * 8, 256, iters[w], ctypes.byref(ms),

@@ -145,6 +145,46 @@ __global__ void u1_dfma(const u32* in, u32* out, int iters, long long* cyc) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
 }
 
+// which 7: exact FP64 Cooley-Tukey butterfly on signed residues (|x| < 2^51):
+// reduce the multiplicand, T = Y w mod q via an exact two-product and a
+// magic-number rounded quotient (|T| < 0.9 q), X' = X + T, Y' = X - T.
+__device__ __forceinline__ double dp_reduce(double y, double q, double qinv) {
+    const double M = 6755399441055744.0;                // 1.5 * 2^52
+    const double k = fma(y, qinv, M) - M;
+    return fma(-k, q, y);                               // |.| <= q/2 + small
+}
+__device__ __forceinline__ void dp_bfly(double& X, double& Y, double w, double q, double qinv) {
+    const double M = 6755399441055744.0;
+    const double y = dp_reduce(Y, q, qinv);
+    const double p = y * w;
+    const double e = fma(y, w, -p);
+    const double k = fma(p, qinv, M) - M;
+    const double t = fma(-k, q, p) + e;
+    const double x = X;
+    X = x + t;
+    Y = x - t;
+}
+__global__ void u1_dbfly(const u64* in, u32* out, int iters, long long* cyc) {
+    const double q = (double)in[0], w = (double)in[1], qinv = 1.0 / q;
+    double X[8], Y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { X[i] = (double)((threadIdx.x + i) % in[0]); Y[i] = (double)((threadIdx.x * 7 + i) % in[0]); }
+    long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            dp_bfly(X[i], Y[i], w, q, qinv);
+            X[i] = dp_reduce(X[i], q, qinv);          // amortised pass-boundary reduction (upper bound)
+        }
+    }
+    long long c1 = clock64();
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += X[i] + Y[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = (u32)(long long)s;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
+}
+
 // Runs kernel `which` once (after one warm-up launch); returns the elapsed
 // milliseconds, the in-kernel cycle count of block 0 (SM clock estimate)
 // and the number of operations executed.  0 on success.
@@ -158,7 +198,7 @@ extern "C" int u1_run(int which, int blocks, int threads, int iters, float* ms,
     if (cudaMalloc(&d_in, 64) || cudaMalloc(&d_out, sizeof(u32) * blocks * threads) ||
         cudaMalloc(&d_cyc, sizeof(long long)))
         return 1;
-    if (which >= 3) cudaMemcpy(d_in, h_in64, sizeof(h_in64), cudaMemcpyHostToDevice);
+    if (which >= 3 && which != 5 && which != 6) cudaMemcpy(d_in, h_in64, sizeof(h_in64), cudaMemcpyHostToDevice);
     else {
         u32 h[4] = {3u, 5u, 0x1ffffffu, 0x1234567u};
         cudaMemcpy(d_in, h, sizeof(h), cudaMemcpyHostToDevice);
@@ -177,6 +217,7 @@ extern "C" int u1_run(int which, int blocks, int threads, int iters, float* ms,
             case 4: u1_bfly<true><<<blocks, threads>>>((const u64*)d_in, d_out, iters, d_cyc); per_iter = 8; break;
             case 5: u1_imma<<<blocks, threads>>>(d_in, d_out, iters, d_cyc); per_iter = 4 * 4096.0 / 32; break;
             case 6: u1_dfma<<<blocks, threads>>>(d_in, d_out, iters, d_cyc); per_iter = 8; break;
+            case 7: u1_dbfly<<<blocks, threads>>>((const u64*)d_in, d_out, iters, d_cyc); per_iter = 8; break;
             default: return 2;
         }
         if (rep == 1) cudaEventRecord(e1);
