@@ -88,6 +88,8 @@ extern "C" void he_ctx_destroy(he_ctx* c) {
     cudaFree(c->d_tw_fwd);
     cudaFree(c->d_tw_inv);
     cudaFree(c->d_enc);
+    cudaFree(c->d_twd_fwd);
+    cudaFree(c->d_twd_inv);
     cudaSetDevice(prev);
     free(c->q_host);
     free(c->psi_host);
@@ -115,6 +117,8 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
     {
         const char* m = getenv("HE_MAC");
         c->mac_mode = (m && m[0] == 'i') ? 1 : 0;     // HE_MAC=imad forces the IMAD MAC
+        const char* t = getenv("HE_NTT");
+        c->ntt_mode = (t && t[0] == 'i') ? 1 : 0;     // HE_NTT=int: integer butterflies
     }
     c->logN = r->log2N;
     c->N = N;
@@ -129,6 +133,7 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
     c->psi_host = (u64*)malloc(sizeof(u64) * L);
     c->limb_host = (he_limb*)malloc(sizeof(he_limb) * L);
     std::vector<ulonglong2> fwd((size_t)L * N), inv((size_t)L * N);
+    std::vector<double> fwdd((size_t)L * N), invd((size_t)L * N);
     for (uint32_t j = 0; j < L; ++j) {
         const u64 q = r->q[j];
         c->q_host[j] = q;
@@ -146,6 +151,8 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
             const u64 w = pw[brv(k, r->log2N)], wi = pwi[brv(k, r->log2N)];
             fwd[(size_t)j * N + k] = make_ulonglong2(w, h_shoup(w, q));
             inv[(size_t)j * N + k] = make_ulonglong2(wi, h_shoup(wi, q));
+            fwdd[(size_t)j * N + k] = (double)w;          // exact: w < 2^50
+            invd[(size_t)j * N + k] = (double)wi;
         }
         he_limb& Lm = c->limb_host[j];
         Lm.q = q;
@@ -167,6 +174,8 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
         Lm.r64 = (u64)(((u128)1 << 64) % q);
         Lm.r64_p = h_shoup(Lm.r64, q);
         Lm.one_p = h_shoup(1, q);
+        Lm.qd = (double)q;
+        Lm.qinvd = 1.0 / (double)q;
     }
     int prev = 0;
     cudaGetDevice(&prev);
@@ -179,6 +188,12 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
               cudaMemcpy(c->d_tw_fwd, fwd.data(), sizeof(ulonglong2) * L * N,
                          cudaMemcpyHostToDevice) == cudaSuccess &&
               cudaMemcpy(c->d_tw_inv, inv.data(), sizeof(ulonglong2) * L * N,
+                         cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMalloc(&c->d_twd_fwd, sizeof(double) * L * N) == cudaSuccess &&
+              cudaMalloc(&c->d_twd_inv, sizeof(double) * L * N) == cudaSuccess &&
+              cudaMemcpy(c->d_twd_fwd, fwdd.data(), sizeof(double) * L * N,
+                         cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(c->d_twd_inv, invd.data(), sizeof(double) * L * N,
                          cudaMemcpyHostToDevice) == cudaSuccess;
     if (ok && r->t <= (1u << 20)) {
         // enc_j(m) = (Delta_t mod q_j) m + floor((r_t m + floor(t/2)) / t) mod q_j

@@ -27,6 +27,7 @@ struct he_limb {
     u64 r40, r40_p;         // 2^40 mod q   (byte-split MAC recombination)
     u64 r80, r80_p;         // 2^80 mod q
     u64 one_p;              // Shoup companion of 1  (floor(2^64 / q))
+    double qd, qinvd;       // q and fl(1/q) for the FP64 transforms
 };
 
 struct he_ctx {
@@ -41,6 +42,9 @@ struct he_ctx {
     he_limb* d_limb;        // [L]
     ulonglong2* d_tw_fwd;   // [L][N]  {psi^{brv(k)}, Shoup}
     ulonglong2* d_tw_inv;   // [L][N]  {psi^{-brv(k)}, Shoup}
+    double* d_twd_fwd;      // [L][N]  psi^{brv(k)} as double (FP64 transforms)
+    double* d_twd_inv;      // [L][N]  psi^{-brv(k)} as double
+    int ntt_mode;           // 0: FP64 butterflies (default), 1: integer (HE_NTT=int)
     u64* d_enc;             // [L][t] enc_j(m) table (t <= 2^20), else nullptr
 };
 
@@ -160,10 +164,113 @@ __device__ __forceinline__ void byte_transpose4(u32 a, u32 b, u32 c, u32 d, u32&
     p3 = __byte_perm(t1, t3, 0x7632);
 }
 
-// ---------------------------------------------------- shared-memory NTT
 // Padding: one 8-byte word per 16 (kills bank conflicts for every stride).
 __device__ __forceinline__ int PAD(int i) { return i + (i >> 4); }
 __host__ __device__ constexpr int padded_words(int n) { return n + (n >> 4); }
+
+// ------------------------------------------------------- FP64 residues
+// Residues as integer-valued doubles (|x| < 2^52), so the modular products
+// run on the FP64 pipe.  With |y| w / q < 2^51 (e.g. |y| < 1.4 q, w < q):
+//   p = fl(y w), e = fma(y, w, -p) = y w - p        (exact two-product)
+//   k = rint(p / q) via the 1.5 2^52 magic constant (exact, |p/q| < 2^51)
+//   r = fma(-k, q, p) = p - k q                     (exact, |.| < 2^52)
+//   T = r + e = y w - k q,  |T| < 0.875 q           (k within 0.875 of y w/q)
+static constexpr double DP_MAGIC = 6755399441055744.0;     // 1.5 * 2^52
+
+__device__ __forceinline__ double dp_mulmod(double y, double w, double q, double qinv) {
+    const double p = y * w;
+    const double e = fma(y, w, -p);
+    const double k = fma(p, qinv, DP_MAGIC) - DP_MAGIC;
+    return fma(-k, q, p) + e;
+}
+
+// |result| <= q/2 + 1 for |y| < 2^51.
+__device__ __forceinline__ double dp_reduce(double y, double q, double qinv) {
+    const double k = fma(y, qinv, DP_MAGIC) - DP_MAGIC;
+    return fma(-k, q, y);
+}
+
+// exact u64 (< 2^52) <-> double
+__device__ __forceinline__ double u2d(u64 x) {
+    return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 4503599627370496.0;
+}
+// integer-valued |y| < 2^51 -> canonical residue in [0, q)
+__device__ __forceinline__ u64 d2canon(double y, double q, double qinv) {
+    double r = dp_reduce(y, q, qinv);
+    r = r < 0.0 ? r + q : r;
+    r = r >= q ? r - q : r;
+    return (u64)(__double_as_longlong(r + 4503599627370496.0) & 0xFFFFFFFFFFFFFull);
+}
+
+// FP64 Cooley-Tukey butterfly: X' = X + T, Y' = X - T, T = Y w mod q.
+// Caller guarantees |Y| < 1.4 q (so |Y| w / q < 2^51).
+__device__ __forceinline__ void ct_bfly_dp(double& X, double& Y, double w, double q,
+                                           double qinv) {
+    const double t = dp_mulmod(Y, w, q, qinv);
+    const double x = X;
+    X = x + t;
+    Y = x - t;
+}
+
+// One radix-2^K pass of FP64 CT stages (as ct_pass).  Inputs are reduced
+// to |x| <= q/2 + 1 at the start of the pass; stage r inputs are then below
+// (0.5 + 0.875 r) q, so stages 0 and 1 multiply directly and stage 2
+// reduces the multiplicand first.  Outputs < 3.2 q.
+template <int K>
+__device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0, int seg,
+                                           int split, const double* __restrict__ tw,
+                                           double q, double qinv) {
+    const int lt0 = logN - st0 - 1;
+    const int ltk = lt0 - (K - 1);
+    const int tk = 1 << ltk;
+    const int ngroups = NS >> K;
+    for (int g = threadIdx.x; g < ngroups; g += blockDim.x) {
+        const int blk = g >> ltk, off = g & (tk - 1);
+        const int base = (blk << (lt0 + 1)) + off;
+        double tws[(1 << K) - 1];
+#pragma unroll
+        for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
+            const int twb = (1 << (st0 + r)) + (seg << (st0 + r - split)) + (blk << r);
+#pragma unroll
+            for (int z = 0; z < (1 << r); ++z) tws[o + z] = __ldg(&tw[twb + z]);
+        }
+        double x[1 << K];
+#pragma unroll
+        for (int c = 0; c < (1 << K); ++c) x[c] = dp_reduce(sm[PAD(base + (c << ltk))], q, qinv);
+#pragma unroll
+        for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
+            const int half = 1 << (K - 1 - r);
+#pragma unroll
+            for (int c = 0; c < (1 << K); ++c) {
+                if (c & half) continue;
+                if (r >= 2) x[c + half] = dp_reduce(x[c + half], q, qinv);
+                ct_bfly_dp(x[c], x[c + half], tws[o + (c >> (K - r))], q, qinv);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < (1 << K); ++c) sm[PAD(base + (c << ltk))] = x[c];
+    }
+}
+
+template <int RMAX>
+__device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg, int split,
+                                          const double* tw, double q, double qinv) {
+    int st = split;
+    const int rem = (logN - split) % RMAX;
+    if (rem) {
+        if (rem == 1) ct_pass_dp<1>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        else if (rem == 2) ct_pass_dp<2>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        else ct_pass_dp<3>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        st += rem;
+        __syncthreads();
+    }
+    for (; st < logN; st += RMAX) {
+        ct_pass_dp<RMAX>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------- shared-memory NTT
 
 // One pass of K radix-2 Cooley-Tukey stages (forward NTT, bit-reversed
 // output), on a segment of NS words of an N-point transform held in shared

@@ -63,6 +63,103 @@ struct TileLay {
 };
 static inline int tile_gt(int M) { return M < 16 ? M : 16; }
 
+// Store phase of the forward NTT: canonical values from `val(i)` (local
+// index i of this CTA's segment) in format OUT_FMT.
+template <int OUT_FMT, class F>
+__device__ __forceinline__ void ntt_store(u64* out, int li, int seg, int NS, int N, int L,
+                                          int l, const TileLay& T, F val) {
+    if (OUT_FMT == 2) {
+        unsigned char* A = reinterpret_cast<unsigned char*>(out);
+        const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
+        const int s = 1 << T.logs, M = N >> T.logs, K = T.n_ib << T.logs;
+        for (int i = 4 * threadIdx.x; i < NS; i += 4 * blockDim.x) {
+            u64 x[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] = val(i + e);
+            u32 pl[8];
+            byte_transpose4((u32)x[0], (u32)x[1], (u32)x[2], (u32)x[3], pl[0], pl[1], pl[2],
+                            pl[3]);
+            byte_transpose4((u32)(x[0] >> 32), (u32)(x[1] >> 32), (u32)(x[2] >> 32),
+                            (u32)(x[3] >> 32), pl[4], pl[5], pl[6], pl[7]);
+            const int pos = seg * NS + i;
+            const int g = pos >> T.logs, u = pos & (s - 1);
+            const int gb = g / T.Gt, gi = g - gb * T.Gt;
+            unsigned char* row =
+                A + (((((size_t)l * (M / T.Gt) + gb) * 7) * T.B + b) * T.Gt + gi) * T.Kp +
+                beta * s + u;
+            const size_t pstride = (size_t)T.B * T.Gt * T.Kp;
+            const bool tail = (beta == T.n_ib - 1) && (u + 4 == s) && (T.Kp > K);
+#pragma unroll
+            for (int j = 0; j < 7; ++j) {
+                *reinterpret_cast<u32*>(row + j * pstride) = pl[j];
+                if (tail)
+                    for (int z = 4; z < T.Kp - K + 4; z += 4)
+                        *reinterpret_cast<u32*>(row + j * pstride + z) = 0u;
+            }
+        }
+        return;
+    }
+    u64* dst = out + (size_t)li * N + (size_t)seg * NS;
+    for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
+        u64 x = val(i), y = val(i + 1);
+        if (OUT_FMT == 1) { x = to_split25(x); y = to_split25(y); }
+        *reinterpret_cast<ulonglong2*>(dst + i) = make_ulonglong2(x, y);
+    }
+}
+
+// FP64 variant of ntt_fwd_segment (default; HE_NTT=int selects the integer
+// one): residues as integer-valued doubles, exact FP64 butterflies
+// (he_internal.cuh), twiddles psi^{brv(k)} as doubles.
+template <int S, int OUT_FMT>
+__device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int logN, int L,
+                                                   const he_limb* __restrict__ limbs,
+                                                   const double* __restrict__ twd_all,
+                                                   TileLay T) {
+    extern __shared__ u64 sm_raw[];
+    double* sm = reinterpret_cast<double*>(sm_raw);
+    const int N = 1 << logN, NS = N >> S;
+    const int li = blockIdx.x >> S, seg = blockIdx.x & ((1 << S) - 1);
+    const int l = li % L;
+    const double q = limbs[l].qd, qinv = limbs[l].qinvd;
+    const double* tw = twd_all + (size_t)l * N;
+    const u64* src = in + (size_t)li * N;
+    for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
+        double vx[1 << S], vy[1 << S];
+#pragma unroll
+        for (int r = 0; r < (1 << S); ++r) {
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src + i + r * NS);
+            vx[r] = u2d(v.x);
+            vy[r] = u2d(v.y);
+        }
+#pragma unroll
+        for (int st = 0; st < S; ++st) {
+            const int half = 1 << (S - 1 - st);
+#pragma unroll
+            for (int r = 0; r < (1 << S); ++r) {
+                if (r & half) continue;
+                const double w = __ldg(&tw[(1 << st) + (r >> (S - st))]);
+                if (st >= 1) {
+                    vx[r + half] = dp_reduce(vx[r + half], q, qinv);
+                    vy[r + half] = dp_reduce(vy[r + half], q, qinv);
+                }
+                ct_bfly_dp(vx[r], vx[r + half], w, q, qinv);
+                ct_bfly_dp(vy[r], vy[r + half], w, q, qinv);
+            }
+        }
+        double ox = vx[0], oy = vy[0];
+#pragma unroll
+        for (int r = 1; r < (1 << S); ++r)
+            if (r == seg) { ox = vx[r]; oy = vy[r]; }
+        sm[PAD(i)] = ox;
+        sm[PAD(i + 1)] = oy;
+    }
+    if (S) cg::this_cluster().sync();
+    else __syncthreads();
+    ct_all_dp<3>(sm, logN, NS, seg, S, tw, q, qinv);          // outputs < 3.2 q
+    ntt_store<OUT_FMT>(out, li, seg, NS, N, L, l, T,
+                       [&](int i) { return d2canon(sm[PAD(i)], q, qinv); });
+}
+
 template <int S, int OUT_FMT>
 __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int logN, int L,
                                                 const he_limb* __restrict__ limbs,
@@ -103,45 +200,10 @@ __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int log
     }
     if (S) cg::this_cluster().sync();
     else __syncthreads();
-    ct_all<3, true>(sm, logN, NS, seg, S, tw, q, q2);      // lazy: values < 31 q
+    ct_all<3, true>(sm, logN, NS, seg, S, tw, q, q2);      // lazy: values < 61 q
     const u64 one_p = limbs[l].one_p;
-    if (OUT_FMT == 2) {
-        unsigned char* A = reinterpret_cast<unsigned char*>(out);
-        const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
-        const int s = 1 << T.logs, M = N >> T.logs, K = T.n_ib << T.logs;
-        for (int i = 4 * threadIdx.x; i < NS; i += 4 * blockDim.x) {
-            u64 x[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) x[e] = reduce_full(sm[PAD(i + e)], q, one_p);
-            u32 pl[8];
-            byte_transpose4((u32)x[0], (u32)x[1], (u32)x[2], (u32)x[3], pl[0], pl[1], pl[2],
-                            pl[3]);
-            byte_transpose4((u32)(x[0] >> 32), (u32)(x[1] >> 32), (u32)(x[2] >> 32),
-                            (u32)(x[3] >> 32), pl[4], pl[5], pl[6], pl[7]);
-            const int pos = seg * NS + i;
-            const int g = pos >> T.logs, u = pos & (s - 1);
-            const int gb = g / T.Gt, gi = g - gb * T.Gt;
-            unsigned char* row =
-                A + (((((size_t)l * (M / T.Gt) + gb) * 7) * T.B + b) * T.Gt + gi) * T.Kp +
-                beta * s + u;
-            const size_t pstride = (size_t)T.B * T.Gt * T.Kp;
-            const bool tail = (beta == T.n_ib - 1) && (u + 4 == s) && (T.Kp > K);
-#pragma unroll
-            for (int j = 0; j < 7; ++j) {
-                *reinterpret_cast<u32*>(row + j * pstride) = pl[j];
-                if (tail)
-                    for (int z = 4; z < T.Kp - K + 4; z += 4)
-                        *reinterpret_cast<u32*>(row + j * pstride + z) = 0u;
-            }
-        }
-        return;
-    }
-    u64* dst = out + (size_t)li * N + (size_t)seg * NS;
-    for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
-        u64 x = reduce_full(sm[PAD(i)], q, one_p), y = reduce_full(sm[PAD(i + 1)], q, one_p);
-        if (OUT_FMT == 1) { x = to_split25(x); y = to_split25(y); }
-        *reinterpret_cast<ulonglong2*>(dst + i) = make_ulonglong2(x, y);
-    }
+    ntt_store<OUT_FMT>(out, li, seg, NS, N, L, l, T,
+                       [&](int i) { return reduce_full(sm[PAD(i)], q, one_p); });
 }
 
 template <int OUT_FMT>
@@ -165,6 +227,25 @@ k_ntt_fwd_s2(const u64* in, u64* out, int logN, int L, const he_limb* __restrict
     ntt_fwd_segment<2, OUT_FMT>(in, out, logN, L, limbs, tw_all, T);
 }
 
+template <int OUT_FMT>
+__global__ void __launch_bounds__(512, 2)
+k_ntt_fwd_dp_s0(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
+                const double* __restrict__ tw_all, TileLay T) {
+    ntt_fwd_segment_dp<0, OUT_FMT>(in, out, logN, L, limbs, tw_all, T);
+}
+template <int OUT_FMT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 2)
+k_ntt_fwd_dp_s1(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
+                const double* __restrict__ tw_all, TileLay T) {
+    ntt_fwd_segment_dp<1, OUT_FMT>(in, out, logN, L, limbs, tw_all, T);
+}
+template <int OUT_FMT>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 2)
+k_ntt_fwd_dp_s2(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
+                const double* __restrict__ tw_all, TileLay T) {
+    ntt_fwd_segment_dp<2, OUT_FMT>(in, out, logN, L, limbs, tw_all, T);
+}
+
 // Launch the forward NTT over nlimbs = batch * L limbs.
 static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
                                 long nlimbs, int out_fmt, cudaStream_t st,
@@ -181,6 +262,19 @@ static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
         {k_ntt_fwd_s0<0>, k_ntt_fwd_s0<1>, k_ntt_fwd_s0<2>},
         {k_ntt_fwd_s1<0>, k_ntt_fwd_s1<1>, k_ntt_fwd_s1<2>},
         {k_ntt_fwd_s2<0>, k_ntt_fwd_s2<1>, k_ntt_fwd_s2<2>}};
+    if (c->ntt_mode == 0) {
+        typedef void (*kfd)(const u64*, u64*, int, int, const he_limb*, const double*, TileLay);
+        static kfd const tabd[3][3] = {
+            {k_ntt_fwd_dp_s0<0>, k_ntt_fwd_dp_s0<1>, k_ntt_fwd_dp_s0<2>},
+            {k_ntt_fwd_dp_s1<0>, k_ntt_fwd_dp_s1<1>, k_ntt_fwd_dp_s1<2>},
+            {k_ntt_fwd_dp_s2<0>, k_ntt_fwd_dp_s2<1>, k_ntt_fwd_dp_s2<2>}};
+        kfd kd = tabd[S][out_fmt];
+        if (!set_smem(kd, smem)) return HE_ECUDA;
+        kd<<<(unsigned)(nlimbs << S), threads, smem, st>>>(in, out, logN, c->L, c->d_limb,
+                                                           c->d_twd_fwd, T);
+        HE_CHECK_LAUNCH();
+        return HE_OK;
+    }
     k = tab[S][out_fmt];
     if (!set_smem(k, smem)) return HE_ECUDA;
     k<<<(unsigned)(nlimbs << S), threads, smem, st>>>(in, out, logN, c->L, c->d_limb,

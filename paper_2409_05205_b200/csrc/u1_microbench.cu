@@ -148,22 +148,6 @@ __global__ void u1_dfma(const u32* in, u32* out, int iters, long long* cyc) {
 // which 7: exact FP64 Cooley-Tukey butterfly on signed residues (|x| < 2^51):
 // reduce the multiplicand, T = Y w mod q via an exact two-product and a
 // magic-number rounded quotient (|T| < 0.9 q), X' = X + T, Y' = X - T.
-__device__ __forceinline__ double dp_reduce(double y, double q, double qinv) {
-    const double M = 6755399441055744.0;                // 1.5 * 2^52
-    const double k = fma(y, qinv, M) - M;
-    return fma(-k, q, y);                               // |.| <= q/2 + small
-}
-__device__ __forceinline__ void dp_bfly(double& X, double& Y, double w, double q, double qinv) {
-    const double M = 6755399441055744.0;
-    const double y = dp_reduce(Y, q, qinv);
-    const double p = y * w;
-    const double e = fma(y, w, -p);
-    const double k = fma(p, qinv, M) - M;
-    const double t = fma(-k, q, p) + e;
-    const double x = X;
-    X = x + t;
-    Y = x - t;
-}
 __global__ void u1_dbfly(const u64* in, u32* out, int iters, long long* cyc) {
     const double q = (double)in[0], w = (double)in[1], qinv = 1.0 / q;
     double X[8], Y[8];
@@ -173,8 +157,10 @@ __global__ void u1_dbfly(const u64* in, u32* out, int iters, long long* cyc) {
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            dp_bfly(X[i], Y[i], w, q, qinv);
-            X[i] = dp_reduce(X[i], q, qinv);          // amortised pass-boundary reduction (upper bound)
+            // the kernels' mix: about one reduction per butterfly (pass-start
+            // reductions + the stage-2 multiplicand reduction)
+            Y[i] = dp_reduce(Y[i], q, qinv);
+            ct_bfly_dp(X[i], Y[i], w, q, qinv);
         }
     }
     long long c1 = clock64();
