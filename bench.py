@@ -102,9 +102,9 @@ def u1_peaks(device_index=0):
     lib.u1_run.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p] * 3
     out = {}
     names = ["imad", "imad_wide", "modmac", "ct_bfly", "gs_bfly", "imma_u8",
-             "dfma", "dp_ct_bfly"]
+             "dfma", "dp_ct_bfly", "dp_gs_bfly"]
     iters = {0: 20000, 1: 20000, 2: 20000, 3: 2000, 4: 2000, 5: 2000, 6: 20000,
-             7: 2000}
+             7: 2000, 8: 2000}
     for w, name in enumerate(names):
         ms, cyc, ops = ctypes.c_float(), ctypes.c_longlong(), ctypes.c_double()
         rc = lib.u1_run(w, 148 * 8, 256, iters[w], ctypes.byref(ms),
@@ -427,17 +427,20 @@ def main():
     hbm_gbs, hbm_src = peaks()
     u1 = u1_peaks(local)
     # U1 rates were measured at the in-kernel clock; they are the alu roofs.
+    # transforms run FP64 butterflies by default (HE_NTT=int: integer Shoup)
+    ntt_int = os.environ.get("HE_NTT", "")[:1] == "i"
+    ct_roof = u1["ct_bfly"]["per_s"] if ntt_int else u1["dp_ct_bfly"]["per_s"]
+    gs_roof = u1["gs_bfly"]["per_s"] if ntt_int else u1["dp_gs_bfly"]["per_s"]
     kern = {
-        "ntt_fwd": (st["ntt_fwd"], W_ntt_bfly, u1["ct_bfly"]["per_s"], "Gbutterfly/s",
-                    W_ntt_bytes),
+        "ntt_fwd": (st["ntt_fwd"], W_ntt_bfly, ct_roof, "Gbutterfly/s", W_ntt_bytes),
         # int8 tensor-core MAC: 49 u8 x u8 products per 50-bit modMAC, so its
         # alu roof is the measured mma.sync int8 rate / 49 (HE_MAC=imad runs
         # the IMAD kernel, whose roof is U1 "modmac").
         "mac_fold": (st["mac_fold"], W_macs,
                      u1["modmac"]["per_s"] if os.environ.get("HE_MAC", "")[:1] == "i"
                      else u1["imma_u8"]["per_s"] / 49, "Gmodmac/s", W_mac_bytes),
-        "intt_scatter": (st["intt_scatter"], W_intt_bfly, u1["gs_bfly"]["per_s"],
-                         "Gbutterfly/s", W_intt_bytes),
+        "intt_scatter": (st["intt_scatter"], W_intt_bfly, gs_roof, "Gbutterfly/s",
+                         W_intt_bytes),
     }
     rl = {}
     for name, (ms, ops, alu_peak, unit, byts) in kern.items():
@@ -480,7 +483,7 @@ def main():
     t_ntt = a.elapsed_time(b) / 10 * 1e-3
     logN = N.bit_length() - 1
     ntt = {"N": N, "limbs_per_launch": nl, "limbs_per_s": nl / t_ntt,
-           "alu_roof_limbs_per_s": u1["ct_bfly"]["per_s"] / (N // 2 * logN),
+           "alu_roof_limbs_per_s": ct_roof / (N // 2 * logN),
            "hbm_roof_limbs_per_s": hbm_gbs * 1e9 / (16 * N)}
     ntt["roof_limbs_per_s"] = min(ntt["alu_roof_limbs_per_s"], ntt["hbm_roof_limbs_per_s"])
     ntt["frac"] = ntt["limbs_per_s"] / ntt["roof_limbs_per_s"]

@@ -270,6 +270,72 @@ __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg,
     }
 }
 
+// One radix-2^K pass of FP64 Gentleman-Sande stages over narr M-point arrays
+// (as gs_pass).  Inputs are reduced to |x| <= q/2 + 1 at the start of the
+// pass; X' = X + Y, Y' = (X - Y) w mod q.  Stage 0: |X - Y| <= q + 2;
+// stage 1: <= 2q + 4 < 2^51 (q <= 2^50 - 4): both multiply directly; stage
+// 2 reduces X - Y first.  Outputs < 4q + 8.
+template <int K>
+__device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr, int logM,
+                                           int lt0, int seg, int logMfull,
+                                           const double* __restrict__ tw, double q,
+                                           double qinv) {
+    const int tk = 1 << lt0;
+    const int gper = 1 << (logM - K);
+    const int total = narr * gper;
+    for (int G = threadIdx.x; G < total; G += blockDim.x) {
+        const int a = G >> (logM - K), g = G & (gper - 1);
+        double* s = sm + a * arr_stride;
+        const int blk = g >> lt0, off = g & (tk - 1);
+        const int base = (blk << (lt0 + K)) + off;
+        double tws[(1 << K) - 1];
+#pragma unroll
+        for (int v = 0, o = 0; v < K; o += (1 << (K - 1 - v)), ++v) {
+            const int lt = lt0 + v;
+            const int tb = (1 << (logMfull - lt - 1)) + (seg << (logM - lt - 1)) +
+                           (blk << (K - 1 - v));
+#pragma unroll
+            for (int z = 0; z < (1 << (K - 1 - v)); ++z) tws[o + z] = __ldg(&tw[tb + z]);
+        }
+        double x[1 << K];
+#pragma unroll
+        for (int c = 0; c < (1 << K); ++c) x[c] = dp_reduce(s[PAD(base + (c << lt0))], q, qinv);
+#pragma unroll
+        for (int v = 0, o = 0; v < K; o += (1 << (K - 1 - v)), ++v) {
+            const int half = 1 << v;
+#pragma unroll
+            for (int c = 0; c < (1 << K); ++c) {
+                if (c & half) continue;
+                const double X = x[c], Y = x[c + half];
+                double u = X - Y;
+                if (v >= 2) u = dp_reduce(u, q, qinv);
+                x[c] = X + Y;
+                x[c + half] = dp_mulmod(u, tws[o + (c >> (v + 1))], q, qinv);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < (1 << K); ++c) s[PAD(base + (c << lt0))] = x[c];
+    }
+}
+
+template <int RMAX>
+__device__ __forceinline__ void gs_all_dp(double* sm, int arr_stride, int narr, int logM,
+                                          int seg, int logMfull, const double* tw, double q,
+                                          double qinv) {
+    int lt = 0;
+    const int rem = logM % RMAX;
+    for (; lt + RMAX <= logM; lt += RMAX) {
+        gs_pass_dp<RMAX>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, qinv);
+        __syncthreads();
+    }
+    if (rem) {
+        if (rem == 1) gs_pass_dp<1>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, qinv);
+        else if (rem == 2) gs_pass_dp<2>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, qinv);
+        else gs_pass_dp<3>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, qinv);
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------- shared-memory NTT
 
 // One pass of K radix-2 Cooley-Tukey stages (forward NTT, bit-reversed

@@ -1045,12 +1045,13 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
 // coefficient.  The chunks tile [0, s), so every coefficient
 // of the row is written exactly once, in contiguous runs of u1 - u0 words.
 // Channel arrays sit in shared memory at an odd word stride (conflict-free).
+template <bool DP>
 __global__ void __launch_bounds__(256, 4)
 k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                u64* __restrict__ out, u64* __restrict__ comp, PlanDev P, int B, int L,
                int logN, int cc, int nchunk, int stride, const he_limb* __restrict__ limbs,
-               const ulonglong2* __restrict__ twi_all, const u64* __restrict__ enc_tab, u64 t,
-               u64 r_t, u64 t_inv) {
+               const ulonglong2* __restrict__ twi_all, const double* __restrict__ twid_all,
+               const u64* __restrict__ enc_tab, u64 t, u64 r_t, u64 t_inv) {
     extern __shared__ u64 sm[];
     const int N = 1 << logN, M = N >> P.logs, logM = logN - P.logs;
     int r = blockIdx.x;
@@ -1076,12 +1077,21 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const int idx = base + e * blockDim.x + threadIdx.x;
-            if (idx < tot) sm[(idx >> logM) * stride + PAD(idx & (M - 1))] = v[e];
+            if (idx < tot) {
+                const int a = (idx >> logM) * stride + PAD(idx & (M - 1));
+                if (DP) reinterpret_cast<double*>(sm)[a] = u2d(v[e]);
+                else sm[a] = v[e];
+            }
         }
     }
     __syncthreads();
-    if (logM <= 12) gs_all<3, true>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
-    else gs_all<3>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
+    if (DP)
+        gs_all_dp<3>(reinterpret_cast<double*>(sm), stride, ncc, logM, 0, logM,
+                     twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
+    else if (logM <= 12)
+        gs_all<3, true>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
+    else
+        gs_all<3>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
     const int u0 = ch0 * P.step;
     const int u1 = (ch == nchunk - 1) ? P.s : (ch0 + ncc) * P.step;
     const int w = u1 - u0;
@@ -1138,7 +1148,10 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
 #pragma unroll
         for (int e = 0; e < EB; ++e) {
             if (!go[e]) continue;
-            u64 v = sidx[e] >= 0 ? reduce_full(sm[sidx[e]], q, Lm.one_p) : 0;
+            u64 v = 0;
+            if (sidx[e] >= 0)
+                v = DP ? d2canon(reinterpret_cast<const double*>(sm)[sidx[e]], Lm.qd, Lm.qinvd)
+                       : reduce_full(sm[sidx[e]], q, Lm.one_p);
             v = addmod(v, en[e], q);
             if (orow) orow[ii[e]] = v;
             if (vi[e] >= 0) crow[vi[e]] = v;
@@ -1213,11 +1226,12 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     while ((stride & 15) != want && !(cc >= 16 && (stride & 1))) ++stride;
     const int nchunk = (P.c_ob + cc - 1) / cc;
     const size_t smem = sizeof(u64) * (size_t)cc * stride;
-    if (!set_smem(k_intt_scatter, smem)) return HE_ECUDA;
+    auto k4 = c->ntt_mode == 0 ? k_intt_scatter<true> : k_intt_scatter<false>;
+    if (!set_smem(k4, smem)) return HE_ECUDA;
     rec(ev, 2, st);
-    k_intt_scatter<<<(unsigned)(B * P.n_ob * c->L * nchunk), 256, smem, st>>>(
+    k4<<<(unsigned)(B * P.n_ob * c->L * nchunk), 256, smem, st>>>(
         fold, d_phi1, (u64*)d_out, (u64*)d_compact, P, B, c->L, c->logN, cc, nchunk, stride,
-        c->d_limb, c->d_tw_inv, c->d_enc, c->t, c->r_t, c->t_inv);
+        c->d_limb, c->d_tw_inv, c->d_twd_inv, c->d_enc, c->t, c->r_t, c->t_inv);
     HE_CHECK_LAUNCH();
     rec(ev, 3, st);
     return HE_OK;

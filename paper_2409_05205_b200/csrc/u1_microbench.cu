@@ -9,6 +9,8 @@
 //            loop-carried operands)                   -> MAC / s
 //   which 3: Shoup Cooley-Tukey butterfly (ct_bfly)      -> butterflies / s
 //   which 4: Shoup Gentleman-Sande butterfly (gs_bfly)   -> butterflies / s
+//   which 5: int8 mma.sync; 6: DFMA; 7/8: FP64 CT / GS butterflies (the
+//            default transforms, he_internal.cuh)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -171,6 +173,30 @@ __global__ void u1_dbfly(const u64* in, u32* out, int iters, long long* cyc) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
 }
 
+// which 8: FP64 Gentleman-Sande butterfly as in gs_pass_dp (X' = X + Y,
+// Y' = (X - Y) w mod q, about one reduction per butterfly).
+__global__ void u1_dgsbfly(const u64* in, u32* out, int iters, long long* cyc) {
+    const double q = (double)in[0], w = (double)in[1], qinv = 1.0 / q;
+    double X[8], Y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { X[i] = (double)((threadIdx.x + i) % in[0]); Y[i] = (double)((threadIdx.x * 7 + i) % in[0]); }
+    long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double x = dp_reduce(X[i], q, qinv), y = Y[i];
+            X[i] = x + y;
+            Y[i] = dp_mulmod(x - y, w, q, qinv);
+        }
+    }
+    long long c1 = clock64();
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += X[i] + Y[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = (u32)(long long)s;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
+}
+
 // Runs kernel `which` once (after one warm-up launch); returns the elapsed
 // milliseconds, the in-kernel cycle count of block 0 (SM clock estimate)
 // and the number of operations executed.  0 on success.
@@ -184,7 +210,7 @@ extern "C" int u1_run(int which, int blocks, int threads, int iters, float* ms,
     if (cudaMalloc(&d_in, 64) || cudaMalloc(&d_out, sizeof(u32) * blocks * threads) ||
         cudaMalloc(&d_cyc, sizeof(long long)))
         return 1;
-    if (which >= 3 && which != 5 && which != 6) cudaMemcpy(d_in, h_in64, sizeof(h_in64), cudaMemcpyHostToDevice);
+    if (which == 3 || which == 4 || which == 7 || which == 8) cudaMemcpy(d_in, h_in64, sizeof(h_in64), cudaMemcpyHostToDevice);
     else {
         u32 h[4] = {3u, 5u, 0x1ffffffu, 0x1234567u};
         cudaMemcpy(d_in, h, sizeof(h), cudaMemcpyHostToDevice);
@@ -204,6 +230,7 @@ extern "C" int u1_run(int which, int blocks, int threads, int iters, float* ms,
             case 5: u1_imma<<<blocks, threads>>>(d_in, d_out, iters, d_cyc); per_iter = 4 * 4096.0 / 32; break;
             case 6: u1_dfma<<<blocks, threads>>>(d_in, d_out, iters, d_cyc); per_iter = 8; break;
             case 7: u1_dbfly<<<blocks, threads>>>((const u64*)d_in, d_out, iters, d_cyc); per_iter = 8; break;
+            case 8: u1_dgsbfly<<<blocks, threads>>>((const u64*)d_in, d_out, iters, d_cyc); per_iter = 8; break;
             default: return 2;
         }
         if (rep == 1) cudaEventRecord(e1);
