@@ -285,10 +285,12 @@ static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
 
 // ============================================================ inverse NTT
 // Full N-point inverse (bit-reversed in, natural out, x N^{-1}).
+template <bool DP>
 __global__ void __launch_bounds__(512)
-k_ntt_inv(const u64* in, u64* out, int logN, int L,
-          const he_limb* __restrict__ limbs, const ulonglong2* __restrict__ twi_all) {
+k_ntt_inv(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
+          const ulonglong2* __restrict__ twi_all, const double* __restrict__ twid_all) {
     extern __shared__ u64 sm[];
+    double* smd = reinterpret_cast<double*>(sm);
     const int N = 1 << logN;
     const int li = blockIdx.x, l = li % L;
     const he_limb& Lm = limbs[l];
@@ -296,16 +298,31 @@ k_ntt_inv(const u64* in, u64* out, int logN, int L,
     const u64* src = in + (size_t)li * N;
     for (int i = 2 * threadIdx.x; i < N; i += 2 * blockDim.x) {
         const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src + i);
-        sm[PAD(i)] = v.x;
-        sm[PAD(i + 1)] = v.y;
+        if (DP) {
+            smd[PAD(i)] = u2d(v.x);
+            smd[PAD(i + 1)] = u2d(v.y);
+        } else {
+            sm[PAD(i)] = v.x;
+            sm[PAD(i + 1)] = v.y;
+        }
     }
     __syncthreads();
-    gs_all<4>(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
+    if (DP) gs_all_dp<3>(smd, 0, 1, logN, 0, logN, twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
+    else gs_all<4>(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
     u64* dst = out + (size_t)li * N;
     const u64 ni = Lm.ninv, nip = Lm.ninv_p;
+    const double nid = (double)Lm.ninv;
     for (int i = 2 * threadIdx.x; i < N; i += 2 * blockDim.x) {
-        const u64 x = csub(shoup_mul(sm[PAD(i)], ni, nip, q), q);
-        const u64 y = csub(shoup_mul(sm[PAD(i + 1)], ni, nip, q), q);
+        u64 x, y;
+        if (DP) {
+            x = d2canon(dp_mulmod(dp_reduce(smd[PAD(i)], Lm.qd, Lm.qinvd), nid, Lm.qd, Lm.qinvd),
+                        Lm.qd, Lm.qinvd);
+            y = d2canon(dp_mulmod(dp_reduce(smd[PAD(i + 1)], Lm.qd, Lm.qinvd), nid, Lm.qd,
+                                  Lm.qinvd), Lm.qd, Lm.qinvd);
+        } else {
+            x = csub(shoup_mul(sm[PAD(i)], ni, nip, q), q);
+            y = csub(shoup_mul(sm[PAD(i + 1)], ni, nip, q), q);
+        }
         *reinterpret_cast<ulonglong2*>(dst + i) = make_ulonglong2(x, y);
     }
 }
@@ -350,9 +367,10 @@ static he_status launch_ntt_inv(const he_ctx* c, const u64* in, u64* out,
     const int N = c->N;
     if (c->logN <= 14) {
         const size_t smem = sizeof(u64) * padded_words(N);
-        if (!set_smem(k_ntt_inv, smem)) return HE_ECUDA;
-        k_ntt_inv<<<(unsigned)nlimbs, ntt_threads(N), smem, st>>>(
-            in, out, c->logN, c->L, c->d_limb, c->d_tw_inv);
+        auto k = c->ntt_mode == 0 ? k_ntt_inv<true> : k_ntt_inv<false>;
+        if (!set_smem(k, smem)) return HE_ECUDA;
+        k<<<(unsigned)nlimbs, ntt_threads(N), smem, st>>>(in, out, c->logN, c->L, c->d_limb,
+                                                         c->d_tw_inv, c->d_twd_inv);
     } else {
         const size_t smem = sizeof(u64) * padded_words(N / 2);
         if (!set_smem(k_ntt_inv_split, smem)) return HE_ECUDA;
@@ -1395,12 +1413,15 @@ extern "C" he_status he_pack_fc_weights(const he_ctx* c, const he_fc_desc* f,
 
 // Per (b, l): pointwise product with the weight spectrum, N-point inverse
 // NTT (N^{-1} pre-folded), first n_o coefficients + enc(bias) + enc(phi1).
+template <bool DP>
 __global__ void __launch_bounds__(512)
 k_fc_inv(const u64* __restrict__ spec, const ulonglong2* __restrict__ wspec,
          const u64* __restrict__ bias_enc, const u32* __restrict__ phi1, u64* __restrict__ out,
          int n_o, int L, int logN, const he_limb* __restrict__ limbs,
-         const ulonglong2* __restrict__ twi_all, u64 t, u64 r_t, u64 t_inv) {
+         const ulonglong2* __restrict__ twi_all, const double* __restrict__ twid_all, u64 t,
+         u64 r_t, u64 t_inv) {
     extern __shared__ u64 sm[];
+    double* smd = reinterpret_cast<double*>(sm);
     const int N = 1 << logN;
     const int li = blockIdx.x, l = li % L, b = li / L;
     const he_limb Lm = limbs[l];
@@ -1409,12 +1430,14 @@ k_fc_inv(const u64* __restrict__ spec, const ulonglong2* __restrict__ wspec,
     const ulonglong2* ws = wspec + (size_t)l * N;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         const ulonglong2 w = __ldg(&ws[i]);
-        sm[PAD(i)] = shoup_mul(src[i], w.x, w.y, q);      // [0, 2q)
+        if (DP) smd[PAD(i)] = dp_mulmod(u2d(src[i]), (double)w.x, Lm.qd, Lm.qinvd);
+        else sm[PAD(i)] = shoup_mul(src[i], w.x, w.y, q);      // [0, 2q)
     }
     __syncthreads();
-    gs_all<4>(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
+    if (DP) gs_all_dp<3>(smd, 0, 1, logN, 0, logN, twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
+    else gs_all<4>(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
     for (int k = threadIdx.x; k < n_o; k += blockDim.x) {
-        u64 v = csub(sm[PAD(k)], q);
+        u64 v = DP ? d2canon(smd[PAD(k)], Lm.qd, Lm.qinvd) : csub(sm[PAD(k)], q);
         v = addmod(v, bias_enc[(size_t)l * n_o + k], q);
         if (phi1) v = addmod(v, enc_plain(phi1[(size_t)b * n_o + k], Lm, t, r_t, t_inv), q);
         out[(size_t)li * n_o + k] = v;
@@ -1444,11 +1467,12 @@ extern "C" he_status he_fc_ex(const he_ctx* c, const he_fc_desc* f, const uint64
     he_status s = launch_ntt_fwd(c, (const u64*)d_c0, spec, (long)B * c->L, 0, st);
     if (s != HE_OK) return s;
     const size_t smem = sizeof(u64) * padded_words(c->N);
-    if (!set_smem(k_fc_inv, smem)) return HE_ECUDA;
+    auto kf = c->ntt_mode == 0 ? k_fc_inv<true> : k_fc_inv<false>;
+    if (!set_smem(kf, smem)) return HE_ECUDA;
     rec(ev, 1, st);
-    k_fc_inv<<<(unsigned)(B * c->L), ntt_threads(c->N), smem, st>>>(
+    kf<<<(unsigned)(B * c->L), ntt_threads(c->N), smem, st>>>(
         spec, (const ulonglong2*)d_wspec, (const u64*)d_bias_enc, d_phi1, (u64*)d_out, f->n_o,
-        c->L, c->logN, c->d_limb, c->d_tw_inv, c->t, c->r_t, c->t_inv);
+        c->L, c->logN, c->d_limb, c->d_tw_inv, c->d_twd_inv, c->t, c->r_t, c->t_inv);
     HE_CHECK_LAUNCH();
     rec(ev, 2, st);
     return HE_OK;

@@ -374,3 +374,24 @@ def test_phi1_generate_matches_oracle(he):
         ctx.phi1_generate(seed, out)
         assert np.array_equal(out.cpu().numpy().view(np.uint32),
                               R.phi1_stream(seed, n, 65537))
+
+
+def test_integer_transform_path(he, monkeypatch):
+    """HE_NTT=int selects the integer (Shoup) transforms instead of the FP64
+    ones; both must be bit-exact (conv, FC, NTT round trip)."""
+    monkeypatch.setenv("HE_NTT", "int")
+    cfg = synth.CONFIGS[4]
+    ctx = he.Context(cfg.primes, cfg.log2N, cfg.t)
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    for li in (1, 14):
+        run_conv(he, ctx, ring, cfg.conv[li], cfg.B, seed=cfg.seed + 11 * li,
+                 check_b=[0, cfg.B - 1])
+    x = synth.uniform_residues((2, cfg.L, cfg.N), cfg.primes, 3, "misc")
+    d = dev(x)
+    ctx.ntt_forward(d)
+    ctx.ntt_inverse(d)
+    assert np.array_equal(u64(d), x)
+    cfg5 = synth.CONFIGS[5]
+    ctx5 = he.Context(cfg5.primes, cfg5.log2N, cfg5.t)
+    run_conv(he, ctx5, R.Ring(cfg5.N, cfg5.primes, cfg5.t), cfg5.conv[0], 32,
+             seed=9, check_b=[0, 31])
