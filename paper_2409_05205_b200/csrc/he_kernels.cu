@@ -1116,63 +1116,87 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     const u32* ph = phi1 ? phi1 + ((size_t)b * P.n_ob + ob) * N : nullptr;
     u64* orow = out ? out + (((size_t)b * P.n_ob + ob) * L + l) * N : nullptr;
     u64* crow = comp ? comp + (((size_t)b * P.n_ob + ob) * L + l) * P.n_valid : nullptr;
-    const float inv_hp = 1.0f / (float)P.h_p;
     int lstr = 0;                         // stride is a power of two (checked on host)
     while ((1 << lstr) < P.stride) ++lstr;
-    int lw = 0, ls = 0;                   // log2 w, log2 step (if powers of 2)
-    while ((1 << lw) < w) ++lw;
-    while ((1 << ls) < P.step) ++ls;
-    const bool pow2 = (1 << lw) == w && (1 << ls) == P.step;
-    constexpr int EB = 4;                 // outputs per thread per batch
-    for (int base = 0; base < M * w; base += EB * blockDim.x) {
-        int ii[EB], vi[EB], sidx[EB];
-        bool go[EB];
-        u32 m[EB];
+    // Row writer.  Thread (uo, jt) owns slot column u = u0 + uo of every
+    // group j = jt, jt + jstep, ...: its channel, ownership and smem base are
+    // per-thread constants, and the (row, column) of j for the payload test
+    // are advanced incrementally.  Four phi1 / table loads in flight.
+    const int jstep = blockDim.x / w;
+    const int uo = threadIdx.x % w, jt = threadIdx.x / w;
+    if (jstep > 0 && jt < jstep) {
+        const int u = u0 + uo;
+        const int nl = u / P.step;
+        const bool owned = u == nl * P.step && nl < ch0 + ncc;
+        const int abase = owned ? (nl - ch0) * stride : 0;
+        const bool want_c = crow && owned;
+        // j = kr * h_p + lc, tracked incrementally
+        int kr = jt / P.h_p, lc = jt - kr * P.h_p;
+        const int dk = jstep / P.h_p, dl = jstep - dk * P.h_p;
+        constexpr int EB = 4;
+        for (int j0 = jt; j0 < M; j0 += EB * jstep) {
+            u32 m[EB];
+            int vi[EB];
 #pragma unroll
-        for (int e = 0; e < EB; ++e) {
-            const int idx = base + e * blockDim.x + threadIdx.x;
-            int j, u, nl;
-            if (pow2) {
-                j = idx >> lw;
-                u = u0 + (idx & (w - 1));
-                nl = u >> ls;
-            } else {
-                j = idx / w;
-                u = u0 + (idx - j * w);
-                nl = u / P.step;
+            for (int e = 0; e < EB; ++e) {
+                const int j = j0 + e * jstep;
+                vi[e] = -1;
+                if (want_c && j < M) {
+                    const int K_ = kr >> lstr, L_ = lc >> lstr;
+                    if (((kr | lc) & (P.stride - 1)) == 0 && K_ < P.w_o && L_ < P.h_o)
+                        vi[e] = (K_ * P.h_o + L_) * P.c_ob + nl;
+                }
+                m[e] = (ph && j < M && (orow || vi[e] >= 0)) ? ph[(j << P.logs) + u] : 0u;
+                kr += dk;
+                lc += dl;
+                if (lc >= P.h_p) { lc -= P.h_p; ++kr; }
             }
-            ii[e] = (j << P.logs) + u;
-            const bool owned = u == nl * P.step && nl < ch0 + ncc;
-            sidx[e] = owned ? (nl - ch0) * stride + PAD(j) : -1;
-            // valid slot (a8): j = stride*(K h_p + L), K < w_o, L < h_o
+            u64 en[EB];
+#pragma unroll
+            for (int e = 0; e < EB; ++e) {
+                const int j = j0 + e * jstep;
+                en[e] = (ph && j < M && (orow || vi[e] >= 0))
+                            ? enc_lookup(enc_tab, l, t, m[e], Lm, r_t, t_inv) : 0;
+            }
+#pragma unroll
+            for (int e = 0; e < EB; ++e) {
+                const int j = j0 + e * jstep;
+                if (j >= M || (!orow && vi[e] < 0)) continue;
+                u64 v = 0;
+                if (owned)
+                    v = DP ? d2canon(reinterpret_cast<const double*>(sm)[abase + PAD(j)], Lm.qd,
+                                     Lm.qinvd)
+                           : reduce_full(sm[abase + PAD(j)], q, Lm.one_p);
+                v = addmod(v, en[e], q);
+                if (orow) orow[(j << P.logs) + u] = v;
+                if (vi[e] >= 0) crow[vi[e]] = v;
+            }
+        }
+    }
+    // (w > blockDim, i.e. more than 256 slot columns per chunk: a second
+    //  sweep covers the remaining columns)
+    for (int ub = blockDim.x; ub < w; ub += blockDim.x) {
+        const int u = u0 + ub + threadIdx.x;
+        if (u >= u1) continue;
+        const int nl = u / P.step;
+        const bool owned = u == nl * P.step && nl < ch0 + ncc;
+        for (int j = 0; j < M; ++j) {
+            const int kr = j / P.h_p, lc = j - kr * P.h_p;
             int vidx = -1;
             if (crow && owned) {
-                int kr = (int)((float)j * inv_hp);
-                if (kr * P.h_p > j) --kr;
-                if ((kr + 1) * P.h_p <= j) ++kr;
-                const int lc = j - kr * P.h_p;
                 const int K_ = kr >> lstr, L_ = lc >> lstr;
                 if (((kr | lc) & (P.stride - 1)) == 0 && K_ < P.w_o && L_ < P.h_o)
                     vidx = (K_ * P.h_o + L_) * P.c_ob + nl;
             }
-            vi[e] = vidx;
-            go[e] = idx < M * w && (orow || vidx >= 0);
-            m[e] = (ph && go[e]) ? ph[ii[e]] : 0u;
-        }
-        u64 en[EB];
-#pragma unroll
-        for (int e = 0; e < EB; ++e)
-            en[e] = (ph && go[e]) ? enc_lookup(enc_tab, l, t, m[e], Lm, r_t, t_inv) : 0;
-#pragma unroll
-        for (int e = 0; e < EB; ++e) {
-            if (!go[e]) continue;
+            if (!orow && vidx < 0) continue;
             u64 v = 0;
-            if (sidx[e] >= 0)
-                v = DP ? d2canon(reinterpret_cast<const double*>(sm)[sidx[e]], Lm.qd, Lm.qinvd)
-                       : reduce_full(sm[sidx[e]], q, Lm.one_p);
-            v = addmod(v, en[e], q);
-            if (orow) orow[ii[e]] = v;
-            if (vi[e] >= 0) crow[vi[e]] = v;
+            if (owned)
+                v = DP ? d2canon(reinterpret_cast<const double*>(sm)[(nl - ch0) * stride + PAD(j)],
+                                 Lm.qd, Lm.qinvd)
+                       : reduce_full(sm[(nl - ch0) * stride + PAD(j)], q, Lm.one_p);
+            if (ph) v = addmod(v, enc_lookup(enc_tab, l, t, ph[(j << P.logs) + u], Lm, r_t, t_inv), q);
+            if (orow) orow[(j << P.logs) + u] = v;
+            if (vidx >= 0) crow[vidx] = v;
         }
     }
 }
