@@ -54,6 +54,8 @@ def parse():
                     help="split every layer's image batch into this many "
                          "sub-batches, each on its own CUDA stream (1 = one launch "
                          "sequence per layer)")
+    ap.add_argument("--graph", type=int, default=1,
+                    help="1: replay the step as a captured CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true",
@@ -247,7 +249,9 @@ def main():
     dev = torch.device("cuda", local)
     B, N, L = cfg.B, cfg.N, cfg.L
     ctx = he.Context(cfg.primes, cfg.log2N, cfg.t, local)
-    stream = torch.cuda.current_stream()
+    # all work on a dedicated (non-default) stream: CUDA-graph capture needs it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
 
     def d(a):
         a = np.ascontiguousarray(a)
@@ -347,6 +351,16 @@ def main():
 
     for _ in range(args.warmup):
         step()
+    graph = None
+    if args.graph and not args.profile:
+        # the whole step (both sub-batch streams, every layer) as one graph
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
+    run_step = graph.replay if graph is not None else step
     mk = lambda: torch.cuda.Event(enable_timing=True)
     # ---- timed region 1 (the headline value): the step as configured
     e0, e1 = mk(), mk()
@@ -355,7 +369,7 @@ def main():
     with (sampler if not args.profile else _Null()):
         e0.record()
         for k in range(args.steps):
-            step()
+            run_step()
         e1.record()
         barrier()
     ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
@@ -610,7 +624,7 @@ def main():
                                    f"N={N}, L={L}, B={B}/GPU",
                        "global_batch": B * world, "N": N, "L": L,
                        "parallelism": f"dp{world} (batch-sharded, no collective)",
-                       "streams": nstr,
+                       "streams": nstr, "cuda_graph": graph is not None,
                        "l2": "inputs larger than L2 (>1 GB touched per step)"},
             "ms_per_plain20_image": ms_step / B if cfg.idx == 4 else None,
             "sequential_ms_per_step": ms_seq,
