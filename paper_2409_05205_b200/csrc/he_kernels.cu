@@ -891,131 +891,141 @@ template <int TB16>
 __global__ void __launch_bounds__(512)
 k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
            u64* __restrict__ out, int B, int L, int M, int c_o, int Kp, int G, int GS,
-           int KC, int Gt, const he_limb* __restrict__ limbs) {
+           int KC, int Gt, int nbuf, const he_limb* __restrict__ limbs) {
     extern __shared__ u32 sm32[];
     constexpr int rows = 16 * TB16;
     const int nrow = (c_o + 7) & ~7, nnt = nrow >> 3;
     const int swc = imma_sw_dev(KC);
     const int rw = imma_sw_dev(GS * KC);                  // A row: GS groups x KC bytes
     const int gb = 7 * nrow * swc;                        // B words per group
-    u32* sA = sm32;                                       // [7][rows][rw]
-    u32* sB = sm32 + 7 * rows * rw;                       // [GS][7][nrow][swc]
+    const int buf_words = 7 * rows * rw + GS * gb;        // one staging buffer
     const int nGc = (M + G - 1) / G;
     const int l = blockIdx.x / nGc, g0 = (blockIdx.x - l * nGc) * G;
     const int b0 = blockIdx.y * rows;
     const int gcnt = min(G, M - g0);
     const int nkc = Kp / KC;
-    // padded B rows (n >= c_o) stay zero for the whole kernel
-    for (int e = threadIdx.x; e < GS * 7 * (nrow - c_o) * swc; e += blockDim.x) {
-        const int w = e % swc, r = e / swc;
-        const int n = c_o + r % (nrow - c_o), gj = r / (nrow - c_o);
-        sB[(gj * nrow + n) * swc + w] = 0;
+    const int nunits = ((gcnt + GS - 1) / GS) * nkc;      // (group block, k-chunk)
+    // padded B rows (n >= c_o) stay zero for the whole kernel (every buffer)
+    for (int bf = 0; bf < nbuf; ++bf) {
+        u32* sB = sm32 + bf * buf_words + 7 * rows * rw;
+        for (int e = threadIdx.x; e < GS * 7 * (nrow - c_o) * swc; e += blockDim.x) {
+            const int w = e % swc, r = e / swc;
+            const int n = c_o + r % (nrow - c_o), gj = r / (nrow - c_o);
+            sB[(gj * nrow + n) * swc + w] = 0;
+        }
     }
+    // cp.async one unit into staging buffer `bf`
+    auto issue = [&](int u, int bf) {
+        const int gu = (u / nkc) * GS, kc = u - (u / nkc) * nkc;
+        const int gsn = min(GS, gcnt - gu), k0 = kc * KC;
+        u32* sA = sm32 + bf * buf_words;
+        u32* sB = sA + 7 * rows * rw;
+        {   // A: per (plane, image) the unit's gsn groups x KC bytes are contiguous
+            const int gbk = (g0 + gu) / Gt, gi0 = (g0 + gu) - gbk * Gt;
+            const int rcpr = (gsn * KC) >> 4;
+            const FastDiv drc(rcpr);
+            const int per = rows * rcpr;
+            const size_t plane_stride = (size_t)B * Gt * Kp;
+            const unsigned char* a0 = A + ((((size_t)l * (M / Gt) + gbk) * 7) * B + b0) * Gt * Kp +
+                                      (size_t)gi0 * Kp + k0;
+            for (int e = threadIdx.x; e < per; e += blockDim.x) {
+                const int bl = drc.div(e), c = e - bl * rcpr;
+                const bool ok = b0 + bl < B;
+                const unsigned char* src = a0 + (size_t)bl * Gt * Kp + c * 16;
+                unsigned char* dst = reinterpret_cast<unsigned char*>(sA + (size_t)bl * rw) + c * 16;
+#pragma unroll
+                for (int j = 0; j < 7; ++j)
+                    cp_async_n<16>(dst + (size_t)j * rows * rw * 4, ok ? src + j * plane_stride : A,
+                                   ok);
+            }
+        }
+        {   // B: per (group, plane) a contiguous c_o x KC block
+            const int cpr2 = KC >> 4;
+            const FastDiv dc(cpr2), dn(c_o * cpr2);
+            const int per = c_o * cpr2, total = gsn * per;
+            const unsigned char* f0 = Fpl + (((size_t)l * M + g0 + gu) * 7) * c_o * Kp + k0;
+            for (int e = threadIdx.x; e < total; e += blockDim.x) {
+                const int gi = dn.div(e), rem = e - gi * per;
+                const int n = dc.div(rem), c = rem - n * cpr2;
+                const unsigned char* src = f0 + ((size_t)gi * 7 * c_o + n) * Kp + c * 16;
+                unsigned char* dst =
+                    reinterpret_cast<unsigned char*>(sB + ((size_t)gi * 7 * nrow + n) * swc) + c * 16;
+#pragma unroll
+                for (int j = 0; j < 7; ++j)
+                    cp_async_n<16>(dst + (size_t)j * nrow * swc * 4, src + (size_t)j * c_o * Kp, true);
+            }
+        }
+        cp_async_commit();
+    };
+
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gq = lane >> 2, tq = lane & 3;
     const int bt = warp / nnt, nt = warp - bt * nnt;
     const he_limb Lm = limbs[l];
     int acc[13][4];
-    for (int gu = 0; gu < gcnt; gu += GS) {
-        const int gsn = min(GS, gcnt - gu);
-        for (int kc = 0; kc < nkc; ++kc) {
-            const int k0 = kc * KC;
-            // ---- stage A: per (plane, image) the unit's gsn groups x KC bytes
-            //      are contiguous (KC = Kp, or gsn = 1): rows of rcpr 16-byte chunks
-            {
-                const int gbk = (g0 + gu) / Gt, gi0 = (g0 + gu) - gbk * Gt;
-                const int rcpr = (gsn * KC) >> 4;
-                const FastDiv drc(rcpr);
-                const int per = rows * rcpr;
-                const size_t plane_stride = (size_t)B * Gt * Kp;
-                const unsigned char* a0 =
-                    A + ((((size_t)l * (M / Gt) + gbk) * 7) * B + b0) * Gt * Kp +
-                    (size_t)gi0 * Kp + k0;
-                for (int e = threadIdx.x; e < per; e += blockDim.x) {
-                    const int bl = drc.div(e), c = e - bl * rcpr;
-                    const bool ok = b0 + bl < B;
-                    const unsigned char* src = a0 + (size_t)bl * Gt * Kp + c * 16;
-                    unsigned char* dst =
-                        reinterpret_cast<unsigned char*>(sA + (size_t)bl * rw) + c * 16;
-#pragma unroll
-                    for (int j = 0; j < 7; ++j)
-                        cp_async_n<16>(dst + (size_t)j * rows * rw * 4,
-                                       ok ? src + j * plane_stride : A, ok);
-                }
-            }
-            // ---- stage B: per (group, plane) a contiguous c_o x KC block
-            {
-                const int cpr2 = KC >> 4;
-                const FastDiv dc(cpr2), dn(c_o * cpr2);
-                const int per = c_o * cpr2, total = gsn * per;
-                const unsigned char* f0 = Fpl + (((size_t)l * M + g0 + gu) * 7) * c_o * Kp + k0;
-                for (int e = threadIdx.x; e < total; e += blockDim.x) {
-                    const int gi = dn.div(e), rem = e - gi * per;
-                    const int n = dc.div(rem), c = rem - n * cpr2;
-                    const unsigned char* src = f0 + ((size_t)gi * 7 * c_o + n) * Kp + c * 16;
-                    unsigned char* dst = reinterpret_cast<unsigned char*>(
-                                             sB + ((size_t)gi * 7 * nrow + n) * swc) + c * 16;
-#pragma unroll
-                    for (int j = 0; j < 7; ++j)
-                        cp_async_n<16>(dst + (size_t)j * nrow * swc * 4,
-                                       src + (size_t)j * c_o * Kp, true);
-                }
-            }
-            cp_async_commit();
+    issue(0, 0);
+    for (int u = 0; u < nunits; ++u) {
+        if (nbuf == 2 && u + 1 < nunits) {                 // prefetch the next unit
+            issue(u + 1, (u + 1) & 1);
+            cp_async_wait<1>();
+        } else {
             cp_async_wait<0>();
-            __syncthreads();
-            for (int gi = 0; gi < gsn; ++gi) {
-                if (kc == 0) {
+        }
+        __syncthreads();
+        const int gu = (u / nkc) * GS, kc = u - (u / nkc) * nkc;
+        const int gsn = min(GS, gcnt - gu);
+        const u32* sA = sm32 + (nbuf == 2 ? (u & 1) : 0) * buf_words;
+        const u32* sB = sA + 7 * rows * rw;
+        for (int gi = 0; gi < gsn; ++gi) {
+            if (kc == 0) {
 #pragma unroll
-                    for (int d = 0; d < 13; ++d)
+                for (int d = 0; d < 13; ++d)
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) acc[d][e] = 0;
+                    for (int e = 0; e < 4; ++e) acc[d][e] = 0;
+            }
+            const u32* ab = sA + (bt * 16 + gq) * rw + gi * (KC >> 2) + tq;
+            const u32* bb = sB + (size_t)gi * gb + (nt * 8 + gq) * swc + tq;
+            const int Kw = KC >> 2;
+            int kw = 0;
+            for (; kw + 8 <= Kw; kw += 8) {
+                u32 bf0[7], bf1[7];
+#pragma unroll
+                for (int j = 0; j < 7; ++j) {
+                    bf0[j] = bb[j * nrow * swc + kw];
+                    bf1[j] = bb[j * nrow * swc + kw + 4];
                 }
-                const u32* ab = sA + (bt * 16 + gq) * rw + gi * (KC >> 2) + tq;
-                const u32* bb = sB + (size_t)gi * gb + (nt * 8 + gq) * swc + tq;
-                const int Kw = KC >> 2;
-                int kw = 0;
-                for (; kw + 8 <= Kw; kw += 8) {
-                    u32 bf0[7], bf1[7];
 #pragma unroll
-                    for (int j = 0; j < 7; ++j) {
-                        bf0[j] = bb[j * nrow * swc + kw];
-                        bf1[j] = bb[j * nrow * swc + kw + 4];
-                    }
+                for (int i = 0; i < 7; ++i) {
+                    const u32* ap = ab + i * rows * rw + kw;
+                    const u32 a0 = ap[0], a1 = ap[8 * rw], a2 = ap[4], a3 = ap[8 * rw + 4];
 #pragma unroll
-                    for (int i = 0; i < 7; ++i) {
-                        const u32* ap = ab + i * rows * rw + kw;
-                        const u32 a0 = ap[0], a1 = ap[8 * rw], a2 = ap[4], a3 = ap[8 * rw + 4];
-#pragma unroll
-                        for (int j = 0; j < 7; ++j)
-                            mma_k32(acc[i + j], a0, a1, a2, a3, bf0[j], bf1[j]);
-                    }
-                }
-                if (kw < Kw) {                               // one k16 step
-                    u32 bf0[7];
-#pragma unroll
-                    for (int j = 0; j < 7; ++j) bf0[j] = bb[j * nrow * swc + kw];
-#pragma unroll
-                    for (int i = 0; i < 7; ++i) {
-                        const u32* ap = ab + i * rows * rw + kw;
-                        const u32 a0 = ap[0], a1 = ap[8 * rw];
-#pragma unroll
-                        for (int j = 0; j < 7; ++j) mma_k16(acc[i + j], a0, a1, bf0[j]);
-                    }
-                }
-                if (kc == nkc - 1) {
-                    const int g = g0 + gu + gi;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int b = b0 + bt * 16 + gq + 8 * (e >> 1);
-                        const int n = nt * 8 + 2 * tq + (e & 1);
-                        if (b < B && n < c_o)
-                            out[(((size_t)l * B + b) * c_o + n) * M + g] = reduce13(acc, e, Lm);
-                    }
+                    for (int j = 0; j < 7; ++j) mma_k32(acc[i + j], a0, a1, a2, a3, bf0[j], bf1[j]);
                 }
             }
-            __syncthreads();
+            if (kw < Kw) {                                   // one k16 step
+                u32 bf0[7];
+#pragma unroll
+                for (int j = 0; j < 7; ++j) bf0[j] = bb[j * nrow * swc + kw];
+#pragma unroll
+                for (int i = 0; i < 7; ++i) {
+                    const u32* ap = ab + i * rows * rw + kw;
+                    const u32 a0 = ap[0], a1 = ap[8 * rw];
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) mma_k16(acc[i + j], a0, a1, bf0[j]);
+                }
+            }
+            if (kc == nkc - 1) {
+                const int g = g0 + gu + gi;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int b = b0 + bt * 16 + gq + 8 * (e >> 1);
+                    const int n = nt * 8 + 2 * tq + (e & 1);
+                    if (b < B && n < c_o)
+                        out[(((size_t)l * B + b) * c_o + n) * M + g] = reduce13(acc, e, Lm);
+                }
+            }
         }
+        __syncthreads();                                   // buffer free for refill
     }
 }
 
@@ -1026,29 +1036,38 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
     const int Kp = imma_kp(K);
     const int nrow = (c_o + 7) & ~7, nnt = nrow / 8;
     if (nnt > 32) return HE_ESHAPE;                       // c_o <= 256
-    const int TB16 = (nnt <= 8 && B > 16) ? 2 : 1;
-    const int rows = 16 * TB16, warps = TB16 * nnt;
-    const size_t budget = 48 * 1024;                      // several CTAs per SM
-    // one unit = GS groups x KC bytes of k
     const int Gt = tile_gt(M);
-    auto unit_bytes = [&](int gs, int kc) {
+    const size_t budget = 48 * 1024;                      // per staging buffer
+    auto unit_bytes = [&](int rows, int gs, int kc) {
         return sizeof(u32) * 7 * ((size_t)rows * imma_sw(gs * kc) + (size_t)gs * nrow * imma_sw(kc));
     };
+    // 32-image tiles for small c_o; 16-image tiles (<= 256 threads, two
+    // CTAs per SM) when the whole K does not fit one buffer
+    int TB16 = (nnt <= 8 && B > 16) ? 2 : 1;
+    if (TB16 == 2 && unit_bytes(32, 1, Kp) > budget) TB16 = 1;
+    const int rows = 16 * TB16, warps = TB16 * nnt;
     int KC = Kp, GS = 1, G = 1;
-    if (unit_bytes(1, Kp) <= budget) {
+    if (unit_bytes(rows, 1, Kp) <= budget) {
         GS = 1;
-        while (GS < Gt && unit_bytes(GS * 2, Kp) <= budget) GS *= 2;
+        while (GS < Gt && unit_bytes(rows, GS * 2, Kp) <= budget) GS *= 2;
         G = GS;
     } else {
         KC = (Kp % 64 == 0) ? 64 : ((Kp % 32 == 0) ? 32 : 16);
-        GS = G = 1;
+        GS = 1;
+        // several groups per CTA so the k-chunk pipeline has depth, while
+        // keeping >= ~4 CTAs of work per SM
+        const long ctas1 = (long)L * M * ((B + rows - 1) / rows);
+        G = 1;
+        while (G < Gt && ctas1 / (G * 2) >= 4 * 148) G *= 2;
     }
-    const size_t smem = unit_bytes(GS, KC);
+    const int nunits = ((G + GS - 1) / GS) * (Kp / KC);
+    const int nbuf = nunits > 1 ? 2 : 1;
+    const size_t smem = nbuf * unit_bytes(rows, GS, KC);
     if (smem > 227 * 1024) return HE_ESHAPE;
     auto k = TB16 == 2 ? k_mac_imma<2> : k_mac_imma<1>;
     if (!set_smem(k, smem)) return HE_ECUDA;
     dim3 grid(L * ((M + G - 1) / G), (B + rows - 1) / rows);
-    k<<<grid, 32 * warps, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, G, GS, KC, Gt, limbs);
+    k<<<grid, 32 * warps, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, G, GS, KC, Gt, nbuf, limbs);
     return HE_OK;
 }
 
