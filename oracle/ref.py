@@ -730,3 +730,63 @@ def phi1_stream(seed: int, n: int, t: int) -> np.ndarray:
         z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         z = z ^ (z >> np.uint64(31))
     return (z % np.uint64(t)).astype(np.uint32)
+
+
+# ---------------------------------------------------------------------------
+# Client mirror path of Algorithm 1 as separate steps (pinned through
+# conv_protocol_decrypt's decryption test and tests/test_oracle_protocol.py).
+# ---------------------------------------------------------------------------
+def server_p(W: np.ndarray, plan: ConvPlan, ring: Ring, a: np.ndarray,
+             ef: Dict[Tuple[int, int], np.ndarray]) -> np.ndarray:
+    """Alg. 1 Line 5: p_beta^{(n)} = fhat_beta^{(n)} a + e_f
+    (fhat with the Eq. (7) shift).  a [L][N]; ef[(n, beta)] int64 [N].
+    Returns uint64 [c_o][n_ib][L][N]."""
+    out = np.empty((plan.c_o, plan.n_ib, ring.L, ring.N), np.uint64)
+    for n in range(plan.c_o):
+        for beta in range(plan.n_ib):
+            terms = filter_terms(W, plan, n, beta, shifted=True)
+            e = signed_to_residues(ef[(n, beta)], ring)
+            for j, q in enumerate(ring.primes):
+                out[n, beta, j] = ((sparse_mul(a[j], terms, q).astype(object)
+                                    + e[j].astype(object)) % q).astype(np.uint64)
+    return out
+
+
+def client_c1r(vs: np.ndarray, p: np.ndarray, plan: ConvPlan, ring: Ring
+               ) -> np.ndarray:
+    """Alg. 1 Lines 21-24: c1^{(n)} = sum_beta
+    (v_beta s) p_beta^{(n)} at the valid slots s j + t_n of channel n
+    (Lines 22-24 gather exactly c0^r's slots), 0 elsewhere (R13, R14).
+    vs uint64 [B][n_ib][L][N] (residues of v_beta s); p from server_p.
+    Returns uint64 [B][n_ob][L][N]."""
+    B = vs.shape[0]
+    N = ring.N
+    out = np.zeros((B, plan.n_ob, ring.L, N), np.uint64)
+    pos_block = output_positions(plan)
+    for b in range(B):
+        for ob in range(plan.n_ob):
+            for nl in range(plan.c_ob):
+                n = ob * plan.c_ob + nl
+                if n >= plan.c_o:
+                    break
+                pos = pos_block[nl::plan.c_ob]            # this channel's slots
+                for j, q in enumerate(ring.primes):
+                    acc = np.zeros(pos.size, dtype=object)
+                    for beta in range(plan.n_ib):
+                        acc = (acc + negacyclic_at(vs[b, beta, j], p[n, beta, j], q,
+                                                   pos).astype(object)) % q
+                    out[b, ob, j, pos] = acc.astype(np.uint64)
+    return out
+
+
+def decrypt_round(r: np.ndarray, ring: Ring) -> np.ndarray:
+    """Eq. (2) in the BFV reading: m = round(t CRT(r) / Q) mod t, per
+    coefficient of r [..][L][N] (exact big integers).  uint32 [..][N]."""
+    r = np.asarray(r)
+    lead = r.shape[:-2]
+    flat = r.reshape((-1, ring.L, ring.N))
+    out = np.empty((flat.shape[0], ring.N), np.uint32)
+    for i in range(flat.shape[0]):
+        out[i] = np.array(crt_decode([flat[i, j] for j in range(ring.L)], ring),
+                          dtype=np.uint32)
+    return out.reshape(lead + (ring.N,))

@@ -76,3 +76,99 @@ def test_fc_protocol_decrypts_to_wi_plus_b():
     ef = synth.gauss_poly(cfg.N, 3.2, seed, "ef", 0)
     dec = R.fc_protocol_decrypt(ring, W, out[0], s_key, a, v, ef, phi[0])
     assert np.array_equal(dec, R.centered_mod_t(W @ I + Bv, cfg.t))
+
+
+def _client_steps(cfg_idx: int, layer, B: int = 2):
+    """The client mirror path as separate oracle steps (server_p,
+    client_c1r, decrypt_round) decrypts to the brute-force conv mod t."""
+    cfg = synth.CONFIGS[cfg_idx]
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    plan = R.plan_conv(layer, cfg.N)
+    seed = cfg.seed + 5
+    s_key = synth.secret_key(cfg.N, cfg.h, seed)
+    a = synth.uniform_residues((ring.L, cfg.N), cfg.primes, seed, "a")
+    b_pk = R.keygen(ring, s_key, a, synth.gauss_poly(cfg.N, cfg.sigma, seed, "e0", 9))
+    rng = np.random.default_rng(seed)
+    # the config's value ranges keep the noise inside Delta/2 (config 1 has
+    # a single 30-bit limb)
+    imgs = rng.integers(cfg.img_lo, cfg.img_hi + 1,
+                        (B, layer.c_i, layer.w_i, layer.h_i))
+    W = rng.integers(cfg.w_lo, cfg.w_hi + 1,
+                     (layer.c_o, layer.c_i, layer.f_w, layer.f_h))
+    phi = synth.phi1((B, plan.n_ob, cfg.N), cfg.t, seed)
+    c0 = np.empty((B, plan.n_ib, ring.L, cfg.N), np.uint64)
+    vs = np.empty_like(c0)
+    for b in range(B):
+        ip = R.pack_input_int(imgs[b], plan)
+        for beta in range(plan.n_ib):
+            v = synth.v_poly(cfg.N, seed, b, beta)
+            c0[b, beta] = R.encrypt_c0(ring, ip[beta], b_pk, v, synth.gauss_poly(
+                cfg.N, cfg.sigma, seed, "e0", b, beta))
+            vs[b, beta] = R.signed_to_residues(
+                np.array(R.schoolbook_py(v, s_key, cfg.N)), ring)
+    out = R.conv_server(c0, W, plan, ring, phi)
+    ef = {(n, beta): synth.gauss_poly(cfg.N, cfg.sigma, seed, "ef", n, beta)
+          for n in range(plan.c_o) for beta in range(plan.n_ib)}
+    p = R.server_p(W, plan, ring, a, ef)
+    c1 = R.client_c1r(vs, p, plan, ring)
+    # c1^r is zero outside the valid slots, like c0^r's payload
+    pos = R.output_positions(plan)
+    mask = np.ones(cfg.N, bool)
+    mask[pos] = False
+    assert not c1[..., mask].any()
+    qo = np.array(ring.primes, dtype=object)[None, None, :, None]
+    m = R.decrypt_round((out.astype(object) + c1.astype(object)) % qo, ring)
+    for b in range(B):
+        ref = R.centered_mod_t(R.conv2d_ref(imgs[b], W, plan), cfg.t)
+        for ob in range(plan.n_ob):
+            got = (m[b, ob, pos].astype(np.int64) - phi[b, ob, pos]) % cfg.t
+            got = np.where(got > cfg.t // 2, got - cfg.t, got)
+            for nl in range(plan.c_ob):
+                n = ob * plan.c_ob + nl
+                if n < plan.c_o:
+                    assert np.array_equal(got[nl::plan.c_ob],
+                                          ref[n].ravel()), (b, n)
+
+
+def test_client_steps_config1():
+    _client_steps(1, synth.CONFIGS[1].conv[0])
+
+
+def test_client_steps_two_blocks_each_way():
+    # n_ib = n_ob = 2 on config 1's ring: c_i = c_o = 2 s
+    L0 = synth.CONFIGS[1].conv[0]
+    plan0 = R.plan_conv(L0, 1024)
+    Ly = synth.ConvLayer(c_i=2 * plan0.s, c_o=2 * plan0.s, w_i=L0.w_i, h_i=L0.h_i,
+                         f_w=3, f_h=3, stride=1, pad=1)
+    plan = R.plan_conv(Ly, 1024)
+    assert plan.n_ib == 2 and plan.n_ob == 2
+    _client_steps(1, Ly, B=1)
+
+
+def test_decrypt_round_definition():
+    # round(t r / Q) mod t by exact rationals with an independent CRT on
+    # random residues, and Delta m + small noise decrypts to m (Eq. (2) in
+    # the BFV reading R1)
+    from fractions import Fraction
+    cfg = synth.CONFIGS[2]
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    rng = np.random.default_rng(3)
+    r = np.stack([rng.integers(0, q, cfg.N, dtype=np.uint64) for q in ring.primes])
+    got = R.decrypt_round(r, ring)
+    Q = 1
+    for q in ring.primes:
+        Q *= q
+    for k in range(0, cfg.N, 97):
+        val = 0
+        for j, q in enumerate(ring.primes):
+            Qj = Q // q
+            val += int(r[j, k]) * Qj * pow(Qj, -1, q)
+        val %= Q
+        want = (Fraction(cfg.t * val, Q) + Fraction(1, 2)).__floor__() % cfg.t
+        assert int(got[k]) == want
+    m = rng.integers(0, cfg.t, cfg.N).astype(np.uint32)
+    enc = R.encode(m, ring)
+    noise = rng.integers(-1000, 1000, cfg.N)
+    enc_n = np.stack([(enc[j].astype(object) + noise) % q
+                      for j, q in enumerate(ring.primes)]).astype(np.uint64)
+    assert np.array_equal(R.decrypt_round(enc_n, ring), m)
