@@ -247,6 +247,63 @@ he_status he_ntt_forward(const he_ctx* ctx, uint64_t* d_data, int batch,
 he_status he_ntt_inverse(const he_ctx* ctx, uint64_t* d_data, int batch,
                          void* stream);
 
+/* ----------------------------------------------- client mirror path (§8 f) */
+/* Server initialisation, Alg. 1 Line 5:
+ *   p_beta^{(n)} = fhat_beta^{(n)} a + e_f,
+ * fhat the Eq. (7)-shifted filter polynomial of the same
+ * weights he_pack_filters takes.  d_w int32 [c_o][c_i][f_w][f_h];
+ * d_a uint64 [L][N] canonical residues of the public a; d_ef int32
+ * [c_o][n_ib][N] signed noise e_f (NULL = 0); d_p uint64 [c_o][n_ib][L][N]
+ * (output, canonical).  Full negacyclic products via NTT.  Workspace
+ * he_server_p_workspace_bytes, caller-owned.  Errors: HE_EINVAL null
+ * pointer, HE_ESHAPE foreign plan, HE_ENOMEM workspace too small. */
+size_t he_server_p_workspace_bytes(const he_ctx* ctx, const he_conv_plan* plan);
+he_status he_server_init_p(const he_ctx* ctx, const he_conv_plan* plan,
+                           const int32_t* d_w, const uint64_t* d_a,
+                           const int32_t* d_ef, uint64_t* d_p, void* d_ws,
+                           size_t ws_bytes, void* stream);
+
+/* Client side of Alg. 1 Lines 21-24: from the server's
+ * p (layout of he_server_init_p) build, in he_pack_filters' layout, the
+ * spectra of X^{-t_n} p_beta^{(n)}, so that
+ *   he_conv(ctx, plan, d_vs, B, d_pspec, NULL, d_c1r, ...)
+ * with d_vs[b][beta] = residues of v_beta s returns c1^r: the coefficients
+ * s j + t_n of sum_beta v_beta s p_beta^{(n)} at exactly the slots of c0^r
+ * (zeros elsewhere; d_compact gives the packed payload order).  d_pspec
+ * needs he_filter_bytes; workspace he_pack_filters_workspace_bytes. */
+he_status he_pack_client_p(const he_ctx* ctx, const he_conv_plan* plan,
+                           const uint64_t* d_p, uint64_t* d_pspec, void* d_ws,
+                           size_t ws_bytes, void* stream);
+
+/* Signed small integers -> residues: d_out[i][j][k] = d_x[i][k] mod q_j.
+ * d_x int32 [n_polys][N]; d_out uint64 [n_polys][L][N]. (encryption
+ * randomness v, s, e of Alg. 1 as RNS polynomials) */
+he_status he_residues_from_int(const he_ctx* ctx, const int32_t* d_x,
+                               long n_polys, uint64_t* d_out, void* stream);
+
+/* Negacyclic products in R_Q:
+ *   d_out[b] = d_x[b] * d_y[y_batch == 1 ? 0 : b],  b < B,
+ * all [.][L][N] canonical residues (d_out may alias d_x, not d_y).
+ * Workspace: y_batch x L x N x 8 bytes (the spectra of y).  y_batch must be
+ * 1 or B. */
+he_status he_poly_mul(const he_ctx* ctx, const uint64_t* d_x,
+                      const uint64_t* d_y, int B, int y_batch, uint64_t* d_out,
+                      void* d_ws, size_t ws_bytes, void* stream);
+
+/* Decryption rounding, Eq. (2) in the BFV reading (R1):
+ *   m = round(t r / Q) mod t,  r = CRT(c0r + c1r)   (c1r NULL = 0),
+ * per coefficient of n_polys polynomials of `len` coefficients, stored
+ * [n_polys][L][len] (len = N for full rows, n_valid for the compact
+ * payload).  Computed in RNS: sum_j floor/frac of y_j t / q_j with
+ * y_j = r_j (Q/q_j)^{-1} mod q_j; the integer parts are exact and the
+ * fractional parts are summed in FP64 (error < L 2^-52: a coefficient
+ * decodes differently from the exact definition only if t r / Q lies within
+ * that distance of a half-integer, which a valid ciphertext's noise bound
+ * excludes).  d_m uint32 [n_polys][len]. */
+he_status he_decrypt_round(const he_ctx* ctx, const uint64_t* d_c0r,
+                           const uint64_t* d_c1r, long n_polys, long len,
+                           uint32_t* d_m, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -755,21 +755,21 @@ def server_p(W: np.ndarray, plan: ConvPlan, ring: Ring, a: np.ndarray,
 def client_c1r(vs: np.ndarray, p: np.ndarray, plan: ConvPlan, ring: Ring
                ) -> np.ndarray:
     """Alg. 1 Lines 21-24: c1^{(n)} = sum_beta
-    (v_beta s) p_beta^{(n)} at the valid slots s j + t_n of channel n
-    (Lines 22-24 gather exactly c0^r's slots), 0 elsewhere (R13, R14).
+    (v_beta s) p_beta^{(n)} at the slots s j + t_n, all j, 0 elsewhere --
+    the layout of conv_server's full c0^r (R13, R14); Lines 22-24's payload
+    is compact() of it (the valid slots).
     vs uint64 [B][n_ib][L][N] (residues of v_beta s); p from server_p.
     Returns uint64 [B][n_ob][L][N]."""
     B = vs.shape[0]
     N = ring.N
     out = np.zeros((B, plan.n_ob, ring.L, N), np.uint64)
-    pos_block = output_positions(plan)
     for b in range(B):
         for ob in range(plan.n_ob):
             for nl in range(plan.c_ob):
                 n = ob * plan.c_ob + nl
                 if n >= plan.c_o:
                     break
-                pos = pos_block[nl::plan.c_ob]            # this channel's slots
+                pos = np.arange(plan.t_n(n), N, plan.s)
                 for j, q in enumerate(ring.primes):
                     acc = np.zeros(pos.size, dtype=object)
                     for beta in range(plan.n_ib):

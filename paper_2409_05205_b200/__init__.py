@@ -103,6 +103,13 @@ _sig("he_residues_unpack50", [_P, _SZ, _P, _P])
 _sig("he_phi1_generate", [_P, ctypes.c_uint64, _SZ, _P, _P])
 _sig("he_ntt_forward", [_P, _P, _I, _P])
 _sig("he_ntt_inverse", [_P, _P, _I, _P])
+_sig("he_server_p_workspace_bytes", [_P, ctypes.POINTER(ConvPlan)], _SZ)
+_sig("he_server_init_p", [_P, ctypes.POINTER(ConvPlan), _P, _P, _P, _P, _P,
+                          _SZ, _P])
+_sig("he_pack_client_p", [_P, ctypes.POINTER(ConvPlan), _P, _P, _P, _SZ, _P])
+_sig("he_residues_from_int", [_P, _P, ctypes.c_long, _P, _P])
+_sig("he_poly_mul", [_P, _P, _P, _I, _I, _P, _P, _SZ, _P])
+_sig("he_decrypt_round", [_P, _P, _P, ctypes.c_long, ctypes.c_long, _P, _P])
 
 EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_conv_plan_make", "he_pack_input", "he_filter_bytes",
@@ -111,7 +118,9 @@ EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_pack_fc_input", "he_fc_wspec_bytes", "he_fc_workspace_bytes",
             "he_pack_fc_weights", "he_fc", "he_fc_ex", "he_residues_pack50",
             "he_residues_unpack50", "he_phi1_generate", "he_ntt_forward",
-            "he_ntt_inverse"]
+            "he_ntt_inverse", "he_server_p_workspace_bytes", "he_server_init_p",
+            "he_pack_client_p", "he_residues_from_int", "he_poly_mul",
+            "he_decrypt_round"]
 
 
 def _events(events):
@@ -363,3 +372,69 @@ class Context:
         _check(_lib.he_ntt_inverse(self._h, self._ptr(data), batch,
                                    _stream(stream)), "he_ntt_inverse")
         return data
+
+    # ------------------------------------------- client mirror path (§8 f)
+    def server_init_p(self, p: ConvPlan, W: torch.Tensor, a: torch.Tensor,
+                      ef: Optional[torch.Tensor] = None, stream=None):
+        """Alg. 1 Line 5: p_beta^{(n)} = fhat_beta^{(n)} a + e_f
+        -> int64 view [c_o][n_ib][L][N]."""
+        out = self.empty_u64(p.d.c_o, p.n_ib, self.L, self.N)
+        wsb = _lib.he_server_p_workspace_bytes(self._h, ctypes.byref(p))
+        ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        self._dev(W, a, ef)
+        _check(_lib.he_server_init_p(self._h, ctypes.byref(p), self._ptr(W),
+                                     self._ptr(a), self._ptr(ef),
+                                     self._ptr(out), self._ptr(ws), wsb,
+                                     _stream(stream)), "he_server_init_p")
+        return out
+
+    def pack_client_p(self, p: ConvPlan, pp: torch.Tensor, stream=None):
+        """Spectra of X^{-t_n} p in he_pack_filters' layout (for conv)."""
+        nb = _lib.he_filter_bytes(self._h, ctypes.byref(p))
+        pspec = self.empty_u64(nb // 8)
+        wsb = _lib.he_pack_filters_workspace_bytes(self._h, ctypes.byref(p))
+        ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        self._dev(pp)
+        _check(_lib.he_pack_client_p(self._h, ctypes.byref(p), self._ptr(pp),
+                                     self._ptr(pspec), self._ptr(ws), wsb,
+                                     _stream(stream)), "he_pack_client_p")
+        return pspec
+
+    def residues_from_int(self, x: torch.Tensor, stream=None):
+        """int32 [..][N] -> int64 view [..][L][N] of x mod q_j."""
+        n = x.numel() // self.N
+        out = self.empty_u64(*x.shape[:-1], self.L, self.N)
+        self._dev(x)
+        _check(_lib.he_residues_from_int(self._h, self._ptr(x), n,
+                                         self._ptr(out), _stream(stream)),
+               "he_residues_from_int")
+        return out
+
+    def poly_mul(self, x: torch.Tensor, y: torch.Tensor,
+                 out: Optional[torch.Tensor] = None, stream=None):
+        """Negacyclic products x[b] * y[b or 0] over [B][L][N]."""
+        B = x.numel() // (self.L * self.N)
+        yb = y.numel() // (self.L * self.N)
+        if out is None:
+            out = torch.empty_like(x)
+        wsb = 8 * yb * self.L * self.N
+        ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        self._dev(x, y, out)
+        _check(_lib.he_poly_mul(self._h, self._ptr(x), self._ptr(y), B, yb,
+                                self._ptr(out), self._ptr(ws), wsb,
+                                _stream(stream)), "he_poly_mul")
+        return out
+
+    def decrypt_round(self, c0r: torch.Tensor,
+                      c1r: Optional[torch.Tensor] = None, stream=None):
+        """m = round(t CRT(c0r + c1r) / Q) mod t over [..][L][len]
+        -> int32 view (uint32 values) [..][len]."""
+        ln = c0r.shape[-1]
+        n = c0r.numel() // (self.L * ln)
+        m = torch.empty(*c0r.shape[:-2], ln, dtype=torch.int32,
+                        device=self.device)
+        self._dev(c0r, c1r)
+        _check(_lib.he_decrypt_round(self._h, self._ptr(c0r), self._ptr(c1r),
+                                     n, ln, self._ptr(m), _stream(stream)),
+               "he_decrypt_round")
+        return m

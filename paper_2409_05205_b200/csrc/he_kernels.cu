@@ -596,6 +596,9 @@ extern "C" size_t he_pack_filters_workspace_bytes(const he_ctx* c,
     return he_filter_bytes(c, p);
 }
 
+static he_status finish_filter_spectra(const he_ctx* c, const PlanDev& P, u64* ws,
+                                       uint64_t* d_fspec, cudaStream_t st);
+
 extern "C" he_status he_pack_filters(const he_ctx* c, const he_conv_plan* p,
                                      const int32_t* d_w, uint64_t* d_fspec,
                                      void* d_ws, size_t ws_bytes, void* stream) {
@@ -609,6 +612,14 @@ extern "C" he_status he_pack_filters(const he_ctx* c, const he_conv_plan* p,
     k_pack_filter_coeffs<<<grid_for(total, 256), 256, 0, st>>>(d_w, ws, P, c->L,
                                                                 c->logN, c->d_limb);
     HE_CHECK_LAUNCH();
+    return finish_filter_spectra(c, P, ws, d_fspec, st);
+}
+
+// coefficient polynomials ws [c_o][n_ib][L][N] -> NTT (in place) -> the MAC
+// layout of he_pack_filters (times N^{-1}).
+static he_status finish_filter_spectra(const he_ctx* c, const PlanDev& P, u64* ws,
+                                       uint64_t* d_fspec, cudaStream_t st) {
+    const long total = (long)P.c_o * P.n_ib * c->L * c->N;
     he_status s = launch_ntt_fwd(c, ws, ws, (long)P.c_o * P.n_ib * c->L, 0, st);
     if (s != HE_OK) return s;
     if (use_imma(c, P)) {
@@ -1608,6 +1619,217 @@ extern "C" he_status he_phi1_generate(const he_ctx* c, uint64_t seed, size_t n, 
     if (n == 0) return HE_OK;
     if (!d_phi1) return HE_EINVAL;
     k_phi1<<<grid_for((long)n, 256), 256, 0, STREAM(stream)>>>(seed, n, d_phi1, c->t);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+// ================================================= client mirror path (§8 f)
+__device__ __forceinline__ u64 int_to_res(long w, u64 q) {
+    return w >= 0 ? (u64)w % q : q - 1 - ((u64)(-w) - 1) % q;
+}
+
+__global__ void k_residues_from_int(const int32_t* __restrict__ x, long n_polys, int L,
+                                    int logN, const he_limb* __restrict__ limbs,
+                                    u64* __restrict__ out) {
+    const long N = 1L << logN;
+    const long total = n_polys * L * N;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const long k = idx & (N - 1), r = idx >> logN;
+        const int l = (int)(r % L);
+        const long i = r / L;
+        out[idx] = int_to_res(x[i * N + k], limbs[l].q);
+    }
+}
+
+// x[i][l][k] <- x[i][l][k] * y[(ybc ? 0 : i)][l][k] mod q_l (canonical in/out)
+__global__ void k_pointwise_mul(u64* __restrict__ x, const u64* __restrict__ y, long nx,
+                                int ybc, int L, int logN, const he_limb* __restrict__ limbs) {
+    const long N = 1L << logN;
+    const long total = nx * L * N;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const long k = idx & (N - 1), r = idx >> logN;
+        const int l = (int)(r % L);
+        const long yi = ybc ? (long)l * N + k : idx;
+        const he_limb& Lm = limbs[l];
+        x[idx] = d2canon(dp_mulmod(u2d(x[idx]), u2d(y[yi]), Lm.qd, Lm.qinvd), Lm.qd, Lm.qinvd);
+    }
+}
+
+// Negacyclic shift by +-t_n per output channel n (t_n of Eq. (7)):
+//   dir = +1: out[n][beta][l][i] = (X^{t_n} in)[i] + e[n][beta][i]
+//   dir = -1: out[n][beta][l][i] = (X^{-t_n} in)[i]
+__global__ void k_negashift(const u64* __restrict__ in, const int32_t* __restrict__ e,
+                            u64* __restrict__ out, PlanDev P, int dir, int L, int logN,
+                            const he_limb* __restrict__ limbs) {
+    const long N = 1L << logN;
+    const long total = (long)P.c_o * P.n_ib * L * N;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const long i = idx & (N - 1), r = idx >> logN;
+        const long nb = r / L;
+        const int l = (int)(r % L), n = (int)(nb / P.n_ib);
+        const long tn = (long)(n % P.c_ob) * P.step;
+        const u64 q = limbs[l].q;
+        long src = dir > 0 ? i - tn : i + tn;
+        bool neg = false;
+        if (src < 0) { src += N; neg = true; }
+        if (src >= N) { src -= N; neg = true; }
+        u64 v = in[(r << logN) + src];
+        if (neg && v) v = q - v;
+        if (e) v = addmod(v, int_to_res(e[nb * N + i], q), q);
+        out[idx] = v;
+    }
+}
+
+extern "C" size_t he_server_p_workspace_bytes(const he_ctx* c, const he_conv_plan* p) {
+    if (!c || !p) return 0;
+    return sizeof(u64) * ((size_t)p->d.c_o * p->n_ib + 1) * c->L * c->N;
+}
+
+extern "C" he_status he_server_init_p(const he_ctx* c, const he_conv_plan* p,
+                                      const int32_t* d_w, const uint64_t* d_a,
+                                      const int32_t* d_ef, uint64_t* d_p, void* d_ws,
+                                      size_t ws_bytes, void* stream) {
+    if (!c || !p || !d_w || !d_a || !d_p || !d_ws) return HE_EINVAL;
+    if (!plan_ok(c, p)) return HE_ESHAPE;
+    if (ws_bytes < he_server_p_workspace_bytes(c, p)) return HE_ENOMEM;
+    cudaStream_t st = STREAM(stream);
+    const PlanDev P = plan_dev(p);
+    const long nf = (long)P.c_o * P.n_ib;
+    u64* fa = (u64*)d_ws;                          // [c_o][n_ib][L][N]
+    u64* aspec = fa + nf * c->L * c->N;            // [L][N]
+    const long total = nf * c->L * c->N;
+    k_pack_filter_coeffs<<<grid_for(total, 256), 256, 0, st>>>(d_w, fa, P, c->L, c->logN,
+                                                                c->d_limb);
+    HE_CHECK_LAUNCH();
+    he_status s = launch_ntt_fwd(c, fa, fa, nf * c->L, 0, st);
+    if (s != HE_OK) return s;
+    s = launch_ntt_fwd(c, (const u64*)d_a, aspec, c->L, 0, st);
+    if (s != HE_OK) return s;
+    k_pointwise_mul<<<grid_for(total, 256), 256, 0, st>>>(fa, aspec, nf, 1, c->L, c->logN,
+                                                           c->d_limb);
+    HE_CHECK_LAUNCH();
+    s = launch_ntt_inv(c, fa, fa, nf * c->L, st);                 // f a (unshifted)
+    if (s != HE_OK) return s;
+    k_negashift<<<grid_for(total, 256), 256, 0, st>>>(fa, d_ef, (u64*)d_p, P, +1, c->L,
+                                                       c->logN, c->d_limb);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+extern "C" he_status he_pack_client_p(const he_ctx* c, const he_conv_plan* p,
+                                      const uint64_t* d_p, uint64_t* d_pspec, void* d_ws,
+                                      size_t ws_bytes, void* stream) {
+    if (!c || !p || !d_p || !d_pspec || !d_ws) return HE_EINVAL;
+    if (!plan_ok(c, p)) return HE_ESHAPE;
+    if (ws_bytes < he_pack_filters_workspace_bytes(c, p)) return HE_ENOMEM;
+    cudaStream_t st = STREAM(stream);
+    const PlanDev P = plan_dev(p);
+    u64* ws = (u64*)d_ws;
+    const long total = (long)P.c_o * P.n_ib * c->L * c->N;
+    k_negashift<<<grid_for(total, 256), 256, 0, st>>>((const u64*)d_p, nullptr, ws, P, -1,
+                                                       c->L, c->logN, c->d_limb);
+    HE_CHECK_LAUNCH();
+    return finish_filter_spectra(c, P, ws, d_pspec, st);
+}
+
+extern "C" he_status he_residues_from_int(const he_ctx* c, const int32_t* d_x, long n_polys,
+                                          uint64_t* d_out, void* stream) {
+    if (!c || n_polys < 0) return HE_EINVAL;
+    if (n_polys == 0) return HE_OK;
+    if (!d_x || !d_out) return HE_EINVAL;
+    const long total = n_polys * c->L * c->N;
+    k_residues_from_int<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(
+        d_x, n_polys, c->L, c->logN, c->d_limb, (u64*)d_out);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+extern "C" he_status he_poly_mul(const he_ctx* c, const uint64_t* d_x, const uint64_t* d_y,
+                                 int B, int y_batch, uint64_t* d_out, void* d_ws,
+                                 size_t ws_bytes, void* stream) {
+    if (!c || B < 0 || (y_batch != 1 && y_batch != B)) return HE_EINVAL;
+    if (B == 0) return HE_OK;
+    if (!d_x || !d_y || !d_out || !d_ws) return HE_EINVAL;
+    if (ws_bytes < sizeof(u64) * (size_t)y_batch * c->L * c->N) return HE_ENOMEM;
+    cudaStream_t st = STREAM(stream);
+    u64* yspec = (u64*)d_ws;
+    he_status s = launch_ntt_fwd(c, (const u64*)d_y, yspec, (long)y_batch * c->L, 0, st);
+    if (s != HE_OK) return s;
+    s = launch_ntt_fwd(c, (const u64*)d_x, (u64*)d_out, (long)B * c->L, 0, st);
+    if (s != HE_OK) return s;
+    const long total = (long)B * c->L * c->N;
+    k_pointwise_mul<<<grid_for(total, 256), 256, 0, st>>>((u64*)d_out, yspec, B,
+                                                           y_batch == 1 && B > 1, c->L,
+                                                           c->logN, c->d_limb);
+    HE_CHECK_LAUNCH();
+    return launch_ntt_inv(c, (u64*)d_out, (u64*)d_out, (long)B * c->L, st);
+}
+
+// Decryption constants: y_j = r_j * ((Q/q_j)^{-1} mod q_j) (Shoup pair).
+struct DecConst {
+    u64 inv[64], invp[64];
+};
+
+__global__ void k_decrypt_round(const u64* __restrict__ c0r, const u64* __restrict__ c1r,
+                                long n_polys, long len, int L,
+                                const he_limb* __restrict__ limbs, DecConst dc, u64 t,
+                                u32* __restrict__ m) {
+    const long total = n_polys * len;
+    const double td = (double)t;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const long i = idx / len, k = idx - i * len;
+        const u64* r0 = c0r + i * L * len + k;
+        const u64* r1 = c1r ? c1r + i * L * len + k : nullptr;
+        u64 ai = 0;
+        double fr = 0.0;
+        for (int j = 0; j < L; ++j) {
+            const u64 q = limbs[j].q;
+            u64 r = r0[(long)j * len];
+            if (r1) r = addmod(r, r1[(long)j * len], q);
+            const u64 y = csub(shoup_mul(r, dc.inv[j], dc.invp[j], q), q);
+            // y t = a q + b, 0 <= b < q  (y t < 2^82; a < t)
+            long long a = (long long)((double)y * td / (double)q);
+            long long b = (long long)(y * t - (u64)a * q);          // exact mod 2^64
+            while (b < 0) { b += (long long)q; --a; }
+            while (b >= (long long)q) { b -= (long long)q; ++a; }
+            ai += (u64)a;
+            fr += (double)b / (double)q;
+        }
+        m[idx] = (u32)((ai + (u64)rint(fr)) % t);
+    }
+}
+
+static u64 mulmod_h(u64 a, u64 b, u64 q) { return (u64)((unsigned __int128)a * b % q); }
+static u64 powmod_h(u64 a, u64 e, u64 q) {
+    u64 r = 1;
+    for (; e; e >>= 1, a = mulmod_h(a, a, q))
+        if (e & 1) r = mulmod_h(r, a, q);
+    return r;
+}
+
+extern "C" he_status he_decrypt_round(const he_ctx* c, const uint64_t* d_c0r,
+                                      const uint64_t* d_c1r, long n_polys, long len,
+                                      uint32_t* d_m, void* stream) {
+    if (!c || n_polys < 0 || len < 0) return HE_EINVAL;
+    if (n_polys == 0 || len == 0) return HE_OK;
+    if (!d_c0r || !d_m) return HE_EINVAL;
+    DecConst dc;
+    memset(&dc, 0, sizeof(dc));
+    for (int j = 0; j < c->L; ++j) {
+        const u64 q = c->q_host[j];
+        u64 qh = 1;                                    // (Q / q_j) mod q_j
+        for (int i = 0; i < c->L; ++i)
+            if (i != j) qh = mulmod_h(qh, c->q_host[i] % q, q);
+        dc.inv[j] = powmod_h(qh, q - 2, q);
+        dc.invp[j] = (u64)(((unsigned __int128)dc.inv[j] << 64) / q);
+    }
+    const long total = n_polys * len;
+    k_decrypt_round<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(
+        (const u64*)d_c0r, (const u64*)d_c1r, n_polys, len, c->L, c->d_limb, dc, c->t, d_m);
     HE_CHECK_LAUNCH();
     return HE_OK;
 }

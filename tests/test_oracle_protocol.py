@@ -111,11 +111,14 @@ def _client_steps(cfg_idx: int, layer, B: int = 2):
           for n in range(plan.c_o) for beta in range(plan.n_ib)}
     p = R.server_p(W, plan, ring, a, ef)
     c1 = R.client_c1r(vs, p, plan, ring)
-    # c1^r is zero outside the valid slots, like c0^r's payload
+    # c1^r is zero outside the slots s j + t_n (R14), like the full c0^r
+    for ob in range(plan.n_ob):
+        mask = np.ones(cfg.N, bool)
+        for nl in range(plan.c_ob):
+            if ob * plan.c_ob + nl < plan.c_o:
+                mask[plan.t_n(ob * plan.c_ob + nl)::plan.s] = False
+        assert not c1[:, ob][..., mask].any()
     pos = R.output_positions(plan)
-    mask = np.ones(cfg.N, bool)
-    mask[pos] = False
-    assert not c1[..., mask].any()
     qo = np.array(ring.primes, dtype=object)[None, None, :, None]
     m = R.decrypt_round((out.astype(object) + c1.astype(object)) % qo, ring)
     for b in range(B):
