@@ -58,6 +58,8 @@ def parse():
                     help="1: replay the step as a captured CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-client", action="store_true",
+                    help="skip the client mirror-path measurement")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no e2e / cpu baseline / clocks")
     return ap.parse_args()
@@ -587,6 +589,64 @@ def main():
                "wire": "50-bit packed residues (he_residues_pack50/unpack50); "
                        "phi1 drawn on device (he_phi1_generate)"}
 
+    # ---- client mirror path: the client's per-layer work
+    # of Alg. 1 Lines 21-24 + Eq. (2) -- c1^r = valid slots of
+    # sum_beta (v_beta s) p_beta^{(n)} through he_conv on the spectra of
+    # he_pack_client_p, then he_decrypt_round on the compact payloads -- and
+    # the server's offline p = fhat a + e_f (he_server_init_p), timed once.
+    # v_beta s stand-ins are the resident uniform residues c0_d (the kernels'
+    # cost does not depend on the values).
+    client = None
+    if not args.no_client and not args.profile:
+        a_d = d(synth.uniform_residues((L, N), cfg.primes, cfg.seed, "a"))
+        i0, i1 = mk(), mk()
+        i0.record()
+        pps = [ctx.server_init_p(lw.p, d(synth.weights(cfg, lw.idx)), a_d) for lw in layers]
+        i1.record()
+        torch.cuda.synchronize()
+        p_init_ms = i0.elapsed_time(i1)
+        pspecs = [ctx.pack_client_p(lw.p, pp) for lw, pp in zip(layers, pps)]
+        del pps
+        c1s = [torch.empty_like(c) for c in comps]
+        msgs = [torch.empty(c.shape[:2] + (c.shape[-1],), dtype=torch.int32, device=dev)
+                for c in comps]
+        cl_ev = [[mk() for _ in range(3)] for _ in layers]
+
+        def client_step(E=None):
+            for i, lw in enumerate(layers):
+                if E:
+                    E[i][0].record()
+                ctx.conv(lw.p, c0_d[i], pspecs[i], None, None, ws, compact=c1s[i],
+                         full=False)
+                if E:
+                    E[i][1].record()
+                ctx.decrypt_round(comps[i], c1s[i], out=msgs[i])
+                if E:
+                    E[i][2].record()
+
+        for _ in range(2):
+            client_step()
+        barrier()
+        y0, y1 = mk(), mk()
+        y0.record()
+        for _ in range(args.steps):
+            client_step()
+        y1.record()
+        barrier()
+        ms_client = max_over_ranks(y0.elapsed_time(y1) / args.steps)
+        client_step(cl_ev)
+        torch.cuda.synchronize()
+        c1_ms = sum(E[0].elapsed_time(E[1]) for E in cl_ev)
+        dec_ms = sum(E[1].elapsed_time(E[2]) for E in cl_ev)
+        client = {"ms_per_step": ms_client,
+                  "evals_per_s": sum(lw.evals for lw in layers) * world / (ms_client * 1e-3),
+                  "c1r_ms": c1_ms, "decrypt_ms": dec_ms,
+                  "server_init_p_ms": p_init_ms,
+                  "what": "per step: c1^r (he_conv on he_pack_client_p spectra, compact) "
+                          "+ he_decrypt_round over every conv layer's payload; "
+                          "server_init_p_ms: Alg. 1 Line 5 for all layers, once"}
+        del pspecs, c1s, msgs
+
     # ---- CPU baseline: the oracle as it stands, rank 0, bounded sample
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
@@ -631,7 +691,7 @@ def main():
             "ntt": ntt, "stages_ms_per_step": st, "per_layer": per_layer,
             "roofline": roofline,
             "roofline_all": rl, "u1": u1, "init_ms": init_ms,
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "client": client, "clocks": clocks,
             "gpu_launches": launches_step * args.steps,
         }
         print(json.dumps(line), flush=True)

@@ -426,13 +426,14 @@ class Context:
         return out
 
     def decrypt_round(self, c0r: torch.Tensor,
-                      c1r: Optional[torch.Tensor] = None, stream=None):
+                      c1r: Optional[torch.Tensor] = None,
+                      out: Optional[torch.Tensor] = None, stream=None):
         """m = round(t CRT(c0r + c1r) / Q) mod t over [..][L][len]
         -> int32 view (uint32 values) [..][len]."""
         ln = c0r.shape[-1]
         n = c0r.numel() // (self.L * ln)
-        m = torch.empty(*c0r.shape[:-2], ln, dtype=torch.int32,
-                        device=self.device)
+        m = out if out is not None else torch.empty(
+            *c0r.shape[:-2], ln, dtype=torch.int32, device=self.device)
         self._dev(c0r, c1r)
         _check(_lib.he_decrypt_round(self._h, self._ptr(c0r), self._ptr(c1r),
                                      n, ln, self._ptr(m), _stream(stream)),
