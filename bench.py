@@ -83,7 +83,8 @@ class LayerWork:
         M = N // plan.s
         nlimb = B * plan.n_ib * L
         self.evals = B * Ly.c_o * plan.n_ib
-        self.ntt_bfly = nlimb * (N // 2) * (N.bit_length() - 1)
+        # the fold runs the incomplete transform: log2(N/s) stages
+        self.ntt_bfly = nlimb * (N // 2) * (M.bit_length() - 1)
         self.ntt_bytes = nlimb * N * 16
         self.macs = L * N * plan.n_ib * B * Ly.c_o
         self.mac_bytes = 8 * (nlimb * N + Ly.c_o * plan.n_ib * L * N +

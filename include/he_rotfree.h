@@ -246,6 +246,13 @@ he_status he_ntt_forward(const he_ctx* ctx, uint64_t* d_data, int batch,
                          void* stream);
 he_status he_ntt_inverse(const he_ctx* ctx, uint64_t* d_data, int batch,
                          void* stream);
+/* The first log2(N) - skip stages of he_ntt_forward (the incomplete
+ * transform the conv fold runs): block g of 2^skip
+ * consecutive outputs holds the coefficients of a mod (X^{2^skip} - zeta_g),
+ * zeta_g = psi^{brv(2^{logN-skip-1} + g/2)} for even g and its negative for
+ * odd g (zeta = -1 when skip = log2 N).  In place, canonical. */
+he_status he_ntt_forward_partial(const he_ctx* ctx, uint64_t* d_data, int batch,
+                                 int skip, void* stream);
 
 /* ----------------------------------------------- client mirror path (§8 f) */
 /* Server initialisation, Alg. 1 Line 5:

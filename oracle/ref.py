@@ -790,3 +790,33 @@ def decrypt_round(r: np.ndarray, ring: Ring) -> np.ndarray:
         out[i] = np.array(crt_decode([flat[i, j] for j in range(ring.L)], ring),
                           dtype=np.uint32)
     return out.reshape(lead + (ring.N,))
+
+
+def reduce_mod_binomial(a: np.ndarray, s: int, zeta: int, q: int) -> np.ndarray:
+    """a(X) mod (X^s - zeta) over Z_q by definition: X^{j s + u} =
+    zeta^j X^u, so coefficient u is sum_j a[j s + u] zeta^j (DESIGN.md §4,
+    the incomplete transform behind the fold).  Returns uint64 [s]."""
+    a = [int(x) for x in a]
+    N = len(a)
+    out = [0] * s
+    zj = 1
+    for j in range(N // s):
+        for u in range(s):
+            out[u] = (out[u] + a[j * s + u] * zj) % q
+        zj = zj * zeta % q
+    return np.array(out, dtype=np.uint64)
+
+
+def incomplete_ntt_def(a: np.ndarray, q: int, psi: int, s: int) -> np.ndarray:
+    """The transform the conv fold runs on c0 and f: block g
+    (g < N/s) of s outputs = a mod (X^s - zeta_g), zeta_g =
+    psi^{s (2 brv_{log2(N/s)}(g) + 1)}, the N/s roots of Y^{N/s} = -1 (Y = X^s)
+    in the bit-reversed order of the full NTT (s = 1: ntt_def in bit-reversed
+    order).  Returns uint64 [N]."""
+    N = len(a)
+    T = (N // s).bit_length() - 1
+    out = np.empty(N, np.uint64)
+    for g in range(N // s):
+        b = int(format(g, f"0{T}b")[::-1], 2) if T else 0
+        out[g * s:(g + 1) * s] = reduce_mod_binomial(a, s, pow(psi, s * (2 * b + 1), q), q)
+    return out

@@ -103,6 +103,7 @@ _sig("he_residues_unpack50", [_P, _SZ, _P, _P])
 _sig("he_phi1_generate", [_P, ctypes.c_uint64, _SZ, _P, _P])
 _sig("he_ntt_forward", [_P, _P, _I, _P])
 _sig("he_ntt_inverse", [_P, _P, _I, _P])
+_sig("he_ntt_forward_partial", [_P, _P, _I, _I, _P])
 _sig("he_server_p_workspace_bytes", [_P, ctypes.POINTER(ConvPlan)], _SZ)
 _sig("he_server_init_p", [_P, ctypes.POINTER(ConvPlan), _P, _P, _P, _P, _P,
                           _SZ, _P])
@@ -118,7 +119,7 @@ EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_pack_fc_input", "he_fc_wspec_bytes", "he_fc_workspace_bytes",
             "he_pack_fc_weights", "he_fc", "he_fc_ex", "he_residues_pack50",
             "he_residues_unpack50", "he_phi1_generate", "he_ntt_forward",
-            "he_ntt_inverse", "he_server_p_workspace_bytes", "he_server_init_p",
+            "he_ntt_inverse", "he_ntt_forward_partial", "he_server_p_workspace_bytes", "he_server_init_p",
             "he_pack_client_p", "he_residues_from_int", "he_poly_mul",
             "he_decrypt_round"]
 
@@ -364,6 +365,13 @@ class Context:
         batch = data.numel() // (self.L * self.N)
         _check(_lib.he_ntt_forward(self._h, self._ptr(data), batch,
                                    _stream(stream)), "he_ntt_forward")
+        return data
+
+    def ntt_forward_partial(self, data: torch.Tensor, skip: int, stream=None):
+        self._dev(data)
+        batch = data.numel() // (self.L * self.N)
+        _check(_lib.he_ntt_forward_partial(self._h, self._ptr(data), batch, skip,
+                                           _stream(stream)), "he_ntt_forward_partial")
         return data
 
     def ntt_inverse(self, data: torch.Tensor, stream=None):

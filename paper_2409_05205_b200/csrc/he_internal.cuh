@@ -254,9 +254,12 @@ __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0
 
 template <int RMAX>
 __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg, int split,
-                                          const double* tw, double q, double qinv) {
+                                          const double* tw, double q, double qinv,
+                                          int end) {
+    // stages [split, end): end < logN stops early (incomplete transform)
     int st = split;
-    const int rem = (logN - split) % RMAX;
+    if (st >= end) return;
+    const int rem = (end - split) % RMAX;
     if (rem) {
         if (rem == 1) ct_pass_dp<1>(sm, logN, NS, st, seg, split, tw, q, qinv);
         else if (rem == 2) ct_pass_dp<2>(sm, logN, NS, st, seg, split, tw, q, qinv);
@@ -264,7 +267,7 @@ __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg,
         st += rem;
         __syncthreads();
     }
-    for (; st < logN; st += RMAX) {
+    for (; st < end; st += RMAX) {
         ct_pass_dp<RMAX>(sm, logN, NS, st, seg, split, tw, q, qinv);
         __syncthreads();
     }
@@ -436,9 +439,10 @@ __device__ __forceinline__ void gs_pass(u64* sm, int arr_stride, int narr,
 template <int RMAX, bool LAZY = false>
 __device__ __forceinline__ void ct_all(u64* sm, int logN, int NS, int seg,
                                        int split, const ulonglong2* tw, u64 q,
-                                       u64 q2) {
+                                       u64 q2, int end) {
     int st = split;
-    const int rem = (logN - split) % RMAX;
+    if (st >= end) return;
+    const int rem = (end - split) % RMAX;
     if (rem) {
         if (rem == 1) ct_pass<1, LAZY>(sm, logN, NS, st, seg, split, tw, q, q2);
         else if (rem == 2) ct_pass<2, LAZY>(sm, logN, NS, st, seg, split, tw, q, q2);
@@ -446,7 +450,7 @@ __device__ __forceinline__ void ct_all(u64* sm, int logN, int NS, int seg,
         st += rem;
         __syncthreads();
     }
-    for (; st < logN; st += RMAX) {
+    for (; st < end; st += RMAX) {
         ct_pass<RMAX, LAZY>(sm, logN, NS, st, seg, split, tw, q, q2);
         __syncthreads();
     }

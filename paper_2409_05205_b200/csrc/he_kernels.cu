@@ -60,6 +60,7 @@ static inline int ntt_threads(int NS) { return std::min(512, std::max(16, NS / 1
 // int8 MAC stages each operand tile as contiguous blocks.
 struct TileLay {
     int B, n_ib, logs, Kp, Gt;
+    int skip;       // trailing stages not run: log2(s) for the fold (0 = full)
 };
 static inline int tile_gt(int M) { return M < 16 ? M : 16; }
 
@@ -123,6 +124,7 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
     const double q = limbs[l].qd, qinv = limbs[l].qinvd;
     const double* tw = twd_all + (size_t)l * N;
     const u64* src = in + (size_t)li * N;
+    const int end = logN - T.skip;
     for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
         double vx[1 << S], vy[1 << S];
 #pragma unroll
@@ -133,6 +135,7 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
         }
 #pragma unroll
         for (int st = 0; st < S; ++st) {
+            if (st >= end) break;
             const int half = 1 << (S - 1 - st);
 #pragma unroll
             for (int r = 0; r < (1 << S); ++r) {
@@ -155,7 +158,7 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
     }
     if (S) cg::this_cluster().sync();
     else __syncthreads();
-    ct_all_dp<3>(sm, logN, NS, seg, S, tw, q, qinv);          // outputs < 3.2 q
+    ct_all_dp<3>(sm, logN, NS, seg, S, tw, q, qinv, end);     // outputs < 3.2 q
     ntt_store<OUT_FMT>(out, li, seg, NS, N, L, l, T,
                        [&](int i) { return d2canon(sm[PAD(i)], q, qinv); });
 }
@@ -172,6 +175,7 @@ __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int log
     const u64 q = limbs[l].q, q2 = 2 * q;
     const ulonglong2* tw = tw_all + (size_t)l * N;
     const u64* src = in + (size_t)li * N;
+    const int end = logN - T.skip;
     for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
         u64 vx[1 << S], vy[1 << S];
 #pragma unroll
@@ -182,6 +186,7 @@ __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int log
         }
 #pragma unroll
         for (int st = 0; st < S; ++st) {
+            if (st >= end) break;
             const int half = 1 << (S - 1 - st);
 #pragma unroll
             for (int r = 0; r < (1 << S); ++r) {
@@ -200,7 +205,7 @@ __device__ __forceinline__ void ntt_fwd_segment(const u64* in, u64* out, int log
     }
     if (S) cg::this_cluster().sync();
     else __syncthreads();
-    ct_all<3, true>(sm, logN, NS, seg, S, tw, q, q2);      // lazy: values < 61 q
+    ct_all<3, true>(sm, logN, NS, seg, S, tw, q, q2, end); // lazy: values < 61 q
     const u64 one_p = limbs[l].one_p;
     ntt_store<OUT_FMT>(out, li, seg, NS, N, L, l, T,
                        [&](int i) { return reduce_full(sm[PAD(i)], q, one_p); });
@@ -249,7 +254,7 @@ k_ntt_fwd_dp_s2(const u64* in, u64* out, int logN, int L, const he_limb* __restr
 // Launch the forward NTT over nlimbs = batch * L limbs.
 static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
                                 long nlimbs, int out_fmt, cudaStream_t st,
-                                TileLay T = TileLay{1, 1, 0, 16, 1}) {
+                                TileLay T = TileLay{1, 1, 0, 16, 1, 0}) {
     if (nlimbs <= 0) return HE_OK;
     const int logN = c->logN;
     const int S = logN <= 13 ? 0 : logN - 13;
@@ -388,6 +393,13 @@ extern "C" he_status he_ntt_forward(const he_ctx* c, uint64_t* d, int batch,
                           STREAM(stream));
 }
 
+extern "C" he_status he_ntt_forward_partial(const he_ctx* c, uint64_t* d, int batch,
+                                            int skip, void* stream) {
+    if (!c || !d || batch < 0 || skip < 0 || skip > c->logN) return HE_EINVAL;
+    return launch_ntt_fwd(c, (const u64*)d, (u64*)d, (long)batch * c->L, 0, STREAM(stream),
+                          TileLay{1, 1, 0, 16, 1, skip});
+}
+
 extern "C" he_status he_ntt_inverse(const he_ctx* c, uint64_t* d, int batch,
                                     void* stream) {
     if (!c || !d || batch < 0) return HE_EINVAL;
@@ -521,11 +533,38 @@ __global__ void k_pack_filter_coeffs(const int32_t* __restrict__ W, u64* __restr
     }
 }
 
-// spectra [c_o][n_ib][L][N] (canonical, bit-reversed) -> MAC layout
-// F[l][g][k][n] = split25(spec[n][beta][l][g s + u] * N^{-1}), k = beta s + u.
+// Filter operand of the fold on the incomplete transform:
+// after the first nst = log2(N/s) forward stages, group g (s contiguous
+// words) of the filter holds f mod (X^s - zeta_g), and coefficient 0 of
+// c f mod (X^s - zeta_g) is  sum_u c_{g,u} F'_{g,u}  with
+//   F'_{g,u} = (N/s)^{-1} (u == 0 ? f_{g,0} : zeta_g f_{g,s-u}),
+// zeta_g = +-psi^{brv(2^{nst-1} + g/2)} (the last stage's twiddle, - for
+// odd g; -1 when nst = 0).  spec_l: this (n, beta, limb) row.
+__device__ __forceinline__ u64 fold_filter_operand(const u64* __restrict__ spec_l, int g,
+                                                   int u, int logs, int nst,
+                                                   const he_limb& Lm,
+                                                   const ulonglong2* __restrict__ tw_l) {
+    const int s = 1 << logs;
+    const u64 v = spec_l[((long)g << logs) + ((s - u) & (s - 1))];
+    const double q = Lm.qd, qi = Lm.qinvd;
+    u64 fac = d2canon(dp_mulmod(u2d(Lm.ninv), (double)s, q, qi), q, qi);   // (N/s)^{-1}
+    if (u) {
+        u64 z = Lm.q - 1;
+        if (nst) {
+            z = tw_l[(1 << (nst - 1)) + (g >> 1)].x;
+            if (g & 1) z = Lm.q - z;
+        }
+        fac = d2canon(dp_mulmod(u2d(z), u2d(fac), q, qi), q, qi);
+    }
+    return d2canon(dp_mulmod(u2d(v), u2d(fac), q, qi), q, qi);
+}
+
+// incomplete spectra [c_o][n_ib][L][N] (canonical) -> MAC layout
+// F[l][g][k][n] = split25(F'_{g,u} of (n, beta, l)), k = beta s + u.
 __global__ void k_filter_to_mac(const u64* __restrict__ spec, u64* __restrict__ F,
                                 PlanDev P, int L, int logN,
-                                const he_limb* __restrict__ limbs) {
+                                const he_limb* __restrict__ limbs,
+                                const ulonglong2* __restrict__ tw_fwd) {
     const long N = 1L << logN;
     const int K = P.n_ib * P.s;
     const long total = (long)L * N * P.n_ib * P.c_o;  // = L * M * K * c_o
@@ -540,8 +579,9 @@ __global__ void k_filter_to_mac(const u64* __restrict__ spec, u64* __restrict__ 
         const int l = (int)(r / M);
         const int beta = k >> P.logs, u = k & (P.s - 1);
         const he_limb& Lm = limbs[l];
-        const u64 v = spec[(((long)n * P.n_ib + beta) * L + l) * N + ((long)g << P.logs) + u];
-        F[idx] = to_split25(csub(shoup_mul(v, Lm.ninv, Lm.ninv_p, Lm.q), Lm.q));
+        F[idx] = to_split25(fold_filter_operand(spec + (((long)n * P.n_ib + beta) * L + l) * N,
+                                                g, u, P.logs, logN - P.logs, Lm,
+                                                tw_fwd + (long)l * N));
     }
 }
 
@@ -559,7 +599,8 @@ __device__ __forceinline__ int imma_sw_dev(int Kp) { return Kp / 4 + ((4 - Kp / 
 // spec * N^{-1} (k = beta s + u < K; zero for K <= k < Kp).
 __global__ void k_filter_to_imma(const u64* __restrict__ spec, unsigned char* __restrict__ F,
                                  PlanDev P, int L, int logN, int Kp,
-                                 const he_limb* __restrict__ limbs) {
+                                 const he_limb* __restrict__ limbs,
+                                 const ulonglong2* __restrict__ tw_fwd) {
     const long N = 1L << logN;
     const int K = P.n_ib * P.s, M = (int)(N >> P.logs);
     const long total = (long)L * M * P.c_o * Kp;
@@ -574,8 +615,8 @@ __global__ void k_filter_to_imma(const u64* __restrict__ spec, unsigned char* __
         if (k < K) {
             const he_limb& Lm = limbs[l];
             const int beta = k >> P.logs, u = k & (P.s - 1);
-            v = spec[(((long)n * P.n_ib + beta) * L + l) * N + ((long)g << P.logs) + u];
-            v = csub(shoup_mul(v, Lm.ninv, Lm.ninv_p, Lm.q), Lm.q);
+            v = fold_filter_operand(spec + (((long)n * P.n_ib + beta) * L + l) * N, g, u,
+                                    P.logs, logN - P.logs, Lm, tw_fwd + (long)l * N);
         }
         unsigned char* dst = F + (((long)l * M + g) * 7 * P.c_o + n) * Kp + k;
 #pragma unroll
@@ -620,16 +661,19 @@ extern "C" he_status he_pack_filters(const he_ctx* c, const he_conv_plan* p,
 static he_status finish_filter_spectra(const he_ctx* c, const PlanDev& P, u64* ws,
                                        uint64_t* d_fspec, cudaStream_t st) {
     const long total = (long)P.c_o * P.n_ib * c->L * c->N;
-    he_status s = launch_ntt_fwd(c, ws, ws, (long)P.c_o * P.n_ib * c->L, 0, st);
+    // incomplete forward transform: the first log2(N/s) stages only
+    he_status s = launch_ntt_fwd(c, ws, ws, (long)P.c_o * P.n_ib * c->L, 0, st,
+                                 TileLay{1, 1, 0, 16, 1, P.logs});
     if (s != HE_OK) return s;
     if (use_imma(c, P)) {
         const int Kp = imma_kp(P.n_ib * P.s);
         const long tot = (long)c->L * (c->N >> P.logs) * P.c_o * Kp;
         k_filter_to_imma<<<grid_for(tot, 256), 256, 0, st>>>(ws, (unsigned char*)d_fspec, P,
-                                                              c->L, c->logN, Kp, c->d_limb);
+                                                              c->L, c->logN, Kp, c->d_limb,
+                                                              c->d_tw_fwd);
     } else {
         k_filter_to_mac<<<grid_for(total, 256), 256, 0, st>>>(ws, (u64*)d_fspec, P, c->L,
-                                                               c->logN, c->d_limb);
+                                                               c->logN, c->d_limb, c->d_tw_fwd);
     }
     HE_CHECK_LAUNCH();
     return HE_OK;
@@ -1277,7 +1321,7 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     he_status s = launch_ntt_fwd(c, (const u64*)d_c0, spec, (long)B * P.n_ib * c->L,
                                  imma ? 2 : 1, st,
                                  TileLay{B, P.n_ib, P.logs, imma_kp(P.n_ib * P.s),
-                                         tile_gt(c->N >> P.logs)});
+                                         tile_gt(c->N >> P.logs), P.logs});
     if (s != HE_OK) return s;
     rec(ev, 1, st);
     if (imma)

@@ -395,3 +395,29 @@ def test_integer_transform_path(he, monkeypatch):
     ctx5 = he.Context(cfg5.primes, cfg5.log2N, cfg5.t)
     run_conv(he, ctx5, R.Ring(cfg5.N, cfg5.primes, cfg5.t), cfg5.conv[0], 32,
              seed=9, check_b=[0, 31])
+
+
+@pytest.mark.parametrize("N", [256, 1024, 16384, 32768])
+def test_ntt_forward_partial_matches_definition(he, N):
+    """The incomplete forward transform the conv fold runs
+    against the oracle's definition: blocks of 2^skip outputs = a mod
+    (X^{2^skip} - zeta_g).  Sampled blocks for large N."""
+    primes = RINGS[N]
+    ctx = ctx_for(he, N, primes)
+    logN = N.bit_length() - 1
+    x = synth.uniform_residues((2, len(primes), N), primes, 4, "misc", N)
+    skips = range(logN + 1) if N <= 1024 else (1, 3, 5, 7, logN)
+    for skip in skips:
+        d = dev(x)
+        ctx.ntt_forward_partial(d, skip)
+        got = u64(d)
+        s = 1 << skip
+        M = N // s
+        gs = range(M) if N <= 1024 else sorted(g for g in {0, 1, M - 1, M // 2 + 1} if g < M)
+        for j, q in enumerate(primes):
+            psi = ctx.psi(j)
+            T = M.bit_length() - 1
+            for g in gs:
+                b = int(format(g, f"0{T}b")[::-1], 2) if T else 0
+                want = R.reduce_mod_binomial(x[1, j], s, pow(psi, s * (2 * b + 1), q), q)
+                assert np.array_equal(got[1, j, g * s:(g + 1) * s], want), (skip, j, g)

@@ -133,3 +133,32 @@ def test_splitmix64_phi1_stream():
         assert [int(x) for x in v] == [R.splitmix64_py(seed, i) % 65537
                                        for i in range(257)]
         assert v.max() < 65537
+
+
+def test_incomplete_ntt_definition_pins():
+    # s = 1 is the full NTT in bit-reversed order; s = N is a mod (X^N + 1)
+    # = a; and the fold identity of DESIGN.md §4: coefficient 0 of
+    # c f mod (X^s - zeta_g), summed back through an (N/s)-point inverse
+    # transform, gives the coefficients s j of the negacyclic product
+    rng = np.random.default_rng(11)
+    q, N = 7681, 64
+    psi = R.min_psi(q, N)
+    a = rng.integers(0, q, N).astype(np.uint64)
+    full = R.ntt_def(a, q, psi)
+    brv = [int(format(p, "06b")[::-1], 2) for p in range(N)]
+    assert np.array_equal(R.incomplete_ntt_def(a, q, psi, 1), full[brv])
+    assert np.array_equal(R.incomplete_ntt_def(a, q, psi, N), a)
+    f = rng.integers(0, q, N).astype(np.uint64)
+    prod = R.schoolbook_py(a, f, N, q)
+    for s in (2, 4, 8):
+        A = R.incomplete_ntt_def(a, q, psi, s)
+        Fv = R.incomplete_ntt_def(f, q, psi, s)
+        M = N // s
+        T = M.bit_length() - 1
+        for g in range(M):
+            b = int(format(g, f"0{T}b")[::-1], 2)
+            zeta = pow(psi, s * (2 * b + 1), q)
+            c0 = (int(A[g * s]) * int(Fv[g * s]) + zeta * sum(
+                int(A[g * s + u]) * int(Fv[g * s + s - u]) for u in range(1, s))) % q
+            # = R_0(zeta) with R_0(Y) = sum_j prod[s j] Y^j
+            assert c0 == sum(prod[s * j] * pow(zeta, j, q) for j in range(M)) % q
