@@ -781,15 +781,15 @@ def client_c1r(vs: np.ndarray, p: np.ndarray, plan: ConvPlan, ring: Ring
 
 def decrypt_round(r: np.ndarray, ring: Ring) -> np.ndarray:
     """Eq. (2) in the BFV reading: m = round(t CRT(r) / Q) mod t, per
-    coefficient of r [..][L][N] (exact big integers).  uint32 [..][N]."""
+    coefficient of r [..][L][len] (exact big integers).  uint32 [..][len]."""
     r = np.asarray(r)
-    lead = r.shape[:-2]
-    flat = r.reshape((-1, ring.L, ring.N))
-    out = np.empty((flat.shape[0], ring.N), np.uint32)
+    lead, ln = r.shape[:-2], r.shape[-1]
+    flat = r.reshape((-1, ring.L, ln))
+    out = np.empty((flat.shape[0], ln), np.uint32)
     for i in range(flat.shape[0]):
         out[i] = np.array(crt_decode([flat[i, j] for j in range(ring.L)], ring),
                           dtype=np.uint32)
-    return out.reshape(lead + (ring.N,))
+    return out.reshape(lead + (ln,))
 
 
 def reduce_mod_binomial(a: np.ndarray, s: int, zeta: int, q: int) -> np.ndarray:
@@ -819,4 +819,77 @@ def incomplete_ntt_def(a: np.ndarray, q: int, psi: int, s: int) -> np.ndarray:
     for g in range(N // s):
         b = int(format(g, f"0{T}b")[::-1], 2) if T else 0
         out[g * s:(g + 1) * s] = reduce_mod_binomial(a, s, pow(psi, s * (2 * b + 1), q), q)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# FC for n_i n_o > N (§8(f) packing variant).  PAPER.md:205: "If n_i n_o > N,
+# then the weight matrix can be decomposed into sub-matrices whose sizes are
+# smaller or equal to N, and our proposed packing scheme still applies to
+# the decomposed matrices."  Reading R27: sub-matrices of n_ot rows x n_it
+# columns, n_it = min(n_i, N), n_ot = min(n_o, floor(N / n_it)) (Table III's
+# ceil(n_o / floor(N / n_i)) polynomials when n_i <= N); input block beta is
+# its own ciphertext (Eq. (9) with stride n_ot), output tile t sums the
+# products over the input blocks, bias and mask added once.
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class FcPlan:
+    n_i: int
+    n_o: int
+    N: int
+    n_it: int
+    n_ib: int
+    n_ot: int
+    n_t: int
+
+
+def plan_fc(n_i: int, n_o: int, N: int) -> FcPlan:
+    n_it = min(n_i, N)
+    n_ot = min(n_o, N // n_it)
+    return FcPlan(n_i, n_o, N, n_it, -(-n_i // n_it), n_ot, -(-n_o // n_ot))
+
+
+def fc_input_blocks(I: np.ndarray, fp: FcPlan) -> np.ndarray:
+    """Eq. (9) per input block: int64 [n_ib][N]."""
+    return np.stack([fc_input_int(np.asarray(I)[b * fp.n_it:(b + 1) * fp.n_it], fp.n_ot, fp.N)
+                     for b in range(fp.n_ib)])
+
+
+def fc_submatrix(W: np.ndarray, fp: FcPlan, beta: int, t: int) -> np.ndarray:
+    """Rows t n_ot .. +n_ot, columns beta n_it .. +n_it of W, zero-padded to
+    n_ot x n_it (the packing stride of every tile is n_ot)."""
+    sub = np.zeros((fp.n_ot, fp.n_it), dtype=np.int64)
+    blk = np.asarray(W, np.int64)[t * fp.n_ot:(t + 1) * fp.n_ot,
+                                   beta * fp.n_it:(beta + 1) * fp.n_it]
+    sub[:blk.shape[0], :blk.shape[1]] = blk
+    return sub
+
+
+def fc_server_tiled(c0: np.ndarray, W: np.ndarray, bias: Optional[np.ndarray],
+                    ring: Ring, phi1: Optional[np.ndarray] = None) -> np.ndarray:
+    """Algorithm 2 Line 13 per sub-matrix: tile t = sum_beta c0_beta w_{beta,t}
+    (first n_ot coefficients), + enc(B) + enc(phi1).
+    c0 uint64 [B][n_ib][L][N]; phi1 uint32 [B][n_o]; returns uint64
+    [B][L][n_o]."""
+    n_o, n_i = np.asarray(W).shape
+    B = c0.shape[0]
+    fp = plan_fc(n_i, n_o, ring.N)
+    assert c0.shape == (B, fp.n_ib, ring.L, ring.N)
+    qo = np.array(ring.primes, dtype=object)[None, :, None]
+    out = np.empty((B, ring.L, n_o), dtype=np.uint64)
+    for t in range(fp.n_t):
+        k0, k1 = t * fp.n_ot, min(n_o, (t + 1) * fp.n_ot)
+        acc = np.zeros((B, ring.L, fp.n_ot), dtype=object)
+        for beta in range(fp.n_ib):
+            part = fc_server(c0[:, beta], fc_submatrix(W, fp, beta, t), None, ring, None)
+            acc = (acc + part.astype(object)) % qo
+        acc = acc[:, :, :k1 - k0]
+        if bias is not None:
+            acc = (acc + encode(np.mod(np.asarray(bias)[k0:k1], ring.t).astype(np.uint32),
+                                ring).astype(object)[None]) % qo
+        if phi1 is not None:
+            for b in range(B):
+                acc[b] = (acc[b] + encode(np.asarray(phi1)[b, k0:k1].astype(np.uint32),
+                                          ring).astype(object)) % qo[0]
+        out[:, :, k0:k1] = acc.astype(np.uint64)
     return out

@@ -175,3 +175,26 @@ def test_decrypt_round_definition():
     enc_n = np.stack([(enc[j].astype(object) + noise) % q
                       for j, q in enumerate(ring.primes)]).astype(np.uint64)
     assert np.array_equal(R.decrypt_round(enc_n, ring), m)
+
+
+@pytest.mark.parametrize("n_i,n_o", [(20, 30), (300, 5), (16, 16), (7, 200), (257, 3)])
+def test_fc_tiled_decrypts_to_wi_plus_b(n_i, n_o):
+    """R27 sub-matrix tiling for n_i n_o > N: with the
+    trivial-key ciphertexts c0_beta = enc(i_beta) (Eq. (9) per input block),
+    round(t c0^r / Q) - phi1 = W I + B mod t (Thm. 1 per sub-matrix, summed
+    over input blocks)."""
+    N, primes = 256, (7681, 12289, 40961)
+    ring = R.Ring(N, primes, 65537)
+    rng = np.random.default_rng(n_i * 1000 + n_o)
+    W = rng.integers(-8, 8, (n_o, n_i))
+    Bv = rng.integers(-8, 8, n_o)
+    I = rng.integers(0, 256, (2, n_i))
+    fp = R.plan_fc(n_i, n_o, N)
+    assert fp.n_it * fp.n_ot <= N and fp.n_ib * fp.n_it >= n_i and fp.n_t * fp.n_ot >= n_o
+    c0 = np.stack([np.stack([R.encode(np.mod(blk, ring.t).astype(np.uint32), ring)
+                             for blk in R.fc_input_blocks(I[b], fp)]) for b in range(2)])
+    phi = synth.phi1((2, n_o), ring.t, 5)
+    out = R.fc_server_tiled(c0, W, Bv, ring, phi)
+    m = R.decrypt_round(out, ring).astype(np.int64)
+    got = R.centered_mod_t(m - phi, ring.t)
+    assert np.array_equal(got, R.centered_mod_t(I @ W.T + Bv, ring.t))
