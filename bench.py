@@ -648,6 +648,40 @@ def main():
                           "server_init_p_ms: Alg. 1 Line 5 for all layers, once"}
         del pspecs, c1s, msgs
 
+    # ---- FC packing variants (§8(f)): sub-matrix tiling for n_i n_o > N
+    # (R27) on this ring, and the FC at N = 32768 (config 5's ring)
+    fc_var = None
+    if not args.no_client and not args.profile:
+        fc_var = []
+        for (vn, vprimes, vlog, n_i, n_o, vB) in [
+                ("fc512x1000_tiled", cfg.primes, cfg.log2N, 512, 1000, B),
+                ("fc64x100_N32768", synth.CONFIGS[5].primes, synth.CONFIGS[5].log2N, 64, 100, B)]:
+            vctx = he.Context(vprimes, vlog, cfg.t, local)
+            n_it, n_ib, n_ot, n_t = vctx.fc_plan(n_i, n_o)
+            rs = np.random.default_rng(5)
+            Wv = d(rs.integers(-8, 8, (n_o, n_i)).astype(np.int32))
+            bv = d(rs.integers(-8, 8, n_o).astype(np.int32))
+            wsp, ben = vctx.fc_pack_weights(Wv, bv)
+            c0v = d(synth.uniform_residues((vB, n_ib, len(vprimes), 1 << vlog), vprimes,
+                                           cfg.seed, "c0", 98))
+            phv = d(synth.phi1((vB, n_o), cfg.t, cfg.seed, 98))
+            outv = vctx.empty_u64(vB, len(vprimes), n_o)
+            wsv = vctx.fc_workspace(n_i, n_o, vB)
+            for _ in range(3):
+                vctx.fc(n_i, n_o, c0v, wsp, ben, phv, outv, wsv)
+            f0, f1 = mk(), mk()
+            f0.record()
+            for _ in range(args.steps):
+                vctx.fc(n_i, n_o, c0v, wsp, ben, phv, outv, wsv)
+            f1.record()
+            torch.cuda.synchronize()
+            ms = f0.elapsed_time(f1) / args.steps
+            fc_var.append({"name": vn, "N": 1 << vlog, "L": len(vprimes), "B": vB,
+                           "n_i": n_i, "n_o": n_o, "n_it": n_it, "n_ib": n_ib, "n_ot": n_ot,
+                           "n_t": n_t, "ms": ms,
+                           "evals_per_s": vB * n_ib * n_t / (ms * 1e-3)})
+            del vctx, wsp, ben, c0v, phv, outv, wsv
+
     # ---- CPU baseline: the oracle as it stands, rank 0, bounded sample
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
@@ -692,7 +726,7 @@ def main():
             "ntt": ntt, "stages_ms_per_step": st, "per_layer": per_layer,
             "roofline": roofline,
             "roofline_all": rl, "u1": u1, "init_ms": init_ms,
-            "cpu_baseline": cpu, "e2e": e2e, "client": client, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "client": client, "fc_variants": fc_var, "clocks": clocks,
             "gpu_launches": launches_step * args.steps,
         }
         print(json.dumps(line), flush=True)

@@ -170,36 +170,46 @@ he_status he_mask_extract(const he_ctx* ctx, const he_conv_plan* p,
                           void* stream);
 
 /* -------------------------------------------------------------------- FC */
-/* FC layer with n_i inputs, n_o outputs; requires
- * n_i * n_o <= N and N <= 16384 (single-CTA inverse transform). */
+/* FC layer with n_i inputs, n_o outputs, any sizes.
+ * When n_i n_o > N the weight matrix is decomposed into sub-matrices
+ * (reading R27): input blocks of n_it = min(n_i, N) columns
+ * (n_ib = ceil(n_i / n_it) input ciphertexts) and output tiles of
+ * n_ot = min(n_o, floor(N / n_it)) rows (n_t = ceil(n_o / n_ot) products per
+ * input block: Table III's ceil(n_o / floor(N / n_i)) when n_i <= N).
+ * N up to 32768. */
 typedef struct {
     int32_t n_i, n_o;
 } he_fc_desc;
 
-/* Eq. (9): i(X) = sum_l I_l X^{l n_o}, encoded with enc_j;
- * d_in int32 [B][n_i] -> d_pt uint64 [B][L][N]; optional d_ve as in
+/* Eq. (9) per input block: block beta holds
+ * I[beta n_it + l] at X^{l n_ot}, encoded with enc_j; d_in int32 [B][n_i] ->
+ * d_pt uint64 [B][n_ib][L][N]; optional d_ve (same layout) as in
  * he_pack_input. */
 he_status he_pack_fc_input(const he_ctx* ctx, const he_fc_desc* f,
                            const int32_t* d_in, int B, const uint64_t* d_ve,
                            uint64_t* d_pt, void* stream);
 
 /* Server initialisation of Algorithm 2 (Lines 3-4):
- * w(X) per Eq. (10), generalised to N >= n_i n_o (reading R17):
- *   w(X) = sum_k W_{k,0} X^k - sum_{l>=1} sum_k W_{k,l} X^{N - l n_o + k},
- * d_W int32 [n_o][n_i]; stored NTT-domain in d_wspec (he_fc_wspec_bytes()).
- * d_bias int32 [n_o] (or NULL = 0) is encoded into d_bias_enc uint64
- * [L][n_o].  d_ws: he_fc_workspace_bytes(ctx, f, 1) bytes. */
+ * per sub-matrix (beta, t) of n_ot x n_it (zero-padded), w(X) per Eq. (10)
+ * generalised to N >= n_it n_ot (reading R17):
+ *   w(X) = sum_k W_{k,0} X^k - sum_{l>=1} sum_k W_{k,l} X^{N - l n_ot + k},
+ * d_W int32 [n_o][n_i]; stored NTT-domain (times N^{-1}, Shoup pairs) in
+ * d_wspec [n_ib][n_t][L][N] (he_fc_wspec_bytes()).  d_bias int32 [n_o] (or
+ * NULL = 0) is encoded into d_bias_enc uint64 [L][n_o].  d_ws:
+ * he_fc_workspace_bytes(ctx, f, 1) bytes. */
 size_t he_fc_wspec_bytes(const he_ctx* ctx, const he_fc_desc* f);
 he_status he_pack_fc_weights(const he_ctx* ctx, const he_fc_desc* f,
                              const int32_t* d_W, const int32_t* d_bias,
                              uint64_t* d_wspec, uint64_t* d_bias_enc,
                              void* d_ws, size_t ws_bytes, void* stream);
 
-/* a9, Algorithm 2 Line 13, first n_o coefficients only
- * (PAPER.md:267):  d_out[b][j][k] = (c0_b * w)_k + bias_enc[j][k]
- *                                   + enc_j(phi1[b][k]),  k < n_o.
- * d_c0 uint64 [B][L][N]; d_phi1 uint32 [B][n_o] or NULL; d_out uint64
- * [B][L][n_o]; d_ws: he_fc_workspace_bytes(B) bytes. */
+/* a9, Algorithm 2 Line 13, first coefficients only
+ * (PAPER.md:267), per output tile t:
+ *   d_out[b][j][t n_ot + k] = (sum_beta c0_{b,beta} w_{beta,t})_k
+ *                             + bias_enc[j][t n_ot + k] + enc_j(phi1[b][.]),
+ * k < min(n_ot, n_o - t n_ot).  d_c0 uint64 [B][n_ib][L][N]; d_phi1 uint32
+ * [B][n_o] or NULL; d_out uint64 [B][L][n_o]; d_ws:
+ * he_fc_workspace_bytes(B) bytes. */
 size_t he_fc_workspace_bytes(const he_ctx* ctx, const he_fc_desc* f, int B);
 he_status he_fc(const he_ctx* ctx, const he_fc_desc* f, const uint64_t* d_c0,
                 int B, const uint64_t* d_wspec, const uint64_t* d_bias_enc,

@@ -272,13 +272,20 @@ class Context:
         return compact
 
     # ------------------------------------------------------------------ FC
+    def fc_plan(self, n_i, n_o):
+        """(n_it, n_ib, n_ot, n_t) of the sub-matrix tiling (he_rotfree.h)."""
+        n_it = min(n_i, self.N)
+        n_ot = min(n_o, self.N // n_it)
+        return n_it, -(-n_i // n_it), n_ot, -(-n_o // n_ot)
+
     def fc_pack_input(self, n_i, n_o, inp: torch.Tensor,
                       ve: Optional[torch.Tensor] = None,
                       out: Optional[torch.Tensor] = None, stream=None):
+        """-> [B][n_ib][L][N] (one ciphertext per input block)."""
         f = FcDesc(n_i, n_o)
         B = inp.shape[0]
         if out is None:
-            out = self.empty_u64(B, self.L, self.N)
+            out = self.empty_u64(B, self.fc_plan(n_i, n_o)[1], self.L, self.N)
         self._dev(inp, ve, out)
         _check(_lib.he_pack_fc_input(self._h, ctypes.byref(f), self._ptr(inp),
                                      B, self._ptr(ve), self._ptr(out),

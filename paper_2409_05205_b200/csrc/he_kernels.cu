@@ -1393,24 +1393,46 @@ extern "C" he_status he_mask_extract(const he_ctx* c, const he_conv_plan* p,
 }
 
 // ===================================================================== FC
-static bool fc_ok(const he_ctx* c, const he_fc_desc* f) {
-    return f && f->n_i >= 1 && f->n_o >= 1 && (long)f->n_i * f->n_o <= (long)c->N &&
-           c->logN <= 14;
+// Sub-matrix plan (reading R27, "decomposed into sub-matrices
+// whose sizes are smaller or equal to N"): input blocks of n_it = min(n_i, N)
+// columns, output tiles of n_ot = min(n_o, N / n_it) rows.  Input block beta
+// is packed with stride n_ot (Eq. (9)); tile t = sum_beta c0_beta w_{beta,t}.
+struct FcP {
+    int n_i, n_o, n_it, n_ib, n_ot, n_t;
+};
+static FcP fc_plan(const he_ctx* c, const he_fc_desc* f) {
+    FcP p;
+    p.n_i = f->n_i;
+    p.n_o = f->n_o;
+    p.n_it = std::min<int>(f->n_i, c->N);
+    p.n_ib = (f->n_i + p.n_it - 1) / p.n_it;
+    p.n_ot = std::min<int>(f->n_o, c->N / p.n_it);
+    p.n_t = (f->n_o + p.n_ot - 1) / p.n_ot;
+    return p;
 }
 
+static bool fc_ok(const he_ctx* c, const he_fc_desc* f) {
+    return c && f && f->n_i >= 1 && f->n_o >= 1;
+}
+
+// out [B][n_ib][L][N]: block beta holds I[beta n_it + l'] at X^{l' n_ot}
 __global__ void k_pack_fc_input(const int32_t* __restrict__ in, const u64* __restrict__ ve,
-                                u64* __restrict__ out, int n_i, int n_o, int B, int L,
-                                int logN, const he_limb* __restrict__ limbs, u64 t, u64 r_t,
+                                u64* __restrict__ out, FcP P, int B, int L, int logN,
+                                const he_limb* __restrict__ limbs, u64 t, u64 r_t,
                                 u64 t_inv) {
     const long N = 1L << logN;
-    const long total = (long)B * L * N;
+    const long total = (long)B * P.n_ib * L * N;
     for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
          idx += (long)gridDim.x * blockDim.x) {
         const int i = (int)(idx & (N - 1));
         const long r = idx >> logN;
-        const int l = (int)(r % L), b = (int)(r / L);
+        const int l = (int)(r % L);
+        const long bb = r / L;
+        const int beta = (int)(bb % P.n_ib), b = (int)(bb / P.n_ib);
+        const int col = i / P.n_ot, gcol = beta * P.n_it + col;
         long m = 0;
-        if (i % n_o == 0 && i / n_o < n_i) m = in[(long)b * n_i + i / n_o];   // Eq. (9)
+        if (i - col * P.n_ot == 0 && col < P.n_it && gcol < P.n_i)
+            m = in[(long)b * P.n_i + gcol];                                 // Eq. (9)
         long mt = m % (long)t;
         if (mt < 0) mt += t;
         const he_limb& Lm = limbs[l];
@@ -1426,65 +1448,84 @@ extern "C" he_status he_pack_fc_input(const he_ctx* c, const he_fc_desc* f,
     if (!c || !f || !d_in || !d_pt || B < 0) return HE_EINVAL;
     if (!fc_ok(c, f)) return HE_ESHAPE;
     if (B == 0) return HE_OK;
-    const long total = (long)B * c->L * c->N;
+    const FcP P = fc_plan(c, f);
+    const long total = (long)B * P.n_ib * c->L * c->N;
     k_pack_fc_input<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(
-        d_in, (const u64*)d_ve, (u64*)d_pt, f->n_i, f->n_o, B, c->L, c->logN, c->d_limb, c->t,
-        c->r_t, c->t_inv);
+        d_in, (const u64*)d_ve, (u64*)d_pt, P, B, c->L, c->logN, c->d_limb, c->t, c->r_t,
+        c->t_inv);
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
 
-// dense w(X) (R17) per limb
-__global__ void k_fc_weight_coeffs(const int32_t* __restrict__ W, u64* __restrict__ out,
-                                   int n_i, int n_o, int L, int logN,
-                                   const he_limb* __restrict__ limbs) {
+// dense w_{beta,t}(X) (R17 on the n_ot x n_it sub-matrix), [n_ib][n_t][L][N]
+__global__ void k_fc_weight_coeffs(const int32_t* __restrict__ W, u64* __restrict__ out, FcP P,
+                                   int L, int logN, const he_limb* __restrict__ limbs) {
     const long N = 1L << logN;
-    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < L * N;
+    const long total = (long)P.n_ib * P.n_t * L * N;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
          idx += (long)gridDim.x * blockDim.x) {
-        const int i = (int)(idx & (N - 1)), l = (int)(idx >> logN);
-        long w = 0;
-        if (i < n_o) {
-            w = W[(long)i * n_i];                                  // W_{i,0} X^i
+        const int i = (int)(idx & (N - 1));
+        const long r = idx >> logN;
+        const int l = (int)(r % L);
+        const long bt = r / L;
+        const int tt = (int)(bt % P.n_t), beta = (int)(bt / P.n_t);
+        long k, lp;
+        if (i < P.n_ot) {
+            k = i;                                                   // W_{k,0} X^k
+            lp = 0;
         } else {
-            const long d = N - i;                                  // = l' n_o - k
-            const long lp = (d + n_o - 1) / n_o;
-            const long k = lp * n_o - d;
-            if (lp >= 1 && lp < n_i) w = -(long)W[k * n_i + lp];   // -W_{k,l'}
+            const long d = N - i;                                    // = l' n_ot - k
+            lp = (d + P.n_ot - 1) / P.n_ot;
+            k = lp * P.n_ot - d;
+        }
+        const long row = (long)tt * P.n_ot + k, col = (long)beta * P.n_it + lp;
+        long w = 0;
+        if (lp < P.n_it && row < P.n_o && col < P.n_i) {
+            w = W[row * P.n_i + col];
+            if (lp) w = -w;                                          // -W_{k,l'}
         }
         const u64 q = limbs[l].q;
         out[idx] = w >= 0 ? (u64)w % q : q - ((u64)(-w) % q);
     }
 }
 
-// spectrum -> {w N^{-1}, Shoup}; bias -> enc
+// spectrum -> {w N^{-1}, Shoup}
 __global__ void k_fc_finish_weights(const u64* __restrict__ spec, ulonglong2* __restrict__ wspec,
-                                    const int32_t* __restrict__ bias, u64* __restrict__ bias_enc,
-                                    int n_o, int L, int logN, const he_limb* __restrict__ limbs,
-                                    u64 t, u64 r_t, u64 t_inv) {
+                                    long nlimbs, int L, int logN,
+                                    const he_limb* __restrict__ limbs) {
     const long N = 1L << logN;
-    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < L * N;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < nlimbs * N;
          idx += (long)gridDim.x * blockDim.x) {
-        const int l = (int)(idx >> logN), i = (int)(idx & (N - 1));
+        const int l = (int)((idx >> logN) % L);
         const he_limb& Lm = limbs[l];
         const u64 w = csub(shoup_mul(spec[idx], Lm.ninv, Lm.ninv_p, Lm.q), Lm.q);
         wspec[idx] = make_ulonglong2(w, (u64)(((unsigned __int128)w << 64) / Lm.q));
-        if (i < n_o) {
-            long m = bias ? bias[i] : 0;
-            long mt = m % (long)t;
-            if (mt < 0) mt += t;
-            bias_enc[(long)l * n_o + i] = enc_plain((u64)mt, Lm, t, r_t, t_inv);
-        }
+    }
+}
+
+__global__ void k_fc_bias(const int32_t* __restrict__ bias, u64* __restrict__ bias_enc, int n_o,
+                          int L, const he_limb* __restrict__ limbs, u64 t, u64 r_t,
+                          u64 t_inv) {
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < (long)L * n_o;
+         idx += (long)gridDim.x * blockDim.x) {
+        const int l = (int)(idx / n_o), k = (int)(idx % n_o);
+        long m = bias ? bias[k] : 0;
+        long mt = m % (long)t;
+        if (mt < 0) mt += t;
+        bias_enc[idx] = enc_plain((u64)mt, limbs[l], t, r_t, t_inv);
     }
 }
 
 extern "C" size_t he_fc_wspec_bytes(const he_ctx* c, const he_fc_desc* f) {
-    if (!c || !f) return 0;
-    return sizeof(ulonglong2) * (size_t)c->L * c->N;
+    if (!fc_ok(c, f)) return 0;
+    const FcP P = fc_plan(c, f);
+    return sizeof(ulonglong2) * (size_t)P.n_ib * P.n_t * c->L * c->N;
 }
 
 extern "C" size_t he_fc_workspace_bytes(const he_ctx* c, const he_fc_desc* f, int B) {
-    if (!c || !f || B < 0) return 0;
-    return sizeof(u64) * (size_t)std::max(B, 1) * c->L * c->N;
+    if (!fc_ok(c, f) || B < 0) return 0;
+    const FcP P = fc_plan(c, f);
+    return sizeof(u64) * (size_t)P.n_ib * std::max(std::max(B, 1), P.n_t) * c->L * c->N;
 }
 
 extern "C" he_status he_pack_fc_weights(const he_ctx* c, const he_fc_desc* f,
@@ -1493,53 +1534,115 @@ extern "C" he_status he_pack_fc_weights(const he_ctx* c, const he_fc_desc* f,
                                         size_t ws_bytes, void* stream) {
     if (!c || !f || !d_W || !d_wspec || !d_bias_enc || !d_ws) return HE_EINVAL;
     if (!fc_ok(c, f)) return HE_ESHAPE;
-    if (ws_bytes < sizeof(u64) * (size_t)c->L * c->N) return HE_ENOMEM;
+    const FcP P = fc_plan(c, f);
+    const long nl = (long)P.n_ib * P.n_t * c->L;
+    if (ws_bytes < sizeof(u64) * (size_t)nl * c->N) return HE_ENOMEM;
     cudaStream_t st = STREAM(stream);
     u64* ws = (u64*)d_ws;
-    const long total = (long)c->L * c->N;
-    k_fc_weight_coeffs<<<grid_for(total, 256), 256, 0, st>>>(d_W, ws, f->n_i, f->n_o, c->L,
-                                                             c->logN, c->d_limb);
+    const long total = nl * c->N;
+    k_fc_weight_coeffs<<<grid_for(total, 256), 256, 0, st>>>(d_W, ws, P, c->L, c->logN,
+                                                             c->d_limb);
     HE_CHECK_LAUNCH();
-    he_status s = launch_ntt_fwd(c, ws, ws, c->L, 0, st);
+    he_status s = launch_ntt_fwd(c, ws, ws, nl, 0, st);
     if (s != HE_OK) return s;
-    k_fc_finish_weights<<<grid_for(total, 256), 256, 0, st>>>(
-        ws, (ulonglong2*)d_wspec, d_bias, (u64*)d_bias_enc, f->n_o, c->L, c->logN, c->d_limb,
-        c->t, c->r_t, c->t_inv);
+    k_fc_finish_weights<<<grid_for(total, 256), 256, 0, st>>>(ws, (ulonglong2*)d_wspec, nl, c->L,
+                                                              c->logN, c->d_limb);
+    HE_CHECK_LAUNCH();
+    k_fc_bias<<<grid_for((long)c->L * f->n_o, 256), 256, 0, st>>>(
+        d_bias, (u64*)d_bias_enc, f->n_o, c->L, c->d_limb, c->t, c->r_t, c->t_inv);
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
 
-// Per (b, l): pointwise product with the weight spectrum, N-point inverse
-// NTT (N^{-1} pre-folded), first n_o coefficients + enc(bias) + enc(phi1).
+// Per (b, tile t, l): sum over input blocks of the pointwise products with
+// the weight spectra, N-point inverse NTT (N^{-1} pre-folded), the tile's
+// first coefficients + enc(bias) + enc(phi1) at outputs t n_ot + k.
 template <bool DP>
 __global__ void __launch_bounds__(512)
 k_fc_inv(const u64* __restrict__ spec, const ulonglong2* __restrict__ wspec,
          const u64* __restrict__ bias_enc, const u32* __restrict__ phi1, u64* __restrict__ out,
-         int n_o, int L, int logN, const he_limb* __restrict__ limbs,
+         FcP P, int L, int logN, const he_limb* __restrict__ limbs,
          const ulonglong2* __restrict__ twi_all, const double* __restrict__ twid_all, u64 t,
          u64 r_t, u64 t_inv) {
     extern __shared__ u64 sm[];
     double* smd = reinterpret_cast<double*>(sm);
     const int N = 1 << logN;
-    const int li = blockIdx.x, l = li % L, b = li / L;
+    const int l = blockIdx.x % L, bt = blockIdx.x / L;
+    const int tt = bt % P.n_t, b = bt / P.n_t;
     const he_limb Lm = limbs[l];
     const u64 q = Lm.q, q2 = 2 * q;
-    const u64* src = spec + (size_t)li * N;
-    const ulonglong2* ws = wspec + (size_t)l * N;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        const ulonglong2 w = __ldg(&ws[i]);
-        if (DP) smd[PAD(i)] = dp_mulmod(u2d(src[i]), (double)w.x, Lm.qd, Lm.qinvd);
-        else sm[PAD(i)] = shoup_mul(src[i], w.x, w.y, q);      // [0, 2q)
+        double accd = 0.0;
+        u64 acc = 0;
+        for (int beta = 0; beta < P.n_ib; ++beta) {
+            const u64 x = spec[(((size_t)b * P.n_ib + beta) * L + l) * N + i];
+            const ulonglong2 w = __ldg(&wspec[(((size_t)beta * P.n_t + tt) * L + l) * N + i]);
+            if (DP) accd = dp_reduce(accd + dp_mulmod(u2d(x), (double)w.x, Lm.qd, Lm.qinvd),
+                                     Lm.qd, Lm.qinvd);
+            else acc = csub(acc + shoup_mul(x, w.x, w.y, q), q2);          // [0, 2q)
+        }
+        if (DP) smd[PAD(i)] = accd;
+        else sm[PAD(i)] = acc;
     }
     __syncthreads();
     if (DP) gs_all_dp<3>(smd, 0, 1, logN, 0, logN, twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
     else gs_all<4>(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
-    for (int k = threadIdx.x; k < n_o; k += blockDim.x) {
+    const int k0 = tt * P.n_ot, nk = min(P.n_ot, P.n_o - k0);
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) {
         u64 v = DP ? d2canon(smd[PAD(k)], Lm.qd, Lm.qinvd) : csub(sm[PAD(k)], q);
-        v = addmod(v, bias_enc[(size_t)l * n_o + k], q);
-        if (phi1) v = addmod(v, enc_plain(phi1[(size_t)b * n_o + k], Lm, t, r_t, t_inv), q);
-        out[(size_t)li * n_o + k] = v;
+        v = addmod(v, bias_enc[(size_t)l * P.n_o + k0 + k], q);
+        if (phi1)
+            v = addmod(v, enc_plain(phi1[(size_t)b * P.n_o + k0 + k], Lm, t, r_t, t_inv), q);
+        out[((size_t)b * L + l) * P.n_o + k0 + k] = v;
     }
+}
+
+// N = 32768: a 2-CTA cluster per (b, t, l) as k_ntt_inv_split; only the
+// tile's first coefficients leave the last (cross-half) stage.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512)
+k_fc_inv_split(const u64* __restrict__ spec, const ulonglong2* __restrict__ wspec,
+               const u64* __restrict__ bias_enc, const u32* __restrict__ phi1,
+               u64* __restrict__ out, FcP P, int L, int logN,
+               const he_limb* __restrict__ limbs, const ulonglong2* __restrict__ twi_all,
+               u64 t, u64 r_t, u64 t_inv) {
+    extern __shared__ u64 sm[];
+    const int N = 1 << logN, NS = N >> 1;
+    const int li = blockIdx.x >> 1, seg = blockIdx.x & 1;
+    const int l = li % L, bt = li / L;
+    const int tt = bt % P.n_t, b = bt / P.n_t;
+    const he_limb Lm = limbs[l];
+    const u64 q = Lm.q, q2 = 2 * q;
+    const ulonglong2* twi = twi_all + (size_t)l * N;
+    for (int i = threadIdx.x; i < NS; i += blockDim.x) {
+        const int gi = seg * NS + i;
+        u64 acc = 0;
+        for (int beta = 0; beta < P.n_ib; ++beta) {
+            const u64 x = spec[(((size_t)b * P.n_ib + beta) * L + l) * N + gi];
+            const ulonglong2 w = __ldg(&wspec[(((size_t)beta * P.n_t + tt) * L + l) * N + gi]);
+            acc = csub(acc + shoup_mul(x, w.x, w.y, q), q2);
+        }
+        sm[PAD(i)] = acc;
+    }
+    __syncthreads();
+    gs_all<4>(sm, 0, 1, logN - 1, seg, logN, twi, q, q2);
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const u64* lo = seg ? cl.map_shared_rank(sm, 0) : sm;
+    const u64* hi = seg ? sm : cl.map_shared_rank(sm, 1);
+    const ulonglong2 w = twi[1];
+    const int k0 = tt * P.n_ot, nk = min(P.n_ot, P.n_o - k0);
+    for (int i = threadIdx.x; i < NS; i += blockDim.x) {
+        const int k = seg * NS + i;
+        if (k >= nk) break;
+        const u64 x = lo[PAD(i)], y = hi[PAD(i)];
+        u64 v = seg ? shoup_mul(x - y + q2, w.x, w.y, q) : csub(x + y, q2);
+        v = csub(v, q);
+        v = addmod(v, bias_enc[(size_t)l * P.n_o + k0 + k], q);
+        if (phi1)
+            v = addmod(v, enc_plain(phi1[(size_t)b * P.n_o + k0 + k], Lm, t, r_t, t_inv), q);
+        out[((size_t)b * L + l) * P.n_o + k0 + k] = v;
+    }
+    cl.sync();                          // keep smem alive for the partner
 }
 
 extern "C" he_status he_fc(const he_ctx* c, const he_fc_desc* f, const uint64_t* d_c0, int B,
@@ -1560,17 +1663,27 @@ extern "C" he_status he_fc_ex(const he_ctx* c, const he_fc_desc* f, const uint64
     if (!d_c0 || !d_wspec || !d_bias_enc || !d_out || !d_ws) return HE_EINVAL;
     if (ws_bytes < he_fc_workspace_bytes(c, f, B)) return HE_ENOMEM;
     cudaStream_t st = STREAM(stream);
+    const FcP P = fc_plan(c, f);
     u64* spec = (u64*)d_ws;
     rec(ev, 0, st);
-    he_status s = launch_ntt_fwd(c, (const u64*)d_c0, spec, (long)B * c->L, 0, st);
+    he_status s = launch_ntt_fwd(c, (const u64*)d_c0, spec, (long)B * P.n_ib * c->L, 0, st);
     if (s != HE_OK) return s;
-    const size_t smem = sizeof(u64) * padded_words(c->N);
-    auto kf = c->ntt_mode == 0 ? k_fc_inv<true> : k_fc_inv<false>;
-    if (!set_smem(kf, smem)) return HE_ECUDA;
     rec(ev, 1, st);
-    kf<<<(unsigned)(B * c->L), ntt_threads(c->N), smem, st>>>(
-        spec, (const ulonglong2*)d_wspec, (const u64*)d_bias_enc, d_phi1, (u64*)d_out, f->n_o,
-        c->L, c->logN, c->d_limb, c->d_tw_inv, c->d_twd_inv, c->t, c->r_t, c->t_inv);
+    const unsigned nblk = (unsigned)((long)B * P.n_t * c->L);
+    if (c->logN <= 14) {
+        const size_t smem = sizeof(u64) * padded_words(c->N);
+        auto kf = c->ntt_mode == 0 ? k_fc_inv<true> : k_fc_inv<false>;
+        if (!set_smem(kf, smem)) return HE_ECUDA;
+        kf<<<nblk, ntt_threads(c->N), smem, st>>>(
+            spec, (const ulonglong2*)d_wspec, (const u64*)d_bias_enc, d_phi1, (u64*)d_out, P,
+            c->L, c->logN, c->d_limb, c->d_tw_inv, c->d_twd_inv, c->t, c->r_t, c->t_inv);
+    } else {
+        const size_t smem = sizeof(u64) * padded_words(c->N / 2);
+        if (!set_smem(k_fc_inv_split, smem)) return HE_ECUDA;
+        k_fc_inv_split<<<2 * nblk, ntt_threads(c->N / 2), smem, st>>>(
+            spec, (const ulonglong2*)d_wspec, (const u64*)d_bias_enc, d_phi1, (u64*)d_out, P,
+            c->L, c->logN, c->d_limb, c->d_tw_inv, c->t, c->r_t, c->t_inv);
+    }
     HE_CHECK_LAUNCH();
     rec(ev, 2, st);
     return HE_OK;

@@ -275,27 +275,39 @@ def test_protocol_config1_gpu_server(he):
 
 # ----------------------------------------------------------------- FC a9
 @pytest.mark.parametrize("N,n_i,n_o,B", [(256, 6, 5, 3), (1024, 10, 100, 2),
-                                         (16384, 64, 100, 32)])
-def test_fc(he, N, n_i, n_o, B):
-    primes = synth.PRIMES_N16384 if N == 16384 else RINGS[N]
-    ctx = ctx_for(he, N, primes)
+                                         (16384, 64, 100, 32),
+                                         # sub-matrix tiling (R27): n_i n_o > N
+                                         (256, 20, 30, 3), (256, 300, 5, 2),
+                                         (1024, 512, 100, 2), (16384, 512, 1000, 4),
+                                         # N = 32768 (2-CTA cluster inverse)
+                                         (32768, 64, 100, 3), (32768, 1024, 100, 2)])
+@pytest.mark.parametrize("ntt", ["", "int"])
+def test_fc(he, N, n_i, n_o, B, ntt, monkeypatch):
+    if ntt:
+        monkeypatch.setenv("HE_NTT", ntt)
+    primes = {16384: synth.PRIMES_N16384[:3],
+              32768: synth.PRIMES_N32768[:3]}.get(N, RINGS[N])
+    ctx = he.Context(primes, N.bit_length() - 1, 65537) if ntt else ctx_for(he, N, primes)
     ring = R.Ring(N, tuple(primes), 65537)
+    fp = R.plan_fc(n_i, n_o, N)
+    assert ctx.fc_plan(n_i, n_o) == (fp.n_it, fp.n_ib, fp.n_ot, fp.n_t)
     rng = np.random.default_rng(N + n_o)
     W = rng.integers(-8, 8, (n_o, n_i)).astype(np.int32)
     bias = rng.integers(-8, 8, n_o).astype(np.int32)
     inp = rng.integers(0, 256, (B, n_i)).astype(np.int32)
-    c0 = synth.uniform_residues((B, ring.L, N), primes, N)
+    c0 = synth.uniform_residues((B, fp.n_ib, ring.L, N), primes, N)
     phi = synth.phi1((B, n_o), 65537, N)
     wspec, benc = ctx.fc_pack_weights(dev(W), dev(bias))
     out = u64(ctx.fc(n_i, n_o, dev(c0), wspec, benc, dev(phi)))
     bs = [0, B - 1]
-    assert np.array_equal(out[bs], R.fc_server(c0[bs], W, bias, ring, phi[bs]))
-    # packed input: enc(Eq. 9)
+    assert np.array_equal(out[bs], R.fc_server_tiled(c0[bs], W, bias, ring, phi[bs]))
+    # packed input: enc(Eq. 9) per input block
     pk = u64(ctx.fc_pack_input(n_i, n_o, dev(inp)))
     for b in bs:
-        enc = R.encode(np.mod(R.fc_input_int(inp[b], n_o, N), 65537)
-                       .astype(np.uint32), ring)
-        assert np.array_equal(pk[b], enc)
+        blocks = R.fc_input_blocks(inp[b], fp)
+        for beta in range(fp.n_ib):
+            enc = R.encode(np.mod(blocks[beta], 65537).astype(np.uint32), ring)
+            assert np.array_equal(pk[b, beta], enc)
 
 
 # --------------------------------------------------------------- errors
