@@ -893,3 +893,32 @@ def fc_server_tiled(c0: np.ndarray, W: np.ndarray, bias: Optional[np.ndarray],
                                           ring).astype(object)) % qo[0]
         out[:, :, k0:k1] = acc.astype(np.uint64)
     return out
+
+
+# ---------------------------------------------------------------------------
+# Modulus switching before the wire (§8(f); the BFV counterpart of the
+# paper's Q -> Q' rescale, PAPER.md:300 and Table II's log Q' factor).
+# Reading R28: Q' = q_0 ... q_{L'-1} (the first L' limbs), each share is
+# switched on its own: x' = round(Q' x / Q) mod Q' with x the canonical
+# CRT value in [0, Q); no ties since Q / Q' is odd.
+# ---------------------------------------------------------------------------
+def mod_switch(r: np.ndarray, ring: Ring, L_keep: int) -> np.ndarray:
+    """r uint64 [..][L][len] -> uint64 [..][L_keep][len], exact big ints."""
+    r = np.asarray(r)
+    lead, ln = r.shape[:-2], r.shape[-1]
+    flat = r.reshape((-1, ring.L, ln))
+    P = 1
+    for q in ring.primes[L_keep:]:
+        P *= q
+    out = np.empty((flat.shape[0], L_keep, ln), np.uint64)
+    for i in range(flat.shape[0]):
+        for k in range(ln):
+            x = 0
+            for j, q in enumerate(ring.primes):          # CRT by definition
+                Qj = ring.Q // q
+                x += int(flat[i, j, k]) * Qj * pow(Qj, -1, q)
+            x %= ring.Q
+            y = (2 * x + P) // (2 * P)                    # round(x / P)
+            for j in range(L_keep):
+                out[i, j, k] = y % ring.primes[j]
+    return out.reshape(lead + (L_keep, ln))

@@ -198,3 +198,51 @@ def test_fc_tiled_decrypts_to_wi_plus_b(n_i, n_o):
     m = R.decrypt_round(out, ring).astype(np.int64)
     got = R.centered_mod_t(m - phi, ring.t)
     assert np.array_equal(got, R.centered_mod_t(I @ W.T + Bv, ring.t))
+
+
+def test_mod_switch_definition_and_protocol():
+    """R28: round(Q' x / Q) by exact rationals, and the switched shares of a
+    real protocol run (config 2, L = 3 -> L' = 1) still decrypt, under Q',
+    to the brute-force conv mod t."""
+    from fractions import Fraction
+    cfg = synth.CONFIGS[2]
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    rng = np.random.default_rng(8)
+    r = np.stack([rng.integers(0, q, 50, dtype=np.uint64) for q in ring.primes])
+    for Lk in (1, 2):
+        sw = R.mod_switch(r, ring, Lk)
+        Qp = 1
+        for q in ring.primes[:Lk]:
+            Qp *= q
+        for k in range(0, 50, 7):
+            x = 0
+            for j, q in enumerate(ring.primes):
+                Qj = ring.Q // q
+                x += int(r[j, k]) * Qj * pow(Qj, -1, q)
+            x %= ring.Q
+            want = (Fraction(Qp * x, ring.Q) + Fraction(1, 2)).__floor__() % Qp
+            assert [int(sw[j, k]) for j in range(Lk)] == [want % q for q in ring.primes[:Lk]]
+    # protocol: switch c0^r (server) and c1^r (client) to one limb
+    Ly = cfg.conv[0]
+    plan = R.plan_conv(Ly, cfg.N)
+    seed = cfg.seed + 9
+    s_key = synth.secret_key(cfg.N, cfg.h, seed)
+    a = synth.uniform_residues((ring.L, cfg.N), cfg.primes, seed, "a")
+    b_pk = R.keygen(ring, s_key, a, synth.gauss_poly(cfg.N, cfg.sigma, seed, "e0", 9))
+    img = synth.images(cfg, 0, 1)
+    W = synth.weights(cfg, 0)
+    v = synth.v_poly(cfg.N, seed, 0, 0)
+    c0 = R.encrypt_c0(ring, R.pack_input_int(img[0], plan)[0], b_pk, v,
+                      synth.gauss_poly(cfg.N, cfg.sigma, seed, "e0", 0, 0))[None, None]
+    phi = synth.phi1((1, plan.n_ob, cfg.N), cfg.t, seed)
+    comp0 = R.compact(R.conv_server(c0, W, plan, ring, phi), plan)
+    ef = {(n, 0): synth.gauss_poly(cfg.N, cfg.sigma, seed, "ef", n, 0) for n in range(Ly.c_o)}
+    vs = R.signed_to_residues(np.array(R.schoolbook_py(v, s_key, cfg.N)), ring)[None, None]
+    comp1 = R.compact(R.client_c1r(vs, R.server_p(W, plan, ring, a, ef), plan, ring), plan)
+    ring1 = R.Ring(cfg.N, cfg.primes[:1], cfg.t)
+    s0, s1 = R.mod_switch(comp0, ring, 1), R.mod_switch(comp1, ring, 1)
+    m = R.decrypt_round((s0.astype(object) + s1.astype(object)) % cfg.primes[0], ring1)
+    got = R.centered_mod_t(m[0, 0].astype(np.int64) - phi[0, 0, R.output_positions(plan)], cfg.t)
+    ref = R.centered_mod_t(R.conv2d_ref(img[0], W, plan), cfg.t)
+    want = np.stack([ref[nl].ravel() for nl in range(plan.c_ob)], 1).ravel()
+    assert np.array_equal(got, want)
