@@ -538,8 +538,13 @@ def main():
         for e in comp_done:
             e.record(stream)
         mask_seed = [0]
+        # variant: the payload switched to one limb (R28) before the wire
+        sw = [ctx.empty_u64(*c.shape[:2], 1, c.shape[-1]) for c in comps]
+        sw_pk_d = [torch.empty(ctx.packed_bytes(t.numel()), dtype=torch.uint8, device=dev)
+                   for t in sw]
+        sw_pk_h = [torch.empty(t.shape, dtype=torch.uint8).pin_memory() for t in sw_pk_d]
 
-        def e2e_step():
+        def e2e_step(ms_keep=0):
             mask_seed[0] += 1
             for i, lw in enumerate(layers):
                 with torch.cuda.stream(h2d_s):
@@ -550,11 +555,18 @@ def main():
                 ctx.unpack50(c0_pk_d[i], c0_d[i])
                 ctx.phi1_generate((mask_seed[0] << 8) + i, phi_d[i])
                 ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], outs[i], ws, compact=comps[i])
-                ctx.pack50(comps[i], comp_pk_d[i])
+                if ms_keep:
+                    ctx.mod_switch(comps[i], ms_keep, out=sw[i])
+                    ctx.pack50(sw[i], sw_pk_d[i])
+                else:
+                    ctx.pack50(comps[i], comp_pk_d[i])
                 comp_done[i].record(stream)
                 with torch.cuda.stream(d2h_s):
                     d2h_s.wait_event(comp_done[i])
-                    comp_pk_h[i].copy_(comp_pk_d[i], non_blocking=True)
+                    if ms_keep:
+                        sw_pk_h[i].copy_(sw_pk_d[i], non_blocking=True)
+                    else:
+                        comp_pk_h[i].copy_(comp_pk_d[i], non_blocking=True)
             if fc:
                 i = len(layers)
                 with torch.cuda.stream(h2d_s):
@@ -589,6 +601,32 @@ def main():
                "d2h_bytes_per_step": d2h,
                "wire": "50-bit packed residues (he_residues_pack50/unpack50); "
                        "phi1 drawn on device (he_phi1_generate)"}
+        # same loop with the conv payloads modulus-switched to one limb
+        for _ in range(2):
+            e2e_step(1)
+        barrier()
+        x0.record()
+        for _ in range(args.steps):
+            e2e_step(1)
+        x1.record()
+        barrier()
+        ms_sw = max_over_ranks(x0.elapsed_time(x1) / args.steps)
+        # the switch kernel alone, every conv payload of the step
+        m0, m1 = mk(), mk()
+        m0.record()
+        for i in range(len(layers)):
+            ctx.mod_switch(comps[i], 1, out=sw[i])
+        m1.record()
+        torch.cuda.synchronize()
+        sw_ms = m0.elapsed_time(m1)
+        sw_bytes = sum(8 * c.numel() + 8 * t.numel() for c, t in zip(comps, sw))
+        e2e["modswitch"] = {
+            "L_keep": 1, "ms_per_step": ms_sw,
+            "value": evals_step * world / (ms_sw * 1e-3),
+            "d2h_bytes_per_step": sum(t.numel() for t in sw_pk_h) +
+            (fc["out_pk_h"].numel() if fc else 0),
+            "kernel_ms_per_step": sw_ms,
+            "kernel_hbm_frac": sw_bytes / (sw_ms * 1e-3) / 1e9 / peaks()[0]}
 
     # ---- client mirror path: the client's per-layer work
     # of Alg. 1 Lines 21-24 + Eq. (2) -- c1^r = valid slots of

@@ -321,6 +321,22 @@ he_status he_decrypt_round(const he_ctx* ctx, const uint64_t* d_c0r,
                            const uint64_t* d_c1r, long n_polys, long len,
                            uint32_t* d_m, void* stream);
 
+/* Modulus switching before the wire (§8(f); the BFV counterpart of the
+ * paper's rescale to Q', Table II's log Q' factor; reading
+ * R28): each residue polynomial is mapped to Q' = q_0 ... q_{L_keep-1},
+ *   x' = round(Q' x / Q) mod q_j,  j < L_keep,
+ * x the canonical CRT value in [0, Q).  Applied to the server's payload
+ * (c0^r) and, by the client, to its share c1^r; r' = c0' + c1' then
+ * decrypts under Q' (he_decrypt_round on a context over the first L_keep
+ * primes) while the wire carries L_keep / L of the bytes.  The division
+ * by P = Q / Q' is exact in RNS except for the final rounding of
+ * sum_i y_i / p_i, done in FP64 (differs from the exact definition only
+ * within ~L 2^-52 of a half-integer).  d_in [n_polys][L][len], d_out
+ * [n_polys][L_keep][len].  HE_EPARAM if more than 16 limbs are dropped or
+ * L_keep (L - L_keep) + L > 400. */
+he_status he_mod_switch(const he_ctx* ctx, const uint64_t* d_in, long n_polys,
+                        long len, int L_keep, uint64_t* d_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -111,6 +111,7 @@ _sig("he_pack_client_p", [_P, ctypes.POINTER(ConvPlan), _P, _P, _P, _SZ, _P])
 _sig("he_residues_from_int", [_P, _P, ctypes.c_long, _P, _P])
 _sig("he_poly_mul", [_P, _P, _P, _I, _I, _P, _P, _SZ, _P])
 _sig("he_decrypt_round", [_P, _P, _P, ctypes.c_long, ctypes.c_long, _P, _P])
+_sig("he_mod_switch", [_P, _P, ctypes.c_long, ctypes.c_long, _I, _P, _P])
 
 EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_conv_plan_make", "he_pack_input", "he_filter_bytes",
@@ -121,7 +122,7 @@ EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_residues_unpack50", "he_phi1_generate", "he_ntt_forward",
             "he_ntt_inverse", "he_ntt_forward_partial", "he_server_p_workspace_bytes", "he_server_init_p",
             "he_pack_client_p", "he_residues_from_int", "he_poly_mul",
-            "he_decrypt_round"]
+            "he_decrypt_round", "he_mod_switch"]
 
 
 def _events(events):
@@ -454,3 +455,15 @@ class Context:
                                      n, ln, self._ptr(m), _stream(stream)),
                "he_decrypt_round")
         return m
+
+    def mod_switch(self, x: torch.Tensor, L_keep: int,
+                   out: Optional[torch.Tensor] = None, stream=None):
+        """[..][L][len] -> [..][L_keep][len]: round(Q' x / Q) mod q_j."""
+        ln = x.shape[-1]
+        n = x.numel() // (self.L * ln)
+        if out is None:
+            out = self.empty_u64(*x.shape[:-2], L_keep, ln)
+        self._dev(x, out)
+        _check(_lib.he_mod_switch(self._h, self._ptr(x), n, ln, L_keep,
+                                  self._ptr(out), _stream(stream)), "he_mod_switch")
+        return out

@@ -1990,3 +1990,87 @@ extern "C" he_status he_decrypt_round(const he_ctx* c, const uint64_t* d_c0r,
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
+
+// ====================================================== modulus switching
+// x' = round(x / P) mod q_j (j < Lk), P = q_Lk ... q_{L-1} (reading R28).
+// With y_i = x_i ((P/p_i)^{-1} mod p_i) for the dropped limbs i,
+//   round(x / P) = (x - sum_i y_i P/p_i) / P + round(sum_i y_i / p_i),
+// so x'_j = (x_j - sum_i y_i [P/p_i]_{q_j}) [P^{-1}]_{q_j} + u  (mod q_j),
+// u = rint(sum_i y_i / p_i) in FP64 (the exact rounding differs only when
+// the fraction is within ~L 2^-52 of one half).  Constants: dinv[i],
+// pinv[j], m[i * Lk + j] = [P/p_i]_{q_j}.
+struct MsConst {
+    int Lk, Ld;
+    u64 v[400];           // dinv[Ld], pinv[Lk], m[Ld * Lk]
+};
+
+__global__ void __launch_bounds__(256)
+k_mod_switch(const u64* __restrict__ in, u64* __restrict__ out, long n_polys, long len, int L,
+             const he_limb* __restrict__ limbs, MsConst C) {
+    const long total = n_polys * len;
+    const u64* dinv = C.v;
+    const u64* pinv = C.v + C.Ld;
+    const u64* mm = C.v + C.Ld + C.Lk;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const long i = idx / len, k = idx - i * len;
+        const u64* x = in + i * L * len + k;
+        u64* o = out + i * C.Lk * len + k;
+        double u = 0.0;
+#pragma unroll 1
+        for (int j = 0; j < C.Lk; ++j) {            // y_d recomputed per kept limb
+            const he_limb& Qm = limbs[j];
+            double acc = 0.0, fr = 0.0;
+#pragma unroll 4
+            for (int d = 0; d < C.Ld; ++d) {
+                const he_limb& Pm = limbs[C.Lk + d];
+                const u64 y = d2canon(dp_mulmod(u2d(x[(long)(C.Lk + d) * len]), u2d(dinv[d]),
+                                                Pm.qd, Pm.qinvd), Pm.qd, Pm.qinvd);
+                if (j == 0) fr += (double)y * Pm.qinvd;
+                acc = dp_reduce(acc + dp_mulmod(u2d(y), u2d(mm[d * C.Lk + j]), Qm.qd, Qm.qinvd),
+                                Qm.qd, Qm.qinvd);
+            }
+            if (j == 0) u = rint(fr);
+            const double dif = u2d(x[(long)j * len]) - acc;                 // |.| < 1.5 q
+            const double v = dp_mulmod(dif, u2d(pinv[j]), Qm.qd, Qm.qinvd) + u;
+            o[(long)j * len] = d2canon(v, Qm.qd, Qm.qinvd);
+        }
+    }
+}
+
+extern "C" he_status he_mod_switch(const he_ctx* c, const uint64_t* d_in, long n_polys,
+                                   long len, int L_keep, uint64_t* d_out, void* stream) {
+    if (!c || n_polys < 0 || len < 0 || L_keep < 1 || L_keep > c->L) return HE_EINVAL;
+    if (n_polys == 0 || len == 0) return HE_OK;
+    if (!d_in || !d_out) return HE_EINVAL;
+    MsConst C;
+    memset(&C, 0, sizeof(C));
+    C.Lk = L_keep;
+    C.Ld = c->L - L_keep;
+    if (C.Ld > 16 || C.Ld + C.Lk + C.Ld * C.Lk > 400) return HE_EPARAM;
+    const u64* q = c->q_host;
+    for (int d = 0; d < C.Ld; ++d) {            // (P/p_d)^{-1} mod p_d
+        const u64 p = q[C.Lk + d];
+        u64 r = 1;
+        for (int e = 0; e < C.Ld; ++e)
+            if (e != d) r = mulmod_h(r, q[C.Lk + e] % p, p);
+        C.v[d] = powmod_h(r, p - 2, p);
+    }
+    for (int j = 0; j < C.Lk; ++j) {            // P^{-1} mod q_j
+        u64 r = 1;
+        for (int e = 0; e < C.Ld; ++e) r = mulmod_h(r, q[C.Lk + e] % q[j], q[j]);
+        C.v[C.Ld + j] = powmod_h(r, q[j] - 2, q[j]);
+    }
+    for (int d = 0; d < C.Ld; ++d)              // [P/p_d]_{q_j}
+        for (int j = 0; j < C.Lk; ++j) {
+            u64 r = 1;
+            for (int e = 0; e < C.Ld; ++e)
+                if (e != d) r = mulmod_h(r, q[C.Lk + e] % q[j], q[j]);
+            C.v[C.Ld + C.Lk + d * C.Lk + j] = r;
+        }
+    const long total = n_polys * len;
+    k_mod_switch<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(
+        (const u64*)d_in, (u64*)d_out, n_polys, len, c->L, c->d_limb, C);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}

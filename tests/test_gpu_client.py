@@ -190,14 +190,30 @@ def test_protocol_end_to_end_on_gpu(he, cfg_idx):
     c1r = ctx.conv(p, vs, pspec, compact=comp1)
     m_full = ctx.decrypt_round(c0r, c1r).cpu().numpy().view(np.uint32)
     m_comp = ctx.decrypt_round(comp, comp1).cpu().numpy().view(np.uint32)
+    # modulus switching of both shares to one limb (R28), decrypted under Q'
+    ctx1 = ctx_for(he, cfg.N, cfg.primes[:1], cfg.t)
+    m_sw = ctx1.decrypt_round(ctx.mod_switch(comp, 1), ctx.mod_switch(comp1, 1)) \
+        .cpu().numpy().view(np.uint32)
     pos = R.output_positions(plan)
     for b in range(B):
         ref = R.centered_mod_t(R.conv2d_ref(imgs[b], W, plan), cfg.t)
         for ob in range(plan.n_ob):
-            for m_row, sel in ((m_full[b, ob, pos], pos), (m_comp[b, ob], pos)):
+            for m_row, sel in ((m_full[b, ob, pos], pos), (m_comp[b, ob], pos),
+                               (m_sw[b, ob], pos)):
                 got = (m_row.astype(np.int64) - phi[b, ob, sel]) % cfg.t
                 got = np.where(got > cfg.t // 2, got - cfg.t, got)
                 for nl in range(plan.c_ob):
                     n = ob * plan.c_ob + nl
                     if n < plan.c_o:
                         assert np.array_equal(got[nl::plan.c_ob], ref[n].ravel()), (b, n)
+
+
+@pytest.mark.parametrize("cfg_idx", [2, 4, 5])
+def test_mod_switch_matches_oracle(he, cfg_idx):
+    cfg = synth.CONFIGS[cfg_idx]
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    ctx = ctx_for(he, cfg.N, cfg.primes, cfg.t)
+    x = synth.uniform_residues((2, ring.L, 97), cfg.primes, 6, "misc", cfg_idx)
+    for Lk in sorted({1, 2, ring.L - 1, ring.L}):
+        got = u64(ctx.mod_switch(dev(x), Lk))
+        assert np.array_equal(got, R.mod_switch(x, ring, Lk)), Lk
