@@ -922,3 +922,42 @@ def mod_switch(r: np.ndarray, ring: Ring, L_keep: int) -> np.ndarray:
             for j in range(L_keep):
                 out[i, j, k] = y % ring.primes[j]
     return out.reshape(lead + (L_keep, ln))
+
+
+# ---------------------------------------------------------------------------
+# Chained pipeline (§8(f), Fig. 5): after each layer the
+# client decrypts, the garbled-circuit stage removes phi1 and applies ReLU,
+# and the client re-packs the activations for the next layer.  The GC is a
+# trusted stub here (reading R29, phi2 = 0): x = centered((m - phi1) mod t),
+# y = min(qmax, max(x, 0) >> shift); the network's global average pooling
+# before the FC (plain-20) is floor(mean) per channel, also in the stub.
+# ---------------------------------------------------------------------------
+def relu_requant(x: np.ndarray, t: int, shift: int, qmax: int) -> np.ndarray:
+    """R29 stub on conv outputs (any integers): centered mod t, ReLU,
+    arithmetic shift, clamp."""
+    c = centered_mod_t(np.asarray(x, np.int64), t)
+    return np.minimum(qmax, np.maximum(c, 0) >> shift).astype(np.int64)
+
+
+def avgpool(x: np.ndarray) -> np.ndarray:
+    """[C][H][W] -> [C]: floor(sum / (H W))."""
+    x = np.asarray(x, np.int64)
+    return x.reshape(x.shape[0], -1).sum(1) // (x.shape[1] * x.shape[2])
+
+
+def plain_chain(img: np.ndarray, Ws, layers, N: int, t: int, shift: int, qmax: int,
+                fcW: Optional[np.ndarray] = None, fcB: Optional[np.ndarray] = None):
+    """Plaintext reference of the chained pipeline for one image: per layer
+    conv2d_ref (Eq. (3)/(4)) -> relu_requant; then avgpool -> FC (W I + B),
+    centered mod t.  Returns (activations per layer, logits or None)."""
+    acts = []
+    x = np.asarray(img, np.int64)
+    for W, Ly in zip(Ws, layers):
+        x = relu_requant(conv2d_ref(x, W, plan_conv(Ly, N)), t, shift, qmax)
+        acts.append(x)
+    logits = None
+    if fcW is not None:
+        v = avgpool(x)
+        logits = centered_mod_t(np.asarray(fcW, np.int64) @ v +
+                                (0 if fcB is None else np.asarray(fcB, np.int64)), t)
+    return acts, logits

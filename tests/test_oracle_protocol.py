@@ -246,3 +246,48 @@ def test_mod_switch_definition_and_protocol():
     ref = R.centered_mod_t(R.conv2d_ref(img[0], W, plan), cfg.t)
     want = np.stack([ref[nl].ravel() for nl in range(plan.c_ob)], 1).ravel()
     assert np.array_equal(got, want)
+
+
+def test_chained_protocol_matches_plain_chain():
+    """R29: two Conv layers (the second with stride 2) and the FC, each run
+    through the oracle's encrypted protocol (c0-only encryption, server,
+    client c1^r, decryption) with the stub between layers, reproduce the
+    plaintext chain exactly (Fig. 5)."""
+    cfg = synth.CONFIGS[1]
+    N, t = cfg.N, cfg.t
+    ring = R.Ring(N, cfg.primes, t)
+    layers = [synth.ConvLayer(1, 2, 8, 8), synth.ConvLayer(2, 2, 8, 8, stride=2)]
+    rng = np.random.default_rng(3)
+    Ws = [rng.integers(-4, 4, (Ly.c_o, Ly.c_i, 3, 3)) for Ly in layers]
+    fcW, fcB = rng.integers(-4, 4, (3, 2)), rng.integers(-4, 4, 3)
+    img = rng.integers(0, 16, (1, 8, 8))
+    shift, qmax = 2, 15
+    acts, logits = R.plain_chain(img, Ws, layers, N, t, shift, qmax, fcW, fcB)
+    seed = 77
+    s_key = synth.secret_key(N, cfg.h, seed)
+    a = synth.uniform_residues((ring.L, N), cfg.primes, seed, "a")
+    b_pk = R.keygen(ring, s_key, a, synth.gauss_poly(N, cfg.sigma, seed, "e0", 9))
+    x = img
+    for li, (W, Ly) in enumerate(zip(Ws, layers)):
+        plan = R.plan_conv(Ly, N)
+        ip = R.pack_input_int(x, plan)
+        vs = [synth.v_poly(N, seed, li, beta) for beta in range(plan.n_ib)]
+        c0 = np.stack([R.encrypt_c0(ring, ip[beta], b_pk, vs[beta],
+                                    synth.gauss_poly(N, cfg.sigma, seed, "e0", li, beta))
+                       for beta in range(plan.n_ib)])[None]
+        phi = synth.phi1((1, plan.n_ob, N), t, seed, li)
+        out = R.conv_server(c0, W, plan, ring, phi)
+        ef = {(n, beta): synth.gauss_poly(N, cfg.sigma, seed, "ef", li, n, beta)
+              for n in range(plan.c_o) for beta in range(plan.n_ib)}
+        dec = R.conv_protocol_decrypt(ring, plan, W, out[0], s_key, a, vs, ef, phi[0])
+        x = np.minimum(qmax, np.maximum(dec, 0) >> shift)
+        assert np.array_equal(x, acts[li]), li
+    v_in = R.avgpool(x)
+    v = synth.v_poly(N, seed, 99)
+    c0 = R.encrypt_c0(ring, R.fc_input_int(v_in, 3, N), b_pk, v,
+                      synth.gauss_poly(N, cfg.sigma, seed, "e0", 99))
+    phi = synth.phi1((1, 3), t, seed, 99)
+    out = R.fc_server(c0[None], fcW, fcB, ring, phi)
+    dec = R.fc_protocol_decrypt(ring, fcW, out[0], s_key, a, v,
+                                synth.gauss_poly(N, cfg.sigma, seed, "ef", 99), phi[0])
+    assert np.array_equal(dec, logits)
