@@ -720,6 +720,44 @@ def main():
                            "evals_per_s": vB * n_ib * n_t / (ms * 1e-3)})
             del vctx, wsp, ben, c0v, phv, outv, wsv
 
+    # ---- chained pipeline (§8(f) row 3): the whole encrypted network, layer
+    # to layer -- client encryption, server Conv/FC, client share,
+    # decryption, R29 stub -- on the same 19 conv layers + FC, B images
+    chain = None
+    if not args.no_client and not args.profile and cfg.fc is not None:
+        from paper_2409_05205_b200.chain import Chain
+        rs = np.random.default_rng(cfg.seed)
+        sk = synth.secret_key(N, cfg.h, cfg.seed)
+        a_h = synth.uniform_residues((L, N), cfg.primes, cfg.seed, "a")
+        b_h = synth.uniform_residues((L, N), cfg.primes, cfg.seed, "misc", 3)  # pk stand-in
+        efs = [d(rs.integers(-8, 9, (lw.Ly.c_o, lw.p.n_ib, N)).astype(np.int32)) for lw in layers]
+        ch = Chain(ctx, [lw.Ly for lw in layers],
+                   [d(synth.weights(cfg, lw.idx)) for lw in layers],
+                   d(synth.fc_weights(cfg)), d(synth.fc_bias(cfg)),
+                   d(sk.astype(np.int32)), d(a_h), d(b_h), efs)
+        vv = [d(rs.integers(-1, 2, (B, lw.p.n_ib, N)).astype(np.int32)) for lw in layers]
+        ee = [d(rs.integers(-8, 9, (B, lw.p.n_ib, N)).astype(np.int32)) for lw in layers]
+        v_fc = d(rs.integers(-1, 2, (B, 1, N)).astype(np.int32))
+        e_fc = d(rs.integers(-8, 9, (B, 1, N)).astype(np.int32))
+        img0 = d(synth.images(cfg, 0))
+        for _ in range(2):
+            ch.run(img0, vv, ee, 1, 8, 255, v_fc, e_fc)
+        barrier()
+        h0, h1 = mk(), mk()
+        h0.record()
+        for k in range(args.steps):
+            ch.run(img0, vv, ee, 2 + k, 8, 255, v_fc, e_fc)
+        h1.record()
+        barrier()
+        ms_chain = max_over_ranks(h0.elapsed_time(h1) / args.steps)
+        chain = {"ms_per_step": ms_chain, "ms_per_image": ms_chain / B,
+                 "images_per_s": B * world / (ms_chain * 1e-3),
+                 "what": "plain-20 encrypted end to end on the device: per layer client "
+                         "encryption (he_pk_mask, he_pack_input), server conv + mask, "
+                         "client c1^r + decryption + R29 stub; avgpool + FC; inputs "
+                         "resident, fresh randomness tensors reused across steps"}
+        del ch
+
     # ---- CPU baseline: the oracle as it stands, rank 0, bounded sample
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
@@ -764,7 +802,7 @@ def main():
             "ntt": ntt, "stages_ms_per_step": st, "per_layer": per_layer,
             "roofline": roofline,
             "roofline_all": rl, "u1": u1, "init_ms": init_ms,
-            "cpu_baseline": cpu, "e2e": e2e, "client": client, "fc_variants": fc_var, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "client": client, "chain": chain, "fc_variants": fc_var, "clocks": clocks,
             "gpu_launches": launches_step * args.steps,
         }
         print(json.dumps(line), flush=True)

@@ -337,6 +337,51 @@ he_status he_decrypt_round(const he_ctx* ctx, const uint64_t* d_c0r,
 he_status he_mod_switch(const he_ctx* ctx, const uint64_t* d_in, long n_polys,
                         long len, int L_keep, uint64_t* d_out, void* stream);
 
+/* --------------------------------------- chained pipeline (§8(f), R29) */
+/* Public-key mask of the c0-only encryption, Eq. (1):
+ *   d_ve[i] = v_i b + e_i  in R_Q,  i < n_polys,
+ * d_v, d_e int32 [n_polys][N] small signed (d_e NULL = 0), d_b uint64
+ * [L][N] the public key; d_ve uint64 [n_polys][L][N], passed to
+ * he_pack_input / he_pack_fc_input as d_ve.  Workspace L N 8 bytes. */
+he_status he_pk_mask(const he_ctx* ctx, const int32_t* d_v, const int32_t* d_e,
+                     long n_polys, const uint64_t* d_b, uint64_t* d_ve,
+                     void* d_ws, size_t ws_bytes, void* stream);
+
+/* Trusted stub of the garbled-circuit stage between layers (Fig. 5,
+ * PAPER.md:270-281; reading R29, phi2 = 0): from the decrypted valid slots
+ * d_m uint32 [B][n_ob][n_valid] (he_decrypt_round of the compact shares)
+ *   x = centered((m - phi1) mod t),  y = min(qmax, max(x, 0) >> shift),
+ * written as the next layer's image d_img int32 [B][c_o][w_o][h_o].
+ * d_phi1 uint32 [B][n_ob][N] (the server's mask) or NULL. */
+he_status he_relu_requant(const he_ctx* ctx, const he_conv_plan* plan,
+                          const uint32_t* d_m, int B, const uint32_t* d_phi1,
+                          int shift, int qmax, int32_t* d_img, void* stream);
+
+/* Global average pooling before the FC (plain-20): d_out[r] =
+ * floor(sum_{i < hw} d_x[r][i] / hw), d_x int32 [rows][hw]. */
+he_status he_avgpool(const int32_t* d_x, long rows, int hw, int32_t* d_out,
+                     void* stream);
+
+/* FC client mirror path (Alg. 2 Lines 5-6, 16-17):
+ * p_{beta,t} = w_{beta,t} a + e (sub-matrices as he_pack_fc_weights),
+ * d_p uint64 [n_ib][n_t][L][N], d_e int32 [n_ib][n_t][N] or NULL; then
+ * he_pack_fc_client_p stores the spectra of p in the d_wspec format, so
+ * he_fc(ctx, f, d_vs, B, d_pspec, zero bias_enc, NULL, d_c1r, ...) with
+ * d_vs[b][beta] = v_beta s returns the client share c1^r [B][L][n_o]. */
+size_t he_fc_server_p_workspace_bytes(const he_ctx* ctx, const he_fc_desc* f);
+he_status he_fc_server_init_p(const he_ctx* ctx, const he_fc_desc* f,
+                              const int32_t* d_W, const uint64_t* d_a,
+                              const int32_t* d_e, uint64_t* d_p, void* d_ws,
+                              size_t ws_bytes, void* stream);
+he_status he_pack_fc_client_p(const he_ctx* ctx, const he_fc_desc* f,
+                              const uint64_t* d_p, uint64_t* d_pspec, void* d_ws,
+                              size_t ws_bytes, void* stream);
+
+/* FC output stub (R29): d_out[i] = centered((d_m[i] - d_phi1[i]) mod t),
+ * int32; d_phi1 NULL = 0. */
+he_status he_unmask(const he_ctx* ctx, const uint32_t* d_m, const uint32_t* d_phi1,
+                    long n, int32_t* d_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -112,6 +112,13 @@ _sig("he_residues_from_int", [_P, _P, ctypes.c_long, _P, _P])
 _sig("he_poly_mul", [_P, _P, _P, _I, _I, _P, _P, _SZ, _P])
 _sig("he_decrypt_round", [_P, _P, _P, ctypes.c_long, ctypes.c_long, _P, _P])
 _sig("he_mod_switch", [_P, _P, ctypes.c_long, ctypes.c_long, _I, _P, _P])
+_sig("he_pk_mask", [_P, _P, _P, ctypes.c_long, _P, _P, _P, _SZ, _P])
+_sig("he_relu_requant", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _I, _I, _P, _P])
+_sig("he_avgpool", [_P, ctypes.c_long, _I, _P, _P])
+_sig("he_unmask", [_P, _P, _P, ctypes.c_long, _P, _P])
+_sig("he_fc_server_p_workspace_bytes", [_P, ctypes.POINTER(FcDesc)], _SZ)
+_sig("he_fc_server_init_p", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _P, _P, _SZ, _P])
+_sig("he_pack_fc_client_p", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _SZ, _P])
 
 EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_conv_plan_make", "he_pack_input", "he_filter_bytes",
@@ -122,7 +129,9 @@ EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_residues_unpack50", "he_phi1_generate", "he_ntt_forward",
             "he_ntt_inverse", "he_ntt_forward_partial", "he_server_p_workspace_bytes", "he_server_init_p",
             "he_pack_client_p", "he_residues_from_int", "he_poly_mul",
-            "he_decrypt_round", "he_mod_switch"]
+            "he_decrypt_round", "he_mod_switch", "he_pk_mask", "he_relu_requant",
+            "he_avgpool", "he_unmask", "he_fc_server_p_workspace_bytes", "he_fc_server_init_p",
+            "he_pack_fc_client_p"]
 
 
 def _events(events):
@@ -466,4 +475,74 @@ class Context:
         self._dev(x, out)
         _check(_lib.he_mod_switch(self._h, self._ptr(x), n, ln, L_keep,
                                   self._ptr(out), _stream(stream)), "he_mod_switch")
+        return out
+
+    # ------------------------------------------ chained pipeline (§8(f))
+    def pk_mask(self, v: torch.Tensor, e: Optional[torch.Tensor], b: torch.Tensor,
+                out: Optional[torch.Tensor] = None, stream=None):
+        """ve = v b + e (Eq. (1)) for int32 v, e [..][N] -> [..][L][N]."""
+        n = v.numel() // self.N
+        if out is None:
+            out = self.empty_u64(*v.shape[:-1], self.L, self.N)
+        ws = torch.empty(8 * self.L * self.N, dtype=torch.uint8, device=self.device)
+        self._dev(v, e, b, out)
+        _check(_lib.he_pk_mask(self._h, self._ptr(v), self._ptr(e), n, self._ptr(b),
+                               self._ptr(out), self._ptr(ws), ws.numel(),
+                               _stream(stream)), "he_pk_mask")
+        return out
+
+    def relu_requant(self, p: ConvPlan, m: torch.Tensor, phi1: Optional[torch.Tensor],
+                     shift: int, qmax: int, out: Optional[torch.Tensor] = None,
+                     stream=None):
+        B = m.shape[0]
+        if out is None:
+            out = torch.empty(B, p.d.c_o, p.w_o, p.h_o, dtype=torch.int32,
+                              device=self.device)
+        self._dev(m, phi1, out)
+        _check(_lib.he_relu_requant(self._h, ctypes.byref(p), self._ptr(m), B,
+                                    self._ptr(phi1), shift, qmax, self._ptr(out),
+                                    _stream(stream)), "he_relu_requant")
+        return out
+
+    def avgpool(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None):
+        """int32 [B][C][H][W] -> [B][C] floor means."""
+        rows, hw = x.shape[0] * x.shape[1], x.shape[2] * x.shape[3]
+        if out is None:
+            out = torch.empty(x.shape[0], x.shape[1], dtype=torch.int32, device=self.device)
+        self._dev(x, out)
+        _check(_lib.he_avgpool(self._ptr(x), rows, hw, self._ptr(out), _stream(stream)),
+               "he_avgpool")
+        return out
+
+    def fc_server_init_p(self, W: torch.Tensor, a: torch.Tensor,
+                         e: Optional[torch.Tensor] = None, stream=None):
+        n_o, n_i = W.shape
+        f = FcDesc(n_i, n_o)
+        n_it, n_ib, n_ot, n_t = self.fc_plan(n_i, n_o)
+        out = self.empty_u64(n_ib, n_t, self.L, self.N)
+        wsb = _lib.he_fc_server_p_workspace_bytes(self._h, ctypes.byref(f))
+        ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        self._dev(W, a, e)
+        _check(_lib.he_fc_server_init_p(self._h, ctypes.byref(f), self._ptr(W), self._ptr(a),
+                                        self._ptr(e), self._ptr(out), self._ptr(ws), wsb,
+                                        _stream(stream)), "he_fc_server_init_p")
+        return out
+
+    def pack_fc_client_p(self, n_i, n_o, pp: torch.Tensor, stream=None):
+        f = FcDesc(n_i, n_o)
+        pspec = self.empty_u64(_lib.he_fc_wspec_bytes(self._h, ctypes.byref(f)) // 8)
+        ws = torch.empty(8 * pp.numel(), dtype=torch.uint8, device=self.device)
+        self._dev(pp)
+        _check(_lib.he_pack_fc_client_p(self._h, ctypes.byref(f), self._ptr(pp),
+                                        self._ptr(pspec), self._ptr(ws), ws.numel(),
+                                        _stream(stream)), "he_pack_fc_client_p")
+        return pspec
+
+    def unmask(self, m: torch.Tensor, phi1: Optional[torch.Tensor] = None,
+               out: Optional[torch.Tensor] = None, stream=None):
+        if out is None:
+            out = torch.empty(m.shape, dtype=torch.int32, device=self.device)
+        self._dev(m, phi1, out)
+        _check(_lib.he_unmask(self._h, self._ptr(m), self._ptr(phi1), m.numel(),
+                              self._ptr(out), _stream(stream)), "he_unmask")
         return out

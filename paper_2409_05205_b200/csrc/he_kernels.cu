@@ -2074,3 +2074,198 @@ extern "C" he_status he_mod_switch(const he_ctx* c, const uint64_t* d_in, long n
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
+
+// ============================================ chained pipeline (§8(f), R29)
+// Public-key mask of the c0-only encryption, Eq. (1):
+// ve = v b + e0 per polynomial, v and e0 small signed integers.
+__global__ void k_add_small(u64* __restrict__ x, const int32_t* __restrict__ e, long n_polys,
+                            int L, int logN, const he_limb* __restrict__ limbs) {
+    const long N = 1L << logN;
+    const long total = n_polys * L * N;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const long k = idx & (N - 1), r = idx >> logN;
+        const int l = (int)(r % L);
+        const u64 q = limbs[l].q;
+        x[idx] = addmod(x[idx], int_to_res(e[(r / L) * N + k], q), q);
+    }
+}
+
+extern "C" he_status he_pk_mask(const he_ctx* c, const int32_t* d_v, const int32_t* d_e,
+                                long n_polys, const uint64_t* d_b, uint64_t* d_ve, void* d_ws,
+                                size_t ws_bytes, void* stream) {
+    if (!c || n_polys < 0) return HE_EINVAL;
+    if (n_polys == 0) return HE_OK;
+    if (!d_v || !d_b || !d_ve || !d_ws) return HE_EINVAL;
+    if (ws_bytes < sizeof(u64) * (size_t)c->L * c->N) return HE_ENOMEM;
+    cudaStream_t st = STREAM(stream);
+    const long total = n_polys * c->L * c->N;
+    k_residues_from_int<<<grid_for(total, 256), 256, 0, st>>>(d_v, n_polys, c->L, c->logN,
+                                                              c->d_limb, (u64*)d_ve);
+    HE_CHECK_LAUNCH();
+    u64* bspec = (u64*)d_ws;
+    he_status s = launch_ntt_fwd(c, (const u64*)d_b, bspec, c->L, 0, st);
+    if (s != HE_OK) return s;
+    s = launch_ntt_fwd(c, (const u64*)d_ve, (u64*)d_ve, n_polys * c->L, 0, st);
+    if (s != HE_OK) return s;
+    k_pointwise_mul<<<grid_for(total, 256), 256, 0, st>>>((u64*)d_ve, bspec, n_polys, 1, c->L,
+                                                           c->logN, c->d_limb);
+    HE_CHECK_LAUNCH();
+    s = launch_ntt_inv(c, (u64*)d_ve, (u64*)d_ve, n_polys * c->L, st);
+    if (s != HE_OK) return s;
+    if (d_e) {
+        k_add_small<<<grid_for(total, 256), 256, 0, st>>>((u64*)d_ve, d_e, n_polys, c->L,
+                                                           c->logN, c->d_limb);
+        HE_CHECK_LAUNCH();
+    }
+    return HE_OK;
+}
+
+// Stub between layers (R29): decrypted compact slots -> next layer image.
+__global__ void k_relu_requant(const u32* __restrict__ m, const u32* __restrict__ phi1,
+                               PlanDev P, int B, int logN, u64 t, int shift, int qmax,
+                               int32_t* __restrict__ img) {
+    const long N = 1L << logN;
+    const long total = (long)B * P.n_ob * P.n_valid;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const int v = (int)(idx % P.n_valid);
+        const long bo = idx / P.n_valid;
+        const int ob = (int)(bo % P.n_ob), b = (int)(bo / P.n_ob);
+        const int nl = v % P.c_ob, Pq = v / P.c_ob;
+        const int Lc = Pq % P.h_o, Kr = Pq / P.h_o;
+        const int n = ob * P.c_ob + nl;
+        if (n >= P.c_o) continue;
+        long x = (long)m[idx];
+        if (phi1) {
+            const long i = (long)P.s * (P.stride * Kr * (long)P.h_p + P.stride * Lc) +
+                           (long)nl * P.step;
+            x -= (long)phi1[bo * N + i];
+            if (x < 0) x += (long)t;
+        }
+        if (x > (long)(t / 2)) x -= (long)t;                  // centered mod t
+        const long y = x > 0 ? min((long)qmax, x >> shift) : 0;
+        img[(((long)b * P.c_o + n) * P.w_o + Kr) * P.h_o + Lc] = (int32_t)y;
+    }
+}
+
+extern "C" he_status he_relu_requant(const he_ctx* c, const he_conv_plan* p, const uint32_t* d_m,
+                                     int B, const uint32_t* d_phi1, int shift, int qmax,
+                                     int32_t* d_img, void* stream) {
+    if (!c || !p || B < 0 || shift < 0 || shift > 62 || qmax < 0) return HE_EINVAL;
+    if (!plan_ok(c, p)) return HE_ESHAPE;
+    if (B == 0) return HE_OK;
+    if (!d_m || !d_img) return HE_EINVAL;
+    const PlanDev P = plan_dev(p);
+    const long total = (long)B * P.n_ob * P.n_valid;
+    k_relu_requant<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(
+        d_m, d_phi1, P, B, c->logN, c->t, shift, qmax, d_img);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+__global__ void k_avgpool(const int32_t* __restrict__ x, long rows, int hw,
+                          int32_t* __restrict__ out) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (long r = warp; r < rows; r += nw) {
+        long sacc = 0;
+        for (int i = lane; i < hw; i += 32) sacc += x[r * hw + i];
+        for (int o = 16; o; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        if (lane == 0) {
+            long q = sacc / hw;
+            if (sacc % hw != 0 && sacc < 0) --q;              // floor
+            out[r] = (int32_t)q;
+        }
+    }
+}
+
+extern "C" he_status he_avgpool(const int32_t* d_x, long rows, int hw, int32_t* d_out,
+                                void* stream) {
+    if (rows < 0 || hw < 1) return HE_EINVAL;
+    if (rows == 0) return HE_OK;
+    if (!d_x || !d_out) return HE_EINVAL;
+    k_avgpool<<<grid_for(rows * 32, 256), 256, 0, STREAM(stream)>>>(d_x, rows, hw, d_out);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+// FC client mirror path (Alg. 2 Lines 5-6 and 16-17):
+// p_{beta,t} = w_{beta,t} a + e, and its spectra in the he_pack_fc_weights
+// format so that he_fc(vs, pspec, zero bias, NULL) gives c1^r.
+extern "C" size_t he_fc_server_p_workspace_bytes(const he_ctx* c, const he_fc_desc* f) {
+    if (!fc_ok(c, f)) return 0;
+    const FcP P = fc_plan(c, f);
+    return sizeof(u64) * ((size_t)P.n_ib * P.n_t + 1) * c->L * c->N;
+}
+
+extern "C" he_status he_fc_server_init_p(const he_ctx* c, const he_fc_desc* f, const int32_t* d_W,
+                                         const uint64_t* d_a, const int32_t* d_e, uint64_t* d_p,
+                                         void* d_ws, size_t ws_bytes, void* stream) {
+    if (!c || !f || !d_W || !d_a || !d_p || !d_ws) return HE_EINVAL;
+    if (!fc_ok(c, f)) return HE_ESHAPE;
+    if (ws_bytes < he_fc_server_p_workspace_bytes(c, f)) return HE_ENOMEM;
+    cudaStream_t st = STREAM(stream);
+    const FcP P = fc_plan(c, f);
+    const long nl = (long)P.n_ib * P.n_t * c->L, total = nl * c->N;
+    u64* aspec = (u64*)d_ws;
+    u64* wp = (u64*)d_p;
+    k_fc_weight_coeffs<<<grid_for(total, 256), 256, 0, st>>>(d_W, wp, P, c->L, c->logN,
+                                                             c->d_limb);
+    HE_CHECK_LAUNCH();
+    he_status s = launch_ntt_fwd(c, wp, wp, nl, 0, st);
+    if (s != HE_OK) return s;
+    s = launch_ntt_fwd(c, (const u64*)d_a, aspec, c->L, 0, st);
+    if (s != HE_OK) return s;
+    k_pointwise_mul<<<grid_for(total, 256), 256, 0, st>>>(wp, aspec, (long)P.n_ib * P.n_t, 1,
+                                                           c->L, c->logN, c->d_limb);
+    HE_CHECK_LAUNCH();
+    s = launch_ntt_inv(c, wp, wp, nl, st);
+    if (s != HE_OK) return s;
+    if (d_e) {
+        k_add_small<<<grid_for(total, 256), 256, 0, st>>>(wp, d_e, (long)P.n_ib * P.n_t, c->L,
+                                                           c->logN, c->d_limb);
+        HE_CHECK_LAUNCH();
+    }
+    return HE_OK;
+}
+
+extern "C" he_status he_pack_fc_client_p(const he_ctx* c, const he_fc_desc* f,
+                                         const uint64_t* d_p, uint64_t* d_pspec, void* d_ws,
+                                         size_t ws_bytes, void* stream) {
+    if (!c || !f || !d_p || !d_pspec || !d_ws) return HE_EINVAL;
+    if (!fc_ok(c, f)) return HE_ESHAPE;
+    const FcP P = fc_plan(c, f);
+    const long nl = (long)P.n_ib * P.n_t * c->L;
+    if (ws_bytes < sizeof(u64) * (size_t)nl * c->N) return HE_ENOMEM;
+    cudaStream_t st = STREAM(stream);
+    u64* ws = (u64*)d_ws;
+    he_status s = launch_ntt_fwd(c, (const u64*)d_p, ws, nl, 0, st);
+    if (s != HE_OK) return s;
+    k_fc_finish_weights<<<grid_for(nl * c->N, 256), 256, 0, st>>>(ws, (ulonglong2*)d_pspec, nl,
+                                                                  c->L, c->logN, c->d_limb);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+// FC stub (R29): logits = centered((m - phi1) mod t).
+__global__ void k_unmask(const u32* __restrict__ m, const u32* __restrict__ phi1, long n, u64 t,
+                         int32_t* __restrict__ out) {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
+         i += (long)gridDim.x * blockDim.x) {
+        long x = (long)m[i] - (phi1 ? (long)phi1[i] : 0);
+        if (x < 0) x += (long)t;
+        if (x > (long)(t / 2)) x -= (long)t;
+        out[i] = (int32_t)x;
+    }
+}
+
+extern "C" he_status he_unmask(const he_ctx* c, const uint32_t* d_m, const uint32_t* d_phi1,
+                               long n, int32_t* d_out, void* stream) {
+    if (!c || n < 0) return HE_EINVAL;
+    if (n == 0) return HE_OK;
+    if (!d_m || !d_out) return HE_EINVAL;
+    k_unmask<<<grid_for(n, 256), 256, 0, STREAM(stream)>>>(d_m, d_phi1, n, c->t, d_out);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
