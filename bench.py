@@ -56,6 +56,9 @@ def parse():
                          "sequence per layer)")
     ap.add_argument("--graph", type=int, default=1,
                     help="1: replay the step as a captured CUDA graph")
+    ap.add_argument("--payload-only", type=int, default=0,
+                    help="1: the step writes only the masked valid-slot payload "
+                         "(he_conv_ex with d_out = NULL), not the full c0^r")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-client", action="store_true",
@@ -320,10 +323,14 @@ def main():
     from paper_2409_05205_b200.dist import shard_range
     sub = [shard_range(B, k, nstr) for k in range(nstr)]
 
+    po_flag = [bool(args.payload_only)]
+
     def step():
+        po = po_flag[0]
         if nstr == 1:
             for i, lw in enumerate(layers):
-                ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], outs[i], ws, compact=comps[i])
+                ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], None if po else outs[i], ws,
+                         compact=comps[i], full=not po)
         else:
             fork_ev[0].record(stream)
             for k in range(1, nstr):
@@ -331,8 +338,8 @@ def main():
             for i, lw in enumerate(layers):
                 for k, (lo, hi) in enumerate(sub):
                     ctx.conv(lw.p, c0_d[i][lo:hi], fspecs[i], phi_d[i][lo:hi],
-                             outs[i][lo:hi], ws_all[k], compact=comps[i][lo:hi],
-                             stream=side[k])
+                             None if po else outs[i][lo:hi], ws_all[k],
+                             compact=comps[i][lo:hi], full=not po, stream=side[k])
             for k in range(1, nstr):
                 fork_ev[k].record(side[k])
                 stream.wait_event(fork_ev[k])
@@ -376,6 +383,32 @@ def main():
         e1.record()
         barrier()
     ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    # ---- the same step writing only the masked valid-slot payload (what the
+    # server sends), reported beside the headline
+    payload_only = None
+    if not args.profile and not args.payload_only:
+        po_flag[0] = True
+        step()
+        g2 = None
+        if args.graph:
+            torch.cuda.synchronize()
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2, stream=stream):
+                step()
+            g2.replay()
+        run2 = g2.replay if g2 is not None else step
+        barrier()
+        e0.record()
+        for k in range(args.steps):
+            run2()
+        e1.record()
+        barrier()
+        ms_po = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        payload_only = {"ms_per_step": ms_po, "value": evals_step * world / (ms_po * 1e-3),
+                        "what": "he_conv_ex with d_out = NULL: extraction, mask and "
+                                "payload fused, full c0^r not materialised"}
+        po_flag[0] = False
+        del g2
     # ---- timed region 2 (kernel analysis): one launch sequence per layer
     # (streams = 1) with stage events from he_conv_ex / he_fc_ex, so each
     # kernel's duration is measured without overlap
@@ -601,6 +634,39 @@ def main():
                "d2h_bytes_per_step": d2h,
                "wire": "50-bit packed residues (he_residues_pack50/unpack50); "
                        "phi1 drawn on device (he_phi1_generate)"}
+        # PCIe roof of the end-to-end step: the same H2D bytes copied alone
+        # (pinned -> device, one stream), and H2D + D2H concurrently
+        big_h = torch.empty(h2d, dtype=torch.uint8).pin_memory()
+        big_d = torch.empty(h2d, dtype=torch.uint8, device=dev)
+        out_h = torch.empty(d2h, dtype=torch.uint8).pin_memory()
+        out_d = torch.empty(d2h, dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            big_d.copy_(big_h, non_blocking=True)
+        torch.cuda.synchronize()
+        x0.record()
+        for _ in range(args.steps):
+            big_d.copy_(big_h, non_blocking=True)
+        x1.record()
+        torch.cuda.synchronize()
+        ms_h2d = x0.elapsed_time(x1) / args.steps
+        x0.record()
+        for _ in range(args.steps):
+            with torch.cuda.stream(h2d_s):
+                big_d.copy_(big_h, non_blocking=True)
+            with torch.cuda.stream(d2h_s):
+                out_h.copy_(out_d, non_blocking=True)
+            stream.wait_stream(h2d_s)
+            stream.wait_stream(d2h_s)
+        x1.record()
+        torch.cuda.synchronize()
+        ms_both = x0.elapsed_time(x1) / args.steps
+        e2e["pcie"] = {"h2d_gbs": h2d / (ms_h2d * 1e-3) / 1e9,
+                       "h2d_only_ms": ms_h2d, "h2d_plus_d2h_ms": ms_both,
+                       "frac": ms_h2d / ms_e2e,
+                       "note": "copy-only times of the step's own wire bytes; frac = the "
+                               "H2D-only copy time / the e2e step time (1.0 = the step "
+                               "runs at the PCIe H2D roof)"}
+        del big_h, big_d, out_h, out_d
         # same loop with the conv payloads modulus-switched to one limb
         for _ in range(2):
             e2e_step(1)
@@ -802,7 +868,7 @@ def main():
             "ntt": ntt, "stages_ms_per_step": st, "per_layer": per_layer,
             "roofline": roofline,
             "roofline_all": rl, "u1": u1, "init_ms": init_ms,
-            "cpu_baseline": cpu, "e2e": e2e, "client": client, "chain": chain, "fc_variants": fc_var, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "payload_only": payload_only, "client": client, "chain": chain, "fc_variants": fc_var, "clocks": clocks,
             "gpu_launches": launches_step * args.steps,
         }
         print(json.dumps(line), flush=True)
