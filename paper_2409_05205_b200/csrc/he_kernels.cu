@@ -918,7 +918,11 @@ struct FastDiv {
     bool p2;
     __device__ __forceinline__ explicit FastDiv(int dd) : d(dd), sh(0),
                                                          p2((dd & (dd - 1)) == 0) {
+#ifdef __CUDA_ARCH__
+        sh = 31 - __clz(dd);
+#else
         while ((1 << sh) < dd) ++sh;
+#endif
     }
     __device__ __forceinline__ int div(int x) const { return p2 ? (x >> sh) : (x / d); }
 };
@@ -971,7 +975,8 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
     }
     // cp.async one unit into staging buffer `bf`
     auto issue = [&](int u, int bf) {
-        const int gu = (u / nkc) * GS, kc = u - (u / nkc) * nkc;
+        const int uq = nkc == 1 ? u : u / nkc;
+        const int gu = uq * GS, kc = u - uq * nkc;
         const int gsn = min(GS, gcnt - gu), k0 = kc * KC;
         u32* sA = sm32 + bf * buf_words;
         u32* sB = sA + 7 * rows * rw;
@@ -1027,7 +1032,8 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
             cp_async_wait<0>();
         }
         __syncthreads();
-        const int gu = (u / nkc) * GS, kc = u - (u / nkc) * nkc;
+        const int uq = nkc == 1 ? u : u / nkc;
+        const int gu = uq * GS, kc = u - uq * nkc;
         const int gsn = min(GS, gcnt - gu);
         const u32* sA = sm32 + (nbuf == 2 ? (u & 1) : 0) * buf_words;
         const u32* sB = sA + 7 * rows * rw;
