@@ -54,6 +54,10 @@ def parse():
                     help="split every layer's image batch into this many "
                          "sub-batches, each on its own CUDA stream (1 = one launch "
                          "sequence per layer)")
+    ap.add_argument("--overlap", choices=["batch", "layers"], default="layers",
+                    help="with --streams > 1: split each layer's batch across the "
+                         "streams (batch) or put whole layers on alternating streams "
+                         "(layers: independent layer jobs overlap)")
     ap.add_argument("--graph", type=int, default=1,
                     help="1: replay the step as a captured CUDA graph")
     ap.add_argument("--payload-only", type=int, default=0,
@@ -317,7 +321,8 @@ def main():
     torch.cuda.synchronize()
 
     evals_step = sum(lw.evals for lw in layers) + (B if fc else 0)
-    launches_step = 3 * len(layers) * nstr + (2 if fc else 0)
+    launches_step = 3 * len(layers) * (nstr if args.overlap == "batch" else 1) + \
+        (2 if fc else 0)
 
     fork_ev = [torch.cuda.Event() for _ in range(nstr)]
     from paper_2409_05205_b200.dist import shard_range
@@ -336,6 +341,11 @@ def main():
             for k in range(1, nstr):
                 side[k].wait_event(fork_ev[0])
             for i, lw in enumerate(layers):
+                if args.overlap == "layers":
+                    k = i % nstr
+                    ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], None if po else outs[i],
+                             ws_all[k], compact=comps[i], full=not po, stream=side[k])
+                    continue
                 for k, (lo, hi) in enumerate(sub):
                     ctx.conv(lw.p, c0_d[i][lo:hi], fspecs[i], phi_d[i][lo:hi],
                              None if po else outs[i][lo:hi], ws_all[k],
@@ -509,12 +519,22 @@ def main():
                         "frac": byts / t / 1e9 / hbm_gbs, "traffic": None,
                         "share_of_step": ms / ms_seq,
                         "alu_frac": (ops / t) / alu_peak}
+    # DRAM traffic per launch from the committed ncu pass (profiles/), beside
+    # the algorithmic bytes per launch (traffic well above it = re-reads)
+    tr_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                           "traffic_r01.json")
+    tr = json.load(open(tr_path)) if os.path.exists(tr_path) else {}
+    for name, (ms, ops, alu_peak, unit, byts) in kern.items():
+        rl[name]["algorithmic_bytes_per_launch"] = byts / len(layers)
+        if name in tr:
+            rl[name]["traffic"] = tr[name]["mean_dram_bytes_per_launch"]
+            rl[name]["traffic_source"] = "profiles/traffic_r01.json (ncu, " + \
+                str(tr[name]["launches"]) + " launches)"
     dom = max(kern, key=lambda k: kern[k][0])
     roofline = dict(rl[dom])
     roofline["kernel"] = dom
     roofline["peak_source"] = ("U1 register-resident microbenchmark on this GPU"
                                if roofline["bound"] == "alu" else hbm_src)
-    roofline["traffic_note"] = "per-launch DRAM bytes: see profiles/ ncu summary"
     roofline["timed_in"] = ("sequential analysis pass (streams=1) of the same step, "
                             "CUDA events around each kernel (he_conv_ex)")
 
@@ -861,7 +881,8 @@ def main():
                                    f"N={N}, L={L}, B={B}/GPU",
                        "global_batch": B * world, "N": N, "L": L,
                        "parallelism": f"dp{world} (batch-sharded, no collective)",
-                       "streams": nstr, "cuda_graph": graph is not None,
+                       "streams": nstr, "overlap": args.overlap,
+                       "cuda_graph": graph is not None,
                        "l2": "inputs larger than L2 (>1 GB touched per step)"},
             "ms_per_plain20_image": ms_step / B if cfg.idx == 4 else None,
             "sequential_ms_per_step": ms_seq,
