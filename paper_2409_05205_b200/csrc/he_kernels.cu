@@ -1144,7 +1144,7 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
 // of the row is written exactly once, in contiguous runs of u1 - u0 words.
 // Channel arrays sit in shared memory at an odd word stride (conflict-free).
 template <bool DP>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, 3)
 k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                u64* __restrict__ out, u64* __restrict__ comp, PlanDev P, int B, int L,
                int logN, int cc, int nchunk, int stride, const he_limb* __restrict__ limbs,
@@ -1184,7 +1184,7 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     }
     __syncthreads();
     if (DP)
-        gs_all_dp<3>(reinterpret_cast<double*>(sm), stride, ncc, logM, 0, logM,
+        gs_all_dp<4>(reinterpret_cast<double*>(sm), stride, ncc, logM, 0, logM,
                      twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
     else if (logM <= 12)
         gs_all<3, true>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
