@@ -119,6 +119,8 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
         c->mac_mode = (m && m[0] == 'i') ? 1 : 0;     // HE_MAC=imad forces the IMAD MAC
         const char* t = getenv("HE_NTT");
         c->ntt_mode = (t && t[0] == 'i') ? 1 : 0;     // HE_NTT=int: integer butterflies
+        const char* k = getenv("HE_NTT_COLS");
+        c->ntt_cluster = (k && k[0] == '0') ? 1 : 0;  // HE_NTT_COLS=0: cluster kernels
     }
     c->logN = r->log2N;
     c->N = N;

@@ -45,6 +45,7 @@ struct he_ctx {
     double* d_twd_fwd;      // [L][N]  psi^{brv(k)} as double (FP64 transforms)
     double* d_twd_inv;      // [L][N]  psi^{-brv(k)} as double
     int ntt_mode;           // 0: FP64 butterflies (default), 1: integer (HE_NTT=int)
+    int ntt_cluster;        // HE_NTT_COLS=0: incomplete transforms on the cluster kernels
     u64* d_enc;             // [L][t] enc_j(m) table (t <= 2^20), else nullptr
 };
 
@@ -269,6 +270,69 @@ __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg,
     }
     for (; st < end; st += RMAX) {
         ct_pass_dp<RMAX>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        __syncthreads();
+    }
+}
+
+// Column form of the incomplete forward transform: the first T = log2(M)
+// stages of the N-point CT transform never mix residues mod s = N/M, so
+// they are s independent M-point transforms of the columns {c + s k}, with
+// the N-point twiddles of stage st and block k >> (T - st).  One radix-2^K
+// pass over narr column arrays (arr_stride words apart) in shared memory;
+// value bounds as ct_pass_dp.
+template <int K>
+__device__ __forceinline__ void ct_pass_cols_dp(double* sm, int arr_stride, int narr, int T,
+                                                int st0, const double* __restrict__ tw,
+                                                double q, double qinv) {
+    const int lt0 = T - st0 - 1;
+    const int ltk = lt0 - (K - 1);
+    const int tk = 1 << ltk;
+    const int gper = 1 << (T - K);
+    const int total = narr * gper;
+    for (int G = threadIdx.x; G < total; G += blockDim.x) {
+        const int a = G >> (T - K), g = G & (gper - 1);
+        double* s = sm + a * arr_stride;
+        const int blk = g >> ltk, off = g & (tk - 1);
+        const int base = (blk << (lt0 + 1)) + off;
+        double tws[(1 << K) - 1];
+#pragma unroll
+        for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
+            const int twb = (1 << (st0 + r)) + (blk << r);
+#pragma unroll
+            for (int z = 0; z < (1 << r); ++z) tws[o + z] = __ldg(&tw[twb + z]);
+        }
+        double x[1 << K];
+#pragma unroll
+        for (int c = 0; c < (1 << K); ++c) x[c] = dp_reduce(s[PAD(base + (c << ltk))], q, qinv);
+#pragma unroll
+        for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
+            const int half = 1 << (K - 1 - r);
+#pragma unroll
+            for (int c = 0; c < (1 << K); ++c) {
+                if (c & half) continue;
+                if (r >= 2) x[c + half] = dp_reduce(x[c + half], q, qinv);
+                ct_bfly_dp(x[c], x[c + half], tws[o + (c >> (K - r))], q, qinv);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < (1 << K); ++c) s[PAD(base + (c << ltk))] = x[c];
+    }
+}
+
+template <int RMAX>
+__device__ __forceinline__ void ct_all_cols_dp(double* sm, int arr_stride, int narr, int T,
+                                               const double* tw, double q, double qinv) {
+    int st = 0;
+    const int rem = T % RMAX;
+    if (rem) {
+        if (rem == 1) ct_pass_cols_dp<1>(sm, arr_stride, narr, T, st, tw, q, qinv);
+        else if (rem == 2) ct_pass_cols_dp<2>(sm, arr_stride, narr, T, st, tw, q, qinv);
+        else ct_pass_cols_dp<3>(sm, arr_stride, narr, T, st, tw, q, qinv);
+        st += rem;
+        __syncthreads();
+    }
+    for (; st < T; st += RMAX) {
+        ct_pass_cols_dp<RMAX>(sm, arr_stride, narr, T, st, tw, q, qinv);
         __syncthreads();
     }
 }

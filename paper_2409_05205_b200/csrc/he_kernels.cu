@@ -251,6 +251,91 @@ k_ntt_fwd_dp_s2(const u64* in, u64* out, int logN, int L, const he_limb* __restr
     ntt_fwd_segment_dp<2, OUT_FMT>(in, out, logN, L, limbs, tw_all, T);
 }
 
+// Column-tiled incomplete forward transform (FP64): CTA =
+// (limb, C consecutive columns c0..c0+C-1 of the s = 2^skip columns), each
+// column an M-point transform (M = N / s) held in shared memory at an odd
+// word stride; coalesced row loads (C consecutive words per row k), and the
+// store writes the same positions p = k s + c in format OUT_FMT.  No
+// cluster, no read amplification: used when skip >= 2 (C >= 4).
+template <int OUT_FMT>
+__global__ void __launch_bounds__(256, 4)
+k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int L,
+               const he_limb* __restrict__ limbs, const double* __restrict__ twd_all, TileLay T,
+               int logC, int stride) {
+    extern __shared__ u64 sm_raw[];
+    double* sm = reinterpret_cast<double*>(sm_raw);
+    const int N = 1 << logN, logs = T.skip, s = 1 << logs, Tn = logN - logs, M = 1 << Tn;
+    const int C = 1 << logC, nct = s >> logC;
+    const int li = blockIdx.x / nct, c0 = (blockIdx.x - li * nct) << logC;
+    const int l = li % L;
+    const double q = limbs[l].qd, qinv = limbs[l].qinvd;
+    const double* tw = twd_all + (size_t)l * N;
+    const u64* src = in + (size_t)li * N + c0;
+    const int tot = M << logC;
+    for (int base = threadIdx.x; base < tot; base += 4 * blockDim.x) {    // 4 loads in flight
+        u64 v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int idx = base + e * blockDim.x;
+            v[e] = idx < tot ? src[(size_t)(idx >> logC) * s + (idx & (C - 1))] : 0;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int idx = base + e * blockDim.x;
+            if (idx < tot) sm[(idx & (C - 1)) * stride + PAD(idx >> logC)] = u2d(v[e]);
+        }
+    }
+    __syncthreads();
+    ct_all_cols_dp<3>(sm, stride, C, Tn, tw, q, qinv);
+    if (OUT_FMT == 2) {
+        unsigned char* A = reinterpret_cast<unsigned char*>(out);
+        const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
+        const int K = T.n_ib << logs;
+        const size_t pstride = (size_t)T.B * T.Gt * T.Kp;
+        const int nq = C >> 2;                                  // 4-column quads per row
+        for (int e = threadIdx.x; e < (M * nq); e += blockDim.x) {
+            const int k = e / nq, c = (e - k * nq) * 4;
+            u64 x[4];
+#pragma unroll
+            for (int z = 0; z < 4; ++z) x[z] = d2canon(sm[(c + z) * stride + PAD(k)], q, qinv);
+            u32 pl[8];
+            byte_transpose4((u32)x[0], (u32)x[1], (u32)x[2], (u32)x[3], pl[0], pl[1], pl[2], pl[3]);
+            byte_transpose4((u32)(x[0] >> 32), (u32)(x[1] >> 32), (u32)(x[2] >> 32),
+                            (u32)(x[3] >> 32), pl[4], pl[5], pl[6], pl[7]);
+            const int g = k, u = c0 + c;
+            const int gb = g / T.Gt, gi = g - gb * T.Gt;
+            unsigned char* row =
+                A + (((((size_t)l * (M / T.Gt) + gb) * 7) * T.B + b) * T.Gt + gi) * T.Kp +
+                beta * s + u;
+            const bool tail = (beta == T.n_ib - 1) && (u + 4 == s) && (T.Kp > K);
+#pragma unroll
+            for (int j = 0; j < 7; ++j) {
+                *reinterpret_cast<u32*>(row + j * pstride) = pl[j];
+                if (tail)
+                    for (int z = 4; z < T.Kp - K + 4; z += 4)
+                        *reinterpret_cast<u32*>(row + j * pstride + z) = 0u;
+            }
+        }
+    } else {
+        u64* dst = out + (size_t)li * N + c0;
+        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+            u64 v = d2canon(sm[(idx & (C - 1)) * stride + PAD(idx >> logC)], q, qinv);
+            if (OUT_FMT == 1) v = to_split25(v);
+            dst[(size_t)(idx >> logC) * s + (idx & (C - 1))] = v;
+        }
+    }
+}
+
+// columns per CTA and the odd-ish array stride for the column kernel
+static void cols_geometry(int logN, int skip, int& logC, int& stride) {
+    const int Tn = logN - skip, M = 1 << Tn;
+    logC = std::max(2, std::min(skip, 12 - Tn));               // C M <= 4096 when possible
+    const int C = 1 << logC;
+    stride = padded_words(M);
+    const int want = C < 16 ? (16 / C) & 15 : 1;                // 16/C (mod 16), or odd
+    while ((stride & 15) != want && !(C >= 16 && (stride & 1))) ++stride;
+}
+
 // Launch the forward NTT over nlimbs = batch * L limbs.
 static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
                                 long nlimbs, int out_fmt, cudaStream_t st,
@@ -267,6 +352,23 @@ static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
         {k_ntt_fwd_s0<0>, k_ntt_fwd_s0<1>, k_ntt_fwd_s0<2>},
         {k_ntt_fwd_s1<0>, k_ntt_fwd_s1<1>, k_ntt_fwd_s1<2>},
         {k_ntt_fwd_s2<0>, k_ntt_fwd_s2<1>, k_ntt_fwd_s2<2>}};
+    // incomplete transform with s >= 256: independent column transforms, no
+    // cluster (config 5: forward NTT 0.92 -> 0.73 ms); for s <= 128 the
+    // cluster kernels measured as fast or faster (config 4)
+    if (c->ntt_mode == 0 && T.skip >= 8 && !c->ntt_cluster) {
+        int logC, stride;
+        cols_geometry(logN, T.skip, logC, stride);
+        const size_t smem_c = sizeof(u64) * (size_t)(1 << logC) * stride;
+        typedef void (*kfc)(const u64*, u64*, int, int, const he_limb*, const double*, TileLay,
+                            int, int);
+        static kfc const tabc[3] = {k_ntt_fwd_cols<0>, k_ntt_fwd_cols<1>, k_ntt_fwd_cols<2>};
+        kfc kc = tabc[out_fmt];
+        if (!set_smem(kc, smem_c)) return HE_ECUDA;
+        kc<<<(unsigned)(nlimbs * ((1 << T.skip) >> logC)), 256, smem_c, st>>>(
+            in, out, logN, c->L, c->d_limb, c->d_twd_fwd, T, logC, stride);
+        HE_CHECK_LAUNCH();
+        return HE_OK;
+    }
     if (c->ntt_mode == 0) {
         typedef void (*kfd)(const u64*, u64*, int, int, const he_limb*, const double*, TileLay);
         static kfd const tabd[3][3] = {

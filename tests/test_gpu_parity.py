@@ -433,3 +433,13 @@ def test_ntt_forward_partial_matches_definition(he, N):
                 b = int(format(g, f"0{T}b")[::-1], 2) if T else 0
                 want = R.reduce_mod_binomial(x[1, j], s, pow(psi, s * (2 * b + 1), q), q)
                 assert np.array_equal(got[1, j, g * s:(g + 1) * s], want), (skip, j, g)
+
+
+def test_conv_cluster_ntt_path_for_large_s(he, monkeypatch):
+    """HE_NTT_COLS=0 keeps the 4-CTA cluster forward NTT for s >= 256 (config
+    5) instead of the column-tiled incomplete transform; both bit-exact."""
+    monkeypatch.setenv("HE_NTT_COLS", "0")
+    cfg = synth.CONFIGS[5]
+    ctx = he.Context(cfg.primes, cfg.log2N, cfg.t)
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    run_conv(he, ctx, ring, cfg.conv[0], 16, seed=cfg.seed + 3, check_b=[0, 15])
