@@ -1048,8 +1048,8 @@ __device__ __forceinline__ void cp_async_n(void* smem_dst, const void* gsrc, boo
 // contiguous in global memory and are copied with 16-byte cp.async into
 // padded shared rows (stride = 4 mod 8 words: conflict-free fragments).
 // Reduced outputs go straight to the transposed fold out[l][b][n][g].
-template <int TB16>
-__global__ void __launch_bounds__(512)
+template <int TB16, int MINB = 1>
+__global__ void __launch_bounds__(MINB > 1 ? 128 : 512, MINB)
 k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
            u64* __restrict__ out, int B, int L, int M, int c_o, int Kp, int G, int GS,
            int KC, int Gt, int nbuf, const he_limb* __restrict__ limbs) {
@@ -1192,6 +1192,9 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
     }
 }
 
+#ifndef HE_MAC_K16_MINB
+#define HE_MAC_K16_MINB 5
+#endif
 static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fpl, u64* out,
                                  int B, int n_ib, int L, int logN, int logs, int c_o,
                                  const he_limb* limbs, cudaStream_t st) {
@@ -1200,7 +1203,9 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
     const int nrow = (c_o + 7) & ~7, nnt = nrow / 8;
     if (nnt > 32) return HE_ESHAPE;                       // c_o <= 256
     const int Gt = tile_gt(M);
-    const size_t budget = 48 * 1024;                      // per staging buffer
+    // per staging buffer; the K = 16 small-CTA case targets 5 CTAs per SM
+    const bool k16c = Kp == 16 && HE_MAC_K16_MINB > 1;
+    const size_t budget = k16c ? 227 * 1024 / HE_MAC_K16_MINB - 1024 : 48 * 1024;
     auto unit_bytes = [&](int rows, int gs, int kc) {
         return sizeof(u32) * 7 * ((size_t)rows * imma_sw(gs * kc) + (size_t)gs * nrow * imma_sw(kc));
     };
@@ -1227,7 +1232,11 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
     const int nbuf = nunits > 1 ? 2 : 1;
     const size_t smem = nbuf * unit_bytes(rows, GS, KC);
     if (smem > 227 * 1024) return HE_ESHAPE;
-    auto k = TB16 == 2 ? k_mac_imma<2> : k_mac_imma<1>;
+    // K = 16 with one unit per CTA and <= 4 warps: cap registers so five
+    // CTAs share an SM (occupancy-bound small-K case)
+    const bool k16 = k16c && nunits == 1 && 32 * warps <= 128;
+    auto k = TB16 == 2 ? (k16 ? k_mac_imma<2, HE_MAC_K16_MINB> : k_mac_imma<2>)
+                       : (k16 ? k_mac_imma<1, HE_MAC_K16_MINB> : k_mac_imma<1>);
     if (!set_smem(k, smem)) return HE_ECUDA;
     dim3 grid(L * ((M + G - 1) / G), (B + rows - 1) / rows);
     k<<<grid, 32 * warps, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, G, GS, KC, Gt, nbuf, limbs);
