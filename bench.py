@@ -296,8 +296,10 @@ def main():
         outs.append(ctx.empty_u64(B, p.n_ob, L, N))
         comps.append(ctx.empty_u64(B, p.n_ob, L, p.n_valid))
     nstr = max(1, args.streams)
+    # workspaces cover the dense (client) plans too
     ws_all = [torch.empty(max(ctx.conv_workspace(p, B).numel() for p in
-                              [lw.p for lw in layers]), dtype=torch.uint8, device=dev)
+                              [lw.p for lw in layers] + [ctx.dense_plan(lw.p) for lw in layers]),
+                          dtype=torch.uint8, device=dev)
               for _ in range(nstr)]
     ws = ws_all[0]
     side = [stream] + [torch.cuda.Stream(dev) for _ in range(nstr - 1)]
@@ -741,7 +743,7 @@ def main():
             for i, lw in enumerate(layers):
                 if E:
                     E[i][0].record()
-                ctx.conv(lw.p, c0_d[i], pspecs[i], None, None, ws, compact=c1s[i],
+                ctx.conv(ctx.dense_plan(lw.p), c0_d[i], pspecs[i], None, None, ws, compact=c1s[i],
                          full=False)
                 if E:
                     E[i][1].record()

@@ -93,6 +93,13 @@ typedef struct {
 typedef struct {
     he_conv_desc d;
     int32_t s, c_ib, n_ib, c_ob, n_ob, w_p, h_p, w_o, h_o, n_valid;
+    /* columns u < k_u of each fold group enter the MAC (K = n_ib k_u).  The
+     * filter polynomials of Eq. (6) have exponents -m mod s (m < c_ib), so
+     * after the incomplete transform their operand is zero for u >= c_ib:
+     * he_conv_plan_make sets k_u = c_ib rounded up to a multiple of 4 (<= s).
+     * A dense second operand (the client's p of Alg. 1 Line 5) needs
+     * k_u = s: he_conv_plan_dense. */
+    int32_t k_u;
 } he_conv_plan;
 
 /* Host-only, deterministic.  s_override = 0 applies R11; otherwise it must
@@ -102,6 +109,10 @@ typedef struct {
  * for a stride that is not a power of two. */
 he_status he_conv_plan_make(const he_ctx* ctx, const he_conv_desc* d,
                             int s_override, he_conv_plan* out);
+
+/* The same plan with k_u = s, for he_pack_client_p / he_conv on the
+ * client's dense operand.  HE_EINVAL on NULL. */
+he_status he_conv_plan_dense(const he_conv_plan* p, he_conv_plan* out);
 
 /* a1, client side (Eq. (5); Alg. 1 Line 2).  Packs
  * d_img int32 [B][c_i][w_i][h_i] into the input polynomials

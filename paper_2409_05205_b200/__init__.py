@@ -48,7 +48,7 @@ class ConvDesc(ctypes.Structure):
 class ConvPlan(ctypes.Structure):
     _fields_ = [("d", ConvDesc)] + [(n, ctypes.c_int32) for n in
                                      ("s", "c_ib", "n_ib", "c_ob", "n_ob", "w_p",
-                                      "h_p", "w_o", "h_o", "n_valid")]
+                                      "h_p", "w_o", "h_o", "n_valid", "k_u")]
 
     def __repr__(self):
         return (f"ConvPlan(s={self.s}, c_ib={self.c_ib}, n_ib={self.n_ib}, "
@@ -79,6 +79,7 @@ _sig("he_ctx_destroy", [_P], None)
 _sig("he_ctx_psi", [_P, ctypes.c_uint32], ctypes.c_uint64)
 _sig("he_conv_plan_make", [_P, ctypes.POINTER(ConvDesc), _I,
                            ctypes.POINTER(ConvPlan)])
+_sig("he_conv_plan_dense", [ctypes.POINTER(ConvPlan), ctypes.POINTER(ConvPlan)])
 _sig("he_pack_input", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _P])
 _sig("he_filter_bytes", [_P, ctypes.POINTER(ConvPlan)], _SZ)
 _sig("he_pack_filters_workspace_bytes", [_P, ctypes.POINTER(ConvPlan)], _SZ)
@@ -121,7 +122,7 @@ _sig("he_fc_server_init_p", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _P, _P, _SZ
 _sig("he_pack_fc_client_p", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _SZ, _P])
 
 EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
-            "he_conv_plan_make", "he_pack_input", "he_filter_bytes",
+            "he_conv_plan_make", "he_conv_plan_dense", "he_pack_input", "he_filter_bytes",
             "he_pack_filters_workspace_bytes", "he_pack_filters",
             "he_conv_workspace_bytes", "he_conv", "he_conv_ex", "he_mask_extract",
             "he_pack_fc_input", "he_fc_wspec_bytes", "he_fc_workspace_bytes",
@@ -413,8 +414,18 @@ class Context:
                                      _stream(stream)), "he_server_init_p")
         return out
 
+    def dense_plan(self, p: ConvPlan) -> ConvPlan:
+        """The plan with k_u = s (he_conv_plan_dense): for the client's conv
+        on he_pack_client_p spectra."""
+        out = ConvPlan()
+        _check(_lib.he_conv_plan_dense(ctypes.byref(p), ctypes.byref(out)),
+               "he_conv_plan_dense")
+        return out
+
     def pack_client_p(self, p: ConvPlan, pp: torch.Tensor, stream=None):
-        """Spectra of X^{-t_n} p in he_pack_filters' layout (for conv)."""
+        """Spectra of X^{-t_n} p in he_pack_filters' layout, for
+        conv(dense_plan(p), vs, pspec).  p may be the normal plan."""
+        p = self.dense_plan(p)
         nb = _lib.he_filter_bytes(self._h, ctypes.byref(p))
         pspec = self.empty_u64(nb // 8)
         wsb = _lib.he_pack_filters_workspace_bytes(self._h, ctypes.byref(p))

@@ -33,6 +33,7 @@ class Chain:
         self.b_pk = b_pk
         # server initialisation: filter spectra (Alg. 1 Line 4) and p (Line 5)
         self.fspecs = [ctx.pack_filters(p, W) for p, W in zip(self.plans, Ws)]
+        self.dplans = [ctx.dense_plan(p) for p in self.plans]   # client operand is dense
         self.pspecs = [ctx.pack_client_p(p, ctx.server_init_p(p, W, a, e))
                        for p, W, e in zip(self.plans, Ws, ef)]
         self.s_res = ctx.residues_from_int(s_key.reshape(1, -1))
@@ -67,7 +68,7 @@ class Chain:
             vs = ctx.poly_mul(ctx.residues_from_int(v[li]).reshape(-1, ctx.L, ctx.N),
                               self.s_res).reshape(B, p.n_ib, ctx.L, ctx.N)
             comp1 = ctx.empty_u64(B, p.n_ob, ctx.L, p.n_valid)
-            ctx.conv(p, vs, self.pspecs[li], None, compact=comp1, full=False)
+            ctx.conv(self.dplans[li], vs, self.pspecs[li], None, compact=comp1, full=False)
             m = ctx.decrypt_round(comp0, comp1)
             x = ctx.relu_requant(p, m, phi, shift, qmax)
             if keep or li == len(self.plans) - 1:

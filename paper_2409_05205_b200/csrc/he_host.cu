@@ -5,6 +5,8 @@
 
 #include <vector>
 
+#include <algorithm>
+
 #include "he_internal.cuh"
 
 typedef unsigned __int128 u128;
@@ -120,7 +122,8 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
         const char* t = getenv("HE_NTT");
         c->ntt_mode = (t && t[0] == 'i') ? 1 : 0;     // HE_NTT=int: integer butterflies
         const char* k = getenv("HE_NTT_COLS");
-        c->ntt_cluster = (k && k[0] == '0') ? 1 : 0;  // HE_NTT_COLS=0: cluster kernels
+        // HE_NTT_COLS=0: cluster kernels only; =1: column kernel whenever possible
+        c->ntt_cluster = (k && k[0] == '0') ? 1 : ((k && k[0] == '1') ? 2 : 0);
     }
     c->logN = r->log2N;
     c->N = N;
@@ -253,7 +256,16 @@ extern "C" he_status he_conv_plan_make(const he_ctx* c, const he_conv_desc* d,
     p.w_o = (int32_t)((w_p - d->f_w + 1) / d->stride);
     p.h_o = (int32_t)((h_p - d->f_h + 1) / d->stride);
     p.n_valid = p.c_ob * p.w_o * p.h_o;
+    // columns of each fold group that meet nonzero filter operands
+    p.k_u = std::min<int32_t>((int32_t)s, (p.c_ib + 3) & ~3);
     if ((long)p.n_ib * s > 4096) return HE_ESHAPE;       // MAC headroom
     *out = p;
+    return HE_OK;
+}
+
+extern "C" he_status he_conv_plan_dense(const he_conv_plan* p, he_conv_plan* out) {
+    if (!p || !out) return HE_EINVAL;
+    *out = *p;
+    out->k_u = p->s;
     return HE_OK;
 }

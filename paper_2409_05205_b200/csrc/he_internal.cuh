@@ -45,7 +45,7 @@ struct he_ctx {
     double* d_twd_fwd;      // [L][N]  psi^{brv(k)} as double (FP64 transforms)
     double* d_twd_inv;      // [L][N]  psi^{-brv(k)} as double
     int ntt_mode;           // 0: FP64 butterflies (default), 1: integer (HE_NTT=int)
-    int ntt_cluster;        // HE_NTT_COLS=0: incomplete transforms on the cluster kernels
+    int ntt_cluster;        // HE_NTT_COLS: 0 auto, 1 cluster kernels only, 2 columns forced
     u64* d_enc;             // [L][t] enc_j(m) table (t <= 2^20), else nullptr
 };
 

@@ -61,6 +61,7 @@ static inline int ntt_threads(int NS) { return std::min(512, std::max(16, NS / 1
 struct TileLay {
     int B, n_ib, logs, Kp, Gt;
     int skip;       // trailing stages not run: log2(s) for the fold (0 = full)
+    int Ku;         // MAC-tile: columns u < Ku of each block are stored (k = beta Ku + u)
 };
 static inline int tile_gt(int M) { return M < 16 ? M : 16; }
 
@@ -72,8 +73,9 @@ __device__ __forceinline__ void ntt_store(u64* out, int li, int seg, int NS, int
     if (OUT_FMT == 2) {
         unsigned char* A = reinterpret_cast<unsigned char*>(out);
         const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
-        const int s = 1 << T.logs, M = N >> T.logs, K = T.n_ib << T.logs;
+        const int s = 1 << T.logs, M = N >> T.logs, K = T.n_ib * T.Ku;
         for (int i = 4 * threadIdx.x; i < NS; i += 4 * blockDim.x) {
+            if (((seg * NS + i) & (s - 1)) >= T.Ku) continue;     // column unused by the MAC
             u64 x[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) x[e] = val(i + e);
@@ -87,9 +89,9 @@ __device__ __forceinline__ void ntt_store(u64* out, int li, int seg, int NS, int
             const int gb = g / T.Gt, gi = g - gb * T.Gt;
             unsigned char* row =
                 A + (((((size_t)l * (M / T.Gt) + gb) * 7) * T.B + b) * T.Gt + gi) * T.Kp +
-                beta * s + u;
+                beta * T.Ku + u;
             const size_t pstride = (size_t)T.B * T.Gt * T.Kp;
-            const bool tail = (beta == T.n_ib - 1) && (u + 4 == s) && (T.Kp > K);
+            const bool tail = (beta == T.n_ib - 1) && (u + 4 == T.Ku) && (T.Kp > K);
 #pragma unroll
             for (int j = 0; j < 7; ++j) {
                 *reinterpret_cast<u32*>(row + j * pstride) = pl[j];
@@ -261,11 +263,11 @@ template <int OUT_FMT>
 __global__ void __launch_bounds__(256, 4)
 k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int L,
                const he_limb* __restrict__ limbs, const double* __restrict__ twd_all, TileLay T,
-               int logC, int stride) {
+               int logC, int stride, int nct) {
     extern __shared__ u64 sm_raw[];
     double* sm = reinterpret_cast<double*>(sm_raw);
     const int N = 1 << logN, logs = T.skip, s = 1 << logs, Tn = logN - logs, M = 1 << Tn;
-    const int C = 1 << logC, nct = s >> logC;
+    const int C = 1 << logC;                 // nct column tiles of C columns per limb
     const int li = blockIdx.x / nct, c0 = (blockIdx.x - li * nct) << logC;
     const int l = li % L;
     const double q = limbs[l].qd, qinv = limbs[l].qinvd;
@@ -290,7 +292,7 @@ k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int 
     if (OUT_FMT == 2) {
         unsigned char* A = reinterpret_cast<unsigned char*>(out);
         const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
-        const int K = T.n_ib << logs;
+        const int K = T.n_ib * T.Ku;
         const size_t pstride = (size_t)T.B * T.Gt * T.Kp;
         const int nq = C >> 2;                                  // 4-column quads per row
         for (int e = threadIdx.x; e < (M * nq); e += blockDim.x) {
@@ -303,11 +305,12 @@ k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int 
             byte_transpose4((u32)(x[0] >> 32), (u32)(x[1] >> 32), (u32)(x[2] >> 32),
                             (u32)(x[3] >> 32), pl[4], pl[5], pl[6], pl[7]);
             const int g = k, u = c0 + c;
+            if (u >= T.Ku) continue;                            // column unused by the MAC
             const int gb = g / T.Gt, gi = g - gb * T.Gt;
             unsigned char* row =
                 A + (((((size_t)l * (M / T.Gt) + gb) * 7) * T.B + b) * T.Gt + gi) * T.Kp +
-                beta * s + u;
-            const bool tail = (beta == T.n_ib - 1) && (u + 4 == s) && (T.Kp > K);
+                beta * T.Ku + u;
+            const bool tail = (beta == T.n_ib - 1) && (u + 4 == T.Ku) && (T.Kp > K);
 #pragma unroll
             for (int j = 0; j < 7; ++j) {
                 *reinterpret_cast<u32*>(row + j * pstride) = pl[j];
@@ -339,7 +342,7 @@ static void cols_geometry(int logN, int skip, int& logC, int& stride) {
 // Launch the forward NTT over nlimbs = batch * L limbs.
 static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
                                 long nlimbs, int out_fmt, cudaStream_t st,
-                                TileLay T = TileLay{1, 1, 0, 16, 1, 0}) {
+                                TileLay T = TileLay{1, 1, 0, 16, 1, 0, 0}) {
     if (nlimbs <= 0) return HE_OK;
     const int logN = c->logN;
     const int S = logN <= 13 ? 0 : logN - 13;
@@ -352,20 +355,27 @@ static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
         {k_ntt_fwd_s0<0>, k_ntt_fwd_s0<1>, k_ntt_fwd_s0<2>},
         {k_ntt_fwd_s1<0>, k_ntt_fwd_s1<1>, k_ntt_fwd_s1<2>},
         {k_ntt_fwd_s2<0>, k_ntt_fwd_s2<1>, k_ntt_fwd_s2<2>}};
-    // incomplete transform with s >= 256: independent column transforms, no
-    // cluster (config 5: forward NTT 0.92 -> 0.73 ms); for s <= 128 the
-    // cluster kernels measured as fast or faster (config 4)
-    if (c->ntt_mode == 0 && T.skip >= 8 && !c->ntt_cluster) {
+    // incomplete transform as independent column transforms, no cluster:
+    // for s >= 256 (config 5: forward NTT 0.92 -> 0.73 ms) and whenever the
+    // MAC uses at most half of the columns; otherwise the cluster kernels
+    // measured as fast or faster (config 4).  HE_NTT_COLS=0/1 forces.
+    // With the MAC-tile output only the Ku < s used columns are transformed.
+    const bool cols_ok = c->ntt_mode == 0 && T.skip >= 2 && c->ntt_cluster != 1;
+    const bool cols_pick = c->ntt_cluster == 2 || T.skip >= 8 ||
+                           (out_fmt == 2 && T.skip >= 5 && 2 * T.Ku <= (1 << T.skip));
+    if (cols_ok && cols_pick) {
         int logC, stride;
         cols_geometry(logN, T.skip, logC, stride);
         const size_t smem_c = sizeof(u64) * (size_t)(1 << logC) * stride;
+        const int ncols = out_fmt == 2 ? T.Ku : (1 << T.skip);
+        const int nct = (ncols + (1 << logC) - 1) >> logC;
         typedef void (*kfc)(const u64*, u64*, int, int, const he_limb*, const double*, TileLay,
-                            int, int);
+                            int, int, int);
         static kfc const tabc[3] = {k_ntt_fwd_cols<0>, k_ntt_fwd_cols<1>, k_ntt_fwd_cols<2>};
         kfc kc = tabc[out_fmt];
         if (!set_smem(kc, smem_c)) return HE_ECUDA;
-        kc<<<(unsigned)(nlimbs * ((1 << T.skip) >> logC)), 256, smem_c, st>>>(
-            in, out, logN, c->L, c->d_limb, c->d_twd_fwd, T, logC, stride);
+        kc<<<(unsigned)(nlimbs * nct), 256, smem_c, st>>>(
+            in, out, logN, c->L, c->d_limb, c->d_twd_fwd, T, logC, stride, nct);
         HE_CHECK_LAUNCH();
         return HE_OK;
     }
@@ -499,7 +509,7 @@ extern "C" he_status he_ntt_forward_partial(const he_ctx* c, uint64_t* d, int ba
                                             int skip, void* stream) {
     if (!c || !d || batch < 0 || skip < 0 || skip > c->logN) return HE_EINVAL;
     return launch_ntt_fwd(c, (const u64*)d, (u64*)d, (long)batch * c->L, 0, STREAM(stream),
-                          TileLay{1, 1, 0, 16, 1, skip});
+                          TileLay{1, 1, 0, 16, 1, skip, 0});
 }
 
 extern "C" he_status he_ntt_inverse(const he_ctx* c, uint64_t* d, int batch,
@@ -514,7 +524,15 @@ extern "C" he_status he_ntt_inverse(const he_ctx* c, uint64_t* d, int batch,
 struct PlanDev {
     int c_i, c_o, w_i, h_i, f_w, f_h, stride, padw, padh;
     int s, logs, c_ib, n_ib, c_ob, n_ob, w_p, h_p, w_o, h_o, n_valid, step;
+    int Ku;     // columns u < Ku of each fold group carry the MAC (K = n_ib Ku)
 };
+
+// Only the c_ib columns u < c_ib of each fold group meet nonzero filter
+// operands (F'_{g,u} = 0 for u >= c_ib: the filter's exponents are
+// -m mod s, m < c_ib), so the MAC runs over K = n_ib Ku with Ku = c_ib
+// rounded up to a multiple of 4 (<= s), and the forward transform of c0 is
+// needed on those columns only.
+
 
 static PlanDev plan_dev(const he_conv_plan* p) {
     PlanDev d;
@@ -526,12 +544,15 @@ static PlanDev plan_dev(const he_conv_plan* p) {
     d.c_ib = p->c_ib; d.n_ib = p->n_ib; d.c_ob = p->c_ob; d.n_ob = p->n_ob;
     d.w_p = p->w_p; d.h_p = p->h_p; d.w_o = p->w_o; d.h_o = p->h_o;
     d.n_valid = p->n_valid; d.step = p->s / p->c_ob;
+    d.Ku = p->k_u;
     return d;
 }
 
 static bool plan_ok(const he_ctx* c, const he_conv_plan* p) {
     he_conv_plan chk;
     if (he_conv_plan_make(c, &p->d, p->s, &chk) != HE_OK) return false;
+    if (p->k_u != chk.k_u && p->k_u != p->s) return false;   // default or dense
+    chk.k_u = p->k_u;
     return memcmp(&chk, p, sizeof(chk)) == 0;
 }
 
@@ -668,18 +689,17 @@ __global__ void k_filter_to_mac(const u64* __restrict__ spec, u64* __restrict__ 
                                 const he_limb* __restrict__ limbs,
                                 const ulonglong2* __restrict__ tw_fwd) {
     const long N = 1L << logN;
-    const int K = P.n_ib * P.s;
-    const long total = (long)L * N * P.n_ib * P.c_o;  // = L * M * K * c_o
+    const int K = P.n_ib * P.Ku, M = (int)(N >> P.logs);
+    const long total = (long)L * M * K * P.c_o;
     for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
          idx += (long)gridDim.x * blockDim.x) {
         const int n = (int)(idx % P.c_o);
         long r = idx / P.c_o;
         const int k = (int)(r % K);
         r /= K;
-        const int M = (int)(N >> P.logs);
         const int g = (int)(r % M);
         const int l = (int)(r / M);
-        const int beta = k >> P.logs, u = k & (P.s - 1);
+        const int beta = k / P.Ku, u = k - beta * P.Ku;
         const he_limb& Lm = limbs[l];
         F[idx] = to_split25(fold_filter_operand(spec + (((long)n * P.n_ib + beta) * L + l) * N,
                                                 g, u, P.logs, logN - P.logs, Lm,
@@ -704,7 +724,7 @@ __global__ void k_filter_to_imma(const u64* __restrict__ spec, unsigned char* __
                                  const he_limb* __restrict__ limbs,
                                  const ulonglong2* __restrict__ tw_fwd) {
     const long N = 1L << logN;
-    const int K = P.n_ib * P.s, M = (int)(N >> P.logs);
+    const int K = P.n_ib * P.Ku, M = (int)(N >> P.logs);
     const long total = (long)L * M * P.c_o * Kp;
     for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
          idx += (long)gridDim.x * blockDim.x) {
@@ -716,7 +736,7 @@ __global__ void k_filter_to_imma(const u64* __restrict__ spec, unsigned char* __
         u64 v = 0;
         if (k < K) {
             const he_limb& Lm = limbs[l];
-            const int beta = k >> P.logs, u = k & (P.s - 1);
+            const int beta = k / P.Ku, u = k - beta * P.Ku;
             v = fold_filter_operand(spec + (((long)n * P.n_ib + beta) * L + l) * N, g, u,
                                     P.logs, logN - P.logs, Lm, tw_fwd + (long)l * N);
         }
@@ -728,15 +748,17 @@ __global__ void k_filter_to_imma(const u64* __restrict__ spec, unsigned char* __
 
 extern "C" size_t he_filter_bytes(const he_ctx* c, const he_conv_plan* p) {
     if (!c || !p) return 0;
-    const size_t split = sizeof(u64) * (size_t)p->d.c_o * p->n_ib * c->L * c->N;
     const size_t M = c->N / p->s;
-    const size_t planes = (size_t)c->L * M * 7 * p->d.c_o * imma_kp(p->n_ib * p->s);
+    const size_t K = (size_t)p->n_ib * p->k_u;
+    const size_t split = sizeof(u64) * (size_t)p->d.c_o * c->L * M * K;
+    const size_t planes = (size_t)c->L * M * 7 * p->d.c_o * imma_kp((int)K);
     return std::max(split, (planes + 15) & ~(size_t)15);
 }
 
 extern "C" size_t he_pack_filters_workspace_bytes(const he_ctx* c,
                                                   const he_conv_plan* p) {
-    return he_filter_bytes(c, p);
+    if (!c || !p) return 0;
+    return sizeof(u64) * (size_t)p->d.c_o * p->n_ib * c->L * c->N;   // coefficient polys
 }
 
 static he_status finish_filter_spectra(const he_ctx* c, const PlanDev& P, u64* ws,
@@ -765,17 +787,18 @@ static he_status finish_filter_spectra(const he_ctx* c, const PlanDev& P, u64* w
     const long total = (long)P.c_o * P.n_ib * c->L * c->N;
     // incomplete forward transform: the first log2(N/s) stages only
     he_status s = launch_ntt_fwd(c, ws, ws, (long)P.c_o * P.n_ib * c->L, 0, st,
-                                 TileLay{1, 1, 0, 16, 1, P.logs});
+                                 TileLay{1, 1, 0, 16, 1, P.logs, 0});
     if (s != HE_OK) return s;
     if (use_imma(c, P)) {
-        const int Kp = imma_kp(P.n_ib * P.s);
+        const int Kp = imma_kp(P.n_ib * P.Ku);
         const long tot = (long)c->L * (c->N >> P.logs) * P.c_o * Kp;
         k_filter_to_imma<<<grid_for(tot, 256), 256, 0, st>>>(ws, (unsigned char*)d_fspec, P,
                                                               c->L, c->logN, Kp, c->d_limb,
                                                               c->d_tw_fwd);
     } else {
-        k_filter_to_mac<<<grid_for(total, 256), 256, 0, st>>>(ws, (u64*)d_fspec, P, c->L,
-                                                               c->logN, c->d_limb, c->d_tw_fwd);
+        const long totm = (long)c->L * (c->N >> P.logs) * P.n_ib * P.Ku * P.c_o;
+        k_filter_to_mac<<<grid_for(totm, 256), 256, 0, st>>>(ws, (u64*)d_fspec, P, c->L,
+                                                              c->logN, c->d_limb, c->d_tw_fwd);
     }
     HE_CHECK_LAUNCH();
     return HE_OK;
@@ -833,13 +856,13 @@ template <int TNT>
 __global__ void __launch_bounds__(256, 2)
 k_mac_fold(const u64* __restrict__ C, const u64* __restrict__ F, u64* __restrict__ out,
            int B, int n_ib, int L, int logN, int logs, int c_o, int GI,
-           const he_limb* __restrict__ limbs) {
+           const he_limb* __restrict__ limbs, int Ku) {
     typedef MacTile<TNT> T;
     constexpr int GC = T::GC, KC = T::KC, CW = T::CW, WPG = T::WPG;
     extern __shared__ u64 smem[];
     u64* sCb = smem;                       // [2][GC][32][CW]
     u64* sFb = smem + 2 * T::C_WORDS;      // [2][GC][KC][TNT]
-    const int N = 1 << logN, s = 1 << logs, M = N >> logs, K = n_ib << logs;
+    const int N = 1 << logN, M = N >> logs, K = n_ib * Ku;
     const int nG = (M + GC * GI - 1) / (GC * GI);
     const int l = blockIdx.x / nG, g0 = (blockIdx.x - l * nG) * GC * GI;
     const int b0 = blockIdx.y * 32, n0 = blockIdx.z * TNT;
@@ -858,8 +881,9 @@ k_mac_fold(const u64* __restrict__ C, const u64* __restrict__ F, u64* __restrict
             const int gg = r & (GC - 1), bl = r / GC;
             const int k = k0 + kk, b = b0 + bl, gq = gb + gg;
             const bool ok = k < K && b < B && gq < M;
-            const u64* src = ok ? C + (((size_t)b * n_ib + (k >> logs)) * L + l) * N +
-                                      ((size_t)gq << logs) + (k & (s - 1))
+            const int beta = k / Ku;
+            const u64* src = ok ? C + (((size_t)b * n_ib + beta) * L + l) * N +
+                                      ((size_t)gq << logs) + (k - beta * Ku)
                                 : C;
             cp_async8(sC + (gg * 32 + bl) * CW + kk, src, ok);
         }
@@ -943,7 +967,7 @@ k_mac_fold(const u64* __restrict__ C, const u64* __restrict__ F, u64* __restrict
 template <int TNT>
 static he_status launch_mac_t(const u64* C, const u64* F, u64* out, int B, int n_ib, int L,
                               int logN, int logs, int c_o, const he_limb* limbs,
-                              cudaStream_t st) {
+                              cudaStream_t st, int Ku) {
     typedef MacTile<TNT> T;
     const int M = (1 << logN) >> logs;
     const int btiles = (B + 31) / 32, ntiles = (c_o + TNT - 1) / TNT;
@@ -954,16 +978,16 @@ static he_status launch_mac_t(const u64* C, const u64* F, u64* out, int B, int n
     if (!set_smem(k_mac_fold<TNT>, T::SMEM)) return HE_ECUDA;
     dim3 grid(L * nG, btiles, ntiles);
     k_mac_fold<TNT><<<grid, 256, T::SMEM, st>>>(C, F, out, B, n_ib, L, logN, logs, c_o, GI,
-                                                 limbs);
+                                                 limbs, Ku);
     return HE_OK;
 }
 
 static he_status launch_mac(const u64* C, const u64* F, u64* out, int B, int n_ib, int L,
                             int logN, int logs, int c_o, const he_limb* limbs,
-                            cudaStream_t st) {
-    if (c_o <= 16) return launch_mac_t<16>(C, F, out, B, n_ib, L, logN, logs, c_o, limbs, st);
-    if (c_o <= 32) return launch_mac_t<32>(C, F, out, B, n_ib, L, logN, logs, c_o, limbs, st);
-    return launch_mac_t<64>(C, F, out, B, n_ib, L, logN, logs, c_o, limbs, st);
+                            cudaStream_t st, int Ku) {
+    if (c_o <= 16) return launch_mac_t<16>(C, F, out, B, n_ib, L, logN, logs, c_o, limbs, st, Ku);
+    if (c_o <= 32) return launch_mac_t<32>(C, F, out, B, n_ib, L, logN, logs, c_o, limbs, st, Ku);
+    return launch_mac_t<64>(C, F, out, B, n_ib, L, logN, logs, c_o, limbs, st, Ku);
 }
 
 // ============================================================ K3 (int8)
@@ -1197,8 +1221,8 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
 #endif
 static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fpl, u64* out,
                                  int B, int n_ib, int L, int logN, int logs, int c_o,
-                                 const he_limb* limbs, cudaStream_t st) {
-    const int M = (1 << logN) >> logs, K = n_ib << logs;
+                                 const he_limb* limbs, cudaStream_t st, int Ku) {
+    const int M = (1 << logN) >> logs, K = n_ib * Ku;
     const int Kp = imma_kp(K);
     const int nrow = (c_o + 7) & ~7, nnt = nrow / 8;
     if (nnt > 32) return HE_ESHAPE;                       // c_o <= 256
@@ -1397,7 +1421,8 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
 static size_t spec_words(const he_ctx* c, const he_conv_plan* p, int B) {
     const size_t M = (size_t)c->N / p->s;
     const size_t split = (size_t)B * p->n_ib * c->L * c->N;
-    const size_t tile = ((size_t)c->L * M * 7 * B * imma_kp(p->n_ib * p->s) + 7) / 8;
+    const size_t tile =
+        ((size_t)c->L * M * 7 * B * imma_kp(p->n_ib * p->k_u) + 7) / 8;
     return std::max(split, tile);
 }
 
@@ -1437,16 +1462,16 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     rec(ev, 0, st);
     he_status s = launch_ntt_fwd(c, (const u64*)d_c0, spec, (long)B * P.n_ib * c->L,
                                  imma ? 2 : 1, st,
-                                 TileLay{B, P.n_ib, P.logs, imma_kp(P.n_ib * P.s),
-                                         tile_gt(c->N >> P.logs), P.logs});
+                                 TileLay{B, P.n_ib, P.logs, imma_kp(P.n_ib * P.Ku),
+                                         tile_gt(c->N >> P.logs), P.logs, P.Ku});
     if (s != HE_OK) return s;
     rec(ev, 1, st);
     if (imma)
         s = launch_mac_imma((const unsigned char*)spec, (const unsigned char*)d_fspec, fold, B,
-                            P.n_ib, c->L, c->logN, P.logs, P.c_o, c->d_limb, st);
+                            P.n_ib, c->L, c->logN, P.logs, P.c_o, c->d_limb, st, P.Ku);
     else
         s = launch_mac(spec, (const u64*)d_fspec, fold, B, P.n_ib, c->L, c->logN, P.logs,
-                       P.c_o, c->d_limb, st);
+                       P.c_o, c->d_limb, st, P.Ku);
     if (s != HE_OK) return s;
     HE_CHECK_LAUNCH();
     const int M = c->N >> P.logs;
@@ -1997,7 +2022,7 @@ extern "C" he_status he_pack_client_p(const he_ctx* c, const he_conv_plan* p,
                                       const uint64_t* d_p, uint64_t* d_pspec, void* d_ws,
                                       size_t ws_bytes, void* stream) {
     if (!c || !p || !d_p || !d_pspec || !d_ws) return HE_EINVAL;
-    if (!plan_ok(c, p)) return HE_ESHAPE;
+    if (!plan_ok(c, p) || p->k_u != p->s) return HE_ESHAPE;     // dense plan required
     if (ws_bytes < he_pack_filters_workspace_bytes(c, p)) return HE_ENOMEM;
     cudaStream_t st = STREAM(stream);
     const PlanDev P = plan_dev(p);

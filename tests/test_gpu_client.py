@@ -109,7 +109,7 @@ def test_server_p_and_client_c1r(he, name, N, layer):
     B = 2
     vs = synth.uniform_residues((B, plan.n_ib, ring.L, N), primes, seed, "misc", 77)
     pspec = ctx.pack_client_p(p, p_gpu)
-    c1 = u64(ctx.conv(p, dev(vs), pspec))
+    c1 = u64(ctx.conv(ctx.dense_plan(p), dev(vs), pspec))
     want = R.client_c1r(vs, p_ref, plan, ring)
     assert np.array_equal(c1, want)
 
@@ -187,7 +187,7 @@ def test_protocol_end_to_end_on_gpu(he, cfg_idx):
         B, plan.n_ib, ctx.L, cfg.N)
     pspec = ctx.pack_client_p(p, pp)
     comp1 = ctx.empty_u64(B, p.n_ob, ctx.L, p.n_valid)
-    c1r = ctx.conv(p, vs, pspec, compact=comp1)
+    c1r = ctx.conv(ctx.dense_plan(p), vs, pspec, compact=comp1)
     m_full = ctx.decrypt_round(c0r, c1r).cpu().numpy().view(np.uint32)
     m_comp = ctx.decrypt_round(comp, comp1).cpu().numpy().view(np.uint32)
     # modulus switching of both shares to one limb (R28), decrypted under Q'
