@@ -599,15 +599,30 @@ def main():
                    for t in sw]
         sw_pk_h = [torch.empty(t.shape, dtype=torch.uint8).pin_memory() for t in sw_pk_d]
 
-        def e2e_step(ms_keep=0):
+        # variant: sparse c0 upload (only the k_u columns the conv reads)
+        sp = [lw.p.k_u < lw.p.s for lw in layers]
+        c0c_d = [ctx.c0_compact(lw.p, c0_d[i]) if sp[i] else None for i, lw in enumerate(layers)]
+        c0c_pk_d = [ctx.pack50(t) if t is not None else None for t in c0c_d]
+        c0c_pk_h = [t.cpu().pin_memory() if t is not None else None for t in c0c_pk_d]
+        torch.cuda.synchronize()
+
+        def e2e_step(ms_keep=0, sparse=False):
             mask_seed[0] += 1
             for i, lw in enumerate(layers):
+                spi = sparse and sp[i]
                 with torch.cuda.stream(h2d_s):
                     h2d_s.wait_event(comp_done[i])          # WAR vs previous step
-                    c0_pk_d[i].copy_(c0_pk_h[i], non_blocking=True)
+                    if spi:
+                        c0c_pk_d[i].copy_(c0c_pk_h[i], non_blocking=True)
+                    else:
+                        c0_pk_d[i].copy_(c0_pk_h[i], non_blocking=True)
                     up_done[i].record(h2d_s)
                 stream.wait_event(up_done[i])
-                ctx.unpack50(c0_pk_d[i], c0_d[i])
+                if spi:
+                    ctx.unpack50(c0c_pk_d[i], c0c_d[i])
+                    ctx.c0_expand(lw.p, c0c_d[i], out=c0_d[i])
+                else:
+                    ctx.unpack50(c0_pk_d[i], c0_d[i])
                 ctx.phi1_generate((mask_seed[0] << 8) + i, phi_d[i])
                 ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], outs[i], ws, compact=comps[i])
                 if ms_keep:
@@ -708,6 +723,26 @@ def main():
         torch.cuda.synchronize()
         sw_ms = m0.elapsed_time(m1)
         sw_bytes = sum(8 * c.numel() + 8 * t.numel() for c, t in zip(comps, sw))
+        # both extensions: sparse c0 upload + payload switched to one limb
+        for _ in range(2):
+            e2e_step(1, True)
+        barrier()
+        x0.record()
+        for _ in range(args.steps):
+            e2e_step(1, True)
+        x1.record()
+        barrier()
+        ms_ext = max_over_ranks(x0.elapsed_time(x1) / args.steps)
+        e2e["sparse_upload_modswitch"] = {
+            "ms_per_step": ms_ext, "value": evals_step * world / (ms_ext * 1e-3),
+            "h2d_bytes_per_step": sum(c0c_pk_h[i].numel() if sp[i] else c0_pk_h[i].numel()
+                                      for i in range(len(layers))) +
+            (fc["c0_pk_h"].numel() if fc else 0),
+            "d2h_bytes_per_step": sum(t.numel() for t in sw_pk_h) +
+            (fc["out_pk_h"].numel() if fc else 0),
+            "what": "protocol extensions: the client sends only the k_u columns of c0 "
+                    "the conv reads (he_c0_compact / he_c0_expand), the payload is "
+                    "modulus-switched to one limb"}
         e2e["modswitch"] = {
             "L_keep": 1, "ms_per_step": ms_sw,
             "value": evals_step * world / (ms_sw * 1e-3),

@@ -393,6 +393,18 @@ he_status he_pack_fc_client_p(const he_ctx* ctx, const he_fc_desc* f,
 he_status he_unmask(const he_ctx* ctx, const uint32_t* d_m, const uint32_t* d_phi1,
                     long n, int32_t* d_out, void* stream);
 
+/* Sparse c0 upload (protocol extension): he_conv reads c0
+ * only on the columns u < k_u of each fold group -- the coefficients
+ * g s + u that some filter tap reaches -- so the client may send only those.
+ * he_c0_compact gathers d_c0 [B][n_ib][L][N] into d_c0c [B][n_ib][L][M k_u]
+ * (M = N / s, element g k_u + u); he_c0_expand scatters it back with zeros
+ * elsewhere, and he_conv on the expanded c0 returns exactly the output of
+ * the full c0.  plan: the he_conv_plan_make plan (its k_u). */
+he_status he_c0_compact(const he_ctx* ctx, const he_conv_plan* plan,
+                        const uint64_t* d_c0, int B, uint64_t* d_c0c, void* stream);
+he_status he_c0_expand(const he_ctx* ctx, const he_conv_plan* plan,
+                       const uint64_t* d_c0c, int B, uint64_t* d_c0, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

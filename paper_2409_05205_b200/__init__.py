@@ -117,6 +117,8 @@ _sig("he_pk_mask", [_P, _P, _P, ctypes.c_long, _P, _P, _P, _SZ, _P])
 _sig("he_relu_requant", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _I, _I, _P, _P])
 _sig("he_avgpool", [_P, ctypes.c_long, _I, _P, _P])
 _sig("he_unmask", [_P, _P, _P, ctypes.c_long, _P, _P])
+_sig("he_c0_compact", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P])
+_sig("he_c0_expand", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P])
 _sig("he_fc_server_p_workspace_bytes", [_P, ctypes.POINTER(FcDesc)], _SZ)
 _sig("he_fc_server_init_p", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _P, _P, _SZ, _P])
 _sig("he_pack_fc_client_p", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _SZ, _P])
@@ -131,7 +133,7 @@ EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_ntt_inverse", "he_ntt_forward_partial", "he_server_p_workspace_bytes", "he_server_init_p",
             "he_pack_client_p", "he_residues_from_int", "he_poly_mul",
             "he_decrypt_round", "he_mod_switch", "he_pk_mask", "he_relu_requant",
-            "he_avgpool", "he_unmask", "he_fc_server_p_workspace_bytes", "he_fc_server_init_p",
+            "he_avgpool", "he_unmask", "he_c0_compact", "he_c0_expand", "he_fc_server_p_workspace_bytes", "he_fc_server_init_p",
             "he_pack_fc_client_p"]
 
 
@@ -556,4 +558,26 @@ class Context:
         self._dev(m, phi1, out)
         _check(_lib.he_unmask(self._h, self._ptr(m), self._ptr(phi1), m.numel(),
                               self._ptr(out), _stream(stream)), "he_unmask")
+        return out
+
+    # --------------------------------- sparse c0 upload (protocol extension)
+    def c0_compact(self, p: ConvPlan, c0: torch.Tensor,
+                   out: Optional[torch.Tensor] = None, stream=None):
+        """[B][n_ib][L][N] -> [B][n_ib][L][M k_u]: the columns the conv reads."""
+        B = c0.shape[0]
+        if out is None:
+            out = self.empty_u64(B, p.n_ib, self.L, (self.N // p.s) * p.k_u)
+        self._dev(c0, out)
+        _check(_lib.he_c0_compact(self._h, ctypes.byref(p), self._ptr(c0), B,
+                                  self._ptr(out), _stream(stream)), "he_c0_compact")
+        return out
+
+    def c0_expand(self, p: ConvPlan, c0c: torch.Tensor,
+                  out: Optional[torch.Tensor] = None, stream=None):
+        B = c0c.shape[0]
+        if out is None:
+            out = self.empty_u64(B, p.n_ib, self.L, self.N)
+        self._dev(c0c, out)
+        _check(_lib.he_c0_expand(self._h, ctypes.byref(p), self._ptr(c0c), B,
+                                 self._ptr(out), _stream(stream)), "he_c0_expand")
         return out

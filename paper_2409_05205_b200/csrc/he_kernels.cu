@@ -2411,3 +2411,54 @@ extern "C" he_status he_unmask(const he_ctx* c, const uint32_t* d_m, const uint3
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
+
+// ====================================== sparse c0 upload (protocol extension)
+// The conv reads c0 only on the columns u < k_u of each fold group (DESIGN.md
+// §4), so the client can send just those: [B][n_ib][L][M][k_u].
+__global__ void k_c0_cols(const u64* __restrict__ in, u64* __restrict__ out, long npoly, int logN,
+                          int logs, int Ku, int dir) {
+    const long N = 1L << logN;
+    const int s = 1 << logs, M = (int)(N >> logs);
+    const long per = (long)M * Ku;
+    const long total = npoly * (dir ? N : per);
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        if (dir == 0) {                                         // compact: gather
+            const long pl = idx / per, r = idx - pl * per;
+            const long g = r / Ku, u = r - g * Ku;
+            out[idx] = in[pl * N + g * s + u];
+        } else {                                                // expand: scatter + zeros
+            const long pl = idx >> logN, i = idx & (N - 1);
+            const int u = (int)(i & (s - 1));
+            out[idx] = u < Ku ? in[pl * per + (i >> logs) * Ku + u] : 0;
+        }
+    }
+}
+
+extern "C" he_status he_c0_compact(const he_ctx* c, const he_conv_plan* p, const uint64_t* d_c0,
+                                   int B, uint64_t* d_c0c, void* stream) {
+    if (!c || !p || B < 0) return HE_EINVAL;
+    if (!plan_ok(c, p)) return HE_ESHAPE;
+    if (B == 0) return HE_OK;
+    if (!d_c0 || !d_c0c) return HE_EINVAL;
+    const PlanDev P = plan_dev(p);
+    const long npoly = (long)B * P.n_ib * c->L;
+    k_c0_cols<<<grid_for(npoly * (c->N >> P.logs) * P.Ku, 256), 256, 0, STREAM(stream)>>>(
+        (const u64*)d_c0, (u64*)d_c0c, npoly, c->logN, P.logs, P.Ku, 0);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+extern "C" he_status he_c0_expand(const he_ctx* c, const he_conv_plan* p, const uint64_t* d_c0c,
+                                  int B, uint64_t* d_c0, void* stream) {
+    if (!c || !p || B < 0) return HE_EINVAL;
+    if (!plan_ok(c, p)) return HE_ESHAPE;
+    if (B == 0) return HE_OK;
+    if (!d_c0 || !d_c0c) return HE_EINVAL;
+    const PlanDev P = plan_dev(p);
+    const long npoly = (long)B * P.n_ib * c->L;
+    k_c0_cols<<<grid_for(npoly * c->N, 256), 256, 0, STREAM(stream)>>>(
+        (const u64*)d_c0c, (u64*)d_c0, npoly, c->logN, P.logs, P.Ku, 1);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}

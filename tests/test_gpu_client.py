@@ -217,3 +217,27 @@ def test_mod_switch_matches_oracle(he, cfg_idx):
     for Lk in sorted({1, 2, ring.L - 1, ring.L}):
         got = u64(ctx.mod_switch(dev(x), Lk))
         assert np.array_equal(got, R.mod_switch(x, ring, Lk)), Lk
+
+
+@pytest.mark.parametrize("cfg_idx,li", [(5, 0), (4, 0), (4, 14), (1, 0)])
+def test_sparse_c0_upload(he, cfg_idx, li):
+    """Protocol extension: the client sends only the k_u columns of c0
+    (he_c0_compact); the server expands them (he_c0_expand, zeros elsewhere)
+    and he_conv returns exactly the oracle's output for the full c0."""
+    cfg = synth.CONFIGS[cfg_idx]
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    ctx = ctx_for(he, cfg.N, cfg.primes, cfg.t)
+    Ly = cfg.conv[li]
+    plan = R.plan_conv(Ly, cfg.N)
+    p = ctx.plan(Ly.c_i, Ly.c_o, Ly.w_i, Ly.h_i, Ly.f_w, Ly.f_h, Ly.stride, Ly.pad)
+    B = 4
+    W = synth.weights(cfg, li)
+    c0 = synth.uniform_residues((B, p.n_ib, ring.L, cfg.N), cfg.primes, 12, "misc", li)
+    phi = synth.phi1((B, p.n_ob, cfg.N), cfg.t, 12)
+    fspec = ctx.pack_filters(p, dev(W))
+    c0c = ctx.c0_compact(p, dev(c0))
+    assert c0c.shape[-1] == (cfg.N // p.s) * p.k_u
+    c0x = ctx.c0_expand(p, c0c)
+    out = u64(ctx.conv(p, c0x, fspec, dev(phi.astype(np.uint32))))
+    for b in (0, B - 1):
+        assert np.array_equal(out[b], R.conv_server(c0[b:b + 1], W, plan, ring, phi[b:b + 1])[0])

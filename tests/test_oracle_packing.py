@@ -201,3 +201,22 @@ def test_fc_server_integer_mode():
     for b in range(3):
         for j, q in enumerate(ring.primes):
             assert np.array_equal(out[b, j].astype(np.int64), (W @ I[b]) % q)
+
+
+def test_conv_reads_only_input_channel_columns():
+    """DESIGN.md §4 (k_u): the filter's exponents are -m mod s (m < c_ib), so
+    the server output at the valid slots depends on c0 only through the
+    coefficients g s + u with u < c_ib.  Zeroing every other coefficient of
+    c0 leaves the oracle's full output unchanged (on all s j + t_n slots)."""
+    for Ly, N in [(synth.ConvLayer(3, 8, 8, 8), 1024), (synth.ConvLayer(5, 6, 4, 4), 1024),
+                  (synth.ConvLayer(3, 4, 6, 6, pad=0), 1024)]:
+        ring = R.Ring(N, synth.PRIMES_CFG1, 65537)
+        plan = R.plan_conv(Ly, N)
+        assert plan.c_ib < plan.s
+        rng = np.random.default_rng(N + Ly.c_i)
+        W = rng.integers(-8, 8, (Ly.c_o, Ly.c_i, Ly.f_w, Ly.f_h))
+        c0 = synth.uniform_residues((2, plan.n_ib, ring.L, N), ring.primes, 4, "misc", Ly.c_i)
+        full = R.conv_server(c0, W, plan, ring, None)
+        mask = (np.arange(N) % plan.s) < plan.c_ib
+        sparse = R.conv_server(np.where(mask, c0, 0).astype(np.uint64), W, plan, ring, None)
+        assert np.array_equal(full, sparse)
