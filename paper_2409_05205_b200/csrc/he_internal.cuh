@@ -342,11 +342,12 @@ __device__ __forceinline__ void ct_all_cols_dp(double* sm, int arr_stride, int n
 // pass; X' = X + Y, Y' = (X - Y) w mod q.  Stage 0: |X - Y| <= q + 2;
 // stage 1: <= 2q + 4 < 2^51 (q <= 2^50 - 4): both multiply directly; stage
 // 2 reduces X - Y first.  Outputs < 4q + 8.
-template <int K>
+template <int K, bool RAW = false>
 __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr, int logM,
                                            int lt0, int seg, int logMfull,
                                            const double* __restrict__ tw, double q,
                                            double qinv) {
+    // RAW: the arrays still hold u64 residues (< 2^52) as loaded by cp.async
     const int tk = 1 << lt0;
     const int gper = 1 << (logM - K);
     const int total = narr * gper;
@@ -366,7 +367,12 @@ __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr,
         }
         double x[1 << K];
 #pragma unroll
-        for (int c = 0; c < (1 << K); ++c) x[c] = dp_reduce(s[PAD(base + (c << lt0))], q, qinv);
+        for (int c = 0; c < (1 << K); ++c) {
+            const double v = RAW ? u2d(reinterpret_cast<const u64*>(s)[PAD(base + (c << lt0))])
+                                 : s[PAD(base + (c << lt0))];
+            // canonical raw input: centre into (-q/2, q/2] instead of reducing
+            x[c] = RAW ? (v > 0.5 * q ? v - q : v) : dp_reduce(v, q, qinv);
+        }
 #pragma unroll
         for (int v = 0, o = 0; v < K; o += (1 << (K - 1 - v)), ++v) {
             const int half = 1 << v;
@@ -385,17 +391,34 @@ __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr,
     }
 }
 
-template <int RMAX>
+template <int RMAX, bool RAW = false>
 __device__ __forceinline__ void gs_all_dp(double* sm, int arr_stride, int narr, int logM,
                                           int seg, int logMfull, const double* tw, double q,
                                           double qinv) {
     int lt = 0;
     const int rem = logM % RMAX;
+    if (RAW) {                                  // first pass converts the raw residues
+        if (logM >= RMAX) {
+            gs_pass_dp<RMAX, true>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, qinv);
+            lt += RMAX;
+        } else if (rem == 1) {
+            gs_pass_dp<1, true>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, qinv);
+            lt += 1;
+        } else if (rem == 2) {
+            gs_pass_dp<2, true>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, qinv);
+            lt += 2;
+        } else if (rem == 3) {
+            gs_pass_dp<3, true>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, qinv);
+            lt += 3;
+        }
+        __syncthreads();
+        if (lt >= logM) return;
+    }
     for (; lt + RMAX <= logM; lt += RMAX) {
         gs_pass_dp<RMAX>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, qinv);
         __syncthreads();
     }
-    if (rem) {
+    if (lt < logM) {
         if (rem == 1) gs_pass_dp<1>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, qinv);
         else if (rem == 2) gs_pass_dp<2>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, qinv);
         else gs_pass_dp<3>(sm, arr_stride, narr, logM, lt, seg, logMfull, tw, q, qinv);

@@ -1300,7 +1300,17 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     // fold layout [l][b][n][g]: the chunk's channel rows are contiguous in g
     const u64* fb = fold + (((size_t)l * B + b) * P.c_o + ob * P.c_ob + ch0) * M;
     const int tot = ncc * M, nvalid_a = min(ncc, P.c_o - (ob * P.c_ob + ch0));
-    for (int base = 0; base < tot; base += 8 * blockDim.x) {       // 8 loads in flight
+    const bool raw = DP && logM >= 1;       // cp.async the residues, first pass converts
+    if (raw) {
+        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+            const bool ok = (idx >> logM) < nvalid_a;
+            cp_async_n<8>(sm + (idx >> logM) * stride + PAD(idx & (M - 1)), ok ? fb + idx : fb,
+                          ok);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+    }
+    for (int base = 0; !raw && base < tot; base += 8 * blockDim.x) {   // 8 loads in flight
         u64 v[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -1318,7 +1328,10 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         }
     }
     __syncthreads();
-    if (DP)
+    if (DP && raw)
+        gs_all_dp<4, true>(reinterpret_cast<double*>(sm), stride, ncc, logM, 0, logM,
+                           twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
+    else if (DP)
         gs_all_dp<4>(reinterpret_cast<double*>(sm), stride, ncc, logM, 0, logM,
                      twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
     else if (logM <= 12)
