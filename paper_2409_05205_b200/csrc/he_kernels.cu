@@ -424,7 +424,7 @@ k_ntt_inv(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ 
         }
     }
     __syncthreads();
-    if (DP) gs_all_dp<3>(smd, 0, 1, logN, 0, logN, twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
+    if (DP) gs_all_dp<4>(smd, 0, 1, logN, 0, logN, twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
     else gs_all<4>(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
     u64* dst = out + (size_t)li * N;
     const u64 ni = Lm.ninv, nip = Lm.ninv_p;
@@ -1740,7 +1740,7 @@ k_fc_inv(const u64* __restrict__ spec, const ulonglong2* __restrict__ wspec,
         else sm[PAD(i)] = acc;
     }
     __syncthreads();
-    if (DP) gs_all_dp<3>(smd, 0, 1, logN, 0, logN, twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
+    if (DP) gs_all_dp<4>(smd, 0, 1, logN, 0, logN, twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
     else gs_all<4>(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
     const int k0 = tt * P.n_ot, nk = min(P.n_ot, P.n_o - k0);
     for (int k = threadIdx.x; k < nk; k += blockDim.x) {
