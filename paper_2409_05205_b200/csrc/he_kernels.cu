@@ -127,14 +127,26 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
     const double* tw = twd_all + (size_t)l * N;
     const u64* src = in + (size_t)li * N;
     const int end = logN - T.skip;
+    // software-pipelined loads: the next iteration's 2^S vectors are in
+    // flight while this one's register stages run
+    ulonglong2 nxt[1 << S];
+    {
+        const int i0 = 2 * threadIdx.x;
+#pragma unroll
+        for (int r = 0; r < (1 << S); ++r)
+            if (i0 < NS) nxt[r] = *reinterpret_cast<const ulonglong2*>(src + i0 + r * NS);
+    }
     for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
         double vx[1 << S], vy[1 << S];
 #pragma unroll
         for (int r = 0; r < (1 << S); ++r) {
-            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src + i + r * NS);
-            vx[r] = u2d(v.x);
-            vy[r] = u2d(v.y);
+            vx[r] = u2d(nxt[r].x);
+            vy[r] = u2d(nxt[r].y);
         }
+        const int in_ = i + 2 * blockDim.x;
+#pragma unroll
+        for (int r = 0; r < (1 << S); ++r)
+            if (in_ < NS) nxt[r] = *reinterpret_cast<const ulonglong2*>(src + in_ + r * NS);
 #pragma unroll
         for (int st = 0; st < S; ++st) {
             if (st >= end) break;
