@@ -74,6 +74,7 @@ __device__ __forceinline__ void ntt_store(u64* out, int li, int seg, int NS, int
         unsigned char* A = reinterpret_cast<unsigned char*>(out);
         const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
         const int s = 1 << T.logs, M = N >> T.logs, K = T.n_ib * T.Ku;
+        const int lgt = __ffs(T.Gt) - 1;
         for (int i = 4 * threadIdx.x; i < NS; i += 4 * blockDim.x) {
             if (((seg * NS + i) & (s - 1)) >= T.Ku) continue;     // column unused by the MAC
             u64 x[4];
@@ -86,7 +87,7 @@ __device__ __forceinline__ void ntt_store(u64* out, int li, int seg, int NS, int
                             (u32)(x[3] >> 32), pl[4], pl[5], pl[6], pl[7]);
             const int pos = seg * NS + i;
             const int g = pos >> T.logs, u = pos & (s - 1);
-            const int gb = g / T.Gt, gi = g - gb * T.Gt;
+            const int gb = g >> lgt, gi = g & (T.Gt - 1);     // Gt is a power of two
             unsigned char* row =
                 A + (((((size_t)l * (M / T.Gt) + gb) * 7) * T.B + b) * T.Gt + gi) * T.Kp +
                 beta * T.Ku + u;
@@ -306,6 +307,7 @@ k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int 
         const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
         const int K = T.n_ib * T.Ku;
         const size_t pstride = (size_t)T.B * T.Gt * T.Kp;
+        const int lgt = __ffs(T.Gt) - 1;
         const int nq = C >> 2;                                  // 4-column quads per row
         for (int e = threadIdx.x; e < (M * nq); e += blockDim.x) {
             const int k = e / nq, c = (e - k * nq) * 4;
@@ -318,7 +320,7 @@ k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int 
                             (u32)(x[3] >> 32), pl[4], pl[5], pl[6], pl[7]);
             const int g = k, u = c0 + c;
             if (u >= T.Ku) continue;                            // column unused by the MAC
-            const int gb = g / T.Gt, gi = g - gb * T.Gt;
+            const int gb = g >> lgt, gi = g & (T.Gt - 1);     // Gt is a power of two
             unsigned char* row =
                 A + (((((size_t)l * (M / T.Gt) + gb) * 7) * T.B + b) * T.Gt + gi) * T.Kp +
                 beta * T.Ku + u;
