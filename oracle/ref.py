@@ -885,7 +885,7 @@ def fc_server_tiled(c0: np.ndarray, W: np.ndarray, bias: Optional[np.ndarray],
             acc = (acc + part.astype(object)) % qo
         acc = acc[:, :, :k1 - k0]
         if bias is not None:
-            acc = (acc + encode(np.mod(np.asarray(bias)[k0:k1], ring.t).astype(np.uint32),
+            acc = (acc + encode(np.mod(np.asarray(bias, np.int64)[k0:k1], ring.t).astype(np.uint32),
                                 ring).astype(object)[None]) % qo
         if phi1 is not None:
             for b in range(B):

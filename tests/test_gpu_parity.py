@@ -443,3 +443,23 @@ def test_conv_cluster_ntt_path_for_large_s(he, monkeypatch):
     ctx = he.Context(cfg.primes, cfg.log2N, cfg.t)
     ring = R.Ring(cfg.N, cfg.primes, cfg.t)
     run_conv(he, ctx, ring, cfg.conv[0], 16, seed=cfg.seed + 3, check_b=[0, 15])
+
+
+@pytest.mark.parametrize("t", [3, 257, (1 << 21) + 7, 4294967291])
+def test_conv_and_fc_other_plaintext_moduli(he, t):
+    """The mask encoding enc_j(phi1) for t other than 65537: tables for
+    t <= 2^20, the arithmetic enc_plain path above (t up to 2^32 - 5)."""
+    N = 1024
+    primes = RINGS[N]
+    ring = R.Ring(N, primes, t)
+    ctx = ctx_for(he, N, primes, t)
+    run_conv(he, ctx, ring, synth.ConvLayer(5, 7, 6, 5), 3, seed=t % 1000, mask=True)
+    rng = np.random.default_rng(t % 997)
+    n_i, n_o, B = 10, 30, 2
+    W = rng.integers(-8, 8, (n_o, n_i)).astype(np.int32)
+    bias = rng.integers(-8, 8, n_o).astype(np.int32)
+    c0 = synth.uniform_residues((B, 1, ring.L, N), primes, 7, "misc", 3)
+    phi = (rng.integers(0, t, (B, n_o), dtype=np.int64)).astype(np.uint32)
+    wspec, benc = ctx.fc_pack_weights(dev(W), dev(bias))
+    out = u64(ctx.fc(n_i, n_o, dev(c0), wspec, benc, dev(phi)))
+    assert np.array_equal(out, R.fc_server_tiled(c0, W, bias, ring, phi))
