@@ -88,13 +88,15 @@ class LayerWork:
     def __init__(self, idx, Ly, plan, N, L, B):
         self.idx, self.Ly, self.p = idx, Ly, plan
         M = N // plan.s
+        ku = plan.k_u                      # fold-group columns the MAC uses
         nlimb = B * plan.n_ib * L
         self.evals = B * Ly.c_o * plan.n_ib
-        # the fold runs the incomplete transform: log2(N/s) stages
-        self.ntt_bfly = nlimb * (N // 2) * (M.bit_length() - 1)
-        self.ntt_bytes = nlimb * N * 16
-        self.macs = L * N * plan.n_ib * B * Ly.c_o
-        self.mac_bytes = 8 * (nlimb * N + Ly.c_o * plan.n_ib * L * N +
+        # the fold runs the incomplete transform, log2(N/s) stages, and needs
+        # only the k_u columns of each group
+        self.ntt_bfly = nlimb * ku * (M // 2) * (M.bit_length() - 1)
+        self.ntt_bytes = nlimb * M * ku * 16
+        self.macs = L * M * plan.n_ib * ku * B * Ly.c_o
+        self.mac_bytes = 8 * (nlimb * M * ku + Ly.c_o * plan.n_ib * ku * L * M +
                               L * M * B * Ly.c_o)
         logM = M.bit_length() - 1
         self.intt_bfly = B * plan.n_ob * plan.c_ob * L * (M // 2) * logM
