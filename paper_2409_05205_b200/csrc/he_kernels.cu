@@ -1233,6 +1233,9 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
 #ifndef HE_MAC_K16_MINB
 #define HE_MAC_K16_MINB 5
 #endif
+#ifndef HE_MAC_UG
+#define HE_MAC_UG 4
+#endif
 static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fpl, u64* out,
                                  int B, int n_ib, int L, int logN, int logs, int c_o,
                                  const he_limb* limbs, cudaStream_t st, int Ku) {
@@ -1257,6 +1260,17 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
         GS = 1;
         while (GS < Gt && unit_bytes(rows, GS * 2, Kp) <= budget) GS *= 2;
         G = GS;
+        // CTAs of > 4 warps (not the 5-per-SM small-K variant): walk several
+        // units through the double buffer so loads overlap the MMAs and the
+        // per-CTA setup is amortised, keeping >= ~3 CTAs of work per SM
+        if (!k16c && Kp >= 32) {
+            const long ctas1 = (long)L * ((M + GS - 1) / GS) * ((B + rows - 1) / rows);
+            int ug = 1;
+            while (ug < HE_MAC_UG && G * 2 <= Gt * 4 && ctas1 / (ug * 2) >= 3 * 148 &&
+                   2 * unit_bytes(rows, GS, Kp) <= 227 * 1024)
+                ug *= 2;
+            G = GS * ug;
+        }
     } else {
         KC = (Kp % 64 == 0) ? 64 : ((Kp % 32 == 0) ? 32 : 16);
         GS = 1;
