@@ -463,3 +463,14 @@ def test_conv_and_fc_other_plaintext_moduli(he, t):
     wspec, benc = ctx.fc_pack_weights(dev(W), dev(bias))
     out = u64(ctx.fc(n_i, n_o, dev(c0), wspec, benc, dev(phi)))
     assert np.array_equal(out, R.fc_server_tiled(c0, W, bias, ring, phi))
+
+
+def test_conv_column_ntt_forced(he, monkeypatch):
+    """HE_NTT_COLS=1 runs the column-tiled incomplete transform for every
+    s >= 4 (config 4 layers 0, 1, 8, 14 and config 3); bit-exact."""
+    monkeypatch.setenv("HE_NTT_COLS", "1")
+    for cfg_idx, li, B in [(4, 0, 32), (4, 1, 32), (4, 8, 32), (4, 14, 32), (3, 0, 16)]:
+        cfg = synth.CONFIGS[cfg_idx]
+        ctx = he.Context(cfg.primes, cfg.log2N, cfg.t)
+        ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+        run_conv(he, ctx, ring, cfg.conv[li], B, seed=cfg.seed + 11 * li, check_b=[0, B - 1])
