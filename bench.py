@@ -109,12 +109,22 @@ class LayerWork:
 
 def u1_peaks(device_index=0):
     """Run the U1 register-resident microbenchmarks (libhe_u1.so) on this
-    GPU: returns rates per second and the in-kernel SM clock."""
+    GPU: rates per second (whole GPU, CUDA-event timed) and the implied rate
+    per clock per SM at the GPU's maximum SM clock."""
     import ctypes
     lib = ctypes.CDLL(os.path.join(ROOT, "paper_2409_05205_b200",
                                    "libhe_u1.so"))
     lib.u1_run.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p] * 3
     out = {}
+    import torch
+    nsm = torch.cuda.get_device_properties(device_index).multi_processor_count
+    try:
+        max_mhz = float(subprocess.run(
+            ["nvidia-smi", "--query-gpu=clocks.max.sm", "--format=csv,noheader,nounits",
+             "-i", str(device_index)], capture_output=True, text=True,
+            timeout=20).stdout.strip().splitlines()[0])
+    except Exception:
+        max_mhz = 1965.0
     names = ["imad", "imad_wide", "modmac", "ct_bfly", "gs_bfly", "imma_u8",
              "dfma", "dp_ct_bfly", "dp_gs_bfly"]
     iters = {0: 20000, 1: 20000, 2: 20000, 3: 2000, 4: 2000, 5: 2000, 6: 20000,
@@ -126,9 +136,8 @@ def u1_peaks(device_index=0):
         if rc:
             raise RuntimeError(f"u1 {name} rc={rc}")
         rate = ops.value / (ms.value * 1e-3)
-        mhz = cyc.value / (ms.value * 1e3)
-        out[name] = {"per_s": rate, "sm_mhz_in_kernel": round(mhz, 1),
-                     "per_clk_per_sm": rate / (mhz * 1e6) / 148}
+        out[name] = {"per_s": rate,
+                     "per_clk_per_sm_at_max_clock": rate / (max_mhz * 1e6) / nsm}
     return out
 
 
