@@ -114,7 +114,7 @@ __device__ __forceinline__ void ntt_store(u64* out, int li, int seg, int NS, int
 // FP64 variant of ntt_fwd_segment (default; HE_NTT=int selects the integer
 // one): residues as integer-valued doubles, exact FP64 butterflies
 // (he_internal.cuh), twiddles psi^{brv(k)} as doubles.
-template <int S, int OUT_FMT>
+template <int S, int OUT_FMT, int RM = 3>
 __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int logN, int L,
                                                    const he_limb* __restrict__ limbs,
                                                    const double* __restrict__ twd_all,
@@ -173,7 +173,7 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
     }
     if (S) cg::this_cluster().sync();
     else __syncthreads();
-    ct_all_dp<3>(sm, logN, NS, seg, S, tw, q, qinv, end);     // outputs < 3.2 q
+    ct_all_dp<RM>(sm, logN, NS, seg, S, tw, q, qinv, end);    // outputs < 4 q
     ntt_store<OUT_FMT>(out, li, seg, NS, N, L, l, T,
                        [&](int i) { return d2canon(sm[PAD(i)], q, qinv); });
 }
@@ -264,6 +264,23 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 2)
 k_ntt_fwd_dp_s2(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
                 const double* __restrict__ tw_all, TileLay T) {
     ntt_fwd_segment_dp<2, OUT_FMT>(in, out, logN, L, limbs, tw_all, T);
+}
+// Full transforms (canonical output: filter preparation, FC, client, the
+// NTT limbs/s figure): radix-16 passes, 256 threads, 3 CTAs per SM.
+__global__ void __launch_bounds__(256, 3)
+k_ntt_fwd_dp16_s0(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
+                  const double* __restrict__ tw_all, TileLay T) {
+    ntt_fwd_segment_dp<0, 0, 4>(in, out, logN, L, limbs, tw_all, T);
+}
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 3)
+k_ntt_fwd_dp16_s1(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
+                  const double* __restrict__ tw_all, TileLay T) {
+    ntt_fwd_segment_dp<1, 0, 4>(in, out, logN, L, limbs, tw_all, T);
+}
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 3)
+k_ntt_fwd_dp16_s2(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
+                  const double* __restrict__ tw_all, TileLay T) {
+    ntt_fwd_segment_dp<2, 0, 4>(in, out, logN, L, limbs, tw_all, T);
 }
 
 // Column-tiled incomplete forward transform (FP64): CTA =
@@ -390,6 +407,16 @@ static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
         if (!set_smem(kc, smem_c)) return HE_ECUDA;
         kc<<<(unsigned)(nlimbs * nct), 256, smem_c, st>>>(
             in, out, logN, c->L, c->d_limb, c->d_twd_fwd, T, logC, stride, nct);
+        HE_CHECK_LAUNCH();
+        return HE_OK;
+    }
+    if (c->ntt_mode == 0 && out_fmt == 0 && T.skip == 0 && !getenv("HE_NTT_R8")) {
+        typedef void (*kfd)(const u64*, u64*, int, int, const he_limb*, const double*, TileLay);
+        static kfd const tab16[3] = {k_ntt_fwd_dp16_s0, k_ntt_fwd_dp16_s1, k_ntt_fwd_dp16_s2};
+        kfd kd = tab16[S];
+        if (!set_smem(kd, smem)) return HE_ECUDA;
+        kd<<<(unsigned)(nlimbs << S), std::min(threads, 256), smem, st>>>(
+            in, out, logN, c->L, c->d_limb, c->d_twd_fwd, T);
         HE_CHECK_LAUNCH();
         return HE_OK;
     }
