@@ -570,6 +570,18 @@ def main():
            "hbm_roof_limbs_per_s": hbm_gbs * 1e9 / (16 * N)}
     ntt["roof_limbs_per_s"] = min(ntt["alu_roof_limbs_per_s"], ntt["hbm_roof_limbs_per_s"])
     ntt["frac"] = ntt["limbs_per_s"] / ntt["roof_limbs_per_s"]
+    # inverse transform (he_ntt_inverse), same batch
+    for _ in range(3):
+        ctx.ntt_inverse(buf)
+    a.record()
+    for _ in range(10):
+        ctx.ntt_inverse(buf)
+    b.record()
+    torch.cuda.synchronize()
+    t_inv = a.elapsed_time(b) / 10 * 1e-3
+    ntt["inverse_limbs_per_s"] = nl / t_inv
+    inv_roof = min(gs_roof / (N // 2 * logN), ntt["hbm_roof_limbs_per_s"])
+    ntt["inverse_frac"] = ntt["inverse_limbs_per_s"] / inv_roof
     del buf
 
     # ---- e2e: the server loop through the public API with host buffers.
