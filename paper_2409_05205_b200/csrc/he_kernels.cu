@@ -444,7 +444,7 @@ static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
 // ============================================================ inverse NTT
 // Full N-point inverse (bit-reversed in, natural out, x N^{-1}).
 template <bool DP>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(1024)
 k_ntt_inv(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
           const ulonglong2* __restrict__ twi_all, const double* __restrict__ twid_all) {
     extern __shared__ u64 sm[];
@@ -465,7 +465,7 @@ k_ntt_inv(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ 
         }
     }
     __syncthreads();
-    if (DP) gs_all_dp<4>(smd, 0, 1, logN, 0, logN, twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
+    if (DP) gs_all_dp<3>(smd, 0, 1, logN, 0, logN, twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
     else gs_all<4>(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
     u64* dst = out + (size_t)li * N;
     const u64 ni = Lm.ninv, nip = Lm.ninv_p;
@@ -527,8 +527,8 @@ static he_status launch_ntt_inv(const he_ctx* c, const u64* in, u64* out,
         const size_t smem = sizeof(u64) * padded_words(N);
         auto k = c->ntt_mode == 0 ? k_ntt_inv<true> : k_ntt_inv<false>;
         if (!set_smem(k, smem)) return HE_ECUDA;
-        k<<<(unsigned)nlimbs, ntt_threads(N), smem, st>>>(in, out, c->logN, c->L, c->d_limb,
-                                                         c->d_tw_inv, c->d_twd_inv);
+        k<<<(unsigned)nlimbs, std::min(1024, std::max(32, N / 16)), smem, st>>>(
+            in, out, c->logN, c->L, c->d_limb, c->d_tw_inv, c->d_twd_inv);
     } else {
         const size_t smem = sizeof(u64) * padded_words(N / 2);
         if (!set_smem(k_ntt_inv_split, smem)) return HE_ECUDA;
