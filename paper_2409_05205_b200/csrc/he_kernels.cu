@@ -1768,7 +1768,7 @@ extern "C" he_status he_pack_fc_weights(const he_ctx* c, const he_fc_desc* f,
 // the weight spectra, N-point inverse NTT (N^{-1} pre-folded), the tile's
 // first coefficients + enc(bias) + enc(phi1) at outputs t n_ot + k.
 template <bool DP>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(1024)
 k_fc_inv(const u64* __restrict__ spec, const ulonglong2* __restrict__ wspec,
          const u64* __restrict__ bias_enc, const u32* __restrict__ phi1, u64* __restrict__ out,
          FcP P, int L, int logN, const he_limb* __restrict__ limbs,
@@ -1795,7 +1795,7 @@ k_fc_inv(const u64* __restrict__ spec, const ulonglong2* __restrict__ wspec,
         else sm[PAD(i)] = acc;
     }
     __syncthreads();
-    if (DP) gs_all_dp<4>(smd, 0, 1, logN, 0, logN, twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
+    if (DP) gs_all_dp<3>(smd, 0, 1, logN, 0, logN, twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
     else gs_all<4>(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
     const int k0 = tt * P.n_ot, nk = min(P.n_ot, P.n_o - k0);
     for (int k = threadIdx.x; k < nk; k += blockDim.x) {
@@ -1884,7 +1884,7 @@ extern "C" he_status he_fc_ex(const he_ctx* c, const he_fc_desc* f, const uint64
         const size_t smem = sizeof(u64) * padded_words(c->N);
         auto kf = c->ntt_mode == 0 ? k_fc_inv<true> : k_fc_inv<false>;
         if (!set_smem(kf, smem)) return HE_ECUDA;
-        kf<<<nblk, ntt_threads(c->N), smem, st>>>(
+        kf<<<nblk, std::min(1024, std::max(32, (int)(c->N / 16))), smem, st>>>(
             spec, (const ulonglong2*)d_wspec, (const u64*)d_bias_enc, d_phi1, (u64*)d_out, P,
             c->L, c->logN, c->d_limb, c->d_tw_inv, c->d_twd_inv, c->t, c->r_t, c->t_inv);
     } else {
