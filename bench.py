@@ -774,6 +774,28 @@ def main():
             "kernel_ms_per_step": sw_ms,
             "kernel_hbm_frac": sw_bytes / (sw_ms * 1e-3) / 1e9 / peaks()[0]}
 
+    # ---- multi-GPU: the one exchange of the path -- every
+    # rank's compact payload assembled on all ranks (NCCL all_gather over
+    # NVLink), timed outside the step
+    gather = None
+    if world > 1 and not args.profile:
+        from paper_2409_05205_b200.dist import gather_payload
+        for _ in range(2):
+            for c in comps:
+                gather_payload(c, B * world)
+        barrier()
+        g0, g1 = mk(), mk()
+        g0.record()
+        for _ in range(args.steps):
+            for c in comps:
+                gather_payload(c, B * world)
+        g1.record()
+        barrier()
+        ms_g = max_over_ranks(g0.elapsed_time(g1) / args.steps)
+        gbytes = sum(c.numel() * 8 for c in comps) * world
+        gather = {"ms_per_step": ms_g, "bytes_per_step_all_ranks": gbytes,
+                  "GBps": gbytes / (ms_g * 1e-3) / 1e9}
+
     # ---- client mirror path: the client's per-layer work
     # of Alg. 1 Lines 21-24 + Eq. (2) -- c1^r = valid slots of
     # sum_beta (v_beta s) p_beta^{(n)} through he_conv on the spectra of
@@ -954,7 +976,7 @@ def main():
             "ntt": ntt, "stages_ms_per_step": st, "per_layer": per_layer,
             "roofline": roofline,
             "roofline_all": rl, "u1": u1, "init_ms": init_ms,
-            "cpu_baseline": cpu, "e2e": e2e, "payload_only": payload_only, "client": client, "chain": chain, "fc_variants": fc_var, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "payload_only": payload_only, "gather": gather, "client": client, "chain": chain, "fc_variants": fc_var, "clocks": clocks,
             "gpu_launches": launches_step * args.steps,
         }
         print(json.dumps(line), flush=True)
