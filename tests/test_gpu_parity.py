@@ -474,3 +474,63 @@ def test_conv_column_ntt_forced(he, monkeypatch):
         ctx = he.Context(cfg.primes, cfg.log2N, cfg.t)
         ring = R.Ring(cfg.N, cfg.primes, cfg.t)
         run_conv(he, ctx, ring, cfg.conv[li], B, seed=cfg.seed + 11 * li, check_b=[0, B - 1])
+
+
+def test_conv_in_bench_launch_configuration(he):
+    """The bench step's launch configuration -- config 4 layer jobs dealt to
+    four streams, captured once as a CUDA graph and replayed -- gives
+    bit-exact full outputs and payloads (sampled images vs the oracle)."""
+    cfg = synth.CONFIGS[4]
+    ctx = ctx_for(he, cfg.N, cfg.primes, cfg.t)
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    B = cfg.B
+    lis = [0, 1, 7, 8, 13, 14]
+    jobs = []
+    for li in lis:
+        Ly = cfg.conv[li]
+        p = ctx.plan(Ly.c_i, Ly.c_o, Ly.w_i, Ly.h_i, Ly.f_w, Ly.f_h, Ly.stride, Ly.pad)
+        W = synth.weights(cfg, li)
+        c0 = synth.uniform_residues((B, p.n_ib, ring.L, cfg.N), cfg.primes, cfg.seed, "c0", li)
+        phi = synth.phi1((B, p.n_ob, cfg.N), cfg.t, cfg.seed, li)
+        jobs.append(dict(li=li, p=p, W=W, c0=c0, phi=phi, fspec=ctx.pack_filters(p, dev(W)),
+                         c0_d=dev(c0), phi_d=dev(phi), out=ctx.empty_u64(B, p.n_ob, ring.L, cfg.N),
+                         comp=ctx.empty_u64(B, p.n_ob, ring.L, p.n_valid)))
+    nstr = 4
+    main = torch.cuda.Stream()
+    side = [main] + [torch.cuda.Stream() for _ in range(nstr - 1)]
+    ws = [ctx.conv_workspace(j["p"], B) for j in jobs]
+    wsk = [torch.empty(max(w.numel() for w in ws), dtype=torch.uint8, device="cuda")
+           for _ in range(nstr)]
+    fork = [torch.cuda.Event() for _ in range(nstr)]
+
+    def step():
+        fork[0].record(main)
+        for k in range(1, nstr):
+            side[k].wait_event(fork[0])
+        for i, j in enumerate(jobs):
+            k = i % nstr
+            ctx.conv(j["p"], j["c0_d"], j["fspec"], j["phi_d"], j["out"], wsk[k],
+                     compact=j["comp"], stream=side[k])
+        for k in range(1, nstr):
+            fork[k].record(side[k])
+            main.wait_event(fork[k])
+
+    torch.cuda.synchronize()
+    with torch.cuda.stream(main):
+        step()                                   # warm-up outside capture
+    torch.cuda.synchronize()
+    for j in jobs:
+        j["out"].zero_()
+        j["comp"].zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=main):
+        step()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for j in jobs:
+        plan = R.plan_conv(cfg.conv[j["li"]], cfg.N)
+        for b in (0, B - 1):
+            ref = R.conv_server(j["c0"][b:b + 1], j["W"], plan, ring, j["phi"][b:b + 1])
+            assert np.array_equal(u64(j["out"])[b], ref[0]), j["li"]
+            assert np.array_equal(u64(j["comp"])[b], R.compact(ref, plan)[0]), j["li"]
