@@ -752,7 +752,9 @@ __global__ void k_filter_to_mac(const u64* __restrict__ spec, u64* __restrict__ 
 // agree): the int8 tensor-core MAC for s >= 4 (its operand staging moves
 // whole s-byte runs), else the IMAD MAC.  HE_MAC=imad forces the IMAD MAC.
 static bool use_imma(const he_ctx* c, const PlanDev& P) {
-    return c->mac_mode == 0 && P.s >= 4;
+    // (the tensor-core kernel holds all output channels of a group in one
+    // CTA, one warp per 8: c_o <= 256; wider layers take the IMAD MAC)
+    return c->mac_mode == 0 && P.s >= 4 && P.c_o <= 256;
 }
 static inline int imma_kp(int K) { return (K + 15) & ~15; }
 static inline int imma_sw(int Kp) { return Kp / 4 + ((4 - Kp / 4) & 7); }   // = 4 mod 8

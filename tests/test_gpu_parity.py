@@ -534,3 +534,13 @@ def test_conv_in_bench_launch_configuration(he):
             ref = R.conv_server(j["c0"][b:b + 1], j["W"], plan, ring, j["phi"][b:b + 1])
             assert np.array_equal(u64(j["out"])[b], ref[0]), j["li"]
             assert np.array_equal(u64(j["comp"])[b], R.compact(ref, plan)[0]), j["li"]
+
+
+def test_conv_wide_layer_over_256_channels(he):
+    """c_o > 256: the IMAD MAC path (the tensor-core kernel keeps all of a
+    group's output channels in one CTA); n_ob > 1 blocks, bit-exact."""
+    N = 1024
+    primes = RINGS[N]
+    ctx = ctx_for(he, N, primes)
+    ring = R.Ring(N, primes, 65537)
+    run_conv(he, ctx, ring, synth.ConvLayer(8, 300, 4, 4), 3, seed=300, mask=True)
