@@ -405,6 +405,16 @@ he_status he_c0_compact(const he_ctx* ctx, const he_conv_plan* plan,
 he_status he_c0_expand(const he_ctx* ctx, const he_conv_plan* plan,
                        const uint64_t* d_c0c, int B, uint64_t* d_c0, void* stream);
 
+/* a2 debug export for parity: the coefficient-domain filter polynomials of
+ * Eq. (6), f_beta^{(n)} (shifted = 0) or the Eq. (7)-shifted
+ * fhat_beta^{(n)} = X^{t_n} f_beta^{(n)} (shifted = 1),
+ * residues per limb, d_f uint64 [c_o][n_ib][L][N].  d_ws (c_o n_ib L N 8
+ * bytes) is needed only when shifted.  Not on the hot path: he_pack_filters
+ * stores the transformed operand instead. */
+he_status he_filter_coeffs(const he_ctx* ctx, const he_conv_plan* plan,
+                           const int32_t* d_w, int shifted, uint64_t* d_f, void* d_ws,
+                           size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

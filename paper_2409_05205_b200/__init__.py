@@ -118,6 +118,7 @@ _sig("he_relu_requant", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _I, _I, _P, _
 _sig("he_avgpool", [_P, ctypes.c_long, _I, _P, _P])
 _sig("he_unmask", [_P, _P, _P, ctypes.c_long, _P, _P])
 _sig("he_c0_compact", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P])
+_sig("he_filter_coeffs", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _SZ, _P])
 _sig("he_c0_expand", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P])
 _sig("he_fc_server_p_workspace_bytes", [_P, ctypes.POINTER(FcDesc)], _SZ)
 _sig("he_fc_server_init_p", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _P, _P, _SZ, _P])
@@ -133,7 +134,7 @@ EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_ntt_inverse", "he_ntt_forward_partial", "he_server_p_workspace_bytes", "he_server_init_p",
             "he_pack_client_p", "he_residues_from_int", "he_poly_mul",
             "he_decrypt_round", "he_mod_switch", "he_pk_mask", "he_relu_requant",
-            "he_avgpool", "he_unmask", "he_c0_compact", "he_c0_expand", "he_fc_server_p_workspace_bytes", "he_fc_server_init_p",
+            "he_avgpool", "he_unmask", "he_c0_compact", "he_c0_expand", "he_filter_coeffs", "he_fc_server_p_workspace_bytes", "he_fc_server_init_p",
             "he_pack_fc_client_p"]
 
 
@@ -580,4 +581,16 @@ class Context:
         self._dev(c0c, out)
         _check(_lib.he_c0_expand(self._h, ctypes.byref(p), self._ptr(c0c), B,
                                  self._ptr(out), _stream(stream)), "he_c0_expand")
+        return out
+
+    def filter_coeffs(self, p: ConvPlan, W: torch.Tensor, shifted: bool = True,
+                      stream=None):
+        """a2 debug export: [c_o][n_ib][L][N] coefficient-domain f or fhat."""
+        out = self.empty_u64(p.d.c_o, p.n_ib, self.L, self.N)
+        ws = torch.empty(out.numel() * 8 if shifted else 8, dtype=torch.uint8,
+                         device=self.device)
+        self._dev(W, out)
+        _check(_lib.he_filter_coeffs(self._h, ctypes.byref(p), self._ptr(W), int(shifted),
+                                     self._ptr(out), self._ptr(ws), ws.numel(),
+                                     _stream(stream)), "he_filter_coeffs")
         return out

@@ -2532,3 +2532,29 @@ extern "C" he_status he_c0_expand(const he_ctx* c, const he_conv_plan* p, const 
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
+
+// ============================================== a2 debug export (parity)
+extern "C" he_status he_filter_coeffs(const he_ctx* c, const he_conv_plan* p, const int32_t* d_w,
+                                      int shifted, uint64_t* d_f, void* d_ws, size_t ws_bytes,
+                                      void* stream) {
+    if (!c || !p || !d_w || !d_f) return HE_EINVAL;
+    if (!plan_ok(c, p)) return HE_ESHAPE;
+    cudaStream_t st = STREAM(stream);
+    const PlanDev P = plan_dev(p);
+    const long total = (long)P.c_o * P.n_ib * c->L * c->N;
+    if (!shifted) {
+        k_pack_filter_coeffs<<<grid_for(total, 256), 256, 0, st>>>(d_w, (u64*)d_f, P, c->L,
+                                                                    c->logN, c->d_limb);
+        HE_CHECK_LAUNCH();
+        return HE_OK;
+    }
+    if (!d_ws) return HE_EINVAL;
+    if (ws_bytes < sizeof(u64) * (size_t)total) return HE_ENOMEM;
+    k_pack_filter_coeffs<<<grid_for(total, 256), 256, 0, st>>>(d_w, (u64*)d_ws, P, c->L,
+                                                                c->logN, c->d_limb);
+    HE_CHECK_LAUNCH();
+    k_negashift<<<grid_for(total, 256), 256, 0, st>>>((const u64*)d_ws, nullptr, (u64*)d_f, P,
+                                                       +1, c->L, c->logN, c->d_limb);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}

@@ -544,3 +544,25 @@ def test_conv_wide_layer_over_256_channels(he):
     ctx = ctx_for(he, N, primes)
     ring = R.Ring(N, primes, 65537)
     run_conv(he, ctx, ring, synth.ConvLayer(8, 300, 4, 4), 3, seed=300, mask=True)
+
+
+@pytest.mark.parametrize("case", SMALL[:6], ids=lambda c: f"{c[0]}-N{c[1]}")
+def test_filter_coefficients_eq6_eq7(he, case):
+    """a2 directly: the coefficient-domain filter polynomials of Eq. (6) and
+    the Eq. (7)-shifted ones against the oracle's sparse term lists."""
+    Ly, N, so, _ = case
+    primes = RINGS[N]
+    ctx = ctx_for(he, N, primes)
+    ring = R.Ring(N, primes, 65537)
+    plan = R.plan_conv(Ly, N, so)
+    p = ctx.plan(Ly.c_i, Ly.c_o, Ly.w_i, Ly.h_i, Ly.f_w, Ly.f_h, Ly.stride, Ly.pad, so)
+    W = np.random.default_rng(N + Ly.c_o).integers(-8, 8, (Ly.c_o, Ly.c_i, Ly.f_w, Ly.f_h))
+    for shifted in (False, True):
+        got = u64(ctx.filter_coeffs(p, dev(W.astype(np.int32)), shifted))
+        for n in range(plan.c_o):
+            for beta in range(plan.n_ib):
+                want = np.zeros(N, dtype=np.int64)
+                for e, w in R.filter_terms(W, plan, n, beta, shifted=shifted):
+                    want[e] += w
+                assert np.array_equal(got[n, beta], R.signed_to_residues(want, ring)), \
+                    (shifted, n, beta)
