@@ -854,6 +854,34 @@ def main():
                           "server_init_p_ms: Alg. 1 Line 5 for all layers, once"}
         del pspecs, c1s, msgs
 
+    # ---- ablation: the unfolded path (full N-point products and inverse per
+    # output channel, Alg. 1 Lines 14-17 literally) on the same conv layers,
+    # one launch sequence, to show what the fold + incomplete transform save
+    ablation = None
+    if not args.no_client and not args.profile:
+        import ctypes
+        wsp = torch.empty(max(int(he._lib.he_conv_plain_workspace_bytes(
+            ctx._h, ctypes.byref(lw.p), B)) for lw in layers), dtype=torch.uint8, device=dev)
+        fpl = [ctx.pack_filters_plain(lw.p, d(synth.weights(cfg, lw.idx))) for lw in layers]
+        for i, lw in enumerate(layers):
+            ctx.conv_plain(lw.p, c0_d[i], fpl[i], phi_d[i], outs[i], wsp)
+        torch.cuda.synchronize()
+        a0, a1 = mk(), mk()
+        a0.record()
+        for i, lw in enumerate(layers):
+            ctx.conv_plain(lw.p, c0_d[i], fpl[i], phi_d[i], outs[i], wsp)
+        a1.record()
+        torch.cuda.synchronize()
+        ms_plain = a0.elapsed_time(a1)
+        conv_seq = st["ntt_fwd"] + st["mac_fold"] + st["intt_scatter"] + st["gaps"]
+        ablation = {"unfolded_conv_ms_per_step": ms_plain,
+                    "folded_conv_ms_per_step_sequential": conv_seq,
+                    "fold_speedup": ms_plain / conv_seq,
+                    "what": "he_conv_plain (full N-point products + N-point inverse per "
+                            "(b, n, l), then extraction) vs he_conv, both one launch "
+                            "sequence, all 19 conv layers"}
+        del fpl, wsp
+
     # ---- FC packing variants (§8(f)): sub-matrix tiling for n_i n_o > N
     # (R27) on this ring, and the FC at N = 32768 (config 5's ring)
     fc_var = None
@@ -976,7 +1004,7 @@ def main():
             "ntt": ntt, "stages_ms_per_step": st, "per_layer": per_layer,
             "roofline": roofline,
             "roofline_all": rl, "u1": u1, "init_ms": init_ms,
-            "cpu_baseline": cpu, "e2e": e2e, "payload_only": payload_only, "gather": gather, "client": client, "chain": chain, "fc_variants": fc_var, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "payload_only": payload_only, "gather": gather, "ablation": ablation, "client": client, "chain": chain, "fc_variants": fc_var, "clocks": clocks,
             "gpu_launches": launches_step * args.steps,
         }
         print(json.dumps(line), flush=True)

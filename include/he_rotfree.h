@@ -415,6 +415,19 @@ he_status he_filter_coeffs(const he_ctx* ctx, const he_conv_plan* plan,
                            const int32_t* d_w, int shifted, uint64_t* d_f, void* d_ws,
                            size_t ws_bytes, void* stream);
 
+/* Unfolded reference path (ablation; SURVEY §8(a) "plain variant"): Alg. 1
+ * Lines 14-17 computed literally -- full N-point NTT-domain products
+ * sum_beta c0_beta f_beta^{(n)}, an N-point inverse per (b, n, l), then the
+ * slots s j + t_n extracted and masked.  Output identical to he_conv's full
+ * c0^r; costs the full transforms the fold avoids.  d_fplain uint64
+ * [c_o][n_ib][L][N] from he_pack_filters_plain (plain NTT spectra). */
+size_t he_conv_plain_workspace_bytes(const he_ctx* ctx, const he_conv_plan* plan, int B);
+he_status he_pack_filters_plain(const he_ctx* ctx, const he_conv_plan* plan,
+                                const int32_t* d_w, uint64_t* d_fplain, void* stream);
+he_status he_conv_plain(const he_ctx* ctx, const he_conv_plan* plan, const uint64_t* d_c0,
+                        int B, const uint64_t* d_fplain, const uint32_t* d_phi1,
+                        uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

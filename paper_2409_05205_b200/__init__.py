@@ -119,6 +119,9 @@ _sig("he_avgpool", [_P, ctypes.c_long, _I, _P, _P])
 _sig("he_unmask", [_P, _P, _P, ctypes.c_long, _P, _P])
 _sig("he_c0_compact", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P])
 _sig("he_filter_coeffs", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _SZ, _P])
+_sig("he_conv_plain_workspace_bytes", [_P, ctypes.POINTER(ConvPlan), _I], _SZ)
+_sig("he_pack_filters_plain", [_P, ctypes.POINTER(ConvPlan), _P, _P, _P])
+_sig("he_conv_plain", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _P, _P, _SZ, _P])
 _sig("he_c0_expand", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P])
 _sig("he_fc_server_p_workspace_bytes", [_P, ctypes.POINTER(FcDesc)], _SZ)
 _sig("he_fc_server_init_p", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _P, _P, _SZ, _P])
@@ -134,7 +137,8 @@ EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_ntt_inverse", "he_ntt_forward_partial", "he_server_p_workspace_bytes", "he_server_init_p",
             "he_pack_client_p", "he_residues_from_int", "he_poly_mul",
             "he_decrypt_round", "he_mod_switch", "he_pk_mask", "he_relu_requant",
-            "he_avgpool", "he_unmask", "he_c0_compact", "he_c0_expand", "he_filter_coeffs", "he_fc_server_p_workspace_bytes", "he_fc_server_init_p",
+            "he_avgpool", "he_unmask", "he_c0_compact", "he_c0_expand", "he_filter_coeffs",
+            "he_conv_plain_workspace_bytes", "he_pack_filters_plain", "he_conv_plain", "he_fc_server_p_workspace_bytes", "he_fc_server_init_p",
             "he_pack_fc_client_p"]
 
 
@@ -593,4 +597,28 @@ class Context:
         _check(_lib.he_filter_coeffs(self._h, ctypes.byref(p), self._ptr(W), int(shifted),
                                      self._ptr(out), self._ptr(ws), ws.numel(),
                                      _stream(stream)), "he_filter_coeffs")
+        return out
+
+    # ------------------------------------- unfolded reference path (ablation)
+    def pack_filters_plain(self, p: ConvPlan, W: torch.Tensor, stream=None):
+        out = self.empty_u64(p.d.c_o, p.n_ib, self.L, self.N)
+        self._dev(W, out)
+        _check(_lib.he_pack_filters_plain(self._h, ctypes.byref(p), self._ptr(W),
+                                          self._ptr(out), _stream(stream)),
+               "he_pack_filters_plain")
+        return out
+
+    def conv_plain(self, p: ConvPlan, c0: torch.Tensor, fplain: torch.Tensor,
+                   phi1: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                   ws: Optional[torch.Tensor] = None, stream=None):
+        B = c0.shape[0]
+        if out is None:
+            out = self.empty_u64(B, p.n_ob, self.L, self.N)
+        if ws is None:
+            ws = torch.empty(_lib.he_conv_plain_workspace_bytes(self._h, ctypes.byref(p), B),
+                             dtype=torch.uint8, device=self.device)
+        self._dev(c0, fplain, phi1, out, ws)
+        _check(_lib.he_conv_plain(self._h, ctypes.byref(p), self._ptr(c0), B,
+                                  self._ptr(fplain), self._ptr(phi1), self._ptr(out),
+                                  self._ptr(ws), ws.numel(), _stream(stream)), "he_conv_plain")
         return out

@@ -2558,3 +2558,99 @@ extern "C" he_status he_filter_coeffs(const he_ctx* c, const he_conv_plan* p, co
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
+
+// ============================== unfolded reference path (ablation of the fold)
+// Alg. 1 Lines 14-17 computed literally: every c0_beta x f_beta^{(n)} as a
+// full N-point NTT-domain product, an N-point inverse per (b, n, l), then the
+// slots s j + t_n extracted (SURVEY §8(a) "plain variant").  Same output as
+// he_conv; kept to measure what the fold and the incomplete transform save.
+__global__ void k_mac_plain(const u64* __restrict__ C, const u64* __restrict__ F,
+                            u64* __restrict__ P, PlanDev Pd, int B, int L, int logN,
+                            const he_limb* __restrict__ limbs) {
+    const long N = 1L << logN;
+    const long total = (long)B * Pd.c_o * L * N;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const long k = idx & (N - 1), r = idx >> logN;
+        const int l = (int)(r % L);
+        const long bn = r / L;
+        const int n = (int)(bn % Pd.c_o), b = (int)(bn / Pd.c_o);
+        const he_limb& Lm = limbs[l];
+        double acc = 0.0;
+        for (int beta = 0; beta < Pd.n_ib; ++beta) {
+            const u64 x = C[(((long)b * Pd.n_ib + beta) * L + l) * N + k];
+            const u64 y = F[(((long)n * Pd.n_ib + beta) * L + l) * N + k];
+            acc = dp_reduce(acc + dp_mulmod(u2d(x), u2d(y), Lm.qd, Lm.qinvd), Lm.qd, Lm.qinvd);
+        }
+        P[idx] = d2canon(acc, Lm.qd, Lm.qinvd);
+    }
+}
+
+__global__ void k_extract_plain(const u64* __restrict__ P, const u32* __restrict__ phi1,
+                                u64* __restrict__ out, PlanDev Pd, int B, int L, int logN,
+                                const he_limb* __restrict__ limbs, const u64* __restrict__ enc_tab,
+                                u64 t, u64 r_t, u64 t_inv) {
+    const long N = 1L << logN;
+    const long total = (long)B * Pd.n_ob * L * N;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const long i = idx & (N - 1), r = idx >> logN;
+        const int l = (int)(r % L);
+        const long bo = r / L;
+        const int ob = (int)(bo % Pd.n_ob), b = (int)(bo / Pd.n_ob);
+        const int u = (int)(i & (Pd.s - 1));
+        const int nl = u / Pd.step, n = ob * Pd.c_ob + nl;
+        u64 v = 0;
+        if (u == nl * Pd.step && nl < Pd.c_ob && n < Pd.c_o)
+            v = P[(((long)b * Pd.c_o + n) * L + l) * N + (i - u)];
+        const he_limb& Lm = limbs[l];
+        if (phi1) v = addmod(v, enc_lookup(enc_tab, l, t, phi1[bo * N + i], Lm, r_t, t_inv), Lm.q);
+        out[idx] = v;
+    }
+}
+
+extern "C" size_t he_conv_plain_workspace_bytes(const he_ctx* c, const he_conv_plan* p, int B) {
+    if (!c || !p || B < 0) return 0;
+    return sizeof(u64) * (size_t)std::max(B, 1) * (p->n_ib + p->d.c_o) * c->L * c->N;
+}
+
+extern "C" he_status he_pack_filters_plain(const he_ctx* c, const he_conv_plan* p,
+                                           const int32_t* d_w, uint64_t* d_fplain, void* stream) {
+    if (!c || !p || !d_w || !d_fplain) return HE_EINVAL;
+    if (!plan_ok(c, p)) return HE_ESHAPE;
+    cudaStream_t st = STREAM(stream);
+    const PlanDev P = plan_dev(p);
+    const long total = (long)P.c_o * P.n_ib * c->L * c->N;
+    k_pack_filter_coeffs<<<grid_for(total, 256), 256, 0, st>>>(d_w, (u64*)d_fplain, P, c->L,
+                                                                c->logN, c->d_limb);
+    HE_CHECK_LAUNCH();
+    return launch_ntt_fwd(c, (u64*)d_fplain, (u64*)d_fplain, (long)P.c_o * P.n_ib * c->L, 0, st);
+}
+
+extern "C" he_status he_conv_plain(const he_ctx* c, const he_conv_plan* p, const uint64_t* d_c0,
+                                   int B, const uint64_t* d_fplain, const uint32_t* d_phi1,
+                                   uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream) {
+    if (!c || !p || B < 0) return HE_EINVAL;
+    if (!plan_ok(c, p)) return HE_ESHAPE;
+    if (B == 0) return HE_OK;
+    if (!d_c0 || !d_fplain || !d_out || !d_ws) return HE_EINVAL;
+    if (ws_bytes < he_conv_plain_workspace_bytes(c, p, B)) return HE_ENOMEM;
+    cudaStream_t st = STREAM(stream);
+    const PlanDev P = plan_dev(p);
+    u64* Cs = (u64*)d_ws;
+    u64* Ps = Cs + (size_t)B * P.n_ib * c->L * c->N;
+    he_status s = launch_ntt_fwd(c, (const u64*)d_c0, Cs, (long)B * P.n_ib * c->L, 0, st);
+    if (s != HE_OK) return s;
+    const long tp = (long)B * P.c_o * c->L * c->N;
+    k_mac_plain<<<grid_for(tp, 256), 256, 0, st>>>(Cs, (const u64*)d_fplain, Ps, P, B, c->L,
+                                                   c->logN, c->d_limb);
+    HE_CHECK_LAUNCH();
+    s = launch_ntt_inv(c, Ps, Ps, (long)B * P.c_o * c->L, st);
+    if (s != HE_OK) return s;
+    const long to = (long)B * P.n_ob * c->L * c->N;
+    k_extract_plain<<<grid_for(to, 256), 256, 0, st>>>(Ps, d_phi1, (u64*)d_out, P, B, c->L,
+                                                       c->logN, c->d_limb, c->d_enc, c->t,
+                                                       c->r_t, c->t_inv);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}

@@ -566,3 +566,22 @@ def test_filter_coefficients_eq6_eq7(he, case):
                     want[e] += w
                 assert np.array_equal(got[n, beta], R.signed_to_residues(want, ring)), \
                     (shifted, n, beta)
+
+
+@pytest.mark.parametrize("case", SMALL[3:8], ids=lambda c: f"{c[0]}-N{c[1]}")
+def test_conv_plain_unfolded_path(he, case):
+    """The unfolded reference path (full N-point products and inverse, then
+    extraction) equals the oracle and he_conv's folded output."""
+    Ly, N, so, B = case
+    primes = RINGS[N]
+    ctx = ctx_for(he, N, primes)
+    ring = R.Ring(N, primes, 65537)
+    plan = R.plan_conv(Ly, N, so)
+    p = ctx.plan(Ly.c_i, Ly.c_o, Ly.w_i, Ly.h_i, Ly.f_w, Ly.f_h, Ly.stride, Ly.pad, so)
+    W = np.random.default_rng(B + N).integers(-8, 8, (Ly.c_o, Ly.c_i, Ly.f_w, Ly.f_h)).astype(np.int32)
+    c0 = synth.uniform_residues((B, p.n_ib, ring.L, N), primes, 41, "misc", B)
+    phi = synth.phi1((B, p.n_ob, N), ring.t, 41)
+    out_p = u64(ctx.conv_plain(p, dev(c0), ctx.pack_filters_plain(p, dev(W)), dev(phi)))
+    out_f = u64(ctx.conv(p, dev(c0), ctx.pack_filters(p, dev(W)), dev(phi)))
+    assert np.array_equal(out_p, out_f)
+    assert np.array_equal(out_p, R.conv_server(c0, W, plan, ring, phi))
