@@ -428,6 +428,15 @@ he_status he_conv_plain(const he_ctx* ctx, const he_conv_plan* plan, const uint6
                         int B, const uint64_t* d_fplain, const uint32_t* d_phi1,
                         uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream);
 
+/* The client's per-layer randomness in one pass, sharing NTT(v):
+ * d_ve[i] = v_i b + e_i (Eq. (1)) and d_vs[i] = v_i s (Alg. 1 Line 21),
+ * d_s uint64 [L][N] the residues of the secret key.  Workspace 2 L N 8
+ * bytes. */
+he_status he_pk_mask_vs(const he_ctx* ctx, const int32_t* d_v, const int32_t* d_e,
+                        long n_polys, const uint64_t* d_b, const uint64_t* d_s,
+                        uint64_t* d_ve, uint64_t* d_vs, void* d_ws, size_t ws_bytes,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -114,6 +114,7 @@ _sig("he_poly_mul", [_P, _P, _P, _I, _I, _P, _P, _SZ, _P])
 _sig("he_decrypt_round", [_P, _P, _P, ctypes.c_long, ctypes.c_long, _P, _P])
 _sig("he_mod_switch", [_P, _P, ctypes.c_long, ctypes.c_long, _I, _P, _P])
 _sig("he_pk_mask", [_P, _P, _P, ctypes.c_long, _P, _P, _P, _SZ, _P])
+_sig("he_pk_mask_vs", [_P, _P, _P, ctypes.c_long, _P, _P, _P, _P, _P, _SZ, _P])
 _sig("he_relu_requant", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _I, _I, _P, _P])
 _sig("he_avgpool", [_P, ctypes.c_long, _I, _P, _P])
 _sig("he_unmask", [_P, _P, _P, ctypes.c_long, _P, _P])
@@ -136,7 +137,8 @@ EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_residues_unpack50", "he_phi1_generate", "he_ntt_forward",
             "he_ntt_inverse", "he_ntt_forward_partial", "he_server_p_workspace_bytes", "he_server_init_p",
             "he_pack_client_p", "he_residues_from_int", "he_poly_mul",
-            "he_decrypt_round", "he_mod_switch", "he_pk_mask", "he_relu_requant",
+            "he_decrypt_round", "he_mod_switch", "he_pk_mask", "he_pk_mask_vs",
+            "he_relu_requant",
             "he_avgpool", "he_unmask", "he_c0_compact", "he_c0_expand", "he_filter_coeffs",
             "he_conv_plain_workspace_bytes", "he_pack_filters_plain", "he_conv_plain", "he_fc_server_p_workspace_bytes", "he_fc_server_init_p",
             "he_pack_fc_client_p"]
@@ -622,3 +624,16 @@ class Context:
                                   self._ptr(fplain), self._ptr(phi1), self._ptr(out),
                                   self._ptr(ws), ws.numel(), _stream(stream)), "he_conv_plain")
         return out
+
+    def pk_mask_vs(self, v: torch.Tensor, e: Optional[torch.Tensor], b: torch.Tensor,
+                   s_res: torch.Tensor, stream=None):
+        """(v b + e, v s) for int32 v, e [..][N] -> two [..][L][N] tensors."""
+        n = v.numel() // self.N
+        ve = self.empty_u64(*v.shape[:-1], self.L, self.N)
+        vs = self.empty_u64(*v.shape[:-1], self.L, self.N)
+        ws = torch.empty(16 * self.L * self.N, dtype=torch.uint8, device=self.device)
+        self._dev(v, e, b, s_res, ve, vs)
+        _check(_lib.he_pk_mask_vs(self._h, self._ptr(v), self._ptr(e), n, self._ptr(b),
+                                  self._ptr(s_res), self._ptr(ve), self._ptr(vs),
+                                  self._ptr(ws), ws.numel(), _stream(stream)), "he_pk_mask_vs")
+        return ve, vs

@@ -4,8 +4,8 @@ the rotation-free Conv (Alg. 1) or FC (Alg. 2) with its mask phi1, the
 client computes its share c1^r and decrypts, and the trusted GC stub (R29)
 unmasks, applies ReLU + requantisation and re-packs the activations for the
 next layer.  Orchestration only: every step is a call into
-libhe_rotfree.so (he_pk_mask, he_pack_input, he_phi1_generate, he_conv,
-he_poly_mul, he_decrypt_round, he_relu_requant, he_avgpool, he_fc,
+libhe_rotfree.so (he_pk_mask_vs, he_pack_input, he_phi1_generate, he_conv,
+he_decrypt_round, he_relu_requant, he_avgpool, he_fc,
 he_unmask).  Randomness (v, e0, the server's e_f) is supplied by the caller
 as device tensors, so runs are reproducible and comparable with the oracle.
 """
@@ -36,7 +36,7 @@ class Chain:
         self.dplans = [ctx.dense_plan(p) for p in self.plans]   # client operand is dense
         self.pspecs = [ctx.pack_client_p(p, ctx.server_init_p(p, W, a, e))
                        for p, W, e in zip(self.plans, Ws, ef)]
-        self.s_res = ctx.residues_from_int(s_key.reshape(1, -1))
+        self.s_res = ctx.residues_from_int(s_key.reshape(1, -1)).reshape(ctx.L, ctx.N)
         self.fc = None
         if fcW is not None:
             n_o, n_i = fcW.shape
@@ -57,7 +57,7 @@ class Chain:
         x = img
         for li, p in enumerate(self.plans):
             # client: c0-only encryption of the packed activations
-            ve = ctx.pk_mask(v[li], e0[li], self.b_pk)
+            ve, vs = ctx.pk_mask_vs(v[li], e0[li], self.b_pk, self.s_res)
             c0 = ctx.pack_input(p, x, ve)
             # server: conv + mask, compact payload only
             phi = torch.empty(B, p.n_ob, ctx.N, dtype=torch.int32, device=ctx.device)
@@ -65,8 +65,6 @@ class Chain:
             comp0 = ctx.empty_u64(B, p.n_ob, ctx.L, p.n_valid)
             ctx.conv(p, c0, self.fspecs[li], phi, compact=comp0, full=False)
             # client: share c1^r, decryption, GC stub
-            vs = ctx.poly_mul(ctx.residues_from_int(v[li]).reshape(-1, ctx.L, ctx.N),
-                              self.s_res).reshape(B, p.n_ib, ctx.L, ctx.N)
             comp1 = ctx.empty_u64(B, p.n_ob, ctx.L, p.n_valid)
             ctx.conv(self.dplans[li], vs, self.pspecs[li], None, compact=comp1, full=False)
             m = ctx.decrypt_round(comp0, comp1)
@@ -77,13 +75,11 @@ class Chain:
         if self.fc is not None:
             f = self.fc
             xin = ctx.avgpool(x)
-            ve = ctx.pk_mask(v_fc, e0_fc, self.b_pk)
+            ve, vs = ctx.pk_mask_vs(v_fc, e0_fc, self.b_pk, self.s_res)
             c0 = ctx.fc_pack_input(f["n_i"], f["n_o"], xin, ve)
             phi = torch.empty(B, f["n_o"], dtype=torch.int32, device=ctx.device)
             ctx.phi1_generate(phi_seed * 1000 + 999, phi)
             out0 = ctx.fc(f["n_i"], f["n_o"], c0, f["wspec"], f["benc"], phi)
-            vs = ctx.poly_mul(ctx.residues_from_int(v_fc).reshape(-1, ctx.L, ctx.N),
-                              self.s_res).reshape(c0.shape)
             out1 = ctx.fc(f["n_i"], f["n_o"], vs, f["pspec"], f["zero"], None)
             logits = ctx.unmask(ctx.decrypt_round(out0, out1), phi)
         return acts, logits

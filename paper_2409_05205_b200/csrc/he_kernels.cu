@@ -2654,3 +2654,61 @@ extern "C" he_status he_conv_plain(const he_ctx* c, const he_conv_plan* p, const
     HE_CHECK_LAUNCH();
     return HE_OK;
 }
+
+// out[i][l][k] = x[i][l][k] * y[l][k] mod q_l (y broadcast; out may alias x)
+__global__ void k_pointwise_mul_to(const u64* __restrict__ x, const u64* __restrict__ y,
+                                   u64* __restrict__ out, long nx, int L, int logN,
+                                   const he_limb* __restrict__ limbs) {
+    const long N = 1L << logN;
+    const long total = nx * L * N;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const long k = idx & (N - 1), r = idx >> logN;
+        const int l = (int)(r % L);
+        const he_limb& Lm = limbs[l];
+        out[idx] = d2canon(dp_mulmod(u2d(x[idx]), u2d(y[(long)l * N + k]), Lm.qd, Lm.qinvd),
+                           Lm.qd, Lm.qinvd);
+    }
+}
+
+// Client randomness of one layer in one pass: ve = v b + e (Eq. (1)) and
+// vs = v s (the client's share factor, Alg. 1 Line 21), sharing NTT(v).
+extern "C" he_status he_pk_mask_vs(const he_ctx* c, const int32_t* d_v, const int32_t* d_e,
+                                   long n_polys, const uint64_t* d_b, const uint64_t* d_s,
+                                   uint64_t* d_ve, uint64_t* d_vs, void* d_ws, size_t ws_bytes,
+                                   void* stream) {
+    if (!c || n_polys < 0) return HE_EINVAL;
+    if (n_polys == 0) return HE_OK;
+    if (!d_v || !d_b || !d_s || !d_ve || !d_vs || !d_ws) return HE_EINVAL;
+    if (ws_bytes < 2 * sizeof(u64) * (size_t)c->L * c->N) return HE_ENOMEM;
+    cudaStream_t st = STREAM(stream);
+    const long total = n_polys * c->L * c->N;
+    u64* bspec = (u64*)d_ws;
+    u64* sspec = bspec + (size_t)c->L * c->N;
+    he_status s = launch_ntt_fwd(c, (const u64*)d_b, bspec, c->L, 0, st);
+    if (s != HE_OK) return s;
+    s = launch_ntt_fwd(c, (const u64*)d_s, sspec, c->L, 0, st);
+    if (s != HE_OK) return s;
+    k_residues_from_int<<<grid_for(total, 256), 256, 0, st>>>(d_v, n_polys, c->L, c->logN,
+                                                              c->d_limb, (u64*)d_vs);
+    HE_CHECK_LAUNCH();
+    s = launch_ntt_fwd(c, (const u64*)d_vs, (u64*)d_vs, n_polys * c->L, 0, st);   // V
+    if (s != HE_OK) return s;
+    k_pointwise_mul_to<<<grid_for(total, 256), 256, 0, st>>>((const u64*)d_vs, bspec,
+                                                              (u64*)d_ve, n_polys, c->L,
+                                                              c->logN, c->d_limb);
+    k_pointwise_mul_to<<<grid_for(total, 256), 256, 0, st>>>((const u64*)d_vs, sspec,
+                                                              (u64*)d_vs, n_polys, c->L,
+                                                              c->logN, c->d_limb);
+    HE_CHECK_LAUNCH();
+    s = launch_ntt_inv(c, (u64*)d_ve, (u64*)d_ve, n_polys * c->L, st);
+    if (s != HE_OK) return s;
+    s = launch_ntt_inv(c, (u64*)d_vs, (u64*)d_vs, n_polys * c->L, st);
+    if (s != HE_OK) return s;
+    if (d_e) {
+        k_add_small<<<grid_for(total, 256), 256, 0, st>>>((u64*)d_ve, d_e, n_polys, c->L,
+                                                           c->logN, c->d_limb);
+        HE_CHECK_LAUNCH();
+    }
+    return HE_OK;
+}

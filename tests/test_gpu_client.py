@@ -241,3 +241,27 @@ def test_sparse_c0_upload(he, cfg_idx, li):
     out = u64(ctx.conv(p, c0x, fspec, dev(phi.astype(np.uint32))))
     for b in (0, B - 1):
         assert np.array_equal(out[b], R.conv_server(c0[b:b + 1], W, plan, ring, phi[b:b + 1])[0])
+
+
+def test_pk_mask_vs_matches_separate_products(he):
+    """he_pk_mask_vs (shared NTT(v)) equals v b + e and v s computed by the
+    oracle's negacyclic products."""
+    cfg = synth.CONFIGS[2]
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    ctx = ctx_for(he, cfg.N, cfg.primes, cfg.t)
+    v = np.stack([synth.v_poly(cfg.N, 5, i) for i in range(3)]).astype(np.int32)
+    e = np.stack([synth.gauss_poly(cfg.N, 3.2, 5, "e0", i) for i in range(3)]).astype(np.int32)
+    b = synth.uniform_residues((ring.L, cfg.N), cfg.primes, 5, "a")
+    s_key = synth.secret_key(cfg.N, cfg.h, 5)
+    s_res = R.signed_to_residues(s_key, ring)
+    ve, vs = ctx.pk_mask_vs(dev(v), dev(e), dev(b), dev(s_res))
+    ve, vs = u64(ve), u64(vs)
+    pos = np.array([0, 1, 2, 100, cfg.N // 2, cfg.N - 1])
+    for i in range(3):
+        vr = R.signed_to_residues(v[i].astype(np.int64), ring)
+        er = R.signed_to_residues(e[i].astype(np.int64), ring)
+        for j, q in enumerate(cfg.primes):
+            want_ve = (R.negacyclic_at(vr[j], b[j], q, pos).astype(object) +
+                       er[j][pos].astype(object)) % q
+            assert [int(x) for x in ve[i, j, pos]] == [int(x) for x in want_ve]
+            assert np.array_equal(vs[i, j, pos], R.negacyclic_at(vr[j], s_res[j], q, pos))
