@@ -1418,7 +1418,7 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         // j = kr * h_p + lc, tracked incrementally
         int kr = jt / P.h_p, lc = jt - kr * P.h_p;
         const int dk = jstep / P.h_p, dl = jstep - dk * P.h_p;
-        constexpr int EB = 4;
+        constexpr int EB = 8;
         for (int j0 = jt; j0 < M; j0 += EB * jstep) {
             u32 m[EB];
             int vi[EB];
