@@ -128,10 +128,13 @@ he_status he_pack_input(const he_ctx* ctx, const he_conv_plan* p,
 
 /* a2, server initialisation (Eq. (6)-(7); Alg. 1
  * Line 4).  Packs d_w int32 [c_o][c_i][f_w][f_h] (weights, any sign, used
- * unscaled: R3) into the filter polynomials, takes their forward NTT and
- * stores them in the opaque NTT-domain layout d_fspec (he_filter_bytes()
- * bytes) consumed by he_conv.  d_ws: workspace of
- * he_pack_filters_workspace_bytes() bytes. */
+ * unscaled: R3) into the filter polynomials, runs the incomplete forward
+ * transform (the first log2(N/s) stages) and stores the fold
+ * operand F'_{g,u} = (N/s)^{-1} (u ? zeta_g F_{g,s-u} : F_{g,0}), u < k_u,
+ * in the opaque layout d_fspec (he_filter_bytes() bytes) consumed by
+ * he_conv: byte planes for the int8 tensor-core MAC, 25-bit split words for
+ * the IMAD MAC.  d_ws: workspace of he_pack_filters_workspace_bytes()
+ * bytes (the coefficient polynomials). */
 size_t he_filter_bytes(const he_ctx* ctx, const he_conv_plan* p);
 size_t he_pack_filters_workspace_bytes(const he_ctx* ctx,
                                        const he_conv_plan* p);
