@@ -156,8 +156,11 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
             const u64 w = pw[brv(k, r->log2N)], wi = pwi[brv(k, r->log2N)];
             fwd[(size_t)j * N + k] = make_ulonglong2(w, h_shoup(w, q));
             inv[(size_t)j * N + k] = make_ulonglong2(wi, h_shoup(wi, q));
-            fwdd[(size_t)j * N + k] = (double)w;          // exact: w < 2^50
-            invd[(size_t)j * N + k] = (double)wi;
+            // FP64 twiddles centred into (-q/2, q/2): |w| <= (q-1)/2 lets the
+            // FP64 butterflies multiply operands up to 4q without a prior
+            // reduction (he_internal.cuh, dp_mulmod)
+            fwdd[(size_t)j * N + k] = w > q / 2 ? -(double)(q - w) : (double)w;
+            invd[(size_t)j * N + k] = wi > q / 2 ? -(double)(q - wi) : (double)wi;
         }
         he_limb& Lm = c->limb_host[j];
         Lm.q = q;

@@ -171,11 +171,13 @@ __host__ __device__ constexpr int padded_words(int n) { return n + (n >> 4); }
 
 // ------------------------------------------------------- FP64 residues
 // Residues as integer-valued doubles (|x| < 2^52), so the modular products
-// run on the FP64 pipe.  With |y| w / q < 2^51 (e.g. |y| < 1.4 q, w < q):
+// run on the FP64 pipe.  The twiddle tables are centred, |w| <= (q-1)/2, so
+// |y| w / q < 2^51 holds for every |y| <= 4q + 8 (q <= 2^50 - 3):
 //   p = fl(y w), e = fma(y, w, -p) = y w - p        (exact two-product)
-//   k = rint(p / q) via the 1.5 2^52 magic constant (exact, |p/q| < 2^51)
-//   r = fma(-k, q, p) = p - k q                     (exact, |.| < 2^52)
-//   T = r + e = y w - k q,  |T| < 0.875 q           (k within 0.875 of y w/q)
+//   k = rint(p qinv) via the 1.5 2^52 magic constant: |p/q - k| <= 0.5 +
+//       |p/q| 2^-53 <= 0.75
+//   r = fma(-k, q, p) = p - k q                     (exact, |.| <= 0.75 q)
+//   T = r + e = y w - k q,  |T| <= 0.75 q + ulp(p)/2 <= q   (|p| <= 2 q^2)
 static constexpr double DP_MAGIC = 6755399441055744.0;     // 1.5 * 2^52
 
 __device__ __forceinline__ double dp_mulmod(double y, double w, double q, double qinv) {
@@ -204,7 +206,7 @@ __device__ __forceinline__ u64 d2canon(double y, double q, double qinv) {
 }
 
 // FP64 Cooley-Tukey butterfly: X' = X + T, Y' = X - T, T = Y w mod q.
-// Caller guarantees |Y| < 1.4 q (so |Y| w / q < 2^51).
+// Caller guarantees |Y| < 4 q and |w| <= (q-1)/2 (so |Y| w / q < 2^51).
 __device__ __forceinline__ void ct_bfly_dp(double& X, double& Y, double w, double q,
                                            double qinv) {
     const double t = dp_mulmod(Y, w, q, qinv);
@@ -215,8 +217,8 @@ __device__ __forceinline__ void ct_bfly_dp(double& X, double& Y, double w, doubl
 
 // One radix-2^K pass of FP64 CT stages (as ct_pass).  Inputs are reduced
 // to |x| <= q/2 + 1 at the start of the pass; stage r inputs are then below
-// (0.5 + 0.875 r) q, so stages 0 and 1 multiply directly and stage 2
-// reduces the multiplicand first.  Outputs < 3.2 q.
+// (0.5 + r) q + 1 (|T| <= q), so for K <= 4 every stage multiplies directly
+// (multiplicand < 3.5 q + 1 < 4 q).  Outputs < 4.5 q + 1.
 template <int K>
 __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0, int seg,
                                            int split, const double* __restrict__ tw,
@@ -244,7 +246,7 @@ __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0
 #pragma unroll
             for (int c = 0; c < (1 << K); ++c) {
                 if (c & half) continue;
-                if (r >= 2) x[c + half] = dp_reduce(x[c + half], q, qinv);
+                if (r >= 4) x[c + half] = dp_reduce(x[c + half], q, qinv);
                 ct_bfly_dp(x[c], x[c + half], tws[o + (c >> (K - r))], q, qinv);
             }
         }
@@ -310,7 +312,7 @@ __device__ __forceinline__ void ct_pass_cols_dp(double* sm, int arr_stride, int 
 #pragma unroll
             for (int c = 0; c < (1 << K); ++c) {
                 if (c & half) continue;
-                if (r >= 2) x[c + half] = dp_reduce(x[c + half], q, qinv);
+                if (r >= 4) x[c + half] = dp_reduce(x[c + half], q, qinv);
                 ct_bfly_dp(x[c], x[c + half], tws[o + (c >> (K - r))], q, qinv);
             }
         }
@@ -339,9 +341,10 @@ __device__ __forceinline__ void ct_all_cols_dp(double* sm, int arr_stride, int n
 
 // One radix-2^K pass of FP64 Gentleman-Sande stages over narr M-point arrays
 // (as gs_pass).  Inputs are reduced to |x| <= q/2 + 1 at the start of the
-// pass; X' = X + Y, Y' = (X - Y) w mod q.  Stage 0: |X - Y| <= q + 2;
-// stage 1: <= 2q + 4 < 2^51 (q <= 2^50 - 4): both multiply directly; stage
-// 2 reduces X - Y first.  Outputs < 4q + 8.
+// pass; X' = X + Y, Y' = (X - Y) w mod q (|Y'| <= q).  Stage v: |X - Y| <=
+// 2^v (q + 2): stages 0-2 multiply directly (4q + 8 is within dp_mulmod's
+// 4q + 8 bound with centred twiddles); stage 3 reduces X - Y first.
+// Outputs < 2^K (q/2 + 1).
 template <int K, bool RAW = false>
 __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr, int logM,
                                            int lt0, int seg, int logMfull,
@@ -381,7 +384,7 @@ __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr,
                 if (c & half) continue;
                 const double X = x[c], Y = x[c + half];
                 double u = X - Y;
-                if (v >= 2) u = dp_reduce(u, q, qinv);
+                if (v >= 3) u = dp_reduce(u, q, qinv);
                 x[c] = X + Y;
                 x[c + half] = dp_mulmod(u, tws[o + (c >> (v + 1))], q, qinv);
             }

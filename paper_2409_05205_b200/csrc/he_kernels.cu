@@ -156,10 +156,7 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
             for (int r = 0; r < (1 << S); ++r) {
                 if (r & half) continue;
                 const double w = __ldg(&tw[(1 << st) + (r >> (S - st))]);
-                if (st >= 1) {
-                    vx[r + half] = dp_reduce(vx[r + half], q, qinv);
-                    vy[r + half] = dp_reduce(vy[r + half], q, qinv);
-                }
+                // canonical inputs: stage st multiplicands < (1 + st) q < 4 q
                 ct_bfly_dp(vx[r], vx[r + half], w, q, qinv);
                 ct_bfly_dp(vy[r], vy[r + half], w, q, qinv);
             }

@@ -109,11 +109,72 @@ def test_ntt_inverse_matches_definition(he):
         assert np.array_equal(got[0, j], R.intt_def(nat, q, ctx.psi(j)))
 
 
+def extreme_residues(shape, primes, kind):
+    """Structured worst-case magnitudes, [..., L, N]: every residue q - 1,
+    q - 1 / 0 alternating, (q - 1) / 2 + (i & 1), or q - 1 - (i mod 7)."""
+    N = shape[-1]
+    q = np.array(primes, np.uint64)[:, None]
+    i = np.arange(N, dtype=np.uint64)[None, :]
+    if kind == "max":
+        v = q - 1 + 0 * i
+    elif kind == "alt":
+        v = np.where(i % 2 == 0, q - 1, 0).astype(np.uint64)
+    elif kind == "half":
+        v = (q - 1) // 2 + (i & 1)
+    else:
+        v = q - 1 - i % 7
+    return np.ascontiguousarray(np.broadcast_to(v, shape)).astype(np.uint64)
+
+
+EXTREME = ["max", "alt", "half", "ramp"]
+
+
+@pytest.mark.parametrize("N", [1024, 16384, 32768])
+def test_ntt_extreme_inputs(he, N):
+    """The FP64 transforms keep unreduced values up to 4q + 8 (centred
+    twiddles, he_internal.cuh): structured maximal inputs with the largest
+    50-bit primes still transform exactly (forward vs the definition on
+    sampled outputs; inverse round trip)."""
+    primes = RINGS[N]
+    ctx = ctx_for(he, N, primes)
+    logN = N.bit_length() - 1
+    x = np.stack([extreme_residues((len(primes), N), primes, k) for k in EXTREME])
+    d = dev(x)
+    ctx.ntt_forward(d)
+    got = u64(d)
+    rng = np.random.default_rng(7 * N)
+    pos = np.unique(np.concatenate([[0, 1, 2, N // 2, N - 1], rng.integers(0, N, 24)]))
+    ks = np.array([brv(int(p), logN) for p in pos], np.int32)
+    for b in range(len(EXTREME)):
+        for j, q in enumerate(primes):
+            assert np.array_equal(got[b, j, pos], R.ntt_def(x[b, j], q, ctx.psi(j), ks))
+    ctx.ntt_inverse(d)
+    assert np.array_equal(u64(d), x)
+
+
+@pytest.mark.parametrize("kind", EXTREME)
+def test_conv_extreme_inputs(he, kind):
+    """Config 4 layer 1 (s = 8, n_ib = 2) with structured maximal c0 and
+    extreme filter taps (+7 / -8): the whole path (forward NTT, folded MAC,
+    inverse NTT + scatter + mask) stays exact."""
+    cfg = synth.CONFIGS[4]
+    ctx = ctx_for(he, cfg.N, cfg.primes, cfg.t)
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    Ly = cfg.conv[1]
+    p = R.plan_conv(Ly, cfg.N)
+    B = 2
+    c0 = extreme_residues((B, p.n_ib, ring.L, cfg.N), ring.primes, kind)
+    W = np.where(np.arange(Ly.c_o * Ly.c_i * Ly.f_w * Ly.f_h) % 3 == 0, -8, 7)
+    W = W.reshape(Ly.c_o, Ly.c_i, Ly.f_w, Ly.f_h).astype(np.int32)
+    run_conv(he, ctx, ring, Ly, B, seed=5, c0=c0, W=W)
+
+
 # -------------------------------------------------------------- conv path
 def run_conv(he, ctx, ring, Ly, B, seed, mask=True, s_override=0,
-             ve=False, check_b=None):
+             ve=False, check_b=None, c0=None, W=None):
     """GPU: pack_input -> pack_filters -> conv -> mask_extract; oracle: the
-    same on the sampled images.  Returns the plan."""
+    same on the sampled images (c0 / W: fixed inputs instead of the seeded
+    ones).  Returns the plan."""
     N = ring.N
     plan_o = R.plan_conv(Ly, N, s_override)
     p = ctx.plan(Ly.c_i, Ly.c_o, Ly.w_i, Ly.h_i, Ly.f_w, Ly.f_h, Ly.stride,
@@ -122,8 +183,10 @@ def run_conv(he, ctx, ring, Ly, B, seed, mask=True, s_override=0,
         (plan_o.s, plan_o.c_ib, plan_o.n_ib, plan_o.c_ob, plan_o.n_ob,
          plan_o.w_o, plan_o.h_o, plan_o.n_valid)
     rng = np.random.default_rng(seed)
-    W = rng.integers(-8, 8, (Ly.c_o, Ly.c_i, Ly.f_w, Ly.f_h)).astype(np.int32)
-    c0 = synth.uniform_residues((B, p.n_ib, ring.L, N), ring.primes, seed)
+    if W is None:
+        W = rng.integers(-8, 8, (Ly.c_o, Ly.c_i, Ly.f_w, Ly.f_h)).astype(np.int32)
+    if c0 is None:
+        c0 = synth.uniform_residues((B, p.n_ib, ring.L, N), ring.primes, seed)
     phi = synth.phi1((B, p.n_ob, N), ring.t, seed) if mask else None
     fspec = ctx.pack_filters(p, dev(W))
     d_c0, d_phi = dev(c0), (dev(phi) if mask else None)
