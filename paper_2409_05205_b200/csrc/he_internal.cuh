@@ -193,6 +193,23 @@ __device__ __forceinline__ double dp_reduce(double y, double q, double qinv) {
     return fma(-k, q, y);
 }
 
+// n consecutive twiddles tw[b .. b+n) (n a power of two; b a multiple of
+// min(n, 2)): 16-byte loads, so a warp whose lanes read different runs
+// touches half as many L1 sectors per twiddle.
+__device__ __forceinline__ void load_tw_run(double* dst, const double* __restrict__ tw, int b,
+                                            int nt) {
+    if (nt == 1) {
+        dst[0] = __ldg(&tw[b]);
+    } else {
+#pragma unroll
+        for (int z = 0; z < nt; z += 2) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(tw + b + z));
+            dst[z] = v.x;
+            dst[z + 1] = v.y;
+        }
+    }
+}
+
 // exact u64 (< 2^52) <-> double
 __device__ __forceinline__ double u2d(u64 x) {
     return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 4503599627370496.0;
@@ -234,8 +251,7 @@ __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0
 #pragma unroll
         for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
             const int twb = (1 << (st0 + r)) + (seg << (st0 + r - split)) + (blk << r);
-#pragma unroll
-            for (int z = 0; z < (1 << r); ++z) tws[o + z] = __ldg(&tw[twb + z]);
+            load_tw_run(tws + o, tw, twb, 1 << r);
         }
         double x[1 << K];
 #pragma unroll
@@ -300,8 +316,7 @@ __device__ __forceinline__ void ct_pass_cols_dp(double* sm, int arr_stride, int 
 #pragma unroll
         for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
             const int twb = (1 << (st0 + r)) + (blk << r);
-#pragma unroll
-            for (int z = 0; z < (1 << r); ++z) tws[o + z] = __ldg(&tw[twb + z]);
+            load_tw_run(tws + o, tw, twb, 1 << r);
         }
         double x[1 << K];
 #pragma unroll
@@ -365,8 +380,7 @@ __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr,
             const int lt = lt0 + v;
             const int tb = (1 << (logMfull - lt - 1)) + (seg << (logM - lt - 1)) +
                            (blk << (K - 1 - v));
-#pragma unroll
-            for (int z = 0; z < (1 << (K - 1 - v)); ++z) tws[o + z] = __ldg(&tw[tb + z]);
+            load_tw_run(tws + o, tw, tb, 1 << (K - 1 - v));
         }
         double x[1 << K];
 #pragma unroll
