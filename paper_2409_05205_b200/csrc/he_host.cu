@@ -184,6 +184,10 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
         Lm.one_p = h_shoup(1, q);
         Lm.qd = (double)q;
         Lm.qinvd = 1.0 / (double)q;
+        {
+            const u64 ti = h_inv(r->t % q, q);
+            Lm.tinvd = ti > q / 2 ? -(double)(q - ti) : (double)ti;
+        }
     }
     int prev = 0;
     cudaGetDevice(&prev);

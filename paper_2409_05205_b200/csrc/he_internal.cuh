@@ -28,6 +28,7 @@ struct he_limb {
     u64 r80, r80_p;         // 2^80 mod q
     u64 one_p;              // Shoup companion of 1  (floor(2^64 / q))
     double qd, qinvd;       // q and fl(1/q) for the FP64 transforms
+    double tinvd;           // t^{-1} mod q, centred, as a double (enc_dp)
 };
 
 struct he_ctx {
@@ -208,6 +209,20 @@ __device__ __forceinline__ void load_tw_run(double* dst, const double* __restric
             dst[z + 1] = v.y;
         }
     }
+}
+
+// enc_j(m) = round(Q m / t) mod q_j without a table (R2): Q m = t X + c
+// with X = round(Q m / t) and c the centred remainder of Q m mod t, and
+// Q = 0 mod q_j, so X = -c t^{-1} mod q_j; c = r_t m mods t (r_t = Q mod t).
+// For t <= 2^20 (odd) and m < t: x = r_t m < 2^40 is exact, rint(x / t)
+// is exact (|x/t| 2^-52 << 1/(2t), and t odd has no ties), |c| <= t/2.
+// Result: an integer-valued double with |.| <= q.
+__device__ __forceinline__ double enc_dp(double md, double rtd, double td, double t_inv,
+                                         double tinvq, double q, double qinv) {
+    const double x = rtd * md;                              // exact
+    const double k = fma(x, t_inv, DP_MAGIC) - DP_MAGIC;    // rint(x / t)
+    const double c = fma(-k, td, x);                        // centred remainder
+    return dp_mulmod(-c, tinvq, q, qinv);
 }
 
 // exact u64 (< 2^52) <-> double

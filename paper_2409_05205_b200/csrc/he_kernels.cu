@@ -1416,6 +1416,13 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         int kr = jt / P.h_p, lc = jt - kr * P.h_p;
         const int dk = jstep / P.h_p, dl = jstep - dk * P.h_p;
         constexpr int EB = 8;
+        // FP64 mask encoding (enc_dp) when the context has a table (t <= 2^20):
+        // no random table gathers in the writer
+        const bool encd = DP && enc_tab != nullptr;
+        const double td = (double)t, t_inv_d = 1.0 / (double)t, rtd = (double)r_t;
+        // transform outputs < 8q + 16 when the last pass is radix-16: reduce
+        // before adding the encoding (|sum| must stay below 2^52)
+        const bool xred = (logM & 3) == 0;
         for (int j0 = jt; j0 < M; j0 += EB * jstep) {
             u32 m[EB];
             int vi[EB];
@@ -1432,6 +1439,24 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                 kr += dk;
                 lc += dl;
                 if (lc >= P.h_p) { lc -= P.h_p; ++kr; }
+            }
+            if (encd) {
+#pragma unroll
+                for (int e = 0; e < EB; ++e) {
+                    const int j = j0 + e * jstep;
+                    if (j >= M || (!orow && vi[e] < 0)) continue;
+                    double y = ph ? enc_dp(u2d(m[e]), rtd, td, t_inv_d, Lm.tinvd, Lm.qd, Lm.qinvd)
+                                  : 0.0;
+                    if (owned) {
+                        double x = reinterpret_cast<const double*>(sm)[abase + PAD(j)];
+                        if (xred) x = dp_reduce(x, Lm.qd, Lm.qinvd);
+                        y += x;
+                    }
+                    const u64 v = d2canon(y, Lm.qd, Lm.qinvd);
+                    if (orow) orow[(j << P.logs) + u] = v;
+                    if (vi[e] >= 0) crow[vi[e]] = v;
+                }
+                continue;
             }
             u64 en[EB];
 #pragma unroll

@@ -112,6 +112,27 @@ def test_encode_matches_bigint_definition():
     assert np.array_equal(R.encode(m1, ring1), R.encode_bigint(m1, ring1))
 
 
+def test_encode_centred_remainder_identity():
+    """The identity the K4 writer's FP64 mask encoding relies on (DESIGN.md
+    §6, K4): Q m = t round(Q m / t) + c with c the centred remainder of r_t m
+    mod t, and Q = 0 mod q_j, so enc_j(m) = -c t^{-1} mod q_j.  Checked
+    against the literal R2 definition (big integers) for several t."""
+    for c_idx, t in ((4, 65537), (1, 65537), (2, 257), (3, 3), (4, (1 << 20) - 3)):
+        cfg = synth.CONFIGS[c_idx]
+        ring = R.Ring(cfg.N, cfg.primes, t)
+        rng = np.random.default_rng(t)
+        m = np.unique(np.concatenate([[0, 1, t // 2, t // 2 + 1, t - 1],
+                                      rng.integers(0, t, 200)])).astype(np.uint32)
+        want = R.encode_bigint(m, ring)
+        r_t = ring.Q % t
+        for i, mv in enumerate(m):
+            rem = (r_t * int(mv)) % t
+            cen = rem - t if 2 * rem > t else rem
+            assert abs(cen) <= t // 2
+            for j, q in enumerate(ring.primes):
+                assert (-cen * pow(t, -1, q)) % q == int(want[j, i])
+
+
 def test_encode_decodes_exactly():
     # round(t * enc(m) / Q) = m: the encoding error is at most 1/2 (R2)
     for c in (1, 2, 4):
