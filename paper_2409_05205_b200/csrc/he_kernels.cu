@@ -111,6 +111,9 @@ __device__ __forceinline__ void ntt_store(u64* out, int li, int seg, int NS, int
     }
 }
 
+#ifndef HE_NTT_PF
+#define HE_NTT_PF 1
+#endif
 // FP64 variant of ntt_fwd_segment (default; HE_NTT=int selects the integer
 // one): residues as integer-valued doubles, exact FP64 butterflies
 // (he_internal.cuh), twiddles psi^{brv(k)} as doubles.
@@ -128,45 +131,53 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
     const double* tw = twd_all + (size_t)l * N;
     const u64* src = in + (size_t)li * N;
     const int end = logN - T.skip;
-    // software-pipelined loads: the next iteration's 2^S vectors are in
-    // flight while this one's register stages run
-    ulonglong2 nxt[1 << S];
-    {
-        const int i0 = 2 * threadIdx.x;
+    // software-pipelined loads: the vectors of the next PF iterations are
+    // in flight while this one's register stages run
+    constexpr int PF = HE_NTT_PF;
+    const int step = 2 * blockDim.x;
+    ulonglong2 buf[PF][1 << S];
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+        const int ip = 2 * threadIdx.x + p * step;
 #pragma unroll
         for (int r = 0; r < (1 << S); ++r)
-            if (i0 < NS) nxt[r] = *reinterpret_cast<const ulonglong2*>(src + i0 + r * NS);
+            if (ip < NS) buf[p][r] = *reinterpret_cast<const ulonglong2*>(src + ip + r * NS);
     }
-    for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
-        double vx[1 << S], vy[1 << S];
+    for (int i0 = 2 * threadIdx.x; i0 < NS; i0 += PF * step) {
 #pragma unroll
-        for (int r = 0; r < (1 << S); ++r) {
-            vx[r] = u2d(nxt[r].x);
-            vy[r] = u2d(nxt[r].y);
-        }
-        const int in_ = i + 2 * blockDim.x;
-#pragma unroll
-        for (int r = 0; r < (1 << S); ++r)
-            if (in_ < NS) nxt[r] = *reinterpret_cast<const ulonglong2*>(src + in_ + r * NS);
-#pragma unroll
-        for (int st = 0; st < S; ++st) {
-            if (st >= end) break;
-            const int half = 1 << (S - 1 - st);
+        for (int p = 0; p < PF; ++p) {
+            const int i = i0 + p * step;
+            if (i >= NS) break;
+            double vx[1 << S], vy[1 << S];
 #pragma unroll
             for (int r = 0; r < (1 << S); ++r) {
-                if (r & half) continue;
-                const double w = __ldg(&tw[(1 << st) + (r >> (S - st))]);
-                // canonical inputs: stage st multiplicands < (1 + st) q < 4 q
-                ct_bfly_dp(vx[r], vx[r + half], w, q, qinv);
-                ct_bfly_dp(vy[r], vy[r + half], w, q, qinv);
+                vx[r] = u2d(buf[p][r].x);
+                vy[r] = u2d(buf[p][r].y);
             }
-        }
-        double ox = vx[0], oy = vy[0];
+            const int in_ = i + PF * step;
 #pragma unroll
-        for (int r = 1; r < (1 << S); ++r)
-            if (r == seg) { ox = vx[r]; oy = vy[r]; }
-        sm[PAD(i)] = ox;
-        sm[PAD(i + 1)] = oy;
+            for (int r = 0; r < (1 << S); ++r)
+                if (in_ < NS) buf[p][r] = *reinterpret_cast<const ulonglong2*>(src + in_ + r * NS);
+#pragma unroll
+            for (int st = 0; st < S; ++st) {
+                if (st >= end) break;
+                const int half = 1 << (S - 1 - st);
+#pragma unroll
+                for (int r = 0; r < (1 << S); ++r) {
+                    if (r & half) continue;
+                    const double w = __ldg(&tw[(1 << st) + (r >> (S - st))]);
+                    // canonical inputs: stage st multiplicands < (1 + st) q < 4 q
+                    ct_bfly_dp(vx[r], vx[r + half], w, q, qinv);
+                    ct_bfly_dp(vy[r], vy[r + half], w, q, qinv);
+                }
+            }
+            double ox = vx[0], oy = vy[0];
+#pragma unroll
+            for (int r = 1; r < (1 << S); ++r)
+                if (r == seg) { ox = vx[r]; oy = vy[r]; }
+            sm[PAD(i)] = ox;
+            sm[PAD(i + 1)] = oy;
+        }
     }
     if (S) cg::this_cluster().sync();
     else __syncthreads();
