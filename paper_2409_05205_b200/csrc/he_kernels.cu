@@ -1273,6 +1273,204 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
 #ifndef HE_MAC_UG
 #define HE_MAC_UG 4
 #endif
+
+// ------------------------------------------------------------------ K3 (tcgen05)
+// Folded MAC on the 5th-generation tensor cores for batches of >= 128
+// images (config 5): one CTA per (limb l, group g, 128-image tile).  The
+// A operand is the 128 x K byte plane i of the image spectra, the B
+// operand the c_o x K byte plane j of the filter operand, both staged in
+// shared memory in the canonical K-major no-swizzle layout (8-row x
+// 16-byte core matrices); D_{i+j} += A_i B_j^T accumulates each of the 13
+// byte diagonals in its own TMEM region (M = 128 lanes = images, 16
+// columns per 16-channel chunk: 13 x 16 = 208 of a 256-column allocation,
+// two CTAs per SM).  One thread issues the 49 (x K/32) tcgen05.mma.kind::i8
+// per chunk and commits them to an mbarrier; then every thread owns one
+// image row (its TMEM lane) and recombines its outputs with reduce13 after
+// tcgen05.ld -- the 13 partial sums of an output sit in one lane, so no
+// cross-thread exchange is needed.
+#ifndef HE_MAC_TC_BT
+#define HE_MAC_TC_BT 128
+#endif
+__device__ __forceinline__ uint64_t tc_smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    // K-major, SWIZZLE_NONE: start >> 4 [0,14), LBO >> 4 [16,30), SBO >> 4
+    // [32,46), version 1 [46,48), base offset 0, layout type 0 [61,64)
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, int (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                   "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
+    return ok != 0;
+}
+
+// V = sum_{d<13} S_d 2^{8d} mod q from 13 diagonal sums of one output.
+__device__ __forceinline__ u64 reduce13v(const int (&S)[13], const he_limb& Lm) {
+    u64 P[4];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        P[k] = (u64)(u32)S[4 * k];
+        madw(P[k], (u32)S[4 * k + 1], 1u << 8);
+        madw(P[k], (u32)S[4 * k + 2], 1u << 16);
+        madw(P[k], (u32)S[4 * k + 3], 1u << 24);
+    }
+    P[3] = (u64)(u32)S[12];
+    const u64 lo = P[0] + (P[1] << 32);
+    const u64 hi = P[2] + (P[1] >> 32) + (P[3] << 32) + (lo < P[0] ? 1 : 0);
+    const u64 q = Lm.q;
+    const u64 r = shoup_mul(lo, 1, Lm.one_p, q) + shoup_mul(hi, Lm.r64, Lm.r64_p, q);  // < 4q
+    return csub(csub(r, 2 * q), q);
+}
+
+__global__ void __launch_bounds__(256, 2)
+k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
+         u64* __restrict__ out, int B, int L, int M, int c_o, int Kp, int Gt,
+         const he_limb* __restrict__ limbs) {
+    constexpr int BT = HE_MAC_TC_BT;           // images per CTA (= UMMA M)
+    extern __shared__ __align__(1024) unsigned char smc[];
+    const int Kt = (Kp + 31) & ~31;            // K rounded to the UMMA K step (32 bytes)
+    const int kch = Kt >> 4;                   // 16-byte K chunks per row
+    const int nrow = (c_o + 15) & ~15;         // B rows (channels), 16-column chunks
+    const uint32_t sbo = (uint32_t)kch * 128;  // bytes between 8-row core-matrix groups
+    const size_t a_plane = (size_t)BT * Kt, b_plane = (size_t)nrow * Kt;
+    unsigned char* sA = smc;                   // [7][BT rows][Kt] canonical
+    unsigned char* sB = smc + 7 * a_plane;     // [7][nrow][Kt] canonical
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t s_bar;
+    const int nGc = M;
+    const int l = blockIdx.x / nGc, g = blockIdx.x - l * nGc;
+    const int b0 = blockIdx.y * BT;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&s_tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&s_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    // ---- stage the operands (16-byte cp.async into the core-matrix layout)
+    {
+        const int gb = g / Gt, gi = g - gb * Gt;
+        const size_t plane_stride = (size_t)B * Gt * Kp;
+        const unsigned char* a0 = A + (((size_t)l * (M / Gt) + gb) * 7 * B) * Gt * Kp +
+                                  (size_t)gi * Kp;
+        const int cpr = Kt >> 4;                          // chunks per row
+        for (int e = threadIdx.x; e < 7 * BT * cpr; e += blockDim.x) {
+            const int c = e % cpr, r = (e / cpr) % BT, j = e / (cpr * BT);
+            const int b = b0 + r;
+            const bool ok = b < B && c * 16 < Kp;
+            const unsigned char* src = ok ? a0 + j * plane_stride + (size_t)b * Gt * Kp + c * 16 : A;
+            unsigned char* dst = sA + j * a_plane + (r >> 3) * sbo + c * 128 + (r & 7) * 16;
+            cp_async_n<16>(dst, src, ok);
+        }
+        const unsigned char* f0 = Fpl + (((size_t)l * M + g) * 7) * c_o * Kp;
+        for (int e = threadIdx.x; e < 7 * nrow * cpr; e += blockDim.x) {
+            const int c = e % cpr, n = (e / cpr) % nrow, j = e / (cpr * nrow);
+            const bool ok = n < c_o && c * 16 < Kp;
+            const unsigned char* src = ok ? f0 + ((size_t)j * c_o + n) * Kp + c * 16 : Fpl;
+            unsigned char* dst = sB + j * b_plane + (n >> 3) * sbo + c * 128 + (n & 7) * 16;
+            cp_async_n<16>(dst, src, ok);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = s_tmem;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+    const uint32_t sA_addr = (uint32_t)__cvta_generic_to_shared(sA);
+    const uint32_t sB_addr = (uint32_t)__cvta_generic_to_shared(sB);
+    // instruction descriptor: S32 accumulate, u8 x u8, K-major A and B,
+    // N = 16, M = BT
+    const uint32_t idesc = (2u << 4) | ((16u >> 3) << 17) | ((uint32_t)(BT >> 4) << 24);
+    const he_limb Lm = limbs[l];
+    const int quarter = warp & 3, half = warp >> 2;      // TMEM lane quarter, column half
+    const int r = quarter * 32 + lane;                   // this thread's image row
+    const int b = b0 + r;
+    const int nchunks = nrow >> 4;
+    for (int ch = 0; ch < nchunks; ++ch) {
+        if (threadIdx.x == 0) {
+            for (int ks = 0; ks < (Kt >> 5); ++ks) {
+#pragma unroll
+                for (int i = 0; i < 7; ++i) {
+                    const uint64_t ad =
+                        tc_smem_desc(sA_addr + i * (uint32_t)a_plane + ks * 256, 128, sbo);
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) {
+                        const int d = i + j;
+                        const uint64_t bd = tc_smem_desc(
+                            sB_addr + j * (uint32_t)b_plane + (ch * 2) * sbo + ks * 256, 128, sbo);
+                        // the first product into diagonal d overwrites it
+                        const uint32_t acc = (ks > 0 || i > (d > 6 ? d - 6 : 0)) ? 1u : 0u;
+                        tc_mma_i8(tmem + d * 16, ad, bd, idesc, acc);
+                    }
+                }
+            }
+            asm volatile(
+                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    bar)
+                : "memory");
+        }
+        while (!mbar_try_wait(bar, (uint32_t)(ch & 1))) {
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        // each thread: image row r, columns half*8 .. half*8+7 of the chunk
+        int Sv[13][8];
+#pragma unroll
+        for (int d = 0; d < 13; ++d)
+            tc_ld8(tmem + ((uint32_t)(quarter * 32) << 16) + d * 16 + half * 8, Sv[d]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (b < B) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int n = ch * 16 + half * 8 + e;
+                if (n >= c_o) break;
+                int S[13];
+#pragma unroll
+                for (int d = 0; d < 13; ++d) S[d] = Sv[d][e];
+                out[(((size_t)l * B + b) * c_o + n) * M + g] = reduce13v(S, Lm);
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();                       // TMEM free for the next chunk's MMAs
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    }
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+}
+
+static he_status launch_mac_tc(const unsigned char* A, const unsigned char* Fpl, u64* out, int B,
+                               int L, int M, int c_o, int Kp, const he_limb* limbs,
+                               cudaStream_t st) {
+    const int Kt = (Kp + 31) & ~31, nrow = (c_o + 15) & ~15;
+    const size_t smem = 7 * ((size_t)HE_MAC_TC_BT * Kt + (size_t)nrow * Kt);
+    if (smem > 110 * 1024) return HE_ESHAPE;
+    if (!set_smem(k_mac_tc, smem)) return HE_ECUDA;
+    dim3 grid(L * M, (B + HE_MAC_TC_BT - 1) / HE_MAC_TC_BT);
+    k_mac_tc<<<grid, 256, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, tile_gt(M), limbs);
+    return HE_OK;
+}
+
 static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fpl, u64* out,
                                  int B, int n_ib, int L, int logN, int logs, int c_o,
                                  const he_limb* limbs, cudaStream_t st, int Ku) {
@@ -1280,6 +1478,15 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
     const int Kp = imma_kp(K);
     const int nrow = (c_o + 7) & ~7, nnt = nrow / 8;
     if (nnt > 32) return HE_ESHAPE;                       // c_o <= 256
+    {
+        // batches of >= 128 images: tcgen05 MAC (HE_MAC_TC=0 disables, =1 forces)
+        const char* e = getenv("HE_MAC_TC");
+        const int mode = e ? atoi(e) : 2;
+        const int Kt = (Kp + 31) & ~31, nr16 = (c_o + 15) & ~15;
+        const bool fits = 7 * ((size_t)HE_MAC_TC_BT * Kt + (size_t)nr16 * Kt) <= 110 * 1024;
+        if (fits && (mode == 1 || (mode == 2 && B >= HE_MAC_TC_BT)))
+            return launch_mac_tc(A, Fpl, out, B, L, M, c_o, Kp, limbs, st);
+    }
     const int Gt = tile_gt(M);
     // per staging buffer; the K = 16 small-CTA case targets 5 CTAs per SM
     const bool k16c = Kp == 16 && HE_MAC_K16_MINB > 1;

@@ -599,6 +599,21 @@ def test_conv_in_bench_launch_configuration(he):
             assert np.array_equal(u64(j["comp"])[b], R.compact(ref, plan)[0]), j["li"]
 
 
+@pytest.mark.parametrize("case", SMALL + [
+    (synth.ConvLayer(16, 24, 5, 5), 1024, 0, 130),        # two 128-image tiles, ragged
+    (synth.ConvLayer(64, 64, 8, 8), 8192, 0, 129)],        # K = 64, c_o = 64
+    ids=lambda c: f"{c[0]}-N{c[1]}-B{c[3]}")
+def test_conv_tcgen05_mac_path(he, case, monkeypatch):
+    """The tcgen05 MAC (k_mac_tc, the default for >= 128 images) forced on
+    every shape, including batches below one 128-image tile."""
+    monkeypatch.setenv("HE_MAC_TC", "1")
+    Ly, N, so, B = case
+    ring = R.Ring(N, RINGS[N] if N in RINGS else synth.PRIMES_N8192[:2], 65537)
+    ctx = ctx_for(he, N, ring.primes)
+    check = list(range(B)) if B <= 8 else [0, 1, B // 2, B - 2, B - 1]
+    run_conv(he, ctx, ring, Ly, B, seed=B + N, s_override=so, check_b=check)
+
+
 def test_conv_wide_layer_over_256_channels(he):
     """c_o > 256: the IMAD MAC path (the tensor-core kernel keeps all of a
     group's output channels in one CTA); n_ob > 1 blocks, bit-exact."""
