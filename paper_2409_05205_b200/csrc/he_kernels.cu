@@ -326,7 +326,7 @@ k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int 
         }
     }
     __syncthreads();
-    ct_all_cols_dp<3>(sm, stride, C, Tn, tw, q, qinv);
+    ct_all_cols_dp<4>(sm, stride, C, Tn, tw, q, qinv);
     if (OUT_FMT == 2) {
         unsigned char* A = reinterpret_cast<unsigned char*>(out);
         const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
