@@ -380,7 +380,7 @@ __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr,
                                            int lt0, int seg, int logMfull,
                                            const double* __restrict__ tw, double q,
                                            double qinv) {
-    // RAW: the arrays still hold u64 residues (< 2^52) as loaded by cp.async
+    // RAW: the arrays still hold u64 residues (< 4q < 2^52) as loaded by cp.async
     const int tk = 1 << lt0;
     const int gper = 1 << (logM - K);
     const int total = narr * gper;
@@ -402,8 +402,9 @@ __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr,
         for (int c = 0; c < (1 << K); ++c) {
             const double v = RAW ? u2d(reinterpret_cast<const u64*>(s)[PAD(base + (c << lt0))])
                                  : s[PAD(base + (c << lt0))];
-            // canonical raw input: centre into (-q/2, q/2] instead of reducing
-            x[c] = RAW ? (v > 0.5 * q ? v - q : v) : dp_reduce(v, q, qinv);
+            // raw inputs are lazy residues in [0, 4q) (the MAC's output):
+            // dp_reduce brings every input to |x| <= q/2 + 1
+            x[c] = dp_reduce(v, q, qinv);
         }
 #pragma unroll
         for (int v = 0, o = 0; v < K; o += (1 << (K - 1 - v)), ++v) {

@@ -1071,7 +1071,8 @@ __device__ __forceinline__ void mma_k16(int (&d)[4], u32 a0, u32 a1, u32 b0) {
 // 32-bit-aligned partial sums P_k = sum_{d = 4k..4k+3} S_d 2^{8(d-4k)}
 // (< 2^57, three mad.wide each): V = P0 + P1 2^32 + P2 2^64 + P3 2^96 =
 // lo + hi 2^64, then V mod q = lo + hi (2^64 mod q) with two Shoup products.
-__device__ __forceinline__ u64 reduce13(const int (&acc)[13][4], int e, const he_limb& Lm) {
+__device__ __forceinline__ u64 reduce13(const int (&acc)[13][4], int e, const he_limb& Lm,
+                                        bool lazy) {
     u64 P[4];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -1085,7 +1086,28 @@ __device__ __forceinline__ u64 reduce13(const int (&acc)[13][4], int e, const he
     const u64 hi = P[2] + (P[1] >> 32) + (P[3] << 32) + (lo < P[0] ? 1 : 0);
     const u64 q = Lm.q;
     const u64 r = shoup_mul(lo, 1, Lm.one_p, q) + shoup_mul(hi, Lm.r64, Lm.r64_p, q);  // < 4q
-    return csub(csub(r, 2 * q), q);
+    return lazy ? r : csub(csub(r, 2 * q), q);
+}
+
+// reduce13 for K <= 16 (S_d < 7 * 16 * 255^2 < 2^23): the pairs
+// S_{2m} + 2^8 S_{2m+1} fit 32 bits, so each P_k takes two 32-bit IMADs and
+// one IMAD.WIDE instead of three IMAD.WIDE.
+__device__ __forceinline__ u64 reduce13_k16(const int (&acc)[13][4], int e, const he_limb& Lm,
+                                            bool lazy) {
+    u64 P[4];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const u32 a = (u32)acc[4 * k][e] + ((u32)acc[4 * k + 1][e] << 8);
+        const u32 b = (u32)acc[4 * k + 2][e] + ((u32)acc[4 * k + 3][e] << 8);
+        P[k] = a;
+        madw(P[k], b, 1u << 16);
+    }
+    P[3] = (u64)(u32)acc[12][e];
+    const u64 lo = P[0] + (P[1] << 32);
+    const u64 hi = P[2] + (P[1] >> 32) + (P[3] << 32) + (lo < P[0] ? 1 : 0);
+    const u64 q = Lm.q;
+    const u64 r = shoup_mul(lo, 1, Lm.one_p, q) + shoup_mul(hi, Lm.r64, Lm.r64_p, q);  // < 4q
+    return lazy ? r : csub(csub(r, 2 * q), q);
 }
 
 // x / d for 0 <= x < 2^31 with d fixed per kernel: a shift when d is a power
@@ -1127,7 +1149,7 @@ template <int TB16, int MINB = 1>
 __global__ void __launch_bounds__(MINB > 1 ? 128 : 512, MINB)
 k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
            u64* __restrict__ out, int B, int L, int M, int c_o, int Kp, int G, int GS,
-           int KC, int Gt, int nbuf, const he_limb* __restrict__ limbs) {
+           int KC, int Gt, int nbuf, const he_limb* __restrict__ limbs, int lazy) {
     extern __shared__ u32 sm32[];
     constexpr int rows = 16 * TB16;
     const int nrow = (c_o + 7) & ~7, nnt = nrow >> 3;
@@ -1259,7 +1281,8 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
                     const int b = b0 + bt * 16 + gq + 8 * (e >> 1);
                     const int n = nt * 8 + 2 * tq + (e & 1);
                     if (b < B && n < c_o)
-                        out[(((size_t)l * B + b) * c_o + n) * M + g] = reduce13(acc, e, Lm);
+                        out[(((size_t)l * B + b) * c_o + n) * M + g] =
+                            MINB > 1 ? reduce13_k16(acc, e, Lm, lazy) : reduce13(acc, e, Lm, lazy);
                 }
             }
         }
@@ -1320,7 +1343,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
 }
 
 // V = sum_{d<13} S_d 2^{8d} mod q from 13 diagonal sums of one output.
-__device__ __forceinline__ u64 reduce13v(const int (&S)[13], const he_limb& Lm) {
+__device__ __forceinline__ u64 reduce13v(const int (&S)[13], const he_limb& Lm, bool lazy) {
     u64 P[4];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -1334,13 +1357,13 @@ __device__ __forceinline__ u64 reduce13v(const int (&S)[13], const he_limb& Lm) 
     const u64 hi = P[2] + (P[1] >> 32) + (P[3] << 32) + (lo < P[0] ? 1 : 0);
     const u64 q = Lm.q;
     const u64 r = shoup_mul(lo, 1, Lm.one_p, q) + shoup_mul(hi, Lm.r64, Lm.r64_p, q);  // < 4q
-    return csub(csub(r, 2 * q), q);
+    return lazy ? r : csub(csub(r, 2 * q), q);
 }
 
 __global__ void __launch_bounds__(256, 2)
 k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
          u64* __restrict__ out, int B, int L, int M, int c_o, int Kp, int Gt,
-         const he_limb* __restrict__ limbs) {
+         const he_limb* __restrict__ limbs, int lazy) {
     constexpr int BT = HE_MAC_TC_BT;           // images per CTA (= UMMA M)
     extern __shared__ __align__(1024) unsigned char smc[];
     const int Kt = (Kp + 31) & ~31;            // K rounded to the UMMA K step (32 bytes)
@@ -1448,7 +1471,7 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
                 int S[13];
 #pragma unroll
                 for (int d = 0; d < 13; ++d) S[d] = Sv[d][e];
-                out[(((size_t)l * B + b) * c_o + n) * M + g] = reduce13v(S, Lm);
+                out[(((size_t)l * B + b) * c_o + n) * M + g] = reduce13v(S, Lm, lazy);
             }
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -1461,19 +1484,21 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
 
 static he_status launch_mac_tc(const unsigned char* A, const unsigned char* Fpl, u64* out, int B,
                                int L, int M, int c_o, int Kp, const he_limb* limbs,
-                               cudaStream_t st) {
+                               cudaStream_t st, int lazy) {
     const int Kt = (Kp + 31) & ~31, nrow = (c_o + 15) & ~15;
     const size_t smem = 7 * ((size_t)HE_MAC_TC_BT * Kt + (size_t)nrow * Kt);
     if (smem > 110 * 1024) return HE_ESHAPE;
     if (!set_smem(k_mac_tc, smem)) return HE_ECUDA;
     dim3 grid(L * M, (B + HE_MAC_TC_BT - 1) / HE_MAC_TC_BT);
-    k_mac_tc<<<grid, 256, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, tile_gt(M), limbs);
+    k_mac_tc<<<grid, 256, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, tile_gt(M), limbs, lazy);
     return HE_OK;
 }
 
+// lazy: outputs in [0, 4q) instead of canonical (the FP64 inverse in K4
+// reduces its raw inputs anyway)
 static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fpl, u64* out,
                                  int B, int n_ib, int L, int logN, int logs, int c_o,
-                                 const he_limb* limbs, cudaStream_t st, int Ku) {
+                                 const he_limb* limbs, cudaStream_t st, int Ku, int lazy) {
     const int M = (1 << logN) >> logs, K = n_ib * Ku;
     const int Kp = imma_kp(K);
     const int nrow = (c_o + 7) & ~7, nnt = nrow / 8;
@@ -1485,7 +1510,7 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
         const int Kt = (Kp + 31) & ~31, nr16 = (c_o + 15) & ~15;
         const bool fits = 7 * ((size_t)HE_MAC_TC_BT * Kt + (size_t)nr16 * Kt) <= 110 * 1024;
         if (fits && (mode == 1 || (mode == 2 && B >= HE_MAC_TC_BT)))
-            return launch_mac_tc(A, Fpl, out, B, L, M, c_o, Kp, limbs, st);
+            return launch_mac_tc(A, Fpl, out, B, L, M, c_o, Kp, limbs, st, lazy);
     }
     const int Gt = tile_gt(M);
     // per staging buffer; the K = 16 small-CTA case targets 5 CTAs per SM
@@ -1535,7 +1560,8 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
                        : (k16 ? k_mac_imma<1, HE_MAC_K16_MINB> : k_mac_imma<1>);
     if (!set_smem(k, smem)) return HE_ECUDA;
     dim3 grid(L * ((M + G - 1) / G), (B + rows - 1) / rows);
-    k<<<grid, 32 * warps, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, G, GS, KC, Gt, nbuf, limbs);
+    k<<<grid, 32 * warps, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, G, GS, KC, Gt, nbuf, limbs,
+                                      lazy);
     return HE_OK;
 }
 
@@ -1778,7 +1804,8 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     rec(ev, 1, st);
     if (imma)
         s = launch_mac_imma((const unsigned char*)spec, (const unsigned char*)d_fspec, fold, B,
-                            P.n_ib, c->L, c->logN, P.logs, P.c_o, c->d_limb, st, P.Ku);
+                            P.n_ib, c->L, c->logN, P.logs, P.c_o, c->d_limb, st, P.Ku,
+                            c->ntt_mode == 0);
     else
         s = launch_mac(spec, (const u64*)d_fspec, fold, B, P.n_ib, c->L, c->logN, P.logs,
                        P.c_o, c->d_limb, st, P.Ku);
