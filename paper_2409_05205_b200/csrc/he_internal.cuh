@@ -229,6 +229,13 @@ __device__ __forceinline__ double enc_dp(double md, double rtd, double td, doubl
 __device__ __forceinline__ double u2d(u64 x) {
     return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 4503599627370496.0;
 }
+// integer-valued |y| < 2^52 -> a residue congruent to y in [q/2 - 1, 3q/2 + 1]
+// (not canonical: for the int8 MAC operand, whose byte split takes any
+// value below 2^56)
+__device__ __forceinline__ u64 d2lazy(double y, double q, double qinv) {
+    const double r = dp_reduce(y, q, qinv) + q;
+    return (u64)(__double_as_longlong(r + 4503599627370496.0) & 0xFFFFFFFFFFFFFull);
+}
 // integer-valued |y| < 2^51 -> canonical residue in [0, q)
 __device__ __forceinline__ u64 d2canon(double y, double q, double qinv) {
     double r = dp_reduce(y, q, qinv);

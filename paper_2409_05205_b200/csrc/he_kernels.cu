@@ -183,7 +183,10 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
     else __syncthreads();
     ct_all_dp<RM>(sm, logN, NS, seg, S, tw, q, qinv, end);    // outputs < 4 q
     ntt_store<OUT_FMT>(out, li, seg, NS, N, L, l, T,
-                       [&](int i) { return d2canon(sm[PAD(i)], q, qinv); });
+                       [&](int i) {
+                           return OUT_FMT == 2 ? d2lazy(sm[PAD(i)], q, qinv)
+                                               : d2canon(sm[PAD(i)], q, qinv);
+                       });
 }
 
 template <int S, int OUT_FMT>
@@ -338,7 +341,7 @@ k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int 
             const int k = e / nq, c = (e - k * nq) * 4;
             u64 x[4];
 #pragma unroll
-            for (int z = 0; z < 4; ++z) x[z] = d2canon(sm[(c + z) * stride + PAD(k)], q, qinv);
+            for (int z = 0; z < 4; ++z) x[z] = d2lazy(sm[(c + z) * stride + PAD(k)], q, qinv);
             u32 pl[8];
             byte_transpose4((u32)x[0], (u32)x[1], (u32)x[2], (u32)x[3], pl[0], pl[1], pl[2], pl[3]);
             byte_transpose4((u32)(x[0] >> 32), (u32)(x[1] >> 32), (u32)(x[2] >> 32),
