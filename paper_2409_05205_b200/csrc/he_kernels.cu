@@ -839,7 +839,6 @@ extern "C" he_status he_pack_filters(const he_ctx* c, const he_conv_plan* p,
 // layout of he_pack_filters (times N^{-1}).
 static he_status finish_filter_spectra(const he_ctx* c, const PlanDev& P, u64* ws,
                                        uint64_t* d_fspec, cudaStream_t st) {
-    const long total = (long)P.c_o * P.n_ib * c->L * c->N;
     // incomplete forward transform: the first log2(N/s) stages only
     he_status s = launch_ntt_fwd(c, ws, ws, (long)P.c_o * P.n_ib * c->L, 0, st,
                                  TileLay{1, 1, 0, 16, 1, P.logs, 0});
