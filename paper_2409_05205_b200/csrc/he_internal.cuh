@@ -320,7 +320,7 @@ __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg,
 // the N-point twiddles of stage st and block k >> (T - st).  One radix-2^K
 // pass over narr column arrays (arr_stride words apart) in shared memory;
 // value bounds as ct_pass_dp.
-template <int K>
+template <int K, bool RAW = false>
 __device__ __forceinline__ void ct_pass_cols_dp(double* sm, int arr_stride, int narr, int T,
                                                 int st0, const double* __restrict__ tw,
                                                 double q, double qinv) {
@@ -342,7 +342,11 @@ __device__ __forceinline__ void ct_pass_cols_dp(double* sm, int arr_stride, int 
         }
         double x[1 << K];
 #pragma unroll
-        for (int c = 0; c < (1 << K); ++c) x[c] = dp_reduce(s[PAD(base + (c << ltk))], q, qinv);
+        for (int c = 0; c < (1 << K); ++c)
+            // RAW: canonical u64 residues as copied by cp.async (< q: stage r
+            // multiplicands stay below (1 + r) q <= 4q without a reduction)
+            x[c] = RAW ? u2d(reinterpret_cast<const u64*>(s)[PAD(base + (c << ltk))])
+                       : dp_reduce(s[PAD(base + (c << ltk))], q, qinv);
 #pragma unroll
         for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
             const int half = 1 << (K - 1 - r);
@@ -358,16 +362,20 @@ __device__ __forceinline__ void ct_pass_cols_dp(double* sm, int arr_stride, int 
     }
 }
 
-template <int RMAX>
+template <int RMAX, bool RAW = false>
 __device__ __forceinline__ void ct_all_cols_dp(double* sm, int arr_stride, int narr, int T,
                                                const double* tw, double q, double qinv) {
     int st = 0;
     const int rem = T % RMAX;
     if (rem) {
-        if (rem == 1) ct_pass_cols_dp<1>(sm, arr_stride, narr, T, st, tw, q, qinv);
-        else if (rem == 2) ct_pass_cols_dp<2>(sm, arr_stride, narr, T, st, tw, q, qinv);
-        else ct_pass_cols_dp<3>(sm, arr_stride, narr, T, st, tw, q, qinv);
+        if (rem == 1) ct_pass_cols_dp<1, RAW>(sm, arr_stride, narr, T, st, tw, q, qinv);
+        else if (rem == 2) ct_pass_cols_dp<2, RAW>(sm, arr_stride, narr, T, st, tw, q, qinv);
+        else ct_pass_cols_dp<3, RAW>(sm, arr_stride, narr, T, st, tw, q, qinv);
         st += rem;
+        __syncthreads();
+    } else if (RAW && T > 0) {
+        ct_pass_cols_dp<RMAX, true>(sm, arr_stride, narr, T, st, tw, q, qinv);
+        st += RMAX;
         __syncthreads();
     }
     for (; st < T; st += RMAX) {
@@ -375,6 +383,7 @@ __device__ __forceinline__ void ct_all_cols_dp(double* sm, int arr_stride, int n
         __syncthreads();
     }
 }
+
 
 // One radix-2^K pass of FP64 Gentleman-Sande stages over narr M-point arrays
 // (as gs_pass).  Inputs are reduced to |x| <= q/2 + 1 at the start of the

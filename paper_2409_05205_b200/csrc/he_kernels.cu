@@ -58,6 +58,21 @@ static inline int ntt_threads(int NS) { return std::min(512, std::max(16, NS / 1
 // with zeros in [K, Kp) of every row: a (plane, image) row holds Gt
 // consecutive groups, so a limb writes runs of Gt*s bytes (n_ib = 1) and the
 // int8 MAC stages each operand tile as contiguous blocks.
+// cp.async helpers (Ampere-style async copies, used by several kernels)
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int NW>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NW)); }
+template <int CHUNK>
+__device__ __forceinline__ void cp_async_n(void* smem_dst, const void* gsrc, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    if (CHUNK == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc),
+                     "r"(valid ? 16 : 0));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(gsrc),
+                     "n"(CHUNK), "r"(valid ? CHUNK : 0));
+}
+
 struct TileLay {
     int B, n_ib, logs, Kp, Gt;
     int skip;       // trailing stages not run: log2(s) for the fold (0 = full)
@@ -316,21 +331,22 @@ k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int 
     const double* tw = twd_all + (size_t)l * N;
     const u64* src = in + (size_t)li * N + c0;
     const int tot = M << logC;
-    for (int base = threadIdx.x; base < tot; base += 4 * blockDim.x) {    // 4 loads in flight
-        u64 v[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int idx = base + e * blockDim.x;
-            v[e] = idx < tot ? src[(size_t)(idx >> logC) * s + (idx & (C - 1))] : 0;
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int idx = base + e * blockDim.x;
-            if (idx < tot) sm[(idx & (C - 1)) * stride + PAD(idx >> logC)] = u2d(v[e]);
-        }
-    }
+    // the whole tile in flight at once: 8-byte cp.async of the raw residues
+    // into the padded column arrays; the first pass converts them
+    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x)
+        cp_async_n<8>(sm_raw + (idx & (C - 1)) * stride + PAD(idx >> logC),
+                      src + (size_t)(idx >> logC) * s + (idx & (C - 1)), true);
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
-    ct_all_cols_dp<4>(sm, stride, C, Tn, tw, q, qinv);
+    if (Tn == 0) {                           // no stage: convert in place
+        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+            const int a = (idx & (C - 1)) * stride + PAD(idx >> logC);
+            sm[a] = u2d(sm_raw[a]);
+        }
+        __syncthreads();
+    }
+    ct_all_cols_dp<4, true>(sm, stride, C, Tn, tw, q, qinv);
     if (OUT_FMT == 2) {
         unsigned char* A = reinterpret_cast<unsigned char*>(out);
         const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
@@ -891,9 +907,6 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc),
                  "r"(valid ? 8 : 0));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int NW>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NW)); }
 
 template <int TNT>
 struct MacTile {
@@ -1129,16 +1142,6 @@ struct FastDiv {
     __device__ __forceinline__ int div(int x) const { return p2 ? (x >> sh) : (x / d); }
 };
 
-template <int CHUNK>
-__device__ __forceinline__ void cp_async_n(void* smem_dst, const void* gsrc, bool valid) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-    if (CHUNK == 16)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc),
-                     "r"(valid ? 16 : 0));
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(gsrc),
-                     "n"(CHUNK), "r"(valid ? CHUNK : 0));
-}
 
 // CTA = (limb l, G consecutive groups, 16*TB16-image tile); one warp per
 // 16 x 8 output tile (bt, nt).  Work proceeds in "units" (GS groups x a
