@@ -1366,6 +1366,9 @@ __device__ __forceinline__ u64 reduce13v(const int (&S)[13], const he_limb& Lm, 
     return lazy ? r : csub(csub(r, 2 * q), q);
 }
 
+// TMEM budget: 256 columns per CTA, and 128 registers x 256 threads cap the
+// kernel at two CTAs per SM (512 columns, the whole TMEM), so an allocation
+// never waits on another CTA of this kernel; no other kernel uses TMEM.
 __global__ void __launch_bounds__(256, 2)
 k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
          u64* __restrict__ out, int B, int L, int M, int c_o, int Kp, int Gt,
