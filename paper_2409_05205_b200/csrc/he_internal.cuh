@@ -188,7 +188,8 @@ __device__ __forceinline__ double dp_mulmod(double y, double w, double q, double
     return fma(-k, q, p) + e;
 }
 
-// |result| <= q/2 + 1 for |y| < 2^51.
+// |result| <= q/2 + 2 for integer-valued |y| < 2^53 (k = rint(y qinv) is
+// within 0.5 + 2^-49 of y / q).
 __device__ __forceinline__ double dp_reduce(double y, double q, double qinv) {
     const double k = fma(y, qinv, DP_MAGIC) - DP_MAGIC;
     return fma(-k, q, y);
@@ -236,11 +237,10 @@ __device__ __forceinline__ u64 d2lazy(double y, double q, double qinv) {
     const double r = dp_reduce(y, q, qinv) + q;
     return (u64)(__double_as_longlong(r + 4503599627370496.0) & 0xFFFFFFFFFFFFFull);
 }
-// integer-valued |y| < 2^51 -> canonical residue in [0, q)
+// integer-valued |y| < 2^53 -> canonical residue in [0, q)
 __device__ __forceinline__ u64 d2canon(double y, double q, double qinv) {
-    double r = dp_reduce(y, q, qinv);
-    r = r < 0.0 ? r + q : r;
-    r = r >= q ? r - q : r;
+    double r = dp_reduce(y, q, qinv);       // |r| <= q/2 + 2 < q
+    r = r < 0.0 ? r + q : r;                // one conditional add suffices
     return (u64)(__double_as_longlong(r + 4503599627370496.0) & 0xFFFFFFFFFFFFFull);
 }
 
