@@ -1586,7 +1586,7 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
 // of the row is written exactly once, in contiguous runs of u1 - u0 words.
 // Channel arrays sit in shared memory at an odd word stride (conflict-free).
 template <bool DP>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, 4)
 k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                u64* __restrict__ out, u64* __restrict__ comp, PlanDev P, int B, int L,
                int logN, int cc, int nchunk, int stride, const he_limb* __restrict__ limbs,
