@@ -419,8 +419,10 @@ __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr,
             const double v = RAW ? u2d(reinterpret_cast<const u64*>(s)[PAD(base + (c << lt0))])
                                  : s[PAD(base + (c << lt0))];
             // raw inputs are lazy residues in [0, 4q) (the MAC's output):
-            // dp_reduce brings every input to |x| <= q/2 + 1
-            x[c] = dp_reduce(v, q, qinv);
+            // stage 0 multiplies X - Y (|.| < 4q) directly and reduces only
+            // its sums, after which the bounds below hold as for reduced
+            // inputs; other passes reduce every input to |x| <= q/2 + 2
+            x[c] = RAW ? v : dp_reduce(v, q, qinv);
         }
 #pragma unroll
         for (int v = 0, o = 0; v < K; o += (1 << (K - 1 - v)), ++v) {
@@ -431,7 +433,7 @@ __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr,
                 const double X = x[c], Y = x[c + half];
                 double u = X - Y;
                 if (v >= 3) u = dp_reduce(u, q, qinv);
-                x[c] = X + Y;
+                x[c] = (RAW && v == 0) ? dp_reduce(X + Y, q, qinv) : X + Y;
                 x[c + half] = dp_mulmod(u, tws[o + (c >> (v + 1))], q, qinv);
             }
         }
