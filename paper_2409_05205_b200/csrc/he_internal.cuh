@@ -258,7 +258,7 @@ __device__ __forceinline__ void ct_bfly_dp(double& X, double& Y, double w, doubl
 // to |x| <= q/2 + 1 at the start of the pass; stage r inputs are then below
 // (0.5 + r) q + 1 (|T| <= q), so for K <= 4 every stage multiplies directly
 // (multiplicand < 3.5 q + 1 < 4 q).  Outputs < 4.5 q + 1.
-template <int K>
+template <int K, bool NORED = false>
 __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0, int seg,
                                            int split, const double* __restrict__ tw,
                                            double q, double qinv) {
@@ -277,7 +277,9 @@ __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0
         }
         double x[1 << K];
 #pragma unroll
-        for (int c = 0; c < (1 << K); ++c) x[c] = dp_reduce(sm[PAD(base + (c << ltk))], q, qinv);
+        for (int c = 0; c < (1 << K); ++c)
+            x[c] = NORED ? sm[PAD(base + (c << ltk))]
+                         : dp_reduce(sm[PAD(base + (c << ltk))], q, qinv);
 #pragma unroll
         for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
             const int half = 1 << (K - 1 - r);
@@ -301,11 +303,21 @@ __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg,
     int st = split;
     if (st >= end) return;
     const int rem = (end - split) % RMAX;
+    // the first pass reads the register stages' outputs: canonical inputs
+    // plus at most `split` added |T| <= q, so its stage-r multiplicands stay
+    // below (1 + split + r) q <= 4q when split + K <= 4 -- no reduction
     if (rem) {
-        if (rem == 1) ct_pass_dp<1>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        const bool nr = split + rem <= 4;
+        if (rem == 1) ct_pass_dp<1, true>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        else if (rem == 2 && nr) ct_pass_dp<2, true>(sm, logN, NS, st, seg, split, tw, q, qinv);
         else if (rem == 2) ct_pass_dp<2>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        else if (nr) ct_pass_dp<3, true>(sm, logN, NS, st, seg, split, tw, q, qinv);
         else ct_pass_dp<3>(sm, logN, NS, st, seg, split, tw, q, qinv);
         st += rem;
+        __syncthreads();
+    } else if (split + RMAX <= 4) {
+        ct_pass_dp<RMAX, true>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        st += RMAX;
         __syncthreads();
     }
     for (; st < end; st += RMAX) {
