@@ -1004,6 +1004,10 @@ def main():
                        "parallelism": f"dp{world} (batch-sharded, no collective)",
                        "streams": nstr, "overlap": args.overlap,
                        "cuda_graph": graph is not None,
+                       "mac": ("tcgen05.mma kind::i8, TMEM accumulators (k_mac_tc)"
+                               if (B >= 128 and os.environ.get("HE_MAC_TC", "2") != "0")
+                               or os.environ.get("HE_MAC_TC") == "1"
+                               else "mma.sync int8 byte planes (k_mac_imma)"),
                        "l2": "inputs larger than L2 (>1 GB touched per step)"},
             "ms_per_plain20_image": ms_step / B if cfg.idx == 4 else None,
             "sequential_ms_per_step": ms_seq,
