@@ -1440,29 +1440,32 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
     const int r = quarter * 32 + lane;                   // this thread's image row
     const int b = b0 + r;
     const int nchunks = nrow >> 4;
-    for (int ch = 0; ch < nchunks; ++ch) {
-        if (threadIdx.x == 0) {
-            for (int ks = 0; ks < (Kt >> 5); ++ks) {
+    // chunk ch's MMAs run while the threads recombine chunk ch - 1: once a
+    // chunk's partial sums are in registers the TMEM region is reissued
+    auto issue = [&](int ch) {
+        for (int ks = 0; ks < (Kt >> 5); ++ks) {
 #pragma unroll
-                for (int i = 0; i < 7; ++i) {
-                    const uint64_t ad =
-                        tc_smem_desc(sA_addr + i * (uint32_t)a_plane + ks * 256, 128, sbo);
+            for (int i = 0; i < 7; ++i) {
+                const uint64_t ad =
+                    tc_smem_desc(sA_addr + i * (uint32_t)a_plane + ks * 256, 128, sbo);
 #pragma unroll
-                    for (int j = 0; j < 7; ++j) {
-                        const int d = i + j;
-                        const uint64_t bd = tc_smem_desc(
-                            sB_addr + j * (uint32_t)b_plane + (ch * 2) * sbo + ks * 256, 128, sbo);
-                        // the first product into diagonal d overwrites it
-                        const uint32_t acc = (ks > 0 || i > (d > 6 ? d - 6 : 0)) ? 1u : 0u;
-                        tc_mma_i8(tmem + d * 16, ad, bd, idesc, acc);
-                    }
+                for (int j = 0; j < 7; ++j) {
+                    const int d = i + j;
+                    const uint64_t bd = tc_smem_desc(
+                        sB_addr + j * (uint32_t)b_plane + (ch * 2) * sbo + ks * 256, 128, sbo);
+                    // the first product into diagonal d overwrites it
+                    const uint32_t acc = (ks > 0 || i > (d > 6 ? d - 6 : 0)) ? 1u : 0u;
+                    tc_mma_i8(tmem + d * 16, ad, bd, idesc, acc);
                 }
             }
-            asm volatile(
-                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                    bar)
-                : "memory");
         }
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                bar)
+            : "memory");
+    };
+    if (threadIdx.x == 0) issue(0);
+    for (int ch = 0; ch < nchunks; ++ch) {
         while (!mbar_try_wait(bar, (uint32_t)(ch & 1))) {
         }
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -1472,6 +1475,10 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
         for (int d = 0; d < 13; ++d)
             tc_ld8(tmem + ((uint32_t)(quarter * 32) << 16) + d * 16 + half * 8, Sv[d]);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();                       // every lane read: TMEM free for chunk ch + 1
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        if (threadIdx.x == 0 && ch + 1 < nchunks) issue(ch + 1);
         if (b < B) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
@@ -1483,9 +1490,6 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
                 out[(((size_t)l * B + b) * c_o + n) * M + g] = reduce13v(S, Lm, lazy);
             }
         }
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        __syncthreads();                       // TMEM free for the next chunk's MMAs
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     }
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
