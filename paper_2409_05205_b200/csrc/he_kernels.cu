@@ -1660,7 +1660,8 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     // Row writer.  Thread (uo, jt) owns slot column u = u0 + uo of every
     // group j = jt, jt + jstep, ...: its channel, ownership and smem base are
     // per-thread constants, and the (row, column) of j for the payload test
-    // are advanced incrementally.  Four phi1 / table loads in flight.
+    // are advanced incrementally.  Eight phi1 loads in flight; the mask encoding is
+    // FP64 arithmetic (enc_dp) when the context has a table-sized t.
     const int jstep = blockDim.x / w;
     const int uo = threadIdx.x % w, jt = threadIdx.x / w;
     if (jstep > 0 && jt < jstep) {
