@@ -1660,7 +1660,7 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     // Row writer.  Thread (uo, jt) owns slot column u = u0 + uo of every
     // group j = jt, jt + jstep, ...: its channel, ownership and smem base are
     // per-thread constants, and the (row, column) of j for the payload test
-    // are advanced incrementally.  Eight phi1 loads in flight; the mask encoding is
+    // are advanced incrementally.  Four phi1 loads in flight; the mask encoding is
     // FP64 arithmetic (enc_dp) when the context has a table-sized t.
     const int jstep = blockDim.x / w;
     const int uo = threadIdx.x % w, jt = threadIdx.x / w;
@@ -1673,7 +1673,7 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         // j = kr * h_p + lc, tracked incrementally
         int kr = jt / P.h_p, lc = jt - kr * P.h_p;
         const int dk = jstep / P.h_p, dl = jstep - dk * P.h_p;
-        constexpr int EB = 8;
+        constexpr int EB = 4;
         // FP64 mask encoding (enc_dp) when the context has a table (t <= 2^20):
         // no random table gathers in the writer
         const bool encd = DP && enc_tab != nullptr;
