@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["plain20", "cfg5", "cfg3"],
                     default="plain20")
-    ap.add_argument("--streams", type=int, default=4,
+    ap.add_argument("--streams", type=int, default=6,
                     help="split every layer's image batch into this many "
                          "sub-batches, each on its own CUDA stream (1 = one launch "
                          "sequence per layer)")
