@@ -541,8 +541,9 @@ def test_conv_column_ntt_forced(he, monkeypatch):
 
 def test_conv_in_bench_launch_configuration(he):
     """The bench step's launch configuration -- config 4 layer jobs dealt to
-    four streams, captured once as a CUDA graph and replayed -- gives
-    bit-exact full outputs and payloads (sampled images vs the oracle)."""
+    six streams, the FC job last on the next stream, captured once as a CUDA
+    graph and replayed -- gives bit-exact full outputs, payloads and FC
+    outputs (sampled images vs the oracle)."""
     cfg = synth.CONFIGS[4]
     ctx = ctx_for(he, cfg.N, cfg.primes, cfg.t)
     ring = R.Ring(cfg.N, cfg.primes, cfg.t)
@@ -558,7 +559,15 @@ def test_conv_in_bench_launch_configuration(he):
         jobs.append(dict(li=li, p=p, W=W, c0=c0, phi=phi, fspec=ctx.pack_filters(p, dev(W)),
                          c0_d=dev(c0), phi_d=dev(phi), out=ctx.empty_u64(B, p.n_ob, ring.L, cfg.N),
                          comp=ctx.empty_u64(B, p.n_ob, ring.L, p.n_valid)))
-    nstr = 4
+    fc = cfg.fc
+    fp = R.plan_fc(fc.n_i, fc.n_o, cfg.N)
+    fW, fbias = synth.fc_weights(cfg), synth.fc_bias(cfg)
+    fc0 = synth.uniform_residues((B, fp.n_ib, ring.L, cfg.N), cfg.primes, cfg.seed, "c0", 99)
+    fphi = synth.phi1((B, fc.n_o), cfg.t, cfg.seed, 99)
+    fwspec, fbenc = ctx.fc_pack_weights(dev(fW), dev(fbias))
+    fjob = dict(c0_d=dev(fc0), phi_d=dev(fphi), out=ctx.empty_u64(B, ring.L, fc.n_o),
+                ws=ctx.fc_workspace(fc.n_i, fc.n_o, B))
+    nstr = 6
     main = torch.cuda.Stream()
     side = [main] + [torch.cuda.Stream() for _ in range(nstr - 1)]
     ws = [ctx.conv_workspace(j["p"], B) for j in jobs]
@@ -574,6 +583,8 @@ def test_conv_in_bench_launch_configuration(he):
             k = i % nstr
             ctx.conv(j["p"], j["c0_d"], j["fspec"], j["phi_d"], j["out"], wsk[k],
                      compact=j["comp"], stream=side[k])
+        ctx.fc(fc.n_i, fc.n_o, fjob["c0_d"], fwspec, fbenc, fjob["phi_d"], fjob["out"],
+               fjob["ws"], stream=side[len(jobs) % nstr])
         for k in range(1, nstr):
             fork[k].record(side[k])
             main.wait_event(fork[k])
@@ -585,6 +596,7 @@ def test_conv_in_bench_launch_configuration(he):
     for j in jobs:
         j["out"].zero_()
         j["comp"].zero_()
+    fjob["out"].zero_()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=main):
         step()
@@ -597,6 +609,9 @@ def test_conv_in_bench_launch_configuration(he):
             ref = R.conv_server(j["c0"][b:b + 1], j["W"], plan, ring, j["phi"][b:b + 1])
             assert np.array_equal(u64(j["out"])[b], ref[0]), j["li"]
             assert np.array_equal(u64(j["comp"])[b], R.compact(ref, plan)[0]), j["li"]
+    bs = [0, B - 1]
+    assert np.array_equal(u64(fjob["out"])[bs],
+                          R.fc_server_tiled(fc0[bs], fW, fbias, ring, fphi[bs]))
 
 
 @pytest.mark.parametrize("case", SMALL + [
