@@ -7,10 +7,13 @@ B = 32 images per GPU (weak scaling: every rank serves its own batch, no
 data-path collective).  One step = the server evaluation of
 every layer for the batch: he_conv_ex (forward NTT of c0, folded NTT-domain
 MAC, inverse NTT + slot scatter + enc(phi1) mask, full output and fused
-valid-slot payload) for each Conv layer, then he_fc.  Each layer's batch is
-split into --streams sub-batches (default 2) on separate CUDA streams so the
-sub-batch pipelines overlap; a second, sequential pass (one launch sequence
-per layer, stage events) measures every kernel for the roofline.  Inputs are seeded
+valid-slot payload) for each Conv layer, then he_fc.  Default launch
+configuration (--streams 6 --overlap layers): the 20 independent layer jobs
+are dealt round-robin to six CUDA streams (layer i on stream i % 6, the FC
+job on stream 19 % 6), the whole step captured once as a CUDA graph and
+replayed; --overlap batch instead splits every layer's batch across the
+streams.  A second, sequential pass (one launch sequence per layer, stage
+events) measures every kernel for the roofline.  Inputs are seeded
 synthetic residues (synth/); the per-layer filter spectra (server init,
 Alg. 1 Line 4) are prepared before the timed region and timed separately.
 

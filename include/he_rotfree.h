@@ -255,7 +255,12 @@ he_status he_residues_unpack50(const uint8_t* d_packed, size_t n,
  * generated"; reading R15): d_phi1[i] = SplitMix64(seed, i) mod t for
  * i < n, a counter-based stream (z = seed + (i + 1) 0x9E3779B97F4A7C15,
  * then the SplitMix64 finaliser), reproducible on any device and in the
- * oracle. */
+ * oracle.  FOR REPRODUCIBLE TESTS AND BENCHMARKS ONLY: SplitMix64 is not a
+ * cryptographic generator and a small or guessable seed makes phi1
+ * predictable, and phi1 is what hides the server's conv output from the
+ * client.  A deployment supplies phi1 from a keyed
+ * cryptographic PRF (e.g. ChaCha20 or AES-CTR under a server secret) as the
+ * caller-owned d_phi1 buffer of he_conv / he_fc. */
 he_status he_phi1_generate(const he_ctx* ctx, uint64_t seed, size_t n,
                            uint32_t* d_phi1, void* stream);
 

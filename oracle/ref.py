@@ -11,16 +11,45 @@ library he_oracle.c (unsigned __int128) for the heavy sums.  Citations are
 PAPER.md line numbers with the section / equation / algorithm; readings
 R1..R26 are listed in DESIGN.md.
 
-Pins (tests/test_oracle_*.py, -m "not gpu"):
-  * ring: X^{N-1}*X = -1; schoolbook == sparse == definitional NTT product.
-  * NTT: psi^N = -1; INTT(NTT(a)) = a; NTT(delta_0) = all ones.
-  * packing: integer-mode coefficients equal brute-force Eq. (3)/(4) conv.
-  * protocol: decryption of the server output minus phi1 equals the
-    brute-force conv mod t (configs 1-2) and W I + B mod t for the FC.
-  * FC: Theorem 1 exhaustive; SPEC.md:416/430 worked example (golden).
-  * encoding: C enc == literal round(Q m / t) big-integer definition.
-Parity of GPU ciphertext residues is therefore pinned through these
-identities; no ciphertext value is printed in the paper.
+Pins (tests/test_oracle_*.py, -m "not gpu"), function by function -- each
+function below is checked against something other than itself:
+  is_prime / find_primes / min_psi   test_oracle_ring: SURVEY App. A prime
+        values; q = 1 mod 2N; psi^N = -1 and psi of order exactly 2N.
+  encode / encode_bigint             test_oracle_ring: C encoding == literal
+        big-integer round(Q m / t); centred-remainder identity.
+  schoolbook_py / negacyclic_at / sparse_mul (+ reduce_exp, to_residues)
+        test_oracle_ring: three independent product paths agree;
+        X^{N-1} X = -1 (golden SPEC.md:61).
+  ntt_def / intt_def / ntt_def_py    test_oracle_ring: INTT(NTT(a)) = a;
+        NTT(delta_0) = 1; convolution theorem vs schoolbook.
+  incomplete_ntt_def (+ reduce_mod_binomial)  test_oracle_ring: the reduction
+        mod X^s - zeta_g by long division; fold identity.
+  plan_conv / pack_input_int / filter_poly_int (+ pad_image, filter_terms)
+        test_oracle_packing: integer-mode product equals the brute-force
+        Eq. (3)/(4) conv (conv2d_ref) on 8 shapes; golden SPEC.md:266/284/285.
+  conv2d_ref                         test_oracle_packing: golden SPEC.md:648.
+  output_positions / conv_server / compact   test_oracle_protocol:
+        decryption - phi1 == brute-force conv mod t (configs 1-2).
+  fc_input_int / fc_weight_terms / fc_weight_eq10_literal / fc_server
+        test_oracle_packing: Theorem 1 exhaustive; golden SPEC.md:416/430;
+        protocol decrypts to W I + B.
+  plan_fc / fc_input_blocks / fc_server_tiled (+ fc_submatrix)
+        test_oracle_protocol: trivial-key decryption == W I + B.
+  keygen / encrypt_c0 / crt_decode / conv_protocol_decrypt /
+  fc_protocol_decrypt / centered_mod_t / server_p / client_c1r /
+  decrypt_round                      test_oracle_protocol / test_oracle_ring:
+        full protocol recovers the brute-force conv / FC mod t; CRT by
+        exact big integers.
+  splitmix64_py / phi1_stream        test_oracle_ring: Vigna's published
+        SplitMix64 reference value.
+  mod_switch                         test_oracle_protocol: exact rationals.
+  relu_requant / avgpool             test_oracle_stub: hand-computed golden
+        values (tests/golden/r29_stub.json); ReLU == PAPER.md:86's
+        (X + sign(X) X) / 2.
+  plain_chain                        test_oracle_protocol: the encrypted
+        protocol chain equals it layer by layer.
+No oracle function is unpinned.  GPU ciphertext residues are pinned through
+these identities; no ciphertext value is printed in the paper.
 """
 from __future__ import annotations
 
@@ -567,12 +596,6 @@ def signed_to_residues(x: np.ndarray, ring: Ring) -> np.ndarray:
     for j, q in enumerate(ring.primes):
         out[..., j, :] = np.mod(x, q).astype(np.uint64)
     return out
-
-
-def poly_mul_res(a: np.ndarray, b: np.ndarray, ring: Ring) -> np.ndarray:
-    """Per-limb negacyclic product of residue polys [L][N]."""
-    return np.stack([negacyclic_at(a[j], b[j], q)
-                     for j, q in enumerate(ring.primes)])
 
 
 def keygen(ring: Ring, s_key: np.ndarray, a: np.ndarray, e: np.ndarray):

@@ -124,6 +124,10 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
         const char* k = getenv("HE_NTT_COLS");
         // HE_NTT_COLS=0: cluster kernels only; =1: column kernel whenever possible
         c->ntt_cluster = (k && k[0] == '0') ? 1 : ((k && k[0] == '1') ? 2 : 0);
+        // read once here: the hot path never calls getenv
+        c->ntt_r8 = getenv("HE_NTT_R8") != nullptr;
+        const char* tc = getenv("HE_MAC_TC");
+        c->mac_tc = tc ? atoi(tc) : 2;
     }
     c->logN = r->log2N;
     c->N = N;

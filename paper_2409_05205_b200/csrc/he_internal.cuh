@@ -1,10 +1,11 @@
 // he_internal.cuh -- context layout, 64-bit modular arithmetic and the
 // shared-memory NTT passes used by every kernel of the library.
 //
-// Arithmetic is integer only (no tensor cores: modular 64-bit products are
-// not a float contraction, BASELINE.json north_star).  Residues are < q <
-// 2^50.  Twiddle products use Shoup's precomputed-quotient multiplication;
-// butterflies are Harvey's lazy forms (values kept in [0, 4q) / [0, 2q)).
+// Residues are < q < 2^50.  Two arithmetic families: exact FP64 modular
+// products on the DFMA pipe (the default transforms, dp_* below) and
+// integer Shoup products with Harvey's lazy butterflies (HE_NTT=int).  The
+// folded MAC runs on the int8 tensor cores (exact byte-plane split,
+// he_kernels.cu K3), not here.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -47,6 +48,8 @@ struct he_ctx {
     double* d_twd_inv;      // [L][N]  psi^{-brv(k)} as double
     int ntt_mode;           // 0: FP64 butterflies (default), 1: integer (HE_NTT=int)
     int ntt_cluster;        // HE_NTT_COLS: 0 auto, 1 cluster kernels only, 2 columns forced
+    int ntt_r8;             // HE_NTT_R8 set: radix-8 full forward transforms (A/B only)
+    int mac_tc;             // HE_MAC_TC: 0 never, 1 always, 2 (default) when B >= 128
     u64* d_enc;             // [L][t] enc_j(m) table (t <= 2^20), else nullptr
 };
 

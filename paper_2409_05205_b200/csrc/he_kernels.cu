@@ -20,6 +20,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "he_internal.cuh"
 
@@ -32,11 +34,25 @@ namespace cg = cooperative_groups;
 
 static inline cudaStream_t STREAM(void* s) { return (cudaStream_t)s; }
 
+// Raise a kernel's dynamic shared-memory limit.  The limit only ever grows
+// (per device and kernel, under a mutex), so a launch from one host thread
+// can never be undercut by another thread lowering it, and the
+// attribute call is made once per size class instead of before every launch.
 template <typename F>
 static bool set_smem(F* f, size_t bytes) {
     if (bytes <= 48 * 1024) return true;
-    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)bytes) == cudaSuccess;
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> cur;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    size_t& have = cur[{dev, (const void*)f}];
+    if (bytes <= have) return true;
+    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+        cudaSuccess)
+        return false;
+    have = bytes;
+    return true;
 }
 
 static inline int ntt_threads(int NS) { return std::min(512, std::max(16, NS / 16)); }
@@ -438,7 +454,7 @@ static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
         HE_CHECK_LAUNCH();
         return HE_OK;
     }
-    if (c->ntt_mode == 0 && out_fmt == 0 && T.skip == 0 && !getenv("HE_NTT_R8")) {
+    if (c->ntt_mode == 0 && out_fmt == 0 && T.skip == 0 && !c->ntt_r8) {
         typedef void (*kfd)(const u64*, u64*, int, int, const he_limb*, const double*, TileLay);
         static kfd const tab16[3] = {k_ntt_fwd_dp16_s0, k_ntt_fwd_dp16_s1, k_ntt_fwd_dp16_s2};
         kfd kd = tab16[S];
@@ -1511,15 +1527,15 @@ static he_status launch_mac_tc(const unsigned char* A, const unsigned char* Fpl,
 // reduces its raw inputs anyway)
 static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fpl, u64* out,
                                  int B, int n_ib, int L, int logN, int logs, int c_o,
-                                 const he_limb* limbs, cudaStream_t st, int Ku, int lazy) {
+                                 const he_limb* limbs, cudaStream_t st, int Ku, int lazy,
+                                 int mac_tc) {
     const int M = (1 << logN) >> logs, K = n_ib * Ku;
     const int Kp = imma_kp(K);
     const int nrow = (c_o + 7) & ~7, nnt = nrow / 8;
     if (nnt > 32) return HE_ESHAPE;                       // c_o <= 256
     {
         // batches of >= 128 images: tcgen05 MAC (HE_MAC_TC=0 disables, =1 forces)
-        const char* e = getenv("HE_MAC_TC");
-        const int mode = e ? atoi(e) : 2;
+        const int mode = mac_tc;
         const int Kt = (Kp + 31) & ~31, nr16 = (c_o + 15) & ~15;
         const bool fits = 7 * ((size_t)HE_MAC_TC_BT * Kt + (size_t)nr16 * Kt) <= 110 * 1024;
         if (fits && (mode == 1 || (mode == 2 && B >= HE_MAC_TC_BT)))
@@ -1738,9 +1754,9 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
             }
         }
     }
-    // (w > blockDim, i.e. more than 256 slot columns per chunk: a second
-    //  sweep covers the remaining columns)
-    for (int ub = blockDim.x; ub < w; ub += blockDim.x) {
+    // (w > blockDim, i.e. more than 256 slot columns per chunk: jstep = 0,
+    //  the writer above is skipped and this sweep covers every column)
+    for (int ub = jstep > 0 ? w : 0; ub < w; ub += blockDim.x) {
         const int u = u0 + ub + threadIdx.x;
         if (u >= u1) continue;
         const int nl = u / P.step;
@@ -1819,7 +1835,7 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     if (imma)
         s = launch_mac_imma((const unsigned char*)spec, (const unsigned char*)d_fspec, fold, B,
                             P.n_ib, c->L, c->logN, P.logs, P.c_o, c->d_limb, st, P.Ku,
-                            c->ntt_mode == 0);
+                            c->ntt_mode == 0, c->mac_tc);
     else
         s = launch_mac(spec, (const u64*)d_fspec, fold, B, P.n_ib, c->L, c->logN, P.logs,
                        P.c_o, c->d_limb, st, P.Ku);
