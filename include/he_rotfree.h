@@ -51,6 +51,9 @@ typedef enum {
 } he_status;
 
 const char* he_status_str(he_status s);
+/* Text of the CUDA error behind the last HE_ECUDA returned on the calling
+ * host thread ("no error" if none).  The pointer is static. */
+const char* he_last_cuda_error(void);
 
 /* ------------------------------------------------------------------ ring */
 /* Ring description.  log2N in [8, 15]; 1 <= L <= 64; q[L]

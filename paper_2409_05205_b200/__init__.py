@@ -32,7 +32,10 @@ HE_OK, HE_EINVAL, HE_ESHAPE, HE_EPARAM, HE_ECUDA, HE_ENOMEM = range(6)
 class HeError(RuntimeError):
     def __init__(self, status: int, what: str):
         self.status = status
-        super().__init__(f"{what}: {_lib.he_status_str(status).decode()}")
+        msg = f"{what}: {_lib.he_status_str(status).decode()}"
+        if status == HE_ECUDA:
+            msg += f" ({_lib.he_last_cuda_error().decode()})"
+        super().__init__(msg)
 
 
 class RingDesc(ctypes.Structure):
@@ -74,6 +77,8 @@ def _sig(name, args, res=ctypes.c_int):
 
 _lib.he_status_str.argtypes = [ctypes.c_int]
 _lib.he_status_str.restype = ctypes.c_char_p
+_lib.he_last_cuda_error.argtypes = []
+_lib.he_last_cuda_error.restype = ctypes.c_char_p
 _sig("he_ctx_create", [ctypes.POINTER(RingDesc), _I, ctypes.POINTER(_P)])
 _sig("he_ctx_destroy", [_P], None)
 _sig("he_ctx_psi", [_P, ctypes.c_uint32], ctypes.c_uint64)
@@ -128,7 +133,7 @@ _sig("he_fc_server_p_workspace_bytes", [_P, ctypes.POINTER(FcDesc)], _SZ)
 _sig("he_fc_server_init_p", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _P, _P, _SZ, _P])
 _sig("he_pack_fc_client_p", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _SZ, _P])
 
-EXPORTED = ["he_status_str", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
+EXPORTED = ["he_status_str", "he_last_cuda_error", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_conv_plan_make", "he_conv_plan_dense", "he_pack_input", "he_filter_bytes",
             "he_pack_filters_workspace_bytes", "he_pack_filters",
             "he_conv_workspace_bytes", "he_conv", "he_conv_ex", "he_mask_extract",

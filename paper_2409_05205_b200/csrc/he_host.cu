@@ -191,6 +191,12 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
         {
             const u64 ti = h_inv(r->t % q, q);
             Lm.tinvd = ti > q / 2 ? -(double)(q - ti) : (double)ti;
+            auto centred = [q](u64 v) { return v > q / 2 ? -(double)(q - v) : (double)v; };
+            const u64 c32 = (1ull << 32) % q;
+            const u64 c64 = (u64)(((u128)1 << 64) % q);
+            Lm.c32d = centred(c32);
+            Lm.c64d = centred(c64);
+            Lm.c96d = centred(h_mulmod(c64, c32, q));
         }
     }
     int prev = 0;

@@ -30,6 +30,7 @@ struct he_limb {
     u64 one_p;              // Shoup companion of 1  (floor(2^64 / q))
     double qd, qinvd;       // q and fl(1/q) for the FP64 transforms
     double tinvd;           // t^{-1} mod q, centred, as a double (enc_dp)
+    double c32d, c64d, c96d;  // 2^32, 2^64, 2^96 mod q, centred (FP64 MAC recombination)
 };
 
 struct he_ctx {

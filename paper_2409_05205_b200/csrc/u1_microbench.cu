@@ -11,6 +11,11 @@
 //   which 4: Shoup Gentleman-Sande butterfly (gs_bfly)   -> butterflies / s
 //   which 5: int8 mma.sync; 6: DFMA; 7/8: FP64 CT / GS butterflies (the
 //            default transforms, he_internal.cuh)
+//   which 9..14: tcgen05.mma.cta_group::1.kind::i8 (u8 x u8 -> s32, K = 32,
+//            operands in shared memory, accumulator in TMEM) issued back to
+//            back by one thread per CTA, one CTA per SM:
+//            9: M=128 N=16, 10: M=128 N=32, 11: M=128 N=64, 12: M=128 N=256,
+//            13: M=64 N=32, 14: M=64 N=256           -> int8 MACs / s
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -197,6 +202,77 @@ __global__ void u1_dgsbfly(const u64* in, u32* out, int iters, long long* cyc) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
 }
 
+// which 9..14: tcgen05 int8 MMA issue throughput.  Operands are zero
+// (the tensor datapath's cost does not depend on values); 8 MMAs per
+// iteration rotate over 4 accumulator regions so no two consecutive MMAs
+// write the same TMEM columns.
+__device__ __forceinline__ uint64_t u1_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+template <int M, int N>
+__global__ void __launch_bounds__(128, 1) u1_tc(u32* out, int iters, long long* cyc) {
+    __shared__ __align__(1024) unsigned char sA[M * 32];
+    __shared__ __align__(1024) unsigned char sB[N * 32];
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t s_bar;
+    for (int i = threadIdx.x; i < M * 8; i += blockDim.x) reinterpret_cast<u32*>(sA)[i] = 0;
+    for (int i = threadIdx.x; i < N * 8; i += blockDim.x) reinterpret_cast<u32*>(sB)[i] = 0;
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&s_tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&s_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = s_tmem;
+    long long c0 = clock64();
+    if (threadIdx.x == 0) {
+        const uint64_t ad = u1_desc((uint32_t)__cvta_generic_to_shared(sA), 128, 256);
+        const uint64_t bd = u1_desc((uint32_t)__cvta_generic_to_shared(sB), 128, 256);
+        const uint32_t idesc = (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+        const int stride = N < 128 ? N : 128;
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t d = tmem + (uint32_t)((k & 3) * stride) % 512u;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+                    "l"(ad), "l"(bd), "r"(idesc), "r"(1u));
+            }
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                (uint32_t)__cvta_generic_to_shared(&s_bar))
+            : "memory");
+    }
+    __syncwarp();
+    {
+        uint32_t ok = 0;
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+        while (!ok)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}\n"
+                : "=r"(ok) : "r"(bar) : "memory");
+    }
+    long long c1 = clock64();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 32)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    if (threadIdx.x == 0) out[blockIdx.x] = tmem;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cyc = c1 - c0;
+}
+
 // Runs kernel `which` once (after one warm-up launch); returns the elapsed
 // milliseconds, the in-kernel cycle count of block 0 (SM clock estimate)
 // and the number of operations executed.  0 on success.
@@ -231,6 +307,14 @@ extern "C" int u1_run(int which, int blocks, int threads, int iters, float* ms,
             case 6: u1_dfma<<<blocks, threads>>>(d_in, d_out, iters, d_cyc); per_iter = 8; break;
             case 7: u1_dbfly<<<blocks, threads>>>((const u64*)d_in, d_out, iters, d_cyc); per_iter = 8; break;
             case 8: u1_dgsbfly<<<blocks, threads>>>((const u64*)d_in, d_out, iters, d_cyc); per_iter = 8; break;
+            // tcgen05: one 128-thread CTA per SM (blocks = the SM count);
+            // ops counted per thread below, so per_iter = 8 MMAs x M N K / 128
+            case 9: u1_tc<128, 16><<<blocks, 128>>>(d_out, iters, d_cyc); per_iter = 8.0 * 128 * 16 * 32 / threads; break;
+            case 10: u1_tc<128, 32><<<blocks, 128>>>(d_out, iters, d_cyc); per_iter = 8.0 * 128 * 32 * 32 / threads; break;
+            case 11: u1_tc<128, 64><<<blocks, 128>>>(d_out, iters, d_cyc); per_iter = 8.0 * 128 * 64 * 32 / threads; break;
+            case 12: u1_tc<128, 256><<<blocks, 128>>>(d_out, iters, d_cyc); per_iter = 8.0 * 128 * 256 * 32 / threads; break;
+            case 13: u1_tc<64, 32><<<blocks, 128>>>(d_out, iters, d_cyc); per_iter = 8.0 * 64 * 32 * 32 / threads; break;
+            case 14: u1_tc<64, 256><<<blocks, 128>>>(d_out, iters, d_cyc); per_iter = 8.0 * 64 * 256 * 32 / threads; break;
             default: return 2;
         }
         if (rep == 1) cudaEventRecord(e1);
