@@ -186,6 +186,11 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
         Lm.r64 = (u64)(((u128)1 << 64) % q);
         Lm.r64_p = h_shoup(Lm.r64, q);
         Lm.one_p = h_shoup(1, q);
+        {   // -q^{-1} mod 2^64 by Newton iteration (q odd): x <- x (2 - q x)
+            u64 x = q;                      // q q = 1 mod 8: 3 correct bits
+            for (int it = 0; it < 5; ++it) x *= 2 - q * x;
+            Lm.mq = (u64)0 - x;
+        }
         Lm.qd = (double)q;
         Lm.qinvd = 1.0 / (double)q;
         {

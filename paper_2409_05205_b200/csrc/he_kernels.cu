@@ -27,6 +27,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef HE_MAC_OB
+#define HE_MAC_OB 2          // fold groups per MAC output run (k_mac_imma)
+#endif
+
 // The CUDA error behind the last HE_ECUDA returned on this host thread
 // (he_last_cuda_error), so a caller can report what failed.
 static thread_local cudaError_t g_last_cuda_error = cudaSuccess;
@@ -82,16 +86,11 @@ static inline int ntt_threads(int NS) { return std::min(512, std::max(16, NS / 1
 // coalesced global loads and stores.  OUT_FMT 0: canonical, 1: split25,
 // 2: byte planes (int8 tensor-core MAC operand).
 // MAC-tile layout of the forward spectra (OUT_FMT 2): byte j (j < 7) of the
-// coefficient at position g s + u of limb (b, beta, l), g = gb Gt + gi,
-// column k = beta Ku + u of the fold GEMM, is
-//   A[((((l (M/Gt) + gb) 7 + j) Gt + gi) B + b) Kp + swz_k(b, k, Kp)]  (bytes)
-// with zeros in [K, Kp) of every row (Kp = K rounded up to a power of two
-// >= 16).  Per (plane, group) the B image rows are contiguous, so a 32-image
-// tile of GS consecutive groups is one bulk (TMA) copy per plane, and the
-// 16-byte chunks of each row are XOR-swizzled by the row index (swz_k) so the
-// mma.sync fragment loads of 8 consecutive rows hit 32 distinct banks
-// without padding (a bulk copy cannot pad).  The filter operand uses the
-// same row format: Fpl[((l M + g) 7 + j) c_o + n][swz_k(n, k, Kp)].
+// coefficient at position g s + u of limb (b, beta, l), g = gb Gt + gi, is
+//   A[((((l (M/Gt) + gb) 7 + j) B + b) Gt + gi) Kp + beta s + u]   (bytes),
+// with zeros in [K, Kp) of every row: a (plane, image) row holds Gt
+// consecutive groups, so a limb writes runs of Gt*s bytes (n_ib = 1) and the
+// int8 MAC stages each operand tile as contiguous blocks.
 // cp.async helpers (Ampere-style async copies, used by several kernels)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int NW>
@@ -105,18 +104,6 @@ __device__ __forceinline__ void cp_async_n(void* smem_dst, const void* gsrc, boo
     else
         asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(gsrc),
                      "n"(CHUNK), "r"(valid ? CHUNK : 0));
-}
-
-// 16-byte-chunk XOR swizzle of a Kp-byte row r (Kp a power of two >= 16):
-// the chunk index is XORed with bits of r chosen so that any 8 consecutive
-// rows read at the same logical word land in 8 distinct 4-bank groups.
-__host__ __device__ __forceinline__ int chunk_swz(int r, int Kp) {
-    const int nch = Kp >> 4;
-    const int sh = nch >= 8 ? 0 : (nch == 4 ? 1 : (nch == 2 ? 2 : 3));
-    return (r >> sh) & (nch - 1);
-}
-__host__ __device__ __forceinline__ int swz_k(int r, int k, int Kp) {
-    return (((k >> 4) ^ chunk_swz(r, Kp)) << 4) | (k & 15);
 }
 
 struct TileLay {
@@ -150,16 +137,16 @@ __device__ __forceinline__ void ntt_store(u64* out, int li, int seg, int NS, int
             const int g = pos >> T.logs, u = pos & (s - 1);
             const int gb = g >> lgt, gi = g & (T.Gt - 1);     // Gt is a power of two
             unsigned char* row =
-                A + (((((size_t)l * (M / T.Gt) + gb) * 7) * T.Gt + gi) * T.B + b) * T.Kp;
-            const size_t pstride = (size_t)T.Gt * T.B * T.Kp;
-            const int ko = swz_k(b, beta * T.Ku + u, T.Kp);
+                A + (((((size_t)l * (M / T.Gt) + gb) * 7) * T.B + b) * T.Gt + gi) * T.Kp +
+                beta * T.Ku + u;
+            const size_t pstride = (size_t)T.B * T.Gt * T.Kp;
             const bool tail = (beta == T.n_ib - 1) && (u + 4 == T.Ku) && (T.Kp > K);
 #pragma unroll
             for (int j = 0; j < 7; ++j) {
-                *reinterpret_cast<u32*>(row + j * pstride + ko) = pl[j];
+                *reinterpret_cast<u32*>(row + j * pstride) = pl[j];
                 if (tail)
-                    for (int z = K; z < T.Kp; z += 4)
-                        *reinterpret_cast<u32*>(row + j * pstride + swz_k(b, z, T.Kp)) = 0u;
+                    for (int z = 4; z < T.Kp - K + 4; z += 4)
+                        *reinterpret_cast<u32*>(row + j * pstride + z) = 0u;
             }
         }
         return;
@@ -397,7 +384,7 @@ k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int 
         unsigned char* A = reinterpret_cast<unsigned char*>(out);
         const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
         const int K = T.n_ib * T.Ku;
-        const size_t pstride = (size_t)T.Gt * T.B * T.Kp;
+        const size_t pstride = (size_t)T.B * T.Gt * T.Kp;
         const int lgt = __ffs(T.Gt) - 1;
         const int nq = C >> 2;                                  // 4-column quads per row
         for (int e = threadIdx.x; e < (M * nq); e += blockDim.x) {
@@ -413,15 +400,15 @@ k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int 
             if (u >= T.Ku) continue;                            // column unused by the MAC
             const int gb = g >> lgt, gi = g & (T.Gt - 1);     // Gt is a power of two
             unsigned char* row =
-                A + (((((size_t)l * (M / T.Gt) + gb) * 7) * T.Gt + gi) * T.B + b) * T.Kp;
-            const int ko = swz_k(b, beta * T.Ku + u, T.Kp);
+                A + (((((size_t)l * (M / T.Gt) + gb) * 7) * T.B + b) * T.Gt + gi) * T.Kp +
+                beta * T.Ku + u;
             const bool tail = (beta == T.n_ib - 1) && (u + 4 == T.Ku) && (T.Kp > K);
 #pragma unroll
             for (int j = 0; j < 7; ++j) {
-                *reinterpret_cast<u32*>(row + j * pstride + ko) = pl[j];
+                *reinterpret_cast<u32*>(row + j * pstride) = pl[j];
                 if (tail)
-                    for (int z = K; z < T.Kp; z += 4)
-                        *reinterpret_cast<u32*>(row + j * pstride + swz_k(b, z, T.Kp)) = 0u;
+                    for (int z = 4; z < T.Kp - K + 4; z += 4)
+                        *reinterpret_cast<u32*>(row + j * pstride + z) = 0u;
             }
         }
     } else {
@@ -830,18 +817,12 @@ static bool use_imma(const he_ctx* c, const PlanDev& P) {
     // CTA, one warp per 8: c_o <= 256; wider layers take the IMAD MAC)
     return c->mac_mode == 0 && P.s >= 4 && P.c_o <= 256;
 }
-// MAC-tile row length: K rounded up to a power of two >= 16 (swz_k)
-static inline int imma_kp(int K) {
-    int kp = 16;
-    while (kp < K) kp *= 2;
-    return kp;
-}
+static inline int imma_kp(int K) { return (K + 15) & ~15; }
 static inline int imma_sw(int Kp) { return Kp / 4 + ((4 - Kp / 4) & 7); }   // = 4 mod 8
 __device__ __forceinline__ int imma_sw_dev(int Kp) { return Kp / 4 + ((4 - Kp / 4) & 7); }
 
-// spectra [c_o][n_ib][L][N] -> byte planes Fpl[l][g][7][c_o][Kp] of the fold
-// filter operand (k = beta Ku + u < K; zero for K <= k < Kp), each Kp-byte
-// row chunk-swizzled by its channel n (swz_k, as the image spectra).
+// spectra [c_o][n_ib][L][N] -> byte planes Fpl[l][g][7][c_o][Kp] of
+// spec * N^{-1} (k = beta s + u < K; zero for K <= k < Kp).
 __global__ void k_filter_to_imma(const u64* __restrict__ spec, unsigned char* __restrict__ F,
                                  PlanDev P, int L, int logN, int Kp,
                                  const he_limb* __restrict__ limbs,
@@ -862,8 +843,10 @@ __global__ void k_filter_to_imma(const u64* __restrict__ spec, unsigned char* __
             const int beta = k / P.Ku, u = k - beta * P.Ku;
             v = fold_filter_operand(spec + (((long)n * P.n_ib + beta) * L + l) * N, g, u,
                                     P.logs, logN - P.logs, Lm, tw_fwd + (long)l * N);
+            // Montgomery form (x R mod q, R = 2^64) for the MAC's REDC (redc128)
+            v = d2canon(dp_mulmod(u2d(v), u2d(Lm.r64), Lm.qd, Lm.qinvd), Lm.qd, Lm.qinvd);
         }
-        unsigned char* dst = F + (((long)l * M + g) * 7 * P.c_o + n) * Kp + swz_k(n, k, Kp);
+        unsigned char* dst = F + (((long)l * M + g) * 7 * P.c_o + n) * Kp + k;
 #pragma unroll
         for (int j = 0; j < 7; ++j) dst[(long)j * P.c_o * Kp] = (unsigned char)(v >> (8 * j));
     }
@@ -1135,47 +1118,41 @@ __device__ __forceinline__ void mma_k16(int (&d)[4], u32 a0, u32 a1, u32 b0) {
         : "r"(a0), "r"(a1), "r"(b0));
 }
 
-// V = sum_{d<13} S_d 2^{8d} mod q, S_d < 2^31.  Exact 128-bit assembly from
-// 32-bit-aligned partial sums P_k = sum_{d = 4k..4k+3} S_d 2^{8(d-4k)}
-// (< 2^57, three mad.wide each): V = P0 + P1 2^32 + P2 2^64 + P3 2^96 =
-// lo + hi 2^64, then V mod q = lo + hi (2^64 mod q) with two Shoup products.
-__device__ __forceinline__ u64 reduce13(const int (&acc)[13][4], int e, const he_limb& Lm,
-                                        bool lazy) {
-    u64 P[4];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        P[k] = (u64)(u32)acc[4 * k][e];
-        madw(P[k], (u32)acc[4 * k + 1][e], 1u << 8);
-        madw(P[k], (u32)acc[4 * k + 2][e], 1u << 16);
-        madw(P[k], (u32)acc[4 * k + 3][e], 1u << 24);
-    }
-    P[3] = (u64)(u32)acc[12][e];
-    const u64 lo = P[0] + (P[1] << 32);
-    const u64 hi = P[2] + (P[1] >> 32) + (P[3] << 32) + (lo < P[0] ? 1 : 0);
-    const u64 q = Lm.q;
-    const u64 r = shoup_mul(lo, 1, Lm.one_p, q) + shoup_mul(hi, Lm.r64, Lm.r64_p, q);  // < 4q
-    return lazy ? r : csub(csub(r, 2 * q), q);
+// Montgomery form of the recombination (R = 2^64): the filter operand of the
+// int8 MAC paths is stored pre-multiplied by R mod q (k_filter_to_imma), so
+// the exact 128-bit sum V = lo + hi 2^64 = R (C . F) needs one REDC instead
+// of two Shoup products:  m = lo (-q^{-1}) mod 2^64,
+//   t = (V + m q) / 2^64 = hi + hi64(m q) + (lo != 0)  =  C . F  (mod q),
+// t < V / 2^64 + q < 2q because V < 1.5 K q^2 < q 2^64 (K <= 4096, q < 2^50).
+__device__ __forceinline__ u64 redc128(u64 lo, u64 hi, const he_limb& Lm, bool lazy) {
+    const u64 m = lo * Lm.mq;
+    const u64 t = hi + __umul64hi(m, Lm.q) + (lo != 0 ? 1ull : 0ull);
+    return lazy ? t : csub(t, Lm.q);
 }
-
-// reduce13 for K <= 16 (S_d < 7 * 16 * 255^2 < 2^23): the pairs
-// S_{2m} + 2^8 S_{2m+1} fit 32 bits, so each P_k takes two 32-bit IMADs and
-// one IMAD.WIDE instead of three IMAD.WIDE.
-__device__ __forceinline__ u64 reduce13_k16(const int (&acc)[13][4], int e, const he_limb& Lm,
-                                            bool lazy) {
-    u64 P[4];
+// V = sum_{d<13} S_d 2^{8d} as (lo, hi): P_k = sum_{d=4k..4k+3} S_d 2^{8(d-4k)}
+// (three mad.wide each, or the 32-bit pairs when S_d < 2^23, i.e. K <= 16),
+// V = P0 + P1 2^32 + P2 2^64 + P3 2^96.
+template <bool K16, class S>
+__device__ __forceinline__ u64 reduce13_mont(S sd, const he_limb& Lm, bool lazy) {
+    u64 P[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const u32 a = (u32)acc[4 * k][e] + ((u32)acc[4 * k + 1][e] << 8);
-        const u32 b = (u32)acc[4 * k + 2][e] + ((u32)acc[4 * k + 3][e] << 8);
-        P[k] = a;
-        madw(P[k], b, 1u << 16);
+        if (K16) {
+            const u32 a = (u32)sd(4 * k) + ((u32)sd(4 * k + 1) << 8);
+            const u32 b = (u32)sd(4 * k + 2) + ((u32)sd(4 * k + 3) << 8);
+            P[k] = a;
+            madw(P[k], b, 1u << 16);
+        } else {
+            P[k] = (u64)(u32)sd(4 * k);
+            madw(P[k], (u32)sd(4 * k + 1), 1u << 8);
+            madw(P[k], (u32)sd(4 * k + 2), 1u << 16);
+            madw(P[k], (u32)sd(4 * k + 3), 1u << 24);
+        }
     }
-    P[3] = (u64)(u32)acc[12][e];
+    const u64 P3 = (u64)(u32)sd(12);
     const u64 lo = P[0] + (P[1] << 32);
-    const u64 hi = P[2] + (P[1] >> 32) + (P[3] << 32) + (lo < P[0] ? 1 : 0);
-    const u64 q = Lm.q;
-    const u64 r = shoup_mul(lo, 1, Lm.one_p, q) + shoup_mul(hi, Lm.r64, Lm.r64_p, q);  // < 4q
-    return lazy ? r : csub(csub(r, 2 * q), q);
+    const u64 hi = P[2] + (P[1] >> 32) + (P3 << 32) + (lo < P[0] ? 1 : 0);
+    return redc128(lo, hi, Lm, lazy);
 }
 
 // x / d for 0 <= x < 2^31 with d fixed per kernel: a shift when d is a power
@@ -1195,6 +1172,197 @@ struct FastDiv {
 };
 
 
+// CTA = (limb l, G consecutive groups, 16*TB16-image tile); one warp per
+// 16 x 8 output tile (bt, nt).  Work proceeds in "units" (GS groups x a
+// KC-byte k-chunk): for small K a unit is all G groups with the whole K, for
+// large K one group and a 64-byte k-chunk.  Each unit's A tile (7 planes x
+// rows x KC bytes per group, MAC-tile layout) and F tile (7 x c_o x KC) are
+// contiguous in global memory and are copied with 16-byte cp.async into
+// padded shared rows (stride = 4 mod 8 words: conflict-free fragments).
+// Reduced outputs go straight to the transposed fold out[l][b][n][g].
+template <int TB16, int MINB = 1>
+__global__ void __launch_bounds__(MINB > 1 ? 128 : 512, MINB)
+k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
+           u64* __restrict__ out, int B, int L, int M, int c_o, int Kp, int G, int GS,
+           int KC, int Gt, int nbuf, const he_limb* __restrict__ limbs, int lazy) {
+    extern __shared__ u32 sm32[];
+    constexpr int rows = 16 * TB16;
+    const int nrow = (c_o + 7) & ~7, nnt = nrow >> 3;
+    const int swc = imma_sw_dev(KC);
+    const int rw = imma_sw_dev(GS * KC);                  // A row: GS groups x KC bytes
+    const int gb = 7 * nrow * swc;                        // B words per group
+    const int buf_words = 7 * rows * rw + GS * gb;        // one staging buffer
+    const int nGc = (M + G - 1) / G;
+    const int l = blockIdx.x / nGc, g0 = (blockIdx.x - l * nGc) * G;
+    const int b0 = blockIdx.y * rows;
+    const int gcnt = min(G, M - g0);
+    const int nkc = Kp / KC;
+    const int nunits = ((gcnt + GS - 1) / GS) * nkc;      // (group block, k-chunk)
+    // padded B rows (n >= c_o) stay zero for the whole kernel (every buffer)
+    for (int bf = 0; bf < nbuf; ++bf) {
+        u32* sB = sm32 + bf * buf_words + 7 * rows * rw;
+        for (int e = threadIdx.x; e < GS * 7 * (nrow - c_o) * swc; e += blockDim.x) {
+            const int w = e % swc, r = e / swc;
+            const int n = c_o + r % (nrow - c_o), gj = r / (nrow - c_o);
+            sB[(gj * nrow + n) * swc + w] = 0;
+        }
+    }
+    // cp.async one unit into staging buffer `bf`
+    auto issue = [&](int u, int bf) {
+        const int uq = nkc == 1 ? u : u / nkc;
+        const int gu = uq * GS, kc = u - uq * nkc;
+        const int gsn = min(GS, gcnt - gu), k0 = kc * KC;
+        u32* sA = sm32 + bf * buf_words;
+        u32* sB = sA + 7 * rows * rw;
+        {   // A: per (plane, image) the unit's gsn groups x KC bytes are contiguous
+            const int gbk = (g0 + gu) / Gt, gi0 = (g0 + gu) - gbk * Gt;
+            const int rcpr = (gsn * KC) >> 4;
+            const FastDiv drc(rcpr);
+            const int per = rows * rcpr;
+            const size_t plane_stride = (size_t)B * Gt * Kp;
+            const unsigned char* a0 = A + ((((size_t)l * (M / Gt) + gbk) * 7) * B + b0) * Gt * Kp +
+                                      (size_t)gi0 * Kp + k0;
+            for (int e = threadIdx.x; e < per; e += blockDim.x) {
+                const int bl = drc.div(e), c = e - bl * rcpr;
+                const bool ok = b0 + bl < B;
+                const unsigned char* src = a0 + (size_t)bl * Gt * Kp + c * 16;
+                unsigned char* dst = reinterpret_cast<unsigned char*>(sA + (size_t)bl * rw) + c * 16;
+#pragma unroll
+                for (int j = 0; j < 7; ++j)
+                    cp_async_n<16>(dst + (size_t)j * rows * rw * 4, ok ? src + j * plane_stride : A,
+                                   ok);
+            }
+        }
+        {   // B: per (group, plane) a contiguous c_o x KC block
+            const int cpr2 = KC >> 4;
+            const FastDiv dc(cpr2), dn(c_o * cpr2);
+            const int per = c_o * cpr2, total = gsn * per;
+            const unsigned char* f0 = Fpl + (((size_t)l * M + g0 + gu) * 7) * c_o * Kp + k0;
+            for (int e = threadIdx.x; e < total; e += blockDim.x) {
+                const int gi = dn.div(e), rem = e - gi * per;
+                const int n = dc.div(rem), c = rem - n * cpr2;
+                const unsigned char* src = f0 + ((size_t)gi * 7 * c_o + n) * Kp + c * 16;
+                unsigned char* dst =
+                    reinterpret_cast<unsigned char*>(sB + ((size_t)gi * 7 * nrow + n) * swc) + c * 16;
+#pragma unroll
+                for (int j = 0; j < 7; ++j)
+                    cp_async_n<16>(dst + (size_t)j * nrow * swc * 4, src + (size_t)j * c_o * Kp, true);
+            }
+        }
+        cp_async_commit();
+    };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int bt = warp / nnt, nt = warp - bt * nnt;
+    const he_limb Lm = limbs[l];
+    int acc[13][4];
+    u64 ob[HE_MAC_OB][4];
+    int nob = 0;
+    issue(0, 0);
+    for (int u = 0; u < nunits; ++u) {
+        if (nbuf == 2 && u + 1 < nunits) {                 // prefetch the next unit
+            issue(u + 1, (u + 1) & 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int uq = nkc == 1 ? u : u / nkc;
+        const int gu = uq * GS, kc = u - uq * nkc;
+        const int gsn = min(GS, gcnt - gu);
+        const u32* sA = sm32 + (nbuf == 2 ? (u & 1) : 0) * buf_words;
+        const u32* sB = sA + 7 * rows * rw;
+        for (int gi = 0; gi < gsn; ++gi) {
+            if (kc == 0) {
+#pragma unroll
+                for (int d = 0; d < 13; ++d)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[d][e] = 0;
+            }
+            const u32* ab = sA + (bt * 16 + gq) * rw + gi * (KC >> 2) + tq;
+            const u32* bb = sB + (size_t)gi * gb + (nt * 8 + gq) * swc + tq;
+            const int Kw = KC >> 2;
+            int kw = 0;
+            for (; kw + 8 <= Kw; kw += 8) {
+                u32 bf0[7], bf1[7];
+#pragma unroll
+                for (int j = 0; j < 7; ++j) {
+                    bf0[j] = bb[j * nrow * swc + kw];
+                    bf1[j] = bb[j * nrow * swc + kw + 4];
+                }
+#pragma unroll
+                for (int i = 0; i < 7; ++i) {
+                    const u32* ap = ab + i * rows * rw + kw;
+                    const u32 a0 = ap[0], a1 = ap[8 * rw], a2 = ap[4], a3 = ap[8 * rw + 4];
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) mma_k32(acc[i + j], a0, a1, a2, a3, bf0[j], bf1[j]);
+                }
+            }
+            if (kw < Kw) {                                   // one k16 step
+                u32 bf0[7];
+#pragma unroll
+                for (int j = 0; j < 7; ++j) bf0[j] = bb[j * nrow * swc + kw];
+#pragma unroll
+                for (int i = 0; i < 7; ++i) {
+                    const u32* ap = ab + i * rows * rw + kw;
+                    const u32 a0 = ap[0], a1 = ap[8 * rw];
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) mma_k16(acc[i + j], a0, a1, bf0[j]);
+                }
+            }
+            if (kc == nkc - 1) {
+                // outputs of HE_MAC_OB consecutive groups are kept (shift
+                // register ob, newest last) and leave as one run of HE_MAC_OB
+                // words per (b, n) row of the fold, instead of 8-byte writes
+                // scattered over 32 rows per warp instruction
+                constexpr int OB = HE_MAC_OB;
+                const int g = g0 + gu + gi;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+#pragma unroll
+                    for (int z = 0; z < OB - 1; ++z) ob[z][e] = ob[z + 1][e];
+                    ob[OB - 1][e] =
+                        MINB > 1 ? reduce13_mont<true>([&](int d) { return acc[d][e]; }, Lm, lazy)
+                                 : reduce13_mont<false>([&](int d) { return acc[d][e]; }, Lm, lazy);
+                }
+                ++nob;
+                if (nob == OB || gu + gi == gcnt - 1) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int b = b0 + bt * 16 + gq + 8 * (e >> 1);
+                        const int n = nt * 8 + 2 * tq + (e & 1);
+                        if (b >= B || n >= c_o) continue;
+                        u64* row = out + (((size_t)l * B + b) * c_o + n) * M + (g - (OB - 1));
+                        if (nob == OB && ((g - (OB - 1)) & (OB - 1)) == 0) {
+#pragma unroll
+                            for (int z = 0; z < OB; z += 2)
+                                reinterpret_cast<ulonglong2*>(row)[z / 2] =
+                                    make_ulonglong2(ob[z][e], ob[z + 1][e]);
+                        } else {
+#pragma unroll
+                            for (int z = 0; z < OB; ++z)
+                                if (z >= OB - nob) row[z] = ob[z][e];
+                        }
+                    }
+                    nob = 0;
+                }
+            }
+        }
+        __syncthreads();                                   // buffer free for refill
+    }
+}
+
+#ifndef HE_MAC_K16_MINB
+#define HE_MAC_K16_MINB 5
+#endif
+#ifndef HE_MAC_UG
+#define HE_MAC_UG 4
+#endif
+#ifndef HE_MAC_GMAX
+#define HE_MAC_GMAX 16
+#endif
+
 // ------------------------------------------------------------------ K3 (tcgen05)
 // Folded MAC on the 5th-generation tensor cores for batches of >= 128
 // images (config 5): one CTA per (limb l, group g, 128-image tile).  The
@@ -1206,7 +1374,7 @@ struct FastDiv {
 // columns per 16-channel chunk: 13 x 16 = 208 of a 256-column allocation,
 // two CTAs per SM).  One thread issues the 49 (x K/32) tcgen05.mma.kind::i8
 // per chunk and commits them to an mbarrier; then every thread owns one
-// image row (its TMEM lane) and recombines its outputs with reduce13 after
+// image row (its TMEM lane) and recombines its outputs with reduce13_mont after
 // tcgen05.ld -- the 13 partial sums of an output sit in one lane, so no
 // cross-thread exchange is needed.
 #ifndef HE_MAC_TC_BT
@@ -1238,24 +1406,6 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
         "selp.u32 %0, 1, 0, p;\n\t}\n"
         : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
     return ok != 0;
-}
-
-// V = sum_{d<13} S_d 2^{8d} mod q from 13 diagonal sums of one output.
-__device__ __forceinline__ u64 reduce13v(const int (&S)[13], const he_limb& Lm, bool lazy) {
-    u64 P[4];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        P[k] = (u64)(u32)S[4 * k];
-        madw(P[k], (u32)S[4 * k + 1], 1u << 8);
-        madw(P[k], (u32)S[4 * k + 2], 1u << 16);
-        madw(P[k], (u32)S[4 * k + 3], 1u << 24);
-    }
-    P[3] = (u64)(u32)S[12];
-    const u64 lo = P[0] + (P[1] << 32);
-    const u64 hi = P[2] + (P[1] >> 32) + (P[3] << 32) + (lo < P[0] ? 1 : 0);
-    const u64 q = Lm.q;
-    const u64 r = shoup_mul(lo, 1, Lm.one_p, q) + shoup_mul(hi, Lm.r64, Lm.r64_p, q);  // < 4q
-    return lazy ? r : csub(csub(r, 2 * q), q);
 }
 
 // TMEM budget: 256 columns per CTA, and 128 registers x 256 threads cap the
@@ -1293,15 +1443,15 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
     // ---- stage the operands (16-byte cp.async into the core-matrix layout)
     {
         const int gb = g / Gt, gi = g - gb * Gt;
-        const size_t plane_stride = (size_t)Gt * B * Kp;
-        const unsigned char* a0 = A + ((((size_t)l * (M / Gt) + gb) * 7) * Gt + gi) * B * Kp;
+        const size_t plane_stride = (size_t)B * Gt * Kp;
+        const unsigned char* a0 = A + (((size_t)l * (M / Gt) + gb) * 7 * B) * Gt * Kp +
+                                  (size_t)gi * Kp;
         const int cpr = Kt >> 4;                          // chunks per row
         for (int e = threadIdx.x; e < 7 * BT * cpr; e += blockDim.x) {
             const int c = e % cpr, r = (e / cpr) % BT, j = e / (cpr * BT);
             const int b = b0 + r;
             const bool ok = b < B && c * 16 < Kp;
-            const unsigned char* src =
-                ok ? a0 + j * plane_stride + (size_t)b * Kp + ((c ^ chunk_swz(b, Kp)) << 4) : A;
+            const unsigned char* src = ok ? a0 + j * plane_stride + (size_t)b * Gt * Kp + c * 16 : A;
             unsigned char* dst = sA + j * a_plane + (r >> 3) * sbo + c * 128 + (r & 7) * 16;
             cp_async_n<16>(dst, src, ok);
         }
@@ -1309,8 +1459,7 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
         for (int e = threadIdx.x; e < 7 * nrow * cpr; e += blockDim.x) {
             const int c = e % cpr, n = (e / cpr) % nrow, j = e / (cpr * nrow);
             const bool ok = n < c_o && c * 16 < Kp;
-            const unsigned char* src =
-                ok ? f0 + ((size_t)j * c_o + n) * Kp + ((c ^ chunk_swz(n, Kp)) << 4) : Fpl;
+            const unsigned char* src = ok ? f0 + ((size_t)j * c_o + n) * Kp + c * 16 : Fpl;
             unsigned char* dst = sB + j * b_plane + (n >> 3) * sbo + c * 128 + (n & 7) * 16;
             cp_async_n<16>(dst, src, ok);
         }
@@ -1380,7 +1529,8 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
                 int S[13];
 #pragma unroll
                 for (int d = 0; d < 13; ++d) S[d] = Sv[d][e];
-                out[(((size_t)l * B + b) * c_o + n) * M + g] = reduce13v(S, Lm, lazy);
+                out[(((size_t)l * B + b) * c_o + n) * M + g] =
+                    reduce13_mont<false>([&](int d) { return S[d]; }, Lm, lazy);
             }
         }
     }
@@ -1400,240 +1550,16 @@ static he_status launch_mac_tc(const unsigned char* A, const unsigned char* Fpl,
     return HE_OK;
 }
 
-// ------------------------------------------------------ K3 (int8, pipelined)
-// Folded MAC for batches below one 128-image tcgen05 tile (config 4's
-// 32-image layers).  The per-group GEMMs [32 x K] x [K x c_o] are small
-// (K, c_o <= 64): tcgen05.mma reads both operands from shared memory and
-// U1 measures it operand-bandwidth bound at these N (M = 128, N = 16: 1388
-// int8 MAC/clk/SM, one MMA per ~47 clk) below mma.sync with register
-// operands (1919), so the contraction stays on mma.sync and the kernel is
-// built around what the round-1 profile showed it waiting on:
-//  * persistent CTAs (2 per SM) walk units = (limb, GS consecutive groups,
-//    32-image tile) through an NS-stage shared-memory ring; one producer
-//    warp fills stages with TMA bulk copies (cp.async.bulk ... complete_tx
-//    on an mbarrier: one copy per byte plane of the image tile, one for the
-//    GS groups' filter planes), the consumer warps release a stage through
-//    a second mbarrier -- loads of units k+1..k+NS-1 overlap unit k's math;
-//  * rows are unpadded (bulk copies) and conflict-free through the chunk
-//    swizzle swz_k;
-//  * each consumer warp owns 16 x 8 output tiles (13 diagonal accumulators,
-//    49 MMAs per 32-byte k-step) and recombines on the FP64 pipe
-//    (reduce13_dp), which is otherwise idle in this kernel, instead of ~40
-//    IMAD-class instructions per output.
-// Stage layout: A [7][GS][32 rows][Kp], then F [GS][7][c_o][Kp] (the global
-// row formats, so each is one contiguous copy when B = 32).
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
-    while (!mbar_try_wait(bar, phase)) {
-    }
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
-            "r"(dst), "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
-}
-
-// V = sum_{d<13} S_d 2^{8d} mod q on the FP64 pipe.  With S_d < 7 K 255^2
-// (< 2^26.8 for K <= 256) the 32-bit-aligned partial sums
-// P_k = S_{4k} + S_{4k+1} 2^8 + S_{4k+2} 2^16 + S_{4k+3} 2^24 (k < 3) are
-// below 2^50.8 and P_3 = S_12, all exact as doubles, and
-//   V = P_0 + P_1 2^32 + P_2 2^64 + P_3 2^96 = P_0 + sum_k P_k c_k  (mod q),
-// c_k = 2^{32k} mod q centred: three exact dp_mulmod (|P_k c_k / q| < 2^51,
-// each result congruent and below 2q in magnitude), so |V| < 2^51 + 6q and
-// one dp_reduce leaves |V| <= q/2 + 2.  K <= 16 (S_d < 2^23): the pairs
-// S_{2m} + 2^8 S_{2m+1} fit 32 bits (two IMADs and one IMAD.WIDE per P_k).
-template <bool K16>
-__device__ __forceinline__ double reduce13_dp(const int (&acc)[13][4], int e, const he_limb& Lm) {
-    u64 P[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        if (K16) {
-            const u32 a = (u32)acc[4 * k][e] + ((u32)acc[4 * k + 1][e] << 8);
-            const u32 b = (u32)acc[4 * k + 2][e] + ((u32)acc[4 * k + 3][e] << 8);
-            P[k] = a;
-            madw(P[k], b, 1u << 16);
-        } else {
-            P[k] = (u64)(u32)acc[4 * k][e];
-            madw(P[k], (u32)acc[4 * k + 1][e], 1u << 8);
-            madw(P[k], (u32)acc[4 * k + 2][e], 1u << 16);
-            madw(P[k], (u32)acc[4 * k + 3][e], 1u << 24);
-        }
-    }
-    const double q = Lm.qd, qi = Lm.qinvd;
-    double v = u2d(P[0]);
-    v += dp_mulmod(u2d(P[1]), Lm.c32d, q, qi);
-    v += dp_mulmod(u2d(P[2]), Lm.c64d, q, qi);
-    v += dp_mulmod(u2d((u64)(u32)acc[12][e]), Lm.c96d, q, qi);
-    return dp_reduce(v, q, qi);
-}
-
-#ifndef HE_MAC_DPRED
-#define HE_MAC_DPRED 0
-#endif
-struct MacGeom {
-    int B, L, M, c_o, Kp, Gt, GS, nT, nunits;
-    int a_bytes, f_bytes, stage_bytes;     // per stage: A part, F part, total (16-B multiples)
-};
-
-template <int NW, int NS, bool K16>
-__global__ void __maxnreg__(112)
-k_mac_pipe(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
-           u64* __restrict__ out, MacGeom G, const he_limb* __restrict__ limbs, int lazy) {
-    extern __shared__ __align__(128) unsigned char smp[];
-    __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smp);
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int i = 0; i < NS; ++i) {
-            mbar_init((uint32_t)__cvta_generic_to_shared(&full_bar[i]), 1);
-            mbar_init((uint32_t)__cvta_generic_to_shared(&empty_bar[i]), NW);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    const int Kp = G.Kp, c_o = G.c_o, B = G.B, M = G.M, GS = G.GS;
-    const int nGS = M / GS, nGB = M / G.Gt;
-    if (warp == NW) {                                    // ---- producer (TMA)
-        if (lane == 0) {
-            int k = 0;
-            for (int u = blockIdx.x; u < G.nunits; u += gridDim.x, ++k) {
-                const int st = k % NS;
-                const uint32_t ph = (uint32_t)(k / NS) & 1u;
-                const uint32_t fb = (uint32_t)__cvta_generic_to_shared(&full_bar[st]);
-                mbar_wait((uint32_t)__cvta_generic_to_shared(&empty_bar[st]), ph ^ 1u);
-                const int t = u % G.nT, r = u / G.nT;
-                const int gsl = r % nGS, l = r / nGS;
-                const int g0 = gsl * GS, gb = g0 / G.Gt, gi0 = g0 - gb * G.Gt;
-                const int b0 = t * 32, nb = min(32, B - b0);
-                const uint32_t dA = sbase + st * G.stage_bytes, dF = dA + G.a_bytes;
-                const uint32_t fbytes = (uint32_t)(GS * 7 * c_o * Kp);
-                mbar_arrive_tx(fb, (uint32_t)(7 * GS * nb * Kp) + fbytes);
-                const unsigned char* ab =
-                    A + ((((size_t)l * nGB + gb) * 7) * G.Gt + gi0) * (size_t)B * Kp;
-                const size_t pstride = (size_t)G.Gt * B * Kp;
-#pragma unroll 1
-                for (int j = 0; j < 7; ++j) {
-                    if (B == 32) {
-                        bulk_g2s(dA + j * GS * 32 * Kp, ab + j * pstride, GS * 32 * Kp, fb);
-                    } else {
-#pragma unroll 1
-                        for (int gs = 0; gs < GS; ++gs)
-                            bulk_g2s(dA + (j * GS + gs) * 32 * Kp,
-                                     ab + j * pstride + ((size_t)gs * B + b0) * Kp, nb * Kp, fb);
-                    }
-                }
-                bulk_g2s(dF, Fpl + ((size_t)l * M + g0) * 7 * c_o * Kp, fbytes, fb);
-            }
-        }
-        return;
-    }
-    // ---- consumers: 16 x 8 output tiles (gs, bt, nt)
-    const int gq = lane >> 2, tq = lane & 3;
-    const int nnt = (c_o + 7) >> 3, ntile = GS * 2 * nnt;
-    const int nch = Kp >> 4;
-    int k = 0;
-    for (int u = blockIdx.x; u < G.nunits; u += gridDim.x, ++k) {
-        const int st = k % NS;
-        const uint32_t ph = (uint32_t)(k / NS) & 1u;
-        const int t = u % G.nT, r = u / G.nT;
-        const int gsl = r % nGS, l = r / nGS;
-        const int g0 = gsl * GS, b0 = t * 32;
-        const he_limb& Lm = limbs[l];           // fields read at recombination (registers)
-        mbar_wait((uint32_t)__cvta_generic_to_shared(&full_bar[st]), ph);
-        const unsigned char* sA = smp + st * G.stage_bytes;
-        const unsigned char* sF = sA + G.a_bytes;
-        // tiles dealt round-robin across units (not restarting at warp 0 in
-        // every unit), so no warp is the stage's straggler when NW does not
-        // divide the unit's tile count
-        const int t0 = (int)(((long)k * ntile + NW - warp) % NW);
-        for (int tile = (NW - t0) % NW; tile < ntile; tile += NW) {
-            const int nt = tile % nnt, rr = tile / nnt;
-            const int bt = rr & 1, gs = rr >> 1;
-            int acc[13][4];
-#pragma unroll
-            for (int d = 0; d < 13; ++d)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) acc[d][e] = 0;
-            const int r0 = bt * 16 + gq, n = nt * 8 + gq;
-            const int h0 = chunk_swz(r0, Kp), h1 = chunk_swz(r0 + 8, Kp), hn = chunk_swz(n, Kp);
-            // word pointers of row r0 / r0+8 of plane 0 and row n of plane 0
-            const u32* a0p = reinterpret_cast<const u32*>(sA + ((size_t)gs * 32 + r0) * Kp) + tq;
-            const u32* a1p = a0p + 2 * Kp;                         // + 8 rows
-            const u32* fp = reinterpret_cast<const u32*>(sF + ((size_t)gs * 7 * c_o + n) * Kp) + tq;
-            const int aps = GS * 32 * Kp / 4, fps = c_o * Kp / 4;  // plane strides (words)
-            if (nch == 1) {                                        // K <= 16: one k16 step
-                u32 bf[7];
-#pragma unroll
-                for (int j = 0; j < 7; ++j) bf[j] = fp[j * fps];
-#pragma unroll
-                for (int i = 0; i < 7; ++i) {
-                    const u32 x0 = a0p[i * aps], x1 = a1p[i * aps];
-#pragma unroll
-                    for (int j = 0; j < 7; ++j) mma_k16(acc[i + j], x0, x1, bf[j]);
-                }
-            } else {
-                for (int c = 0; c < nch; c += 2) {                 // k32 steps: chunks c, c+1
-                    const int oa0 = ((c ^ h0) << 2), oa2 = (((c + 1) ^ h0) << 2);
-                    const int ob0 = ((c ^ h1) << 2), ob2 = (((c + 1) ^ h1) << 2);
-                    const int of0 = ((c ^ hn) << 2), of1 = (((c + 1) ^ hn) << 2);
-                    u32 bf0[7], bf1[7];
-#pragma unroll
-                    for (int j = 0; j < 7; ++j) {
-                        bf0[j] = fp[j * fps + of0];
-                        bf1[j] = fp[j * fps + of1];
-                    }
-#pragma unroll
-                    for (int i = 0; i < 7; ++i) {
-                        const u32 x0 = a0p[i * aps + oa0], x1 = a1p[i * aps + ob0];
-                        const u32 x2 = a0p[i * aps + oa2], x3 = a1p[i * aps + ob2];
-#pragma unroll
-                        for (int j = 0; j < 7; ++j) mma_k32(acc[i + j], x0, x1, x2, x3, bf0[j], bf1[j]);
-                    }
-                }
-            }
-            const int g = g0 + gs;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int b = b0 + bt * 16 + gq + 8 * (e >> 1);
-                const int nn = nt * 8 + 2 * tq + (e & 1);
-                if (b < B && nn < c_o) {
-#if HE_MAC_DPRED
-                    const double v = reduce13_dp<K16>(acc, e, Lm);
-                    out[(((size_t)l * B + b) * c_o + nn) * M + g] =
-                        lazy ? d2lazy(v, Lm.qd, Lm.qinvd) : d2canon(v, Lm.qd, Lm.qinvd);
-#else
-                    out[(((size_t)l * B + b) * c_o + nn) * M + g] =
-                        K16 ? reduce13_k16(acc, e, Lm, lazy) : reduce13(acc, e, Lm, lazy);
-#endif
-                }
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive((uint32_t)__cvta_generic_to_shared(&empty_bar[st]));
-    }
-}
-
-// lazy: outputs in [q/2 - 2, 3q/2 + 2] (or [0, 4q) from the tcgen05 kernel)
-// instead of canonical (the FP64 inverse in K4 reduces its raw inputs anyway)
+// lazy: outputs in [0, 4q) instead of canonical (the FP64 inverse in K4
+// reduces its raw inputs anyway)
 static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fpl, u64* out,
                                  int B, int n_ib, int L, int logN, int logs, int c_o,
                                  const he_limb* limbs, cudaStream_t st, int Ku, int lazy,
                                  int mac_tc) {
     const int M = (1 << logN) >> logs, K = n_ib * Ku;
     const int Kp = imma_kp(K);
-    if (c_o > 256) return HE_ESHAPE;
+    const int nrow = (c_o + 7) & ~7, nnt = nrow / 8;
+    if (nnt > 32) return HE_ESHAPE;                       // c_o <= 256
     {
         // batches of >= 128 images: tcgen05 MAC (HE_MAC_TC=0 disables, =1 forces)
         const int mode = mac_tc;
@@ -1642,37 +1568,56 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
         if (fits && (mode == 1 || (mode == 2 && B >= HE_MAC_TC_BT)))
             return launch_mac_tc(A, Fpl, out, B, L, M, c_o, Kp, limbs, st, lazy);
     }
-    if (K > 256) return HE_ESHAPE;                  // reduce13_dp headroom (plan: n_ib s <= 4096)
-    MacGeom G;
-    G.B = B; G.L = L; G.M = M; G.c_o = c_o; G.Kp = Kp; G.Gt = tile_gt(M);
-    G.nT = (B + 31) / 32;
-    // GS consecutive groups per unit: the largest power of two <= Gt with a
-    // stage of at most ~28 KB, so that NS = 4 stages of two CTAs fit an SM
-    const int nrow8 = (c_o + 7) & ~7;
-    auto stage = [&](int gs) {
-        // + slack: fragment loads of rows c_o .. nrow8 - 1 past the last plane
-        return 7 * gs * 32 * Kp + gs * 7 * c_o * Kp + (nrow8 - c_o) * Kp;
+    const int Gt = tile_gt(M);
+    // per staging buffer; the K = 16 small-CTA case targets 5 CTAs per SM
+    const bool k16c = Kp == 16 && HE_MAC_K16_MINB > 1;
+    const size_t budget = k16c ? 227 * 1024 / HE_MAC_K16_MINB - 1024 : 48 * 1024;
+    auto unit_bytes = [&](int rows, int gs, int kc) {
+        return sizeof(u32) * 7 * ((size_t)rows * imma_sw(gs * kc) + (size_t)gs * nrow * imma_sw(kc));
     };
-    int GS = 1;
-    while (GS < G.Gt && stage(2 * GS) <= 28 * 1024) GS *= 2;
-    G.GS = GS;
-    G.a_bytes = 7 * GS * 32 * Kp;
-    G.f_bytes = GS * 7 * c_o * Kp;
-    G.stage_bytes = (stage(GS) + 127) & ~127;
-    G.nunits = L * (M / GS) * G.nT;
-    constexpr int NS = 4;
-    const size_t smem = (size_t)NS * G.stage_bytes;
-    // two CTAs (7 consumer warps each) per SM when four stages fit half the
-    // shared memory, else one CTA with 15 consumer warps
-    const bool two = smem <= 113 * 1024;
-    if (smem > 226 * 1024) return HE_ESHAPE;
-    // (warps per SM = 16: each SM sub-partition's 16K registers hold four
-    //  112-register warps, so a fifth warp on one would fail the launch)
-    auto k = two ? (Kp == 16 ? k_mac_pipe<7, NS, true> : k_mac_pipe<7, NS, false>)
-                 : (Kp == 16 ? k_mac_pipe<15, NS, true> : k_mac_pipe<15, NS, false>);
+    // 32-image tiles for small c_o; 16-image tiles (<= 256 threads, two
+    // CTAs per SM) when the whole K does not fit one buffer
+    int TB16 = (nnt <= 8 && B > 16) ? 2 : 1;
+    if (TB16 == 2 && unit_bytes(32, 1, Kp) > budget) TB16 = 1;
+    const int rows = 16 * TB16, warps = TB16 * nnt;
+    int KC = Kp, GS = 1, G = 1;
+    if (unit_bytes(rows, 1, Kp) <= budget) {
+        GS = 1;
+        while (GS < Gt && GS < HE_MAC_GMAX && unit_bytes(rows, GS * 2, Kp) <= budget) GS *= 2;
+        G = GS;
+        // CTAs of > 4 warps (not the 5-per-SM small-K variant): walk several
+        // units through the double buffer so loads overlap the MMAs and the
+        // per-CTA setup is amortised, keeping >= ~3 CTAs of work per SM
+        if (!k16c && Kp >= 32) {
+            const long ctas1 = (long)L * ((M + GS - 1) / GS) * ((B + rows - 1) / rows);
+            int ug = 1;
+            while (ug < HE_MAC_UG && G * 2 <= Gt * 4 && ctas1 / (ug * 2) >= 3 * 148 &&
+                   2 * unit_bytes(rows, GS, Kp) <= 227 * 1024)
+                ug *= 2;
+            G = GS * ug;
+        }
+    } else {
+        KC = (Kp % 64 == 0) ? 64 : ((Kp % 32 == 0) ? 32 : 16);
+        GS = 1;
+        // several groups per CTA so the k-chunk pipeline has depth, while
+        // keeping >= ~4 CTAs of work per SM
+        const long ctas1 = (long)L * M * ((B + rows - 1) / rows);
+        G = 1;
+        while (G < Gt && ctas1 / (G * 2) >= 4 * 148) G *= 2;
+    }
+    const int nunits = ((G + GS - 1) / GS) * (Kp / KC);
+    const int nbuf = nunits > 1 ? 2 : 1;
+    const size_t smem = nbuf * unit_bytes(rows, GS, KC);
+    if (smem > 227 * 1024) return HE_ESHAPE;
+    // K = 16 with one unit per CTA and <= 4 warps: cap registers so five
+    // CTAs share an SM (occupancy-bound small-K case)
+    const bool k16 = k16c && nunits == 1 && 32 * warps <= 128;
+    auto k = TB16 == 2 ? (k16 ? k_mac_imma<2, HE_MAC_K16_MINB> : k_mac_imma<2>)
+                       : (k16 ? k_mac_imma<1, HE_MAC_K16_MINB> : k_mac_imma<1>);
     if (!set_smem(k, smem)) return HE_ECUDA;
-    const int grid = std::min(G.nunits, (two ? 2 : 1) * 148);
-    k<<<grid, two ? 32 * 8 : 32 * 16, smem, st>>>(A, Fpl, out, G, limbs, lazy);
+    dim3 grid(L * ((M + G - 1) / G), (B + rows - 1) / rows);
+    k<<<grid, 32 * warps, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, G, GS, KC, Gt, nbuf, limbs,
+                                      lazy);
     return HE_OK;
 }
 
