@@ -43,6 +43,9 @@ import synth  # noqa: E402
 
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0           # B200_PROFILING.md fallback
+# FP64 operations of one exact modular butterfly (dp_mulmod: DMUL + 3 DFMA +
+# 2 DADD, plus the add and subtract): the DFMA-pipe roof is DFMA/s / 8
+DP_OPS_PER_BFLY = 8
 
 
 def parse():
@@ -51,8 +54,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["plain20", "cfg5", "cfg3"],
+    ap.add_argument("--workload", choices=["plain20", "cfg5", "cfg3", "cfg2"],
                     default="plain20")
+    ap.add_argument("--scaling", choices=["auto", "weak", "strong"], default="auto",
+                    help="weak: every rank serves the config's own batch (plain20 and "
+                         "cfg3 default); strong: one global batch split over the ranks "
+                         "by image, or by output-channel block when it has fewer "
+                         "images than ranks (cfg5 and cfg2 default)")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the client / chain / ablation / FC-variant sections")
     ap.add_argument("--streams", type=int, default=6,
                     help="split every layer's image batch into this many "
                          "sub-batches, each on its own CUDA stream (1 = one launch "
@@ -75,7 +85,22 @@ def parse():
     return ap.parse_args()
 
 
-WORKLOADS = {"plain20": 4, "cfg5": 5, "cfg3": 3}
+WORKLOADS = {"plain20": 4, "cfg5": 5, "cfg3": 3, "cfg2": 2}
+DEFAULT_SCALING = {"plain20": "weak", "cfg3": "weak", "cfg5": "strong", "cfg2": "strong"}
+
+
+def self_launch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: re-run this command under
+    torch.distributed.run with one rank per GPU (127.0.0.1 rendezvous); rank 0
+    prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def peaks():
@@ -129,12 +154,15 @@ def u1_peaks(device_index=0):
     except Exception:
         max_mhz = 1965.0
     names = ["imad", "imad_wide", "modmac", "ct_bfly", "gs_bfly", "imma_u8",
-             "dfma", "dp_ct_bfly", "dp_gs_bfly"]
+             "dfma", "dp_ct_bfly", "dp_gs_bfly",
+             # tcgen05.mma kind::i8 (int8 MAC/s), one issuing thread per SM
+             "tc_i8_m128n16", "tc_i8_m128n32", "tc_i8_m128n64"]
     iters = {0: 20000, 1: 20000, 2: 20000, 3: 2000, 4: 2000, 5: 2000, 6: 20000,
-             7: 2000, 8: 2000}
+             7: 2000, 8: 2000, 9: 4000, 10: 4000, 11: 4000}
     for w, name in enumerate(names):
         ms, cyc, ops = ctypes.c_float(), ctypes.c_longlong(), ctypes.c_double()
-        rc = lib.u1_run(w, 148 * 8, 256, iters[w], ctypes.byref(ms),
+        blocks, threads = (nsm, 128) if w >= 9 else (148 * 8, 256)
+        rc = lib.u1_run(w, blocks, threads, iters[w], ctypes.byref(ms),
                         ctypes.byref(cyc), ctypes.byref(ops))
         if rc:
             raise RuntimeError(f"u1 {name} rc={rc}")
@@ -197,6 +225,49 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_single_thread(cfg_idx: int, max_s: float = 20.0) -> None:
+    """cpu_baseline leg (child process, OMP_NUM_THREADS=1): the oracle's server
+    work for ONE image through every layer of the config, repeated up to
+    max_s; prints one JSON object."""
+    from oracle import ref as R
+    cfg = synth.CONFIGS[cfg_idx]
+    ring = R.Ring(cfg.N, cfg.primes, cfg.t)
+    plans = [R.plan_conv(Ly, cfg.N) for Ly in cfg.conv]
+    Ws = [synth.weights(cfg, i) for i in range(len(cfg.conv))]
+    c0s = [synth.uniform_residues((1, p.n_ib, ring.L, cfg.N), cfg.primes, cfg.seed, "c0", i)
+           for i, p in enumerate(plans)]
+    phis = [synth.phi1((1, p.n_ob, cfg.N), cfg.t, cfg.seed, i) for i, p in enumerate(plans)]
+    fc = cfg.fc
+    evals = sum(Ly.c_o * p.n_ib for Ly, p in zip(cfg.conv, plans)) + (1 if fc else 0)
+    t0, reps = time.perf_counter(), 0
+    while True:
+        for p, W, c0, ph in zip(plans, Ws, c0s, phis):
+            R.compact(R.conv_server(c0, W, p, ring, ph), p)
+        if fc:
+            R.fc_server(synth.uniform_residues((1, ring.L, cfg.N), cfg.primes, cfg.seed, "c0", 99),
+                        synth.fc_weights(cfg), synth.fc_bias(cfg), ring,
+                        synth.phi1((1, fc.n_o), cfg.t, cfg.seed, 99))
+        reps += 1
+        if time.perf_counter() - t0 > max_s or reps >= 4:
+            break
+    dt = time.perf_counter() - t0
+    print(json.dumps({"value": reps * evals / dt, "unit": "ct×pt evals/s", "cores": 1,
+                      "s_per_image": dt / reps, "cpu_model": cpu_model(),
+                      "sample": f"{reps} x 1 image x all {len(plans)} conv"
+                                f"{' + FC' if fc else ''} layers ({dt:.1f} s wall, "
+                                "OMP_NUM_THREADS=1)"}))
+
+
 # ------------------------------------------------------------ reference
 def run_reference(args, cfg, rank):
     """--impl reference: the CPU oracle as it stands (test infrastructure),
@@ -255,11 +326,14 @@ def run_reference(args, cfg, rank):
 def main():
     args = parse()
     cfg = synth.CONFIGS[WORKLOADS[args.workload]]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, cfg, rank)
+    scaling = DEFAULT_SCALING[args.workload] if args.scaling == "auto" else args.scaling
     if args.profile:
         args.streams = 1            # profiling runs: one launch sequence per layer
 
@@ -269,9 +343,37 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's init log (rank, nRanks) is the evidence of the communicator
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier(device_ids=[local])
+        print(f"[bench] rank {rank}/{world} on cuda:{local}, backend "
+              f"{dist.get_backend()}", file=sys.stderr, flush=True)
     dev = torch.device("cuda", local)
-    B, N, L = cfg.B, cfg.N, cfg.L
+    N, L = cfg.N, cfg.L
+    from paper_2409_05205_b200.dist import (choose_axis, shard_out_blocks, shard_range,
+                                            sub_layer_weights)
+    # ---- partition: weak = every rank its own cfg.B images
+    # (seeded per rank); strong = one global batch of cfg.B images split by
+    # image, or by output-channel block when it has fewer images than ranks
+    ctx0 = he.Context(cfg.primes, cfg.log2N, cfg.t, local)
+    Ly0 = cfg.conv[0]
+    n_ob0 = ctx0.plan(Ly0.c_i, Ly0.c_o, Ly0.w_i, Ly0.h_i, Ly0.f_w, Ly0.f_h, Ly0.stride,
+                      Ly0.pad).n_ob
+    axis = "batch" if scaling == "weak" else choose_axis(cfg.B, n_ob0, world)
+    if scaling == "weak":
+        B, b_lo, seed_r = cfg.B, 0, cfg.seed + 1000 * rank
+        B_global = cfg.B * world
+    elif axis == "batch":
+        b_lo, b_hi = shard_range(cfg.B, rank, world)
+        B, seed_r, B_global = b_hi - b_lo, cfg.seed, cfg.B
+    else:
+        B, b_lo, seed_r, B_global = cfg.B, 0, cfg.seed, cfg.B
+    del ctx0
+    if B == 0 or (axis == "out_block" and n_ob0 < world):
+        raise SystemExit(f"{args.workload} with {scaling} scaling leaves rank {rank} of "
+                         f"{world} without work (batch {cfg.B}, {n_ob0} output blocks)")
     ctx = he.Context(cfg.primes, cfg.log2N, cfg.t, local)
     # all work on a dedicated (non-default) stream: CUDA-graph capture needs it
     stream = torch.cuda.Stream(dev)
@@ -290,19 +392,34 @@ def main():
     t_init0 = time.perf_counter()
     init_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     init_ev[0].record()
+    ob_span = []
     for i, Ly in enumerate(cfg.conv):
+        W = synth.weights(cfg, i)
+        if axis == "out_block":
+            pf = ctx.plan(Ly.c_i, Ly.c_o, Ly.w_i, Ly.h_i, Ly.f_w, Ly.f_h, Ly.stride, Ly.pad)
+            o_lo, o_hi = shard_out_blocks(pf.n_ob, rank, world)
+            ob_span.append((o_lo, o_hi, pf.n_ob))
+            W = sub_layer_weights(W, pf.c_ob, o_lo, o_hi)
+            Ly = synth.ConvLayer(Ly.c_i, W.shape[0], Ly.w_i, Ly.h_i, Ly.f_w, Ly.f_h,
+                                 Ly.stride, Ly.pad)
         p = ctx.plan(Ly.c_i, Ly.c_o, Ly.w_i, Ly.h_i, Ly.f_w, Ly.f_h, Ly.stride,
                      Ly.pad)
         layers.append(LayerWork(i, Ly, p, N, L, B))
-        fspecs.append(ctx.pack_filters(p, d(synth.weights(cfg, i))))
+        fspecs.append(ctx.pack_filters(p, d(W)) if Ly.c_o > 0 else None)
     init_ev[1].record()
     torch.cuda.synchronize()
     init_ms = init_ev[0].elapsed_time(init_ev[1])
     for lw in layers:
         p = lw.p
-        c0 = synth.uniform_residues((B, p.n_ib, L, N), cfg.primes,
-                                    cfg.seed + 1000 * rank, "c0", lw.idx)
-        ph = synth.phi1((B, p.n_ob, N), cfg.t, cfg.seed + 1000 * rank, lw.idx)
+        Bg = B if scaling == "weak" else cfg.B
+        c0 = synth.uniform_residues((Bg, p.n_ib, L, N), cfg.primes,
+                                    seed_r, "c0", lw.idx)[b_lo:b_lo + B]
+        if axis == "out_block":          # this rank's blocks of the full layer's mask
+            o_lo, o_hi, n_ob_full = ob_span[lw.idx]
+            ph = synth.phi1((Bg, n_ob_full, N), cfg.t, seed_r, lw.idx)[:, o_lo:o_hi]
+        else:
+            ph = synth.phi1((Bg, p.n_ob, N), cfg.t, seed_r, lw.idx)[b_lo:b_lo + B]
+        c0, ph = np.ascontiguousarray(c0), np.ascontiguousarray(ph)
         c0_h.append(torch.from_numpy(c0.view(np.int64)).pin_memory())
         phi_h.append(torch.from_numpy(ph.view(np.int32)).pin_memory())
         c0_d.append(c0_h[-1].to(dev))
@@ -322,9 +439,10 @@ def main():
         n_i, n_o = cfg.fc.n_i, cfg.fc.n_o
         wspec, benc = ctx.fc_pack_weights(d(synth.fc_weights(cfg)),
                                           d(synth.fc_bias(cfg)))
-        fc_c0 = synth.uniform_residues((B, L, N), cfg.primes,
-                                       cfg.seed + 1000 * rank, "c0", 99)
-        fc_ph = synth.phi1((B, n_o), cfg.t, cfg.seed + 1000 * rank, 99)
+        Bg = B if scaling == "weak" else cfg.B
+        fc_c0 = np.ascontiguousarray(synth.uniform_residues(
+            (Bg, L, N), cfg.primes, seed_r, "c0", 99)[b_lo:b_lo + B])
+        fc_ph = np.ascontiguousarray(synth.phi1((Bg, n_o), cfg.t, seed_r, 99)[b_lo:b_lo + B])
         fc = dict(n_i=n_i, n_o=n_o, wspec=wspec, benc=benc,
                   c0_h=torch.from_numpy(fc_c0.view(np.int64)).pin_memory(),
                   ph_h=torch.from_numpy(fc_ph.view(np.int32)).pin_memory())
@@ -337,6 +455,11 @@ def main():
     torch.cuda.synchronize()
 
     evals_step = sum(lw.evals for lw in layers) + (B if fc else 0)
+    evals_all = evals_step                # every rank's work (value = all ranks / max time)
+    if world > 1:
+        _t = torch.tensor([evals_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(_t)
+        evals_all = int(_t.item())
     launches_step = 3 * len(layers) * (nstr if args.overlap == "batch" else 1) + \
         (2 if fc else 0)
 
@@ -436,7 +559,7 @@ def main():
         e1.record()
         barrier()
         ms_po = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-        payload_only = {"ms_per_step": ms_po, "value": evals_step * world / (ms_po * 1e-3),
+        payload_only = {"ms_per_step": ms_po, "value": evals_all / (ms_po * 1e-3),
                         "what": "he_conv_ex with d_out = NULL: extraction, mask and "
                                 "payload fused, full c0^r not materialised"}
         po_flag[0] = False
@@ -513,20 +636,31 @@ def main():
     ntt_int = os.environ.get("HE_NTT", "")[:1] == "i"
     ct_roof = u1["ct_bfly"]["per_s"] if ntt_int else u1["dp_ct_bfly"]["per_s"]
     gs_roof = u1["gs_bfly"]["per_s"] if ntt_int else u1["dp_gs_bfly"]["per_s"]
+    # int8 tensor-core MAC: 49 u8 x u8 products per 50-bit modMAC, so its alu
+    # roof is the measured int8 rate of the instruction it issues / 49:
+    # tcgen05.mma M=128 N=16 (k_mac_tc, B >= 128) or mma.sync (k_mac_imma);
+    # HE_MAC=imad runs the IMAD kernel, whose roof is U1 "modmac".
+    mac_tc_used = (B >= 128 and os.environ.get("HE_MAC_TC", "2") != "0") or \
+        os.environ.get("HE_MAC_TC") == "1"
+    if os.environ.get("HE_MAC", "")[:1] == "i":
+        mac_roof, mac_roof_src = u1["modmac"]["per_s"], "U1 modmac (IMAD)"
+    elif mac_tc_used:
+        mac_roof, mac_roof_src = u1["tc_i8_m128n16"]["per_s"] / 49, \
+            "U1 tcgen05.mma kind::i8 M=128 N=16 int8 MAC/s / 49"
+    else:
+        mac_roof, mac_roof_src = u1["imma_u8"]["per_s"] / 49, \
+            "U1 mma.sync m16n8k32 int8 MAC/s / 49"
     kern = {
         "ntt_fwd": (st["ntt_fwd"], W_ntt_bfly, ct_roof, "Gbutterfly/s", W_ntt_bytes),
-        # int8 tensor-core MAC: 49 u8 x u8 products per 50-bit modMAC, so its
-        # alu roof is the measured mma.sync int8 rate / 49 (HE_MAC=imad runs
-        # the IMAD kernel, whose roof is U1 "modmac").
-        "mac_fold": (st["mac_fold"], W_macs,
-                     u1["modmac"]["per_s"] if os.environ.get("HE_MAC", "")[:1] == "i"
-                     else u1["imma_u8"]["per_s"] / 49, "Gmodmac/s", W_mac_bytes),
+        "mac_fold": (st["mac_fold"], W_macs, mac_roof, "Gmodmac/s", W_mac_bytes),
         "intt_scatter": (st["intt_scatter"], W_intt_bfly, gs_roof, "Gbutterfly/s",
                          W_intt_bytes),
     }
     rl = {}
     for name, (ms, ops, alu_peak, unit, byts) in kern.items():
         t = ms * 1e-3
+        if t <= 0:
+            continue
         t_alu, t_hbm = ops / alu_peak, byts / (hbm_gbs * 1e9)
         bound = "alu" if t_alu >= t_hbm else "hbm"
         if bound == "alu":
@@ -541,17 +675,30 @@ def main():
                         "frac": byts / t / 1e9 / hbm_gbs, "traffic": None,
                         "share_of_step": ms / ms_seq,
                         "alu_frac": (ops / t) / alu_peak}
-    # DRAM traffic per launch from the committed ncu pass (profiles/), beside
-    # the algorithmic bytes per launch (traffic well above it = re-reads)
+    for name in ("ntt_fwd", "intt_scatter"):          # FP64 kernels: DFMA-pipe view
+        if name in rl:
+            ms, ops = kern[name][0], kern[name][1]
+            rl[name]["dfma_pipe_frac"] = ops / (ms * 1e-3) * DP_OPS_PER_BFLY / u1["dfma"]["per_s"]
+    if "mac_fold" in rl:
+        rl["mac_fold"]["alu_peak_source"] = mac_roof_src
+    # DRAM traffic per launch from an ncu pass of THIS workload (profiles/
+    # traffic_<workload>.json, written by scripts/traffic_summary.py from the
+    # same bench command), beside the algorithmic bytes per launch (traffic
+    # well above it = re-reads).  A file of another workload is never used.
     tr_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                           "traffic_r01.json")
+                           f"traffic_{args.workload}.json")
     tr = json.load(open(tr_path)) if os.path.exists(tr_path) else {}
+    if tr and tr.get("workload") not in (None, args.workload):
+        tr = {}
     for name, (ms, ops, alu_peak, unit, byts) in kern.items():
+        if name not in rl:
+            continue
         rl[name]["algorithmic_bytes_per_launch"] = byts / len(layers)
         if name in tr:
             rl[name]["traffic"] = tr[name]["mean_dram_bytes_per_launch"]
-            rl[name]["traffic_source"] = "profiles/traffic_r01.json (ncu, " + \
-                str(tr[name]["launches"]) + " launches)"
+            rl[name]["traffic_source"] = f"profiles/traffic_{args.workload}.json (ncu " + \
+                "dram__bytes_read.sum + dram__bytes_write.sum, " + \
+                str(tr[name]["launches"]) + " launches, " + str(tr.get("code", "?")) + ")"
     dom = max(kern, key=lambda k: kern[k][0])
     roofline = dict(rl[dom])
     roofline["kernel"] = dom
@@ -560,6 +707,42 @@ def main():
     roofline["timed_in"] = ("sequential analysis pass (streams=1) of the same step, "
                             "CUDA events around each kernel (he_conv_ex)")
 
+    # ---- NTT limbs/s at every ring size of BASELINE's configs (N = 1024,
+    # 8192, 16384, 32768; he_ntt_forward / he_ntt_inverse alone, >= 256 MB of
+    # limbs per launch so the data is larger than L2), each against the FP64
+    # roofs: U1's measured butterfly sequence and the DFMA pipe at the
+    # algorithmic 8 FP64 operations per butterfly (dp_mulmod's 6 + add/sub)
+    ntt_sweep = []
+    if not args.profile:
+        for (vN, vprimes) in [(1024, synth.PRIMES_CFG1), (8192, synth.PRIMES_N8192[:2]),
+                              (16384, synth.PRIMES_N16384[:2]),
+                              (32768, synth.PRIMES_N32768[:2])]:
+            vctx = he.Context(list(vprimes), vN.bit_length() - 1, cfg.t, local)
+            vL = len(vprimes)
+            nlv = max(vL, (256 << 20) // (8 * vN) // vL * vL)
+            vbuf = torch.from_numpy(synth.uniform_residues(
+                (nlv // vL, vL, vN), list(vprimes), 7, "misc", vN).view(np.int64)).to(dev)
+            res = {"N": vN, "limbs_per_launch": nlv}
+            lg = vN.bit_length() - 1
+            for nm, fn, roof in (("forward", vctx.ntt_forward, ct_roof),
+                                 ("inverse", vctx.ntt_inverse, gs_roof)):
+                for _ in range(3):
+                    fn(vbuf)
+                a0, a1 = mk(), mk()
+                a0.record()
+                for _ in range(5):
+                    fn(vbuf)
+                a1.record()
+                torch.cuda.synchronize()
+                tt = a0.elapsed_time(a1) / 5 * 1e-3
+                lps = nlv / tt
+                bfly = vN // 2 * lg
+                res[nm] = {"limbs_per_s": lps,
+                           "frac_u1_fp64_roof": lps * bfly / roof,
+                           "frac_dfma_pipe": lps * bfly * DP_OPS_PER_BFLY / u1["dfma"]["per_s"],
+                           "hbm_frac": lps * 16 * vN / (hbm_gbs * 1e9)}
+            ntt_sweep.append(res)
+            del vbuf, vctx
     # ---- NTT limbs/s (he_ntt_forward alone, 1024 limbs > L2)
     nl = 1024 // L * L
     buf = torch.from_numpy(synth.uniform_residues(
@@ -591,6 +774,7 @@ def main():
     ntt["inverse_limbs_per_s"] = nl / t_inv
     inv_roof = min(gs_roof / (N // 2 * logN), ntt["hbm_roof_limbs_per_s"])
     ntt["inverse_frac"] = ntt["inverse_limbs_per_s"] / inv_roof
+    ntt["sizes"] = ntt_sweep
     del buf
 
     # ---- e2e: the server loop through the public API with host buffers.
@@ -698,7 +882,7 @@ def main():
         x1.record()
         barrier()
         ms_e2e = max_over_ranks(x0.elapsed_time(x1) / args.steps)
-        e2e = {"value": evals_step * world / (ms_e2e * 1e-3), "unit": "ct×pt evals/s",
+        e2e = {"value": evals_all / (ms_e2e * 1e-3), "unit": "ct×pt evals/s",
                "ms_per_step": ms_e2e, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h,
                "wire": "50-bit packed residues (he_residues_pack50/unpack50); "
@@ -766,7 +950,7 @@ def main():
         barrier()
         ms_ext = max_over_ranks(x0.elapsed_time(x1) / args.steps)
         e2e["sparse_upload_modswitch"] = {
-            "ms_per_step": ms_ext, "value": evals_step * world / (ms_ext * 1e-3),
+            "ms_per_step": ms_ext, "value": evals_all / (ms_ext * 1e-3),
             "h2d_bytes_per_step": sum(c0c_pk_h[i].numel() if sp[i] else c0_pk_h[i].numel()
                                       for i in range(len(layers))) +
             (fc["c0_pk_h"].numel() if fc else 0),
@@ -777,7 +961,7 @@ def main():
                     "modulus-switched to one limb"}
         e2e["modswitch"] = {
             "L_keep": 1, "ms_per_step": ms_sw,
-            "value": evals_step * world / (ms_sw * 1e-3),
+            "value": evals_all / (ms_sw * 1e-3),
             "d2h_bytes_per_step": sum(t.numel() for t in sw_pk_h) +
             (fc["out_pk_h"].numel() if fc else 0),
             "kernel_ms_per_step": sw_ms,
@@ -785,25 +969,50 @@ def main():
 
     # ---- multi-GPU: the one exchange of the path -- every
     # rank's compact payload assembled on all ranks (NCCL all_gather over
-    # NVLink), timed outside the step
+    # NVLink, by image or by output block as partitioned), timed alone and
+    # as part of the step (the step followed by the gather, same clocks)
     gather = None
     if world > 1 and not args.profile:
-        from paper_2409_05205_b200.dist import gather_payload
+        from paper_2409_05205_b200.dist import gather_blocks, gather_payload
+
+        def assemble():
+            for i, c in enumerate(comps):
+                if axis == "out_block":
+                    gather_blocks(c, ob_span[i][2])
+                else:
+                    gather_payload(c, B_global)
+            if fc and axis != "out_block":
+                gather_payload(fc["out"], B_global)
+
         for _ in range(2):
-            for c in comps:
-                gather_payload(c, B * world)
+            assemble()
         barrier()
         g0, g1 = mk(), mk()
         g0.record()
         for _ in range(args.steps):
-            for c in comps:
-                gather_payload(c, B * world)
+            assemble()
         g1.record()
         barrier()
         ms_g = max_over_ranks(g0.elapsed_time(g1) / args.steps)
         gbytes = sum(c.numel() * 8 for c in comps) * world
+        for _ in range(2):
+            run_step()
+            assemble()
+        barrier()
+        g0.record()
+        for _ in range(args.steps):
+            run_step()
+            assemble()
+        g1.record()
+        barrier()
+        ms_sg = max_over_ranks(g0.elapsed_time(g1) / args.steps)
         gather = {"ms_per_step": ms_g, "bytes_per_step_all_ranks": gbytes,
-                  "GBps": gbytes / (ms_g * 1e-3) / 1e9}
+                  "GBps": gbytes / (ms_g * 1e-3) / 1e9, "axis": axis,
+                  "with_gather": {"ms_per_step": ms_sg,
+                                  "value": evals_all / (ms_sg * 1e-3),
+                                  "what": "the headline step followed by the NCCL all_gather "
+                                          "of every layer's compact payload (and the FC "
+                                          "output), K steps timed together"}}
 
     # ---- client mirror path: the client's per-layer work
     # of Alg. 1 Lines 21-24 + Eq. (2) -- c1^r = valid slots of
@@ -812,8 +1021,10 @@ def main():
     # the server's offline p = fhat a + e_f (he_server_init_p), timed once.
     # v_beta s stand-ins are the resident uniform residues c0_d (the kernels'
     # cost does not depend on the values).
+    extras = not (args.no_client or args.no_extras or args.profile or world > 1 or
+                  axis == "out_block")
     client = None
-    if not args.no_client and not args.profile:
+    if extras:
         a_d = d(synth.uniform_residues((L, N), cfg.primes, cfg.seed, "a"))
         i0, i1 = mk(), mk()
         i0.record()
@@ -867,7 +1078,7 @@ def main():
     # output channel, Alg. 1 Lines 14-17 literally) on the same conv layers,
     # one launch sequence, to show what the fold + incomplete transform save
     ablation = None
-    if not args.no_client and not args.profile:
+    if extras:
         import ctypes
         wsp = torch.empty(max(int(he._lib.he_conv_plain_workspace_bytes(
             ctx._h, ctypes.byref(lw.p), B)) for lw in layers), dtype=torch.uint8, device=dev)
@@ -894,7 +1105,7 @@ def main():
     # ---- FC packing variants (§8(f)): sub-matrix tiling for n_i n_o > N
     # (R27) on this ring, and the FC at N = 32768 (config 5's ring)
     fc_var = None
-    if not args.no_client and not args.profile:
+    if extras:
         fc_var = []
         for (vn, vprimes, vlog, n_i, n_o, vB) in [
                 ("fc512x1000_tiled", cfg.primes, cfg.log2N, 512, 1000, B),
@@ -925,11 +1136,59 @@ def main():
                            "evals_per_s": vB * n_ib * n_t / (ms * 1e-3)})
             del vctx, wsp, ben, c0v, phv, outv, wsv
 
+    # ---- multi-image packing (§8(f) row 4b, R31): the same images and layer,
+    # P images per ciphertext at the paper's s = c_i (he_pack_input_multi
+    # layout; he_conv unchanged; he_mask_extract_multi payload), against the
+    # one-image-per-ciphertext step above: time, ciphertexts and bytes per image
+    multi = None
+    if (extras or (args.no_extras and not args.profile and world == 1)) and \
+            cfg.idx in (3, 5) and axis == "batch":
+        Ly = cfg.conv[0]
+        so = Ly.c_i if Ly.c_i & (Ly.c_i - 1) == 0 else 0
+        pm = ctx.plan(Ly.c_i, Ly.c_o, Ly.w_i, Ly.h_i, Ly.f_w, Ly.f_h, Ly.stride, Ly.pad, so)
+        Dm, Pm = ctx.multi_image_spacing(pm)
+        Bc = -(-B // Pm)
+        fm = ctx.pack_filters(pm, d(synth.weights(cfg, 0)))
+        c0m = torch.from_numpy(synth.uniform_residues((Bc, pm.n_ib, L, N), cfg.primes, seed_r,
+                                                      "c0", 77).view(np.int64)).to(dev)
+        phm = d(synth.phi1((Bc, pm.n_ob, N), cfg.t, seed_r, 77))
+        outm = ctx.empty_u64(Bc, pm.n_ob, L, N)
+        compm = ctx.empty_u64(Bc, pm.n_ob, L, Pm * pm.n_valid)
+        wsm = ctx.conv_workspace(pm, Bc)
+
+        def mstep():
+            ctx.conv(pm, c0m, fm, phm, outm, wsm)
+            ctx.mask_extract_multi(pm, outm, Pm, Dm, compact=compm)
+
+        for _ in range(3):
+            mstep()
+        barrier()
+        m0, m1 = mk(), mk()
+        m0.record()
+        for _ in range(args.steps):
+            mstep()
+        m1.record()
+        barrier()
+        ms_m = m0.elapsed_time(m1) / args.steps
+        p1 = layers[0].p
+        multi = {"s": pm.s, "images_per_ciphertext": Pm, "spacing_D": Dm,
+                 "ciphertexts": Bc, "images": B, "ms_per_step": ms_m,
+                 "images_per_s": B / (ms_m * 1e-3),
+                 "one_image_per_ct": {"s": p1.s, "ms_per_step": ms_step,
+                                      "images_per_s": B / (ms_step * 1e-3)},
+                 "c0_bytes_per_image": 8 * pm.n_ib * L * N * Bc / B,
+                 "c0_bytes_per_image_one_per_ct": 8 * p1.n_ib * L * N,
+                 "out_bytes_per_image": 8 * pm.n_ob * L * N * Bc / B,
+                 "out_bytes_per_image_one_per_ct": 8 * p1.n_ob * L * N,
+                 "what": "he_conv (full c0^r) + he_mask_extract_multi on ceil(B/P) "
+                         "multi-image ciphertexts (reading R31) vs the headline step"}
+        del c0m, phm, outm, compm, wsm, fm
+
     # ---- chained pipeline (§8(f) row 3): the whole encrypted network, layer
     # to layer -- client encryption, server Conv/FC, client share,
     # decryption, R29 stub -- on the same 19 conv layers + FC, B images
     chain = None
-    if not args.no_client and not args.profile and cfg.fc is not None:
+    if extras and cfg.fc is not None:
         from paper_2409_05205_b200.chain import Chain
         rs = np.random.default_rng(cfg.seed)
         sk = synth.secret_key(N, cfg.h, cfg.seed)
@@ -965,7 +1224,7 @@ def main():
 
     # ---- CPU baseline: the oracle as it stands, rank 0, bounded sample
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline and not args.profile:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         from oracle import ref as R
         ring = R.Ring(N, cfg.primes, cfg.t)
         nimg = min(B, 32) if cfg.idx == 4 else 1
@@ -989,22 +1248,42 @@ def main():
         cpu = {"value": ev / dt, "unit": "ct×pt evals/s", "cores": os.cpu_count(),
                "kind": "oracle",
                "sample": f"{reps} pass(es) x {nimg} image(s) x all {len(layers)} conv"
-                         f"{' + FC' if fc else ''} layers ({dt:.1f} s wall)"}
+                         f"{' + FC' if fc else ''} layers ({dt:.1f} s wall)",
+               "cpu_model": cpu_model()}
+        # the same oracle on one host thread (the paper's own numbers are
+        # single-thread): a child process with OMP_NUM_THREADS=1
+        # times one image through the same layers
+        try:
+            r1 = subprocess.run(
+                [sys.executable, "-c",
+                 "import sys; sys.path.insert(0, %r); import bench; "
+                 "bench.oracle_single_thread(%d)" % (ROOT, cfg.idx)],
+                env=dict(os.environ, OMP_NUM_THREADS="1", CUDA_VISIBLE_DEVICES=""),
+                capture_output=True, text=True, timeout=300)
+            cpu["single_thread"] = json.loads(r1.stdout.strip().splitlines()[-1])
+        except Exception as exc:                      # reported, not fatal
+            cpu["single_thread"] = {"error": repr(exc)[:200]}
 
     clocks = sampler.summary() if not args.profile else None
     if rank == 0:
-        value = evals_step * world / (ms_step * 1e-3)
+        value = evals_all / (ms_step * 1e-3)
         line = {
             "metric": "Conv+FC layer ct×pt evals/sec", "value": value,
             "unit": "ct×pt evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "u64", "data": "synthetic",
             "config": {"workload": f"cfg{cfg.idx} {cfg.name}: "
                                    f"{len(layers)} conv{' + FC' if fc else ''}, "
-                                   f"N={N}, L={L}, B={B}/GPU",
-                       "global_batch": B * world, "N": N, "L": L,
-                       "parallelism": f"dp{world} (batch-sharded, no collective)",
+                                   f"N={N}, L={L}, "
+                                   + (f"B={B}/GPU" if scaling == "weak" else
+                                      f"B={cfg.B} global"),
+                       "global_batch": B_global, "N": N, "L": L,
+                       "parallelism": (f"dp{world} (batch-sharded, no data-path collective)"
+                                       if axis == "batch" else
+                                       f"ob{world} (output-channel blocks, no data-path "
+                                       f"collective)"),
+                       "partition_axis": axis,
                        "streams": nstr, "overlap": args.overlap,
                        "cuda_graph": graph is not None,
                        "mac": ("tcgen05.mma kind::i8, TMEM accumulators (k_mac_tc)"
@@ -1012,12 +1291,13 @@ def main():
                                or os.environ.get("HE_MAC_TC") == "1"
                                else "mma.sync int8 byte planes (k_mac_imma)"),
                        "l2": "inputs larger than L2 (>1 GB touched per step)"},
-            "ms_per_plain20_image": ms_step / B if cfg.idx == 4 else None,
+            "ms_per_plain20_image": ms_step / B_global if cfg.idx == 4 else None,
             "sequential_ms_per_step": ms_seq,
             "ntt": ntt, "stages_ms_per_step": st, "per_layer": per_layer,
             "roofline": roofline,
             "roofline_all": rl, "u1": u1, "init_ms": init_ms,
-            "cpu_baseline": cpu, "e2e": e2e, "payload_only": payload_only, "gather": gather, "ablation": ablation, "client": client, "chain": chain, "fc_variants": fc_var, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "payload_only": payload_only, "gather": gather,
+            "multi_image": multi, "ablation": ablation, "client": client, "chain": chain, "fc_variants": fc_var, "clocks": clocks,
             "gpu_launches": launches_step * args.steps,
         }
         print(json.dumps(line), flush=True)

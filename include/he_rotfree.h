@@ -186,6 +186,39 @@ he_status he_mask_extract(const he_ctx* ctx, const he_conv_plan* p,
                           const uint32_t* d_phi1, uint64_t* d_compact,
                           void* stream);
 
+/* ------------------------------------------------ multi-image packing */
+/* SURVEY §8(f) row 4b, reading R31, a protocol extension
+ * beyond the paper (which keeps one image per ciphertext):
+ * P images share one input ciphertext at offsets p*D,
+ *   c(X) = sum_{p<P} X^{p D} i_p(X)  (mod X^N + 1),  i_p = Eq. (5) packing,
+ * and he_conv on it (unchanged plan, filters and kernels) leaves image p's
+ * conv outputs at p*D + the single-image valid slots.  D is the least
+ * multiple of s with D > hi and D + lo > v_hi, where [lo, hi] holds the
+ * exponents of i_p f (nonzero pixels, Eq. (6)-(7) filter) and [0, v_hi] the
+ * valid slots; P = floor(N / D).  he_multi_image_spacing returns them
+ * (HE_ESHAPE if P < 1). */
+he_status he_multi_image_spacing(const he_ctx* ctx, const he_conv_plan* p,
+                                 int32_t* D, int32_t* P);
+
+/* a1 for multi-image ciphertexts: d_img int32 [B][c_i][w_i][h_i] (image
+ * b = c*P + p goes to slot p of ciphertext c; a short last ciphertext has
+ * zero images) -> d_pt uint64 [Bc][n_ib][L][N], Bc = ceil(B / P), enc_j of
+ * c(X) (R2), plus the optional d_ve [Bc][n_ib][L][N] (v b + e0) as in
+ * he_pack_input.  P and D must be he_multi_image_spacing's (or P smaller). */
+he_status he_pack_input_multi(const he_ctx* ctx, const he_conv_plan* p,
+                              const int32_t* d_img, int B, int P, int D,
+                              const uint64_t* d_ve, uint64_t* d_pt, void* stream);
+
+/* a7-a8 for multi-image ciphertexts: from d_out uint64 [Bc][n_ob][L][N]
+ * (he_conv on he_pack_input_multi ciphertexts) gather, for p < P, image p's
+ * valid slots p*D + i (i as he_mask_extract) into d_compact uint64
+ * [Bc][n_ob][L][P n_valid] (image-major); + enc_j(phi1[c][ob][p*D + i]) if
+ * d_phi1 uint32 [Bc][n_ob][N] is non-NULL. */
+he_status he_mask_extract_multi(const he_ctx* ctx, const he_conv_plan* p,
+                                const uint64_t* d_out, int Bc, int P, int D,
+                                const uint32_t* d_phi1, uint64_t* d_compact,
+                                void* stream);
+
 /* -------------------------------------------------------------------- FC */
 /* FC layer with n_i inputs, n_o outputs, any sizes.
  * When n_i n_o > N the weight matrix is decomposed into sub-matrices

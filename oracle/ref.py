@@ -43,6 +43,12 @@ function below is checked against something other than itself:
   splitmix64_py / phi1_stream        test_oracle_ring: Vigna's published
         SplitMix64 reference value.
   mod_switch                         test_oracle_protocol: exact rationals.
+  multi_image_spacing / shift_negacyclic / pack_input_multi_int /
+  output_positions_multi / compact_multi   test_oracle_multi: integer-mode
+        products equal every image's brute-force conv at its shifted slots
+        (and one row less of spacing breaks it); a trivially encrypted
+        multi-image ciphertext through conv_server decrypts to every
+        image's conv mod t.
   relu_requant / avgpool             test_oracle_stub: hand-computed golden
         values (tests/golden/r29_stub.json); ReLU == PAPER.md:86's
         (X + sign(X) X) / 2.
@@ -519,6 +525,72 @@ def compact(out_full: np.ndarray, plan: ConvPlan) -> np.ndarray:
     """a8: gather the valid slots ("do not need to be sent").
     [B][n_ob][L][N] -> [B][n_ob][L][n_valid]."""
     return np.ascontiguousarray(out_full[..., output_positions(plan)])
+
+
+# ---------------------------------------------------------------------------
+# Multi-image packing (SURVEY §8(f) row 4b; reading R31 -- a protocol
+# extension beyond the paper, which keeps one image per ciphertext,
+# PAPER.md:304).  P images share one input ciphertext at offsets p*D:
+#   c(X) = sum_{p<P} X^{p D} i_p(X)   (mod X^N + 1),
+# with i_p the Eq. (5) packing of image p.  The server's product with the
+# unchanged Eq. (6)/(7) filters is linear, so image p's conv outputs appear
+# at p*D + (the single-image valid slots) provided no other image's product
+# reaches them.  Counting only the image's nonzero (unpadded) pixels, the
+# product i_p f (with the Eq. (7) shift t_n < s) has exponents in [lo, hi],
+# and image p's valid slots lie in [0, v_hi].  The spacing
+#   D = the least multiple of s with D > hi and D + lo > v_hi,  P = floor(N/D)
+# makes the neighbour below end before p*D and the one above start after the
+# valid slots, and (P*D <= N) the lowest image's negative exponents wrap
+# (negacyclic) above the top image's slots, so every slot is exactly image
+# p's.  D is a multiple of s because the server computes slots s*j + t_n.
+# ---------------------------------------------------------------------------
+def multi_image_spacing(plan: ConvPlan) -> Tuple[int, int]:
+    """(D, P): image spacing and images per ciphertext (R31)."""
+    s, hp = plan.s, plan.h_p
+    pw, ph = (plan.w_p - plan.w_i) // 2, (plan.h_p - plan.h_i) // 2
+    # Eq. (5) exponents of the nonzero pixels, Eq. (6) exponents (+ t_n < s)
+    in_lo = s * ((pw - plan.f_w) * hp + ph)
+    in_hi = s * ((pw + plan.w_i - 1 - plan.f_w) * hp + ph + plan.h_i - 1) + plan.c_ib - 1
+    f_lo = s * (hp - plan.f_h + 1) - (plan.c_ib - 1)
+    f_hi = s * hp * plan.f_w + (s - 1)
+    lo, hi = in_lo + f_lo, in_hi + f_hi
+    S = plan.stride
+    v_hi = s * (S * (plan.w_o - 1) * hp + S * (plan.h_o - 1)) + s - 1
+    D = max(hi + 1, v_hi - lo + 1)
+    D = -(-D // s) * s
+    return D, plan.N // D
+
+
+def shift_negacyclic(a: np.ndarray, k: int) -> np.ndarray:
+    """X^k a(X) mod X^N + 1 for integer coefficient vectors (last axis)."""
+    N = a.shape[-1]
+    out = np.zeros_like(a)
+    for e in range(N):
+        f, sg = reduce_exp(e + k, N)
+        out[..., f] += sg * a[..., e]
+    return out
+
+
+def pack_input_multi_int(imgs: np.ndarray, plan: ConvPlan, D: int) -> np.ndarray:
+    """imgs [P][c_i][w_i][h_i] -> int64 [n_ib][N] = sum_p X^{p D} i_p(X)."""
+    out = np.zeros((plan.n_ib, plan.N), dtype=np.int64)
+    for p in range(imgs.shape[0]):
+        out += shift_negacyclic(pack_input_int(imgs[p], plan), p * D)
+    return out
+
+
+def output_positions_multi(plan: ConvPlan, P: int, D: int) -> np.ndarray:
+    """Valid slots of P images sharing a ciphertext: image p's single-image
+    slots shifted by p*D (all below N for P*D <= N), image-major order."""
+    pos = output_positions(plan)
+    allp = np.concatenate([p * D + pos for p in range(P)])
+    assert allp.max() < plan.N
+    return allp
+
+
+def compact_multi(out_full: np.ndarray, plan: ConvPlan, P: int, D: int) -> np.ndarray:
+    """a8 for multi-image ciphertexts: [B][n_ob][L][N] -> [B][n_ob][L][P n_valid]."""
+    return np.ascontiguousarray(out_full[..., output_positions_multi(plan, P, D)])
 
 
 # ---------------------------------------------------------------------------

@@ -122,6 +122,9 @@ _sig("he_pk_mask", [_P, _P, _P, ctypes.c_long, _P, _P, _P, _SZ, _P])
 _sig("he_pk_mask_vs", [_P, _P, _P, ctypes.c_long, _P, _P, _P, _P, _P, _SZ, _P])
 _sig("he_relu_requant", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _I, _I, _P, _P])
 _sig("he_avgpool", [_P, ctypes.c_long, _I, _P, _P])
+_sig("he_multi_image_spacing", [_P, ctypes.POINTER(ConvPlan), _P, _P])
+_sig("he_pack_input_multi", [_P, ctypes.POINTER(ConvPlan), _P, _I, _I, _I, _P, _P, _P])
+_sig("he_mask_extract_multi", [_P, ctypes.POINTER(ConvPlan), _P, _I, _I, _I, _P, _P, _P])
 _sig("he_unmask", [_P, _P, _P, ctypes.c_long, _P, _P])
 _sig("he_c0_compact", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P])
 _sig("he_filter_coeffs", [_P, ctypes.POINTER(ConvPlan), _P, _I, _P, _P, _SZ, _P])
@@ -133,7 +136,8 @@ _sig("he_fc_server_p_workspace_bytes", [_P, ctypes.POINTER(FcDesc)], _SZ)
 _sig("he_fc_server_init_p", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _P, _P, _SZ, _P])
 _sig("he_pack_fc_client_p", [_P, ctypes.POINTER(FcDesc), _P, _P, _P, _SZ, _P])
 
-EXPORTED = ["he_status_str", "he_last_cuda_error", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
+EXPORTED = ["he_status_str", "he_last_cuda_error", "he_multi_image_spacing",
+            "he_pack_input_multi", "he_mask_extract_multi", "he_ctx_create", "he_ctx_destroy", "he_ctx_psi",
             "he_conv_plan_make", "he_conv_plan_dense", "he_pack_input", "he_filter_bytes",
             "he_pack_filters_workspace_bytes", "he_pack_filters",
             "he_conv_workspace_bytes", "he_conv", "he_conv_ex", "he_mask_extract",
@@ -294,6 +298,39 @@ class Context:
                                     self._ptr(out_full), B, self._ptr(phi1),
                                     self._ptr(compact), _stream(stream)),
                "he_mask_extract")
+        return compact
+
+    # ------------------------------------------------ multi-image packing
+    def multi_image_spacing(self, p: ConvPlan):
+        """(D, P) of he_multi_image_spacing (R31)."""
+        D, P = ctypes.c_int32(), ctypes.c_int32()
+        _check(_lib.he_multi_image_spacing(self._h, ctypes.byref(p), ctypes.byref(D),
+                                           ctypes.byref(P)), "he_multi_image_spacing")
+        return D.value, P.value
+
+    def pack_input_multi(self, p: ConvPlan, img: torch.Tensor, P: int, D: int,
+                         ve: Optional[torch.Tensor] = None,
+                         out: Optional[torch.Tensor] = None, stream=None):
+        B = img.shape[0]
+        Bc = -(-B // P)
+        if out is None:
+            out = self.empty_u64(Bc, p.n_ib, self.L, self.N)
+        self._dev(img, ve, out)
+        _check(_lib.he_pack_input_multi(self._h, ctypes.byref(p), self._ptr(img), B, P, D,
+                                        self._ptr(ve), self._ptr(out), _stream(stream)),
+               "he_pack_input_multi")
+        return out
+
+    def mask_extract_multi(self, p: ConvPlan, out_full: torch.Tensor, P: int, D: int,
+                           phi1: Optional[torch.Tensor] = None,
+                           compact: Optional[torch.Tensor] = None, stream=None):
+        Bc = out_full.shape[0]
+        if compact is None:
+            compact = self.empty_u64(Bc, p.n_ob, self.L, P * p.n_valid)
+        self._dev(out_full, phi1, compact)
+        _check(_lib.he_mask_extract_multi(self._h, ctypes.byref(p), self._ptr(out_full), Bc,
+                                          P, D, self._ptr(phi1), self._ptr(compact),
+                                          _stream(stream)), "he_mask_extract_multi")
         return compact
 
     # ------------------------------------------------------------------ FC

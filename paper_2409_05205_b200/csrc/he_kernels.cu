@@ -1928,6 +1928,148 @@ extern "C" he_status he_mask_extract(const he_ctx* c, const he_conv_plan* p,
     return HE_OK;
 }
 
+// ===================================================== multi-image packing
+// P images at offsets p D of one ciphertext.
+static void multi_spacing(const PlanDev& P, long N, int* D, int* Pn) {
+    const long s = P.s, hp = P.h_p;
+    const long pw = P.padw, ph = P.padh;
+    const long in_lo = s * ((pw - P.f_w) * hp + ph);
+    const long in_hi = s * ((pw + P.w_i - 1 - P.f_w) * hp + ph + P.h_i - 1) + P.c_ib - 1;
+    const long f_lo = s * (hp - P.f_h + 1) - (P.c_ib - 1);
+    const long f_hi = s * hp * P.f_w + (s - 1);
+    const long lo = in_lo + f_lo, hi = in_hi + f_hi;
+    const long S = P.stride;
+    const long v_hi = s * (S * (P.w_o - 1) * hp + S * (P.h_o - 1)) + s - 1;
+    long d = std::max(hi + 1, v_hi - lo + 1);
+    d = (d + s - 1) / s * s;
+    *D = (int)d;
+    *Pn = (int)(N / d);
+}
+
+extern "C" he_status he_multi_image_spacing(const he_ctx* c, const he_conv_plan* p, int32_t* D,
+                                            int32_t* Pn) {
+    if (!c || !p || !D || !Pn) return HE_EINVAL;
+    if (!plan_ok(c, p)) return HE_ESHAPE;
+    int d, n;
+    multi_spacing(plan_dev(p), c->N, &d, &n);
+    if (n < 1) return HE_ESHAPE;
+    *D = d;
+    *Pn = n;
+    return HE_OK;
+}
+
+// coefficient i of ciphertext (cb, beta, l): for each slot p the raw Eq. (5)
+// exponent E with E + p D = i (mod N) is one of i - p D, i - p D -+ N (sign -1
+// for the wrapped ones); at most one (p, E) lands on an image pixel.
+__global__ void k_pack_input_multi(const int32_t* __restrict__ img, const u64* __restrict__ ve,
+                                   u64* __restrict__ out, PlanDev P, int B, int Pn, int D,
+                                   int Bc, int L, int logN, const he_limb* __restrict__ limbs,
+                                   u64 t, u64 r_t, u64 t_inv) {
+    const long N = 1L << logN;
+    const long total = (long)Bc * P.n_ib * L * N;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx & (N - 1));
+        const long r = idx >> logN;
+        const int l = (int)(r % L);
+        const long bb = r / L;
+        const int beta = (int)(bb % P.n_ib), cb = (int)(bb / P.n_ib);
+        long coef = 0;
+        for (int p = 0; p < Pn; ++p) {
+            const int b = cb * Pn + p;
+            if (b >= B) break;
+#pragma unroll
+            for (int cand = 0; cand < 3; ++cand) {
+                const long E = (long)i - (long)p * D + (cand == 0 ? 0 : (cand == 1 ? -N : N));
+                const int m = (int)(E & (P.s - 1));          // E mod s (floor)
+                const long Pq = (E - m) >> P.logs;
+                const int kk = floordiv((int)Pq, P.h_p);
+                const int ll = (int)Pq - kk * P.h_p;
+                const int k = kk + P.f_w;
+                const int ch = beta * P.c_ib + m;
+                if (k >= 0 && k < P.w_p && m < P.c_ib && ch < P.c_i) {
+                    const int ki = k - P.padw, li = ll - P.padh;
+                    if (ki >= 0 && ki < P.w_i && li >= 0 && li < P.h_i) {
+                        const long pix = img[(((long)b * P.c_i + ch) * P.w_i + ki) * P.h_i + li];
+                        coef += cand == 0 ? pix : -pix;
+                    }
+                }
+            }
+        }
+        long mt = coef % (long)t;
+        if (mt < 0) mt += t;
+        const he_limb& Lm = limbs[l];
+        u64 v = enc_plain((u64)mt, Lm, t, r_t, t_inv);
+        if (ve) v = addmod(v, ve[idx], Lm.q);
+        out[idx] = v;
+    }
+}
+
+extern "C" he_status he_pack_input_multi(const he_ctx* c, const he_conv_plan* p,
+                                         const int32_t* d_img, int B, int Pn, int D,
+                                         const uint64_t* d_ve, uint64_t* d_pt, void* stream) {
+    if (!c || !p || B < 0 || Pn < 1 || D < 1) return HE_EINVAL;
+    if (!plan_ok(c, p)) return HE_ESHAPE;
+    int Dm, Pm;
+    multi_spacing(plan_dev(p), c->N, &Dm, &Pm);
+    if (D % p->s || D < Dm || (long)Pn * D > (long)c->N) return HE_ESHAPE;
+    if (B == 0) return HE_OK;
+    if (!d_img || !d_pt) return HE_EINVAL;
+    const int Bc = (B + Pn - 1) / Pn;
+    const long total = (long)Bc * p->n_ib * c->L * c->N;
+    k_pack_input_multi<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(
+        d_img, (const u64*)d_ve, (u64*)d_pt, plan_dev(p), B, Pn, D, Bc, c->L, c->logN,
+        c->d_limb, c->t, c->r_t, c->t_inv);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
+__global__ void k_mask_extract_multi(const u64* __restrict__ full, const u32* __restrict__ phi1,
+                                     u64* __restrict__ comp, PlanDev P, int Bc, int Pn, int D,
+                                     int L, int logN, const he_limb* __restrict__ limbs, u64 t,
+                                     u64 r_t, u64 t_inv) {
+    const long N = 1L << logN;
+    const long per = (long)Pn * P.n_valid;
+    const long total = (long)Bc * P.n_ob * L * per;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long)gridDim.x * blockDim.x) {
+        const long w = idx % per;
+        const long r = idx / per;                      // (cb, ob, l)
+        const int l = (int)(r % L);
+        const long bo = r / L;
+        const int p = (int)(w / P.n_valid), v = (int)(w - (long)p * P.n_valid);
+        const int nl = v % P.c_ob, Pq = v / P.c_ob;
+        const int Lc = Pq % P.h_o, Kr = Pq / P.h_o;
+        const long i = (long)p * D + (long)P.s * (P.stride * Kr * (long)P.h_p + P.stride * Lc) +
+                       (long)nl * P.step;
+        u64 x = full[r * N + i];
+        if (phi1) {
+            const he_limb& Lm = limbs[l];
+            x = addmod(x, enc_plain(phi1[bo * N + i], Lm, t, r_t, t_inv), Lm.q);
+        }
+        comp[idx] = x;
+    }
+}
+
+extern "C" he_status he_mask_extract_multi(const he_ctx* c, const he_conv_plan* p,
+                                           const uint64_t* d_out, int Bc, int Pn, int D,
+                                           const uint32_t* d_phi1, uint64_t* d_compact,
+                                           void* stream) {
+    if (!c || !p || Bc < 0 || Pn < 1 || D < 1) return HE_EINVAL;
+    if (!plan_ok(c, p)) return HE_ESHAPE;
+    int Dm, Pm;
+    multi_spacing(plan_dev(p), c->N, &Dm, &Pm);
+    if (D % p->s || D < Dm || (long)Pn * D > (long)c->N) return HE_ESHAPE;
+    if (Bc == 0) return HE_OK;
+    if (!d_out || !d_compact) return HE_EINVAL;
+    const long total = (long)Bc * p->n_ob * c->L * Pn * p->n_valid;
+    k_mask_extract_multi<<<grid_for(total, 256), 256, 0, STREAM(stream)>>>(
+        (const u64*)d_out, d_phi1, (u64*)d_compact, plan_dev(p), Bc, Pn, D, c->L, c->logN,
+        c->d_limb, c->t, c->r_t, c->t_inv);
+    HE_CHECK_LAUNCH();
+    return HE_OK;
+}
+
 // ===================================================================== FC
 // Sub-matrix plan (reading R27, "decomposed into sub-matrices
 // whose sizes are smaller or equal to N"): input blocks of n_it = min(n_i, N)
