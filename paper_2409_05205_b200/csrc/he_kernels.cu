@@ -30,6 +30,21 @@ namespace cg = cooperative_groups;
 #ifndef HE_MAC_OB
 #define HE_MAC_OB 2          // fold groups per MAC output run (k_mac_imma)
 #endif
+#ifndef HE_K4_ROWS
+#define HE_K4_ROWS 1         // K4: row-writer kernel k_intt_rows
+#endif
+#ifndef HE_K4_MINW
+#define HE_K4_MINW 2         // K4: minimum slot columns per channel chunk
+#endif
+#ifndef HE_K4_ROWS_MAXM
+#define HE_K4_ROWS_MAXM 512  // K4: row-writer kernel for (N/s)-point transforms up to this
+#endif
+#ifndef HE_K4_ROWS_MINB
+#define HE_K4_ROWS_MINB 4    // K4 row writer: CTAs per SM (register cap)
+#endif
+#ifndef HE_K4_WORDS
+#define HE_K4_WORDS 6144     // K4: fold-array budget per CTA (words)
+#endif
 
 // The CUDA error behind the last HE_ECUDA returned on this host thread
 // (he_last_cuda_error), so a caller can report what failed.
@@ -1809,6 +1824,110 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     }
 }
 
+// K4, row-writer form (FP64 transforms, t <= 2^20): the same CTA work as
+// k_intt_scatter -- (N/s)-point inverse transforms of the cc channels of one
+// (b, ob, l) chunk, then the chunk's slot columns [u0, u1) of every group j
+// -- but the writer maps threads to (j, V consecutive columns): V = 2 words
+// leave as one 16-byte store and their phi1 as one 8-byte load, a warp
+// covers whole runs of the row, and the valid-slot payload index comes from
+// a per-CTA table jv[j] = K w_o' + L (or -1), built while the fold rows load,
+// instead of per-element row/column tracking.
+template <int V>
+__global__ void __launch_bounds__(256, HE_K4_ROWS_MINB)
+k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
+            u64* __restrict__ out, u64* __restrict__ comp, PlanDev P, int B, int L, int logN,
+            int cc, int nchunk, int stride, const he_limb* __restrict__ limbs,
+            const double* __restrict__ twid_all, double rtd, double td, double t_inv_d) {
+    extern __shared__ u64 sm[];
+    const int N = 1 << logN, M = N >> P.logs, logM = logN - P.logs;
+    int r = blockIdx.x;
+    const int ch = r % nchunk;
+    r /= nchunk;
+    const int l = r % L;
+    r /= L;
+    const int ob = r % P.n_ob, b = r / P.n_ob;
+    const double qd = limbs[l].qd, qi = limbs[l].qinvd, tinvq = limbs[l].tinvd;
+    const int ch0 = ch * cc, ncc = min(cc, P.c_ob - ch0);
+    const u64* fb = fold + (((size_t)l * B + b) * P.c_o + ob * P.c_ob + ch0) * M;
+    const int tot = ncc * M, nvalid_a = min(ncc, P.c_o - (ob * P.c_ob + ch0));
+    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+        const bool ok = (idx >> logM) < nvalid_a;
+        cp_async_n<8>(sm + (idx >> logM) * stride + PAD(idx & (M - 1)), ok ? fb + idx : fb, ok);
+    }
+    cp_async_commit();
+    int* jv = reinterpret_cast<int*>(sm + (size_t)cc * stride);
+    u64* crow = comp ? comp + (((size_t)b * P.n_ob + ob) * L + l) * P.n_valid : nullptr;
+    if (crow) {
+        for (int j = threadIdx.x; j < M; j += blockDim.x) {
+            const int kr = j / P.h_p, lc = j - kr * P.h_p;
+            const int K_ = kr / P.stride, L_ = lc / P.stride;
+            jv[j] = (kr == K_ * P.stride && lc == L_ * P.stride && K_ < P.w_o && L_ < P.h_o)
+                        ? (K_ * P.h_o + L_) * P.c_ob : -1;
+        }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    gs_all_dp<4, true>(reinterpret_cast<double*>(sm), stride, ncc, logM, 0, logM,
+                       twid_all + (size_t)l * N, qd, qi);
+    const int u0 = ch0 * P.step;
+    const int u1 = (ch == nchunk - 1) ? P.s : (ch0 + ncc) * P.step;
+    const int w = u1 - u0;                         // a multiple of V (host)
+    const int tpj = w / V;                         // threads per group j (a power of two)
+    const int ltpj = __ffs(tpj) - 1;
+    const u32* ph = phi1 ? phi1 + ((size_t)b * P.n_ob + ob) * N : nullptr;
+    u64* orow = out ? out + (((size_t)b * P.n_ob + ob) * L + l) * N : nullptr;
+    const bool xred = (logM & 3) == 0;             // radix-16 last pass: outputs < 8q + 16
+    const double* smd = reinterpret_cast<const double*>(sm);
+    const int lstep = __ffs(P.step) - 1;           // step = s / c_ob, a power of two
+    constexpr int UB = 4;                          // elements per thread in flight
+    const int nel = M * tpj;
+    for (int e0 = threadIdx.x; e0 < nel; e0 += UB * blockDim.x) {
+        uint2 m2[UB];
+        u32 m1[UB];
+#pragma unroll
+        for (int z = 0; z < UB; ++z) {
+            const int e = e0 + z * blockDim.x;
+            const int j = e >> ltpj, uo = (e & (tpj - 1)) * V;
+            m2[z] = make_uint2(0u, 0u);
+            m1[z] = 0u;
+            if (e < nel && ph && (orow || (crow && jv[j] >= 0))) {
+                const u32* pp = ph + ((size_t)j << P.logs) + u0 + uo;
+                if (V == 2) m2[z] = *reinterpret_cast<const uint2*>(pp);
+                else m1[z] = *pp;
+            }
+        }
+#pragma unroll
+        for (int z = 0; z < UB; ++z) {
+            const int e = e0 + z * blockDim.x;
+            if (e >= nel) break;
+            const int j = e >> ltpj, uo = (e & (tpj - 1)) * V;
+            const int jvj = crow ? jv[j] : -1;
+            if (!orow && jvj < 0) continue;
+            u64 v[V];
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                const int u = u0 + uo + k;
+                const u32 mm = V == 2 ? (k ? m2[z].y : m2[z].x) : m1[z];
+                double y = ph ? enc_dp(u2d(mm), rtd, td, t_inv_d, tinvq, qd, qi) : 0.0;
+                const int nl = u >> lstep;
+                const bool owned = (u & (P.step - 1)) == 0 && nl < ch0 + ncc;
+                if (owned) {
+                    double x = smd[(nl - ch0) * stride + PAD(j)];
+                    if (xred) x = dp_reduce(x, qd, qi);
+                    y += x;
+                }
+                v[k] = d2canon(y, qd, qi);
+                if (jvj >= 0 && owned) crow[jvj + nl] = v[k];
+            }
+            if (orow) {
+                u64* op = orow + ((size_t)j << P.logs) + u0 + uo;
+                if (V == 2) *reinterpret_cast<ulonglong2*>(op) = make_ulonglong2(v[0], v[V - 1]);
+                else op[0] = v[0];
+            }
+        }
+    }
+}
+
 // Workspace of he_conv: forward spectra (split25 words, or the MAC-tile
 // byte layout, whichever is larger) followed by the folded products.
 static size_t spec_words(const he_ctx* c, const he_conv_plan* p, int B) {
@@ -1869,6 +1988,36 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     if (s != HE_OK) return s;
     HE_CHECK_LAUNCH();
     const int M = c->N >> P.logs;
+    // row-writer K4 (k_intt_rows): FP64 transforms and the FP64 mask encoding
+    // (t <= 2^20); chunks of at least HE_K4_MINW slot columns when the block
+    // has them, so a chunk's run of each group is at least 32 bytes
+    if (c->ntt_mode == 0 && c->d_enc != nullptr && M >= 2 && M <= HE_K4_ROWS_MAXM &&
+        HE_K4_ROWS) {
+        int cc = std::max(1, std::min(P.c_ob, HE_K4_WORDS / (padded_words(M) + 16)));
+        while (cc & (cc - 1)) cc &= cc - 1;
+        while (cc < P.c_ob && cc * P.step < HE_K4_MINW) cc *= 2;
+        int stride = padded_words(M);
+        const int want = cc < 16 ? (16 / cc) & 15 : 1;
+        while ((stride & 15) != want && !(cc >= 16 && (stride & 1))) ++stride;
+        const int nchunk = (P.c_ob + cc - 1) / cc;
+        const int wl = P.s - (nchunk - 1) * cc * P.step;          // last chunk's width
+        const bool v2 = ((cc * P.step) & 1) == 0 && (wl & 1) == 0;
+        auto pow2 = [](int x) { return x > 0 && (x & (x - 1)) == 0; };
+        // (thread -> (j, column) by shifts: step and both chunk widths powers of two)
+        if (pow2(P.step) && pow2(cc * P.step) && pow2(wl) && wl == cc * P.step) {
+        const size_t smem = sizeof(u64) * (size_t)cc * stride + sizeof(int) * (size_t)M;
+        auto k4 = v2 ? k_intt_rows<2> : k_intt_rows<1>;
+        if (!set_smem(k4, smem)) return HE_ECUDA;
+        rec(ev, 2, st);
+        const double td = (double)c->t;
+        k4<<<(unsigned)(B * P.n_ob * c->L * nchunk), 256, smem, st>>>(
+            fold, d_phi1, (u64*)d_out, (u64*)d_compact, P, B, c->L, c->logN, cc, nchunk, stride,
+            c->d_limb, c->d_twd_inv, (double)c->r_t, td, 1.0 / td);
+        HE_CHECK_LAUNCH();
+        rec(ev, 3, st);
+        return HE_OK;
+        }
+    }
     int cc = std::max(1, std::min(P.c_ob, 6144 / (padded_words(M) + 16)));  // <= 48 KB
     while (cc & (cc - 1)) cc &= cc - 1;                       // power of two
     // array stride (words) = 16/cc (mod 16) for cc < 16, odd otherwise: the
