@@ -1139,16 +1139,19 @@ __device__ __forceinline__ void mma_k16(int (&d)[4], u32 a0, u32 a1, u32 b0) {
 // of two Shoup products:  m = lo (-q^{-1}) mod 2^64,
 //   t = (V + m q) / 2^64 = hi + hi64(m q) + (lo != 0)  =  C . F  (mod q),
 // t < V / 2^64 + q < 2q because V < 1.5 K q^2 < q 2^64 (K <= 4096, q < 2^50).
-__device__ __forceinline__ u64 redc128(u64 lo, u64 hi, const he_limb& Lm, bool lazy) {
-    const u64 m = lo * Lm.mq;
-    const u64 t = hi + __umul64hi(m, Lm.q) + (lo != 0 ? 1ull : 0ull);
-    return lazy ? t : csub(t, Lm.q);
+struct Redc {
+    u64 q, mq;      // q and -q^{-1} mod 2^64, held in registers by the MAC kernels
+};
+__device__ __forceinline__ u64 redc128(u64 lo, u64 hi, Redc R, bool lazy) {
+    const u64 m = lo * R.mq;
+    const u64 t = hi + __umul64hi(m, R.q) + (lo != 0 ? 1ull : 0ull);
+    return lazy ? t : csub(t, R.q);
 }
 // V = sum_{d<13} S_d 2^{8d} as (lo, hi): P_k = sum_{d=4k..4k+3} S_d 2^{8(d-4k)}
 // (three mad.wide each, or the 32-bit pairs when S_d < 2^23, i.e. K <= 16),
 // V = P0 + P1 2^32 + P2 2^64 + P3 2^96.
 template <bool K16, class S>
-__device__ __forceinline__ u64 reduce13_mont(S sd, const he_limb& Lm, bool lazy) {
+__device__ __forceinline__ u64 reduce13_mont(S sd, Redc Lm, bool lazy) {
     u64 P[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -1270,7 +1273,7 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gq = lane >> 2, tq = lane & 3;
     const int bt = warp / nnt, nt = warp - bt * nnt;
-    const he_limb Lm = limbs[l];
+    const Redc Lm = {limbs[l].q, limbs[l].mq};
     int acc[13][4];
     u64 ob[HE_MAC_OB][4];
     int nob = 0;
@@ -1492,7 +1495,7 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
     // instruction descriptor: S32 accumulate, u8 x u8, K-major A and B,
     // N = 16, M = BT
     const uint32_t idesc = (2u << 4) | ((16u >> 3) << 17) | ((uint32_t)(BT >> 4) << 24);
-    const he_limb Lm = limbs[l];
+    const Redc Lm = {limbs[l].q, limbs[l].mq};
     const int quarter = warp & 3, half = warp >> 2;      // TMEM lane quarter, column half
     const int r = quarter * 32 + lane;                   // this thread's image row
     const int b = b0 + r;
