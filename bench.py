@@ -341,16 +341,26 @@ def main():
     import torch.distributed as dist
     import paper_2409_05205_b200 as he
 
+    # HE_BENCH_GLOO_CHECK=1 (host-logic check only, never a measurement):
+    # every rank on cuda:0 with gloo collectives on host copies, so the
+    # multi-rank partition / gather / timing code runs on a one-GPU box
+    gloo_check = os.environ.get("HE_BENCH_GLOO_CHECK") == "1"
+    if gloo_check:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        # NCCL's init log (rank, nRanks) is the evidence of the communicator
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        dist.barrier(device_ids=[local])
+        if gloo_check:
+            dist.init_process_group("gloo")
+        else:
+            # NCCL's init log (rank, nRanks) is the evidence of the communicator
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier(device_ids=[local])
         print(f"[bench] rank {rank}/{world} on cuda:{local}, backend "
               f"{dist.get_backend()}", file=sys.stderr, flush=True)
     dev = torch.device("cuda", local)
+    cdev = torch.device("cpu") if gloo_check else dev     # where collectives run
     N, L = cfg.N, cfg.L
     from paper_2409_05205_b200.dist import (choose_axis, shard_out_blocks, shard_range,
                                             sub_layer_weights)
@@ -457,7 +467,7 @@ def main():
     evals_step = sum(lw.evals for lw in layers) + (B if fc else 0)
     evals_all = evals_step                # every rank's work (value = all ranks / max time)
     if world > 1:
-        _t = torch.tensor([evals_step], dtype=torch.float64, device=dev)
+        _t = torch.tensor([evals_step], dtype=torch.float64, device=cdev)
         dist.all_reduce(_t)
         evals_all = int(_t.item())
     launches_step = 3 * len(layers) * (nstr if args.overlap == "batch" else 1) + \
@@ -503,14 +513,18 @@ def main():
                    fc["ph_d"], fc["out"], fc["ws"])
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if gloo_check:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -976,13 +990,14 @@ def main():
         from paper_2409_05205_b200.dist import gather_blocks, gather_payload
 
         def assemble():
+            hx = (lambda t: t.cpu()) if gloo_check else (lambda t: t)
             for i, c in enumerate(comps):
                 if axis == "out_block":
-                    gather_blocks(c, ob_span[i][2])
+                    gather_blocks(hx(c), ob_span[i][2])
                 else:
-                    gather_payload(c, B_global)
+                    gather_payload(hx(c), B_global)
             if fc and axis != "out_block":
-                gather_payload(fc["out"], B_global)
+                gather_payload(hx(fc["out"]), B_global)
 
         for _ in range(2):
             assemble()

@@ -190,6 +190,11 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
             u64 x = q;                      // q q = 1 mod 8: 3 correct bits
             for (int it = 0; it < 5; ++it) x *= 2 - q * x;
             Lm.mq = (u64)0 - x;
+            auto centred = [q](u64 v) { return v > q / 2 ? -(double)(q - v) : (double)v; };
+            const u64 i32 = h_inv((1ull << 32) % q, q);            // 2^-32
+            Lm.mrd[0] = centred(h_mulmod(i32, i32, q));          // 2^-64
+            Lm.mrd[1] = centred(i32);
+            Lm.mrd[2] = centred((1ull << 32) % q);               // 2^32
         }
         Lm.qd = (double)q;
         Lm.qinvd = 1.0 / (double)q;

@@ -33,6 +33,15 @@ namespace cg = cooperative_groups;
 #ifndef HE_K4_ROWS
 #define HE_K4_ROWS 1         // K4: row-writer kernel k_intt_rows
 #endif
+#ifndef HE_NTT_T
+#define HE_NTT_T 512         // forward NTT (cluster kernels): threads per CTA
+#endif
+#ifndef HE_NTT_MINB
+#define HE_NTT_MINB 2        // forward NTT (cluster kernels): CTAs per SM (register cap)
+#endif
+#ifndef HE_MAC_DPE
+#define HE_MAC_DPE 0         // K <= 16 MAC: outputs (of 4 per thread) reduced on the FP64 pipe
+#endif
 #ifndef HE_K4_MINW
 #define HE_K4_MINW 2         // K4: minimum slot columns per channel chunk
 #endif
@@ -322,20 +331,20 @@ k_ntt_fwd_s2(const u64* in, u64* out, int logN, int L, const he_limb* __restrict
 }
 
 template <int OUT_FMT>
-__global__ void __launch_bounds__(512, 2)
+__global__ void __launch_bounds__(HE_NTT_T, HE_NTT_MINB)
 k_ntt_fwd_dp_s0(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
                 const double* __restrict__ tw_all, TileLay T) {
     ntt_fwd_segment_dp<0, OUT_FMT>(in, out, logN, L, limbs, tw_all, T);
 }
 template <int OUT_FMT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 2)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HE_NTT_T, HE_NTT_MINB)
 k_ntt_fwd_dp_s1(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
                 const double* __restrict__ tw_all, TileLay T) {
     // conv path (MAC-tile output): radix-16 passes (measured 0.839 -> 0.826 ms per step)
     ntt_fwd_segment_dp<1, OUT_FMT, (OUT_FMT == 2 ? 4 : 3)>(in, out, logN, L, limbs, tw_all, T);
 }
 template <int OUT_FMT>
-__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 2)
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(HE_NTT_T, HE_NTT_MINB)
 k_ntt_fwd_dp_s2(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
                 const double* __restrict__ tw_all, TileLay T) {
     ntt_fwd_segment_dp<2, OUT_FMT>(in, out, logN, L, limbs, tw_all, T);
@@ -504,7 +513,7 @@ static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
             {k_ntt_fwd_dp_s2<0>, k_ntt_fwd_dp_s2<1>, k_ntt_fwd_dp_s2<2>}};
         kfd kd = tabd[S][out_fmt];
         if (!set_smem(kd, smem)) return HE_ECUDA;
-        kd<<<(unsigned)(nlimbs << S), threads, smem, st>>>(in, out, logN, c->L, c->d_limb,
+        kd<<<(unsigned)(nlimbs << S), std::min(threads, HE_NTT_T), smem, st>>>(in, out, logN, c->L, c->d_limb,
                                                            c->d_twd_fwd, T);
         HE_CHECK_LAUNCH();
         return HE_OK;
@@ -1141,6 +1150,7 @@ __device__ __forceinline__ void mma_k16(int (&d)[4], u32 a0, u32 a1, u32 b0) {
 // t < V / 2^64 + q < 2q because V < 1.5 K q^2 < q 2^64 (K <= 4096, q < 2^50).
 struct Redc {
     u64 q, mq;      // q and -q^{-1} mod 2^64, held in registers by the MAC kernels
+    const he_limb* L;   // FP64 constants (reduce13_mdp)
 };
 __device__ __forceinline__ u64 redc128(u64 lo, u64 hi, Redc R, bool lazy) {
     const u64 m = lo * R.mq;
@@ -1171,6 +1181,30 @@ __device__ __forceinline__ u64 reduce13_mont(S sd, Redc Lm, bool lazy) {
     const u64 lo = P[0] + (P[1] << 32);
     const u64 hi = P[2] + (P[1] >> 32) + (P3 << 32) + (lo < P[0] ? 1 : 0);
     return redc128(lo, hi, Lm, lazy);
+}
+
+// The same Montgomery-domain result on the FP64 pipe (otherwise idle in the
+// MAC): V 2^-64 = P0 2^-64 + P1 2^-32 + P2 + P3 2^32 (mod q).  For K <= 16
+// the P_k are below 2^48 (exact doubles); three exact dp_mulmod by the
+// centred constants, P2 added as is: |sum| < 2^48 + 3q, one dp_reduce and
+// the lazy conversion give a residue in [q/2 - 2, 3q/2 + 2].
+template <class S>
+__device__ __forceinline__ u64 reduce13_mdp(S sd, Redc R, bool lazy) {
+    u64 P[4];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const u32 a = (u32)sd(4 * k) + ((u32)sd(4 * k + 1) << 8);
+        const u32 b = (u32)sd(4 * k + 2) + ((u32)sd(4 * k + 3) << 8);
+        P[k] = a;
+        madw(P[k], b, 1u << 16);
+    }
+    P[3] = (u64)(u32)sd(12);
+    const double q = R.L->qd, qi = R.L->qinvd;
+    double v = u2d(P[2]);
+    v += dp_mulmod(u2d(P[0]), R.L->mrd[0], q, qi);
+    v += dp_mulmod(u2d(P[1]), R.L->mrd[1], q, qi);
+    v += dp_mulmod(u2d(P[3]), R.L->mrd[2], q, qi);
+    return lazy ? d2lazy(v, q, qi) : d2canon(v, q, qi);
 }
 
 // x / d for 0 <= x < 2^31 with d fixed per kernel: a shift when d is a power
@@ -1273,7 +1307,7 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gq = lane >> 2, tq = lane & 3;
     const int bt = warp / nnt, nt = warp - bt * nnt;
-    const Redc Lm = {limbs[l].q, limbs[l].mq};
+    const Redc Lm = {limbs[l].q, limbs[l].mq, limbs + l};
     int acc[13][4];
     u64 ob[HE_MAC_OB][4];
     int nob = 0;
@@ -1340,9 +1374,12 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
                 for (int e = 0; e < 4; ++e) {
 #pragma unroll
                     for (int z = 0; z < OB - 1; ++z) ob[z][e] = ob[z + 1][e];
-                    ob[OB - 1][e] =
-                        MINB > 1 ? reduce13_mont<true>([&](int d) { return acc[d][e]; }, Lm, lazy)
-                                 : reduce13_mont<false>([&](int d) { return acc[d][e]; }, Lm, lazy);
+                    if (MINB > 1 && lazy && e >= 4 - HE_MAC_DPE)   // K <= 16: FP64 pipe share
+                        ob[OB - 1][e] = reduce13_mdp([&](int d) { return acc[d][e]; }, Lm, lazy);
+                    else
+                        ob[OB - 1][e] =
+                            MINB > 1 ? reduce13_mont<true>([&](int d) { return acc[d][e]; }, Lm, lazy)
+                                     : reduce13_mont<false>([&](int d) { return acc[d][e]; }, Lm, lazy);
                 }
                 ++nob;
                 if (nob == OB || gu + gi == gcnt - 1) {
@@ -1495,7 +1532,7 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
     // instruction descriptor: S32 accumulate, u8 x u8, K-major A and B,
     // N = 16, M = BT
     const uint32_t idesc = (2u << 4) | ((16u >> 3) << 17) | ((uint32_t)(BT >> 4) << 24);
-    const Redc Lm = {limbs[l].q, limbs[l].mq};
+    const Redc Lm = {limbs[l].q, limbs[l].mq, limbs + l};
     const int quarter = warp & 3, half = warp >> 2;      // TMEM lane quarter, column half
     const int r = quarter * 32 + lane;                   // this thread's image row
     const int b = b0 + r;
