@@ -39,6 +39,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_NTT_MINB
 #define HE_NTT_MINB 2        // forward NTT (cluster kernels): CTAs per SM (register cap)
 #endif
+#ifndef HE_MAC_SPEC
+#define HE_MAC_SPEC 1        // MAC: compile-time specialised instances for plain-20 shapes
+#endif
 #ifndef HE_MAC_DPE
 #define HE_MAC_DPE 0         // K <= 16 MAC: outputs (of 4 per thread) reduced on the FP64 pipe
 #endif
@@ -1232,13 +1235,20 @@ struct FastDiv {
 // contiguous in global memory and are copied with 16-byte cp.async into
 // padded shared rows (stride = 4 mod 8 words: conflict-free fragments).
 // Reduced outputs go straight to the transposed fold out[l][b][n][g].
-template <int TB16, int MINB = 1>
+// Compile-time specialisations (KPC, KCC, COC, GSC nonzero: Kp, KC, c_o, GS
+// fixed; LZ 1/0: lazy fixed, -1 runtime) turn the shared-memory strides into
+// immediates (the generic form spends about a fifth of its instructions on
+// address arithmetic); 0 / -1 keep the runtime arguments.
+template <int TB16, int MINB = 1, int KPC = 0, int KCC = 0, int COC = 0, int GSC = 0, int LZ = -1>
 __global__ void __launch_bounds__(MINB > 1 ? 128 : 512, MINB)
 k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
-           u64* __restrict__ out, int B, int L, int M, int c_o, int Kp, int G, int GS,
-           int KC, int Gt, int nbuf, const he_limb* __restrict__ limbs, int lazy) {
+           u64* __restrict__ out, int B, int L, int M, int c_o_, int Kp_, int G, int GS_,
+           int KC_, int Gt, int nbuf, const he_limb* __restrict__ limbs, int lazy_) {
     extern __shared__ u32 sm32[];
     constexpr int rows = 16 * TB16;
+    const int c_o = COC ? COC : c_o_, Kp = KPC ? KPC : Kp_;
+    const int GS = GSC ? GSC : GS_, KC = KCC ? KCC : KC_;
+    const bool lazy = LZ >= 0 ? (LZ == 1) : (lazy_ != 0);
     const int nrow = (c_o + 7) & ~7, nnt = nrow >> 3;
     const int swc = imma_sw_dev(KC);
     const int rw = imma_sw_dev(GS * KC);                  // A row: GS groups x KC bytes
@@ -1251,11 +1261,12 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
     const int nkc = Kp / KC;
     const int nunits = ((gcnt + GS - 1) / GS) * nkc;      // (group block, k-chunk)
     // padded B rows (n >= c_o) stay zero for the whole kernel (every buffer)
-    for (int bf = 0; bf < nbuf; ++bf) {
+    for (int bf = 0; bf < nbuf && nrow > c_o; ++bf) {
         u32* sB = sm32 + bf * buf_words + 7 * rows * rw;
+        const int pad_rows = nrow > c_o ? nrow - c_o : 1;
         for (int e = threadIdx.x; e < GS * 7 * (nrow - c_o) * swc; e += blockDim.x) {
             const int w = e % swc, r = e / swc;
-            const int n = c_o + r % (nrow - c_o), gj = r / (nrow - c_o);
+            const int n = c_o + r % pad_rows, gj = r / pad_rows;
             sB[(gj * nrow + n) * swc + w] = 0;
         }
     }
@@ -1669,6 +1680,19 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
     const bool k16 = k16c && nunits == 1 && 32 * warps <= 128;
     auto k = TB16 == 2 ? (k16 ? k_mac_imma<2, HE_MAC_K16_MINB> : k_mac_imma<2>)
                        : (k16 ? k_mac_imma<1, HE_MAC_K16_MINB> : k_mac_imma<1>);
+    // specialised instances for the plain-20 layer shapes (32-image tiles)
+    if (HE_MAC_SPEC && TB16 == 2 && lazy) {
+        if (k16 && Kp == 16 && KC == 16 && c_o == 16 && GS == 4)
+            k = k_mac_imma<2, HE_MAC_K16_MINB, 16, 16, 16, 4, 1>;
+        else if (!k16 && Kp == 16 && KC == 16 && c_o == 32 && GS == 4)
+            k = k_mac_imma<2, 1, 16, 16, 32, 4, 1>;
+        else if (!k16 && Kp == 32 && KC == 32 && c_o == 32 && GS == 2)
+            k = k_mac_imma<2, 1, 32, 32, 32, 2, 1>;
+        else if (!k16 && Kp == 32 && KC == 32 && c_o == 64 && GS == 1)
+            k = k_mac_imma<2, 1, 32, 32, 64, 1, 1>;
+        else if (!k16 && Kp == 64 && KC == 64 && c_o == 64 && GS == 1)
+            k = k_mac_imma<2, 1, 64, 64, 64, 1, 1>;
+    }
     if (!set_smem(k, smem)) return HE_ECUDA;
     dim3 grid(L * ((M + G - 1) / G), (B + rows - 1) / rows);
     k<<<grid, 32 * warps, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, G, GS, KC, Gt, nbuf, limbs,
