@@ -39,6 +39,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_NTT_MINB
 #define HE_NTT_MINB 2        // forward NTT (cluster kernels): CTAs per SM (register cap)
 #endif
+#ifndef HE_K4_SPEC
+#define HE_K4_SPEC 1         // K4: compile-time instance for the plain-20 s = 8 layers
+#endif
 #ifndef HE_MAC_SPEC
 #define HE_MAC_SPEC 1        // MAC: compile-time specialised instances for plain-20 shapes
 #endif
@@ -1711,15 +1714,22 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
 // coefficient.  The chunks tile [0, s), so every coefficient
 // of the row is written exactly once, in contiguous runs of u1 - u0 words.
 // Channel arrays sit in shared memory at an odd word stride (conflict-free).
-template <bool DP>
+// Template arguments LN, LS, CCC, STC, NCH, COB (nonzero): log2 N, log2 s,
+// cc, the array stride, nchunk and c_ob fixed at compile time -- the plain-20
+// s = 8 instance turns the transform's and the writer's index arithmetic
+// into immediates; 0 keeps the runtime values.
+template <bool DP, int LN = 0, int LS = 0, int CCC = 0, int STC = 0, int NCH = 0, int COB = 0>
 __global__ void __launch_bounds__(256, 4)
 k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                u64* __restrict__ out, u64* __restrict__ comp, PlanDev P, int B, int L,
-               int logN, int cc, int nchunk, int stride, const he_limb* __restrict__ limbs,
+               int logN_, int cc_, int nchunk_, int stride_, const he_limb* __restrict__ limbs,
                const ulonglong2* __restrict__ twi_all, const double* __restrict__ twid_all,
                const u64* __restrict__ enc_tab, u64 t, u64 r_t, u64 t_inv) {
     extern __shared__ u64 sm[];
-    const int N = 1 << logN, M = N >> P.logs, logM = logN - P.logs;
+    const int logN = LN ? LN : logN_, logs = LS ? LS : P.logs;
+    const int cc = CCC ? CCC : cc_, nchunk = NCH ? NCH : nchunk_, stride = STC ? STC : stride_;
+    const int c_ob = COB ? COB : P.c_ob, s_ = 1 << logs, step = COB ? s_ / COB : P.step;
+    const int N = 1 << logN, M = N >> logs, logM = logN - logs;
     int r = blockIdx.x;
     const int ch = r % nchunk;
     r /= nchunk;
@@ -1729,10 +1739,10 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     const he_limb Lm = limbs[l];
     const u64 q = Lm.q, q2 = 2 * q;
     const ulonglong2* twi = twi_all + (size_t)l * N;
-    const int ch0 = ch * cc, ncc = min(cc, P.c_ob - ch0);
+    const int ch0 = ch * cc, ncc = min(cc, c_ob - ch0);
     // fold layout [l][b][n][g]: the chunk's channel rows are contiguous in g
-    const u64* fb = fold + (((size_t)l * B + b) * P.c_o + ob * P.c_ob + ch0) * M;
-    const int tot = ncc * M, nvalid_a = min(ncc, P.c_o - (ob * P.c_ob + ch0));
+    const u64* fb = fold + (((size_t)l * B + b) * P.c_o + ob * c_ob + ch0) * M;
+    const int tot = ncc * M, nvalid_a = min(ncc, P.c_o - (ob * c_ob + ch0));
     const bool raw = DP && logM >= 1;       // cp.async the residues, first pass converts
     if (raw) {
         for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
@@ -1771,8 +1781,8 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         gs_all<3, true>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
     else
         gs_all<3>(sm, stride, ncc, logM, 0, logM, twi, q, q2);
-    const int u0 = ch0 * P.step;
-    const int u1 = (ch == nchunk - 1) ? P.s : (ch0 + ncc) * P.step;
+    const int u0 = ch0 * step;
+    const int u1 = (ch == nchunk - 1) ? s_ : (ch0 + ncc) * step;
     const int w = u1 - u0;
     const u32* ph = phi1 ? phi1 + ((size_t)b * P.n_ob + ob) * N : nullptr;
     u64* orow = out ? out + (((size_t)b * P.n_ob + ob) * L + l) * N : nullptr;
@@ -1788,8 +1798,8 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     const int uo = threadIdx.x % w, jt = threadIdx.x / w;
     if (jstep > 0 && jt < jstep) {
         const int u = u0 + uo;
-        const int nl = u / P.step;
-        const bool owned = u == nl * P.step && nl < ch0 + ncc;
+        const int nl = u / step;
+        const bool owned = u == nl * step && nl < ch0 + ncc;
         const int abase = owned ? (nl - ch0) * stride : 0;
         const bool want_c = crow && owned;
         // j = kr * h_p + lc, tracked incrementally
@@ -1813,9 +1823,9 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                 if (want_c && j < M) {
                     const int K_ = kr >> lstr, L_ = lc >> lstr;
                     if (((kr | lc) & (P.stride - 1)) == 0 && K_ < P.w_o && L_ < P.h_o)
-                        vi[e] = (K_ * P.h_o + L_) * P.c_ob + nl;
+                        vi[e] = (K_ * P.h_o + L_) * c_ob + nl;
                 }
-                m[e] = (ph && j < M && (orow || vi[e] >= 0)) ? ph[(j << P.logs) + u] : 0u;
+                m[e] = (ph && j < M && (orow || vi[e] >= 0)) ? ph[(j << logs) + u] : 0u;
                 kr += dk;
                 lc += dl;
                 if (lc >= P.h_p) { lc -= P.h_p; ++kr; }
@@ -1833,7 +1843,7 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                         y += x;
                     }
                     const u64 v = d2canon(y, Lm.qd, Lm.qinvd);
-                    if (orow) orow[(j << P.logs) + u] = v;
+                    if (orow) orow[(j << logs) + u] = v;
                     if (vi[e] >= 0) crow[vi[e]] = v;
                 }
                 continue;
@@ -1855,7 +1865,7 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                                      Lm.qinvd)
                            : reduce_full(sm[abase + PAD(j)], q, Lm.one_p);
                 v = addmod(v, en[e], q);
-                if (orow) orow[(j << P.logs) + u] = v;
+                if (orow) orow[(j << logs) + u] = v;
                 if (vi[e] >= 0) crow[vi[e]] = v;
             }
         }
@@ -1865,15 +1875,15 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     for (int ub = jstep > 0 ? w : 0; ub < w; ub += blockDim.x) {
         const int u = u0 + ub + threadIdx.x;
         if (u >= u1) continue;
-        const int nl = u / P.step;
-        const bool owned = u == nl * P.step && nl < ch0 + ncc;
+        const int nl = u / step;
+        const bool owned = u == nl * step && nl < ch0 + ncc;
         for (int j = 0; j < M; ++j) {
             const int kr = j / P.h_p, lc = j - kr * P.h_p;
             int vidx = -1;
             if (crow && owned) {
                 const int K_ = kr >> lstr, L_ = lc >> lstr;
                 if (((kr | lc) & (P.stride - 1)) == 0 && K_ < P.w_o && L_ < P.h_o)
-                    vidx = (K_ * P.h_o + L_) * P.c_ob + nl;
+                    vidx = (K_ * P.h_o + L_) * c_ob + nl;
             }
             if (!orow && vidx < 0) continue;
             u64 v = 0;
@@ -1881,8 +1891,8 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                 v = DP ? d2canon(reinterpret_cast<const double*>(sm)[(nl - ch0) * stride + PAD(j)],
                                  Lm.qd, Lm.qinvd)
                        : reduce_full(sm[(nl - ch0) * stride + PAD(j)], q, Lm.one_p);
-            if (ph) v = addmod(v, enc_lookup(enc_tab, l, t, ph[(j << P.logs) + u], Lm, r_t, t_inv), q);
-            if (orow) orow[(j << P.logs) + u] = v;
+            if (ph) v = addmod(v, enc_lookup(enc_tab, l, t, ph[(j << logs) + u], Lm, r_t, t_inv), q);
+            if (orow) orow[(j << logs) + u] = v;
             if (vidx >= 0) crow[vidx] = v;
         }
     }
@@ -2092,6 +2102,9 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     const int nchunk = (P.c_ob + cc - 1) / cc;
     const size_t smem = sizeof(u64) * (size_t)cc * stride;
     auto k4 = c->ntt_mode == 0 ? k_intt_scatter<true> : k_intt_scatter<false>;
+    if (HE_K4_SPEC && c->ntt_mode == 0 && c->logN == 14 && P.logs == 3 && cc == 2 &&
+        stride == 2184 && nchunk == 4 && P.c_ob == 8)
+        k4 = k_intt_scatter<true, 14, 3, 2, 2184, 4, 8>;
     if (!set_smem(k4, smem)) return HE_ECUDA;
     rec(ev, 2, st);
     k4<<<(unsigned)(B * P.n_ob * c->L * nchunk), 256, smem, st>>>(
