@@ -39,8 +39,14 @@ namespace cg = cooperative_groups;
 #ifndef HE_NTT_MINB
 #define HE_NTT_MINB 2        // forward NTT (cluster kernels): CTAs per SM (register cap)
 #endif
+#ifndef HE_NTT_SPEC
+#define HE_NTT_SPEC 1        // forward NTT: compile-time instances for plain-20 layers
+#endif
 #ifndef HE_K4_SPEC
 #define HE_K4_SPEC 1         // K4: compile-time instance for the plain-20 s = 8 layers
+#endif
+#ifndef HE_MAC_KCMAX
+#define HE_MAC_KCMAX 64      // MAC: largest k-chunk per staged unit when K does not fit
 #endif
 #ifndef HE_MAC_SPEC
 #define HE_MAC_SPEC 1        // MAC: compile-time specialised instances for plain-20 shapes
@@ -342,12 +348,24 @@ k_ntt_fwd_dp_s0(const u64* in, u64* out, int logN, int L, const he_limb* __restr
                 const double* __restrict__ tw_all, TileLay T) {
     ntt_fwd_segment_dp<0, OUT_FMT>(in, out, logN, L, limbs, tw_all, T);
 }
-template <int OUT_FMT>
+// LN, SK, NIB, KU, KP, GT nonzero: log2 N, the skipped stages and the MAC-tile
+// geometry fixed at compile time (the plain-20 conv layers' instances: the
+// index arithmetic of the passes and of the byte-plane store folds away)
+template <int OUT_FMT, int LN = 0, int SK = 0, int NIB = 0, int KU = 0, int KP = 0, int GT = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HE_NTT_T, HE_NTT_MINB)
 k_ntt_fwd_dp_s1(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
                 const double* __restrict__ tw_all, TileLay T) {
+    if (LN) {
+        T.logs = SK;
+        T.skip = SK;
+        T.n_ib = NIB;
+        T.Ku = KU;
+        T.Kp = KP;
+        T.Gt = GT;
+    }
     // conv path (MAC-tile output): radix-16 passes (measured 0.839 -> 0.826 ms per step)
-    ntt_fwd_segment_dp<1, OUT_FMT, (OUT_FMT == 2 ? 4 : 3)>(in, out, logN, L, limbs, tw_all, T);
+    ntt_fwd_segment_dp<1, OUT_FMT, (OUT_FMT == 2 ? 4 : 3)>(in, out, LN ? LN : logN, L, limbs,
+                                                          tw_all, T);
 }
 template <int OUT_FMT>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(HE_NTT_T, HE_NTT_MINB)
@@ -518,6 +536,16 @@ static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
             {k_ntt_fwd_dp_s1<0>, k_ntt_fwd_dp_s1<1>, k_ntt_fwd_dp_s1<2>},
             {k_ntt_fwd_dp_s2<0>, k_ntt_fwd_dp_s2<1>, k_ntt_fwd_dp_s2<2>}};
         kfd kd = tabd[S][out_fmt];
+        // compile-time instances for the plain-20 conv layers (N = 16384)
+        if (HE_NTT_SPEC && S == 1 && out_fmt == 2 && logN == 14 && T.Gt == 16 &&
+            T.logs == T.skip) {
+            if (T.skip == 3 && T.n_ib == 2 && T.Ku == 8 && T.Kp == 16)
+                kd = k_ntt_fwd_dp_s1<2, 14, 3, 2, 8, 16, 16>;
+            else if (T.skip == 3 && T.n_ib == 1 && T.Ku == 4 && T.Kp == 16)
+                kd = k_ntt_fwd_dp_s1<2, 14, 3, 1, 4, 16, 16>;
+            else if (T.skip == 5 && T.n_ib == 1 && T.Ku == 32 && T.Kp == 32)
+                kd = k_ntt_fwd_dp_s1<2, 14, 5, 1, 32, 32, 16>;
+        }
         if (!set_smem(kd, smem)) return HE_ECUDA;
         kd<<<(unsigned)(nlimbs << S), std::min(threads, HE_NTT_T), smem, st>>>(in, out, logN, c->L, c->d_limb,
                                                            c->d_twd_fwd, T);
@@ -1666,7 +1694,7 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
             G = GS * ug;
         }
     } else {
-        KC = (Kp % 64 == 0) ? 64 : ((Kp % 32 == 0) ? 32 : 16);
+        KC = (Kp % 64 == 0 && HE_MAC_KCMAX >= 64) ? 64 : ((Kp % 32 == 0) ? 32 : 16);
         GS = 1;
         // several groups per CTA so the k-chunk pipeline has depth, while
         // keeping >= ~4 CTAs of work per SM
@@ -1695,6 +1723,8 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
             k = k_mac_imma<2, 1, 32, 32, 64, 1, 1>;
         else if (!k16 && Kp == 64 && KC == 64 && c_o == 64 && GS == 1)
             k = k_mac_imma<2, 1, 64, 64, 64, 1, 1>;
+        else if (!k16 && Kp == 64 && KC == 32 && c_o == 64 && GS == 1)
+            k = k_mac_imma<2, 1, 64, 32, 64, 1, 1>;
     }
     if (!set_smem(k, smem)) return HE_ECUDA;
     dim3 grid(L * ((M + G - 1) / G), (B + rows - 1) / rows);
@@ -1906,14 +1936,18 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
 // covers whole runs of the row, and the valid-slot payload index comes from
 // a per-CTA table jv[j] = K w_o' + L (or -1), built while the fold rows load,
 // instead of per-element row/column tracking.
-template <int V>
+template <int V, int LN = 0, int LS = 0, int CCC = 0, int STC = 0, int NCH = 0, int COB = 0>
 __global__ void __launch_bounds__(256, HE_K4_ROWS_MINB)
 k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
-            u64* __restrict__ out, u64* __restrict__ comp, PlanDev P, int B, int L, int logN,
-            int cc, int nchunk, int stride, const he_limb* __restrict__ limbs,
+            u64* __restrict__ out, u64* __restrict__ comp, PlanDev P, int B, int L, int logN_,
+            int cc_, int nchunk_, int stride_, const he_limb* __restrict__ limbs,
             const double* __restrict__ twid_all, double rtd, double td, double t_inv_d) {
     extern __shared__ u64 sm[];
-    const int N = 1 << logN, M = N >> P.logs, logM = logN - P.logs;
+    // (compile-time geometry as k_intt_scatter's template arguments; 0 = runtime)
+    const int logN = LN ? LN : logN_, logs = LS ? LS : P.logs;
+    const int cc = CCC ? CCC : cc_, nchunk = NCH ? NCH : nchunk_, stride = STC ? STC : stride_;
+    const int c_ob = COB ? COB : P.c_ob, s_ = 1 << logs, step = COB ? s_ / COB : P.step;
+    const int N = 1 << logN, M = N >> logs, logM = logN - logs;
     int r = blockIdx.x;
     const int ch = r % nchunk;
     r /= nchunk;
@@ -1921,9 +1955,9 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     r /= L;
     const int ob = r % P.n_ob, b = r / P.n_ob;
     const double qd = limbs[l].qd, qi = limbs[l].qinvd, tinvq = limbs[l].tinvd;
-    const int ch0 = ch * cc, ncc = min(cc, P.c_ob - ch0);
-    const u64* fb = fold + (((size_t)l * B + b) * P.c_o + ob * P.c_ob + ch0) * M;
-    const int tot = ncc * M, nvalid_a = min(ncc, P.c_o - (ob * P.c_ob + ch0));
+    const int ch0 = ch * cc, ncc = min(cc, c_ob - ch0);
+    const u64* fb = fold + (((size_t)l * B + b) * P.c_o + ob * c_ob + ch0) * M;
+    const int tot = ncc * M, nvalid_a = min(ncc, P.c_o - (ob * c_ob + ch0));
     for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
         const bool ok = (idx >> logM) < nvalid_a;
         cp_async_n<8>(sm + (idx >> logM) * stride + PAD(idx & (M - 1)), ok ? fb + idx : fb, ok);
@@ -1936,15 +1970,15 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
             const int kr = j / P.h_p, lc = j - kr * P.h_p;
             const int K_ = kr / P.stride, L_ = lc / P.stride;
             jv[j] = (kr == K_ * P.stride && lc == L_ * P.stride && K_ < P.w_o && L_ < P.h_o)
-                        ? (K_ * P.h_o + L_) * P.c_ob : -1;
+                        ? (K_ * P.h_o + L_) * c_ob : -1;
         }
     }
     cp_async_wait<0>();
     __syncthreads();
     gs_all_dp<4, true>(reinterpret_cast<double*>(sm), stride, ncc, logM, 0, logM,
                        twid_all + (size_t)l * N, qd, qi);
-    const int u0 = ch0 * P.step;
-    const int u1 = (ch == nchunk - 1) ? P.s : (ch0 + ncc) * P.step;
+    const int u0 = ch0 * step;
+    const int u1 = (ch == nchunk - 1) ? s_ : (ch0 + ncc) * step;
     const int w = u1 - u0;                         // a multiple of V (host)
     const int tpj = w / V;                         // threads per group j (a power of two)
     const int ltpj = __ffs(tpj) - 1;
@@ -1952,7 +1986,7 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     u64* orow = out ? out + (((size_t)b * P.n_ob + ob) * L + l) * N : nullptr;
     const bool xred = (logM & 3) == 0;             // radix-16 last pass: outputs < 8q + 16
     const double* smd = reinterpret_cast<const double*>(sm);
-    const int lstep = __ffs(P.step) - 1;           // step = s / c_ob, a power of two
+    const int lstep = __ffs(step) - 1;           // step = s / c_ob, a power of two
     constexpr int UB = 4;                          // elements per thread in flight
     const int nel = M * tpj;
     for (int e0 = threadIdx.x; e0 < nel; e0 += UB * blockDim.x) {
@@ -1965,7 +1999,7 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
             m2[z] = make_uint2(0u, 0u);
             m1[z] = 0u;
             if (e < nel && ph && (orow || (crow && jv[j] >= 0))) {
-                const u32* pp = ph + ((size_t)j << P.logs) + u0 + uo;
+                const u32* pp = ph + ((size_t)j << logs) + u0 + uo;
                 if (V == 2) m2[z] = *reinterpret_cast<const uint2*>(pp);
                 else m1[z] = *pp;
             }
@@ -1984,7 +2018,7 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                 const u32 mm = V == 2 ? (k ? m2[z].y : m2[z].x) : m1[z];
                 double y = ph ? enc_dp(u2d(mm), rtd, td, t_inv_d, tinvq, qd, qi) : 0.0;
                 const int nl = u >> lstep;
-                const bool owned = (u & (P.step - 1)) == 0 && nl < ch0 + ncc;
+                const bool owned = (u & (step - 1)) == 0 && nl < ch0 + ncc;
                 if (owned) {
                     double x = smd[(nl - ch0) * stride + PAD(j)];
                     if (xred) x = dp_reduce(x, qd, qi);
@@ -1994,7 +2028,7 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                 if (jvj >= 0 && owned) crow[jvj + nl] = v[k];
             }
             if (orow) {
-                u64* op = orow + ((size_t)j << P.logs) + u0 + uo;
+                u64* op = orow + ((size_t)j << logs) + u0 + uo;
                 if (V == 2) *reinterpret_cast<ulonglong2*>(op) = make_ulonglong2(v[0], v[V - 1]);
                 else op[0] = v[0];
             }
@@ -2081,6 +2115,12 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
         if (pow2(P.step) && pow2(cc * P.step) && pow2(wl) && wl == cc * P.step) {
         const size_t smem = sizeof(u64) * (size_t)cc * stride + sizeof(int) * (size_t)M;
         auto k4 = v2 ? k_intt_rows<2> : k_intt_rows<1>;
+        if (HE_K4_SPEC && v2 && c->logN == 14) {       // plain-20 s = 32 and s = 128 layers
+            if (P.logs == 5 && cc == 8 && stride == 546 && nchunk == 4 && P.c_ob == 32)
+                k4 = k_intt_rows<2, 14, 5, 8, 546, 4, 32>;
+            else if (P.logs == 7 && cc == 32 && stride == 137 && nchunk == 2 && P.c_ob == 64)
+                k4 = k_intt_rows<2, 14, 7, 32, 137, 2, 64>;
+        }
         if (!set_smem(k4, smem)) return HE_ECUDA;
         rec(ev, 2, st);
         const double td = (double)c->t;
