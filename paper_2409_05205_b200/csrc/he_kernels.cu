@@ -45,6 +45,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_K4_SPEC
 #define HE_K4_SPEC 1         // K4: compile-time instance for the plain-20 s = 8 layers
 #endif
+#ifndef HE_MAC_TB2_MAXNNT
+#define HE_MAC_TB2_MAXNNT 4  // MAC: 32-image tiles when c_o <= 8 * this (else 16-image tiles)
+#endif
 #ifndef HE_MAC_KCMAX
 #define HE_MAC_KCMAX 64      // MAC: largest k-chunk per staged unit when K does not fit
 #endif
@@ -1674,7 +1677,7 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
     };
     // 32-image tiles for small c_o; 16-image tiles (<= 256 threads, two
     // CTAs per SM) when the whole K does not fit one buffer
-    int TB16 = (nnt <= 8 && B > 16) ? 2 : 1;
+    int TB16 = (nnt <= HE_MAC_TB2_MAXNNT && B > 16) ? 2 : 1;
     if (TB16 == 2 && unit_bytes(32, 1, Kp) > budget) TB16 = 1;
     const int rows = 16 * TB16, warps = TB16 * nnt;
     int KC = Kp, GS = 1, G = 1;
@@ -1712,6 +1715,17 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
     auto k = TB16 == 2 ? (k16 ? k_mac_imma<2, HE_MAC_K16_MINB> : k_mac_imma<2>)
                        : (k16 ? k_mac_imma<1, HE_MAC_K16_MINB> : k_mac_imma<1>);
     // specialised instances for the plain-20 layer shapes (32-image tiles)
+    if (HE_MAC_SPEC && TB16 == 1 && lazy && k16 && Kp == 16 && KC == 16 && c_o == 32 &&
+        GS == 4)
+        k = k_mac_imma<1, HE_MAC_K16_MINB, 16, 16, 32, 4, 1>;
+    if (HE_MAC_SPEC && TB16 == 1 && lazy && !k16) {       // 16-image tiles, c_o >= 32
+        if (Kp == 32 && KC == 32 && c_o == 32 && GS == 2)
+            k = k_mac_imma<1, 1, 32, 32, 32, 2, 1>;
+        else if (Kp == 32 && KC == 32 && c_o == 64 && GS == 1)
+            k = k_mac_imma<1, 1, 32, 32, 64, 1, 1>;
+        else if (Kp == 64 && KC == 64 && c_o == 64 && GS == 1)
+            k = k_mac_imma<1, 1, 64, 64, 64, 1, 1>;
+    }
     if (HE_MAC_SPEC && TB16 == 2 && lazy) {
         if (k16 && Kp == 16 && KC == 16 && c_o == 16 && GS == 4)
             k = k_mac_imma<2, HE_MAC_K16_MINB, 16, 16, 16, 4, 1>;
