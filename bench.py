@@ -261,11 +261,27 @@ def oracle_single_thread(cfg_idx: int, max_s: float = 20.0) -> None:
         if time.perf_counter() - t0 > max_s or reps >= 4:
             break
     dt = time.perf_counter() - t0
-    print(json.dumps({"value": reps * evals / dt, "unit": "ct×pt evals/s", "cores": 1,
-                      "s_per_image": dt / reps, "cpu_model": cpu_model(),
-                      "sample": f"{reps} x 1 image x all {len(plans)} conv"
-                                f"{' + FC' if fc else ''} layers ({dt:.1f} s wall, "
-                                "OMP_NUM_THREADS=1)"}))
+    res = {"value": reps * evals / dt, "unit": "ct×pt evals/s", "cores": 1,
+           "s_per_image": dt / reps, "cpu_model": cpu_model(),
+           "sample": f"{reps} x 1 image x all {len(plans)} conv"
+                     f"{' + FC' if fc else ''} layers ({dt:.1f} s wall, OMP_NUM_THREADS=1)"}
+    # the CPU textbook-NTT path on one thread, conv layers only
+    from oracle import cpu_baseline as CB
+    fsp = [CB.prepare_filters(W, p, ring) for W, p in zip(Ws, plans)]
+    t0, reps = time.perf_counter(), 0
+    while True:
+        for p, f, c0, ph in zip(plans, fsp, c0s, phis):
+            R.compact(CB.conv_server(c0, f, p, ring, ph), p)
+        reps += 1
+        if time.perf_counter() - t0 > max_s or reps >= 4:
+            break
+    dtn = time.perf_counter() - t0
+    evc = sum(Ly.c_o * p.n_ib for Ly, p in zip(cfg.conv, plans))
+    res["ntt_path"] = {"value": reps * evc / dtn, "unit": "ct×pt evals/s", "cores": 1,
+                       "s_per_image_conv_layers": dtn / reps,
+                       "sample": f"{reps} x 1 image x all {len(plans)} conv layers "
+                                 f"({dtn:.1f} s wall, OMP_NUM_THREADS=1)"}
+    print(json.dumps(res))
 
 
 # ------------------------------------------------------------ reference
@@ -1265,6 +1281,28 @@ def main():
                "sample": f"{reps} pass(es) x {nimg} image(s) x all {len(layers)} conv"
                          f"{' + FC' if fc else ''} layers ({dt:.1f} s wall)",
                "cpu_model": cpu_model()}
+        # the CPU textbook-NTT path (oracle/cpu_baseline.py:
+        # NTT-domain products, pinned to the oracle), same images and layers,
+        # all cores; filter spectra prepared outside the timing
+        try:
+            from oracle import cpu_baseline as CB
+            fsp = [CB.prepare_filters(Ws[i], oplans[i], ring) for i in range(len(layers))]
+            t0, reps = time.perf_counter(), 0
+            while True:
+                for i in range(len(layers)):
+                    R.compact(CB.conv_server(c0n[i], fsp[i], oplans[i], ring, phn[i]), oplans[i])
+                reps += 1
+                if time.perf_counter() - t0 > 10.0 or reps >= 8:
+                    break
+            dtn = time.perf_counter() - t0
+            evn = reps * nimg * sum(lw.evals // B for lw in layers)
+            cpu["ntt_path"] = {"value": evn / dtn, "unit": "ct×pt evals/s",
+                               "cores": os.cpu_count(), "kind": "cpu textbook NTT",
+                               "sample": f"{reps} pass(es) x {nimg} image(s) x all "
+                                         f"{len(layers)} conv layers ({dtn:.1f} s wall)"}
+            del fsp
+        except Exception as exc:                      # reported, not fatal
+            cpu["ntt_path"] = {"error": repr(exc)[:200]}
         # the same oracle on one host thread (the paper's own numbers are
         # single-thread): a child process with OMP_NUM_THREADS=1
         # times one image through the same layers
