@@ -1762,7 +1762,8 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
 // cc, the array stride, nchunk and c_ob fixed at compile time -- the plain-20
 // s = 8 instance turns the transform's and the writer's index arithmetic
 // into immediates; 0 keeps the runtime values.
-template <bool DP, int LN = 0, int LS = 0, int CCC = 0, int STC = 0, int NCH = 0, int COB = 0>
+template <bool DP, int LN = 0, int LS = 0, int CCC = 0, int STC = 0, int NCH = 0, int COB = 0,
+          int HP = 0, int WO = 0, int CST = 0>
 __global__ void __launch_bounds__(256, 4)
 k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                u64* __restrict__ out, u64* __restrict__ comp, PlanDev P, int B, int L,
@@ -1774,6 +1775,9 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     const int cc = CCC ? CCC : cc_, nchunk = NCH ? NCH : nchunk_, stride = STC ? STC : stride_;
     const int c_ob = COB ? COB : P.c_ob, s_ = 1 << logs, step = COB ? s_ / COB : P.step;
     const int N = 1 << logN, M = N >> logs, logM = logN - logs;
+    // (HP, WO, CST: padded row length h_p, output side w_o = h_o, conv stride)
+    const int h_p = HP ? HP : P.h_p, w_o = WO ? WO : P.w_o, h_o = WO ? WO : P.h_o;
+    const int cstr = CST ? CST : P.stride;
     int r = blockIdx.x;
     const int ch = r % nchunk;
     r /= nchunk;
@@ -1832,7 +1836,7 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     u64* orow = out ? out + (((size_t)b * P.n_ob + ob) * L + l) * N : nullptr;
     u64* crow = comp ? comp + (((size_t)b * P.n_ob + ob) * L + l) * P.n_valid : nullptr;
     int lstr = 0;                         // stride is a power of two (checked on host)
-    while ((1 << lstr) < P.stride) ++lstr;
+    while ((1 << lstr) < cstr) ++lstr;
     // Row writer.  Thread (uo, jt) owns slot column u = u0 + uo of every
     // group j = jt, jt + jstep, ...: its channel, ownership and smem base are
     // per-thread constants, and the (row, column) of j for the payload test
@@ -1847,8 +1851,8 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         const int abase = owned ? (nl - ch0) * stride : 0;
         const bool want_c = crow && owned;
         // j = kr * h_p + lc, tracked incrementally
-        int kr = jt / P.h_p, lc = jt - kr * P.h_p;
-        const int dk = jstep / P.h_p, dl = jstep - dk * P.h_p;
+        int kr = jt / h_p, lc = jt - kr * h_p;
+        const int dk = jstep / h_p, dl = jstep - dk * h_p;
         constexpr int EB = 4;
         // FP64 mask encoding (enc_dp) when the context has a table (t <= 2^20):
         // no random table gathers in the writer
@@ -1866,13 +1870,13 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                 vi[e] = -1;
                 if (want_c && j < M) {
                     const int K_ = kr >> lstr, L_ = lc >> lstr;
-                    if (((kr | lc) & (P.stride - 1)) == 0 && K_ < P.w_o && L_ < P.h_o)
-                        vi[e] = (K_ * P.h_o + L_) * c_ob + nl;
+                    if (((kr | lc) & (cstr - 1)) == 0 && K_ < w_o && L_ < h_o)
+                        vi[e] = (K_ * h_o + L_) * c_ob + nl;
                 }
                 m[e] = (ph && j < M && (orow || vi[e] >= 0)) ? ph[(j << logs) + u] : 0u;
                 kr += dk;
                 lc += dl;
-                if (lc >= P.h_p) { lc -= P.h_p; ++kr; }
+                if (lc >= h_p) { lc -= h_p; ++kr; }
             }
             if (encd) {
 #pragma unroll
@@ -1922,12 +1926,12 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         const int nl = u / step;
         const bool owned = u == nl * step && nl < ch0 + ncc;
         for (int j = 0; j < M; ++j) {
-            const int kr = j / P.h_p, lc = j - kr * P.h_p;
+            const int kr = j / h_p, lc = j - kr * h_p;
             int vidx = -1;
             if (crow && owned) {
                 const int K_ = kr >> lstr, L_ = lc >> lstr;
-                if (((kr | lc) & (P.stride - 1)) == 0 && K_ < P.w_o && L_ < P.h_o)
-                    vidx = (K_ * P.h_o + L_) * c_ob + nl;
+                if (((kr | lc) & (cstr - 1)) == 0 && K_ < w_o && L_ < h_o)
+                    vidx = (K_ * h_o + L_) * c_ob + nl;
             }
             if (!orow && vidx < 0) continue;
             u64 v = 0;
@@ -2157,8 +2161,13 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     const size_t smem = sizeof(u64) * (size_t)cc * stride;
     auto k4 = c->ntt_mode == 0 ? k_intt_scatter<true> : k_intt_scatter<false>;
     if (HE_K4_SPEC && c->ntt_mode == 0 && c->logN == 14 && P.logs == 3 && cc == 2 &&
-        stride == 2184 && nchunk == 4 && P.c_ob == 8)
+        stride == 2184 && nchunk == 4 && P.c_ob == 8) {
         k4 = k_intt_scatter<true, 14, 3, 2, 2184, 4, 8>;
+        if (P.h_p == 34 && P.w_o == 32 && P.h_o == 32 && P.stride == 1)
+            k4 = k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 32, 1>;
+        else if (P.h_p == 34 && P.w_o == 16 && P.h_o == 16 && P.stride == 2)
+            k4 = k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 16, 2>;
+    }
     if (!set_smem(k4, smem)) return HE_ECUDA;
     rec(ev, 2, st);
     k4<<<(unsigned)(B * P.n_ob * c->L * nchunk), 256, smem, st>>>(
