@@ -48,6 +48,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_MAC_TB2_MAXNNT
 #define HE_MAC_TB2_MAXNNT 4  // MAC: 32-image tiles when c_o <= 8 * this (else 16-image tiles)
 #endif
+#ifndef HE_MAC_CT16
+#define HE_MAC_CT16 1        // MAC: 16-channel tiles for K = 16, c_o = 32 layers
+#endif
 #ifndef HE_MAC_KCMAX
 #define HE_MAC_KCMAX 64      // MAC: largest k-chunk per staged unit when K does not fit
 #endif
@@ -1277,10 +1280,14 @@ template <int TB16, int MINB = 1, int KPC = 0, int KCC = 0, int COC = 0, int GSC
 __global__ void __launch_bounds__(MINB > 1 ? 128 : 512, MINB)
 k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
            u64* __restrict__ out, int B, int L, int M, int c_o_, int Kp_, int G, int GS_,
-           int KC_, int Gt, int nbuf, const he_limb* __restrict__ limbs, int lazy_) {
+           int KC_, int Gt, int nbuf, const he_limb* __restrict__ limbs, int lazy_,
+           int c_full) {
     extern __shared__ u32 sm32[];
     constexpr int rows = 16 * TB16;
+    // channel tile: channels [n0, n0 + c_o) of the c_full output channels
+    // (blockIdx.z; c_o = c_full when the layer is not tiled)
     const int c_o = COC ? COC : c_o_, Kp = KPC ? KPC : Kp_;
+    const int n0 = blockIdx.z * c_o;
     const int GS = GSC ? GSC : GS_, KC = KCC ? KCC : KC_;
     const bool lazy = LZ >= 0 ? (LZ == 1) : (lazy_ != 0);
     const int nrow = (c_o + 7) & ~7, nnt = nrow >> 3;
@@ -1334,16 +1341,18 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
             const int cpr2 = KC >> 4;
             const FastDiv dc(cpr2), dn(c_o * cpr2);
             const int per = c_o * cpr2, total = gsn * per;
-            const unsigned char* f0 = Fpl + (((size_t)l * M + g0 + gu) * 7) * c_o * Kp + k0;
+            const unsigned char* f0 =
+                Fpl + ((((size_t)l * M + g0 + gu) * 7) * c_full + n0) * Kp + k0;
             for (int e = threadIdx.x; e < total; e += blockDim.x) {
                 const int gi = dn.div(e), rem = e - gi * per;
                 const int n = dc.div(rem), c = rem - n * cpr2;
-                const unsigned char* src = f0 + ((size_t)gi * 7 * c_o + n) * Kp + c * 16;
+                const unsigned char* src = f0 + ((size_t)gi * 7 * c_full + n) * Kp + c * 16;
                 unsigned char* dst =
                     reinterpret_cast<unsigned char*>(sB + ((size_t)gi * 7 * nrow + n) * swc) + c * 16;
 #pragma unroll
                 for (int j = 0; j < 7; ++j)
-                    cp_async_n<16>(dst + (size_t)j * nrow * swc * 4, src + (size_t)j * c_o * Kp, true);
+                    cp_async_n<16>(dst + (size_t)j * nrow * swc * 4, src + (size_t)j * c_full * Kp,
+                                   true);
             }
         }
         cp_async_commit();
@@ -1433,7 +1442,7 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
                         const int b = b0 + bt * 16 + gq + 8 * (e >> 1);
                         const int n = nt * 8 + 2 * tq + (e & 1);
                         if (b >= B || n >= c_o) continue;
-                        u64* row = out + (((size_t)l * B + b) * c_o + n) * M + (g - (OB - 1));
+                        u64* row = out + (((size_t)l * B + b) * c_full + n0 + n) * M + (g - (OB - 1));
                         if (nob == OB && ((g - (OB - 1)) & (OB - 1)) == 0) {
 #pragma unroll
                             for (int z = 0; z < OB; z += 2)
@@ -1658,8 +1667,7 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
                                  int mac_tc) {
     const int M = (1 << logN) >> logs, K = n_ib * Ku;
     const int Kp = imma_kp(K);
-    const int nrow = (c_o + 7) & ~7, nnt = nrow / 8;
-    if (nnt > 32) return HE_ESHAPE;                       // c_o <= 256
+    if (c_o > 256) return HE_ESHAPE;
     {
         // batches of >= 128 images: tcgen05 MAC (HE_MAC_TC=0 disables, =1 forces)
         const int mode = mac_tc;
@@ -1668,6 +1676,13 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
         if (fits && (mode == 1 || (mode == 2 && B >= HE_MAC_TC_BT)))
             return launch_mac_tc(A, Fpl, out, B, L, M, c_o, Kp, limbs, st, lazy);
     }
+    const int c_full = c_o;
+    // K = 16 layers with 32 channels: two 16-channel tiles (grid.z) of the
+    // small-CTA form (5 CTAs per SM) instead of one 8-warp CTA
+    const int ctile = (HE_MAC_CT16 && Kp == 16 && c_o == 32 && B >= 32) ? 16 : c_o;
+    const int nct = c_full / ctile;
+    c_o = ctile;
+    const int nrow = (c_o + 7) & ~7, nnt = nrow / 8;
     const int Gt = tile_gt(M);
     // per staging buffer; the K = 16 small-CTA case targets 5 CTAs per SM
     const bool k16c = Kp == 16 && HE_MAC_K16_MINB > 1;
@@ -1741,9 +1756,9 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
             k = k_mac_imma<2, 1, 64, 32, 64, 1, 1>;
     }
     if (!set_smem(k, smem)) return HE_ECUDA;
-    dim3 grid(L * ((M + G - 1) / G), (B + rows - 1) / rows);
+    dim3 grid(L * ((M + G - 1) / G), (B + rows - 1) / rows, nct);
     k<<<grid, 32 * warps, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, G, GS, KC, Gt, nbuf, limbs,
-                                      lazy);
+                                      lazy, c_full);
     return HE_OK;
 }
 
