@@ -1181,6 +1181,23 @@ __device__ __forceinline__ void mma_k16(int (&d)[4], u32 a0, u32 a1, u32 b0) {
         : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
         : "r"(a0), "r"(a1), "r"(b0));
 }
+// D = A B (zero accumulator input: the first product into a diagonal, so the
+// 52 accumulator registers need no zeroing instructions)
+__device__ __forceinline__ void mma_k32_z(int (&d)[4], u32 a0, u32 a1, u32 a2, u32 a3, u32 b0,
+                                          u32 b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%10,%10,%10,%10};"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(0));
+}
+__device__ __forceinline__ void mma_k16_z(int (&d)[4], u32 a0, u32 a1, u32 b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+        "{%7,%7,%7,%7};"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+        : "r"(a0), "r"(a1), "r"(b0), "r"(0));
+}
 
 // Montgomery form of the recombination (R = 2^64): the filter operand of the
 // int8 MAC paths is stored pre-multiplied by R mod q (k_filter_to_imma), so
@@ -1380,16 +1397,14 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
         const u32* sA = sm32 + (nbuf == 2 ? (u & 1) : 0) * buf_words;
         const u32* sB = sA + 7 * rows * rw;
         for (int gi = 0; gi < gsn; ++gi) {
-            if (kc == 0) {
-#pragma unroll
-                for (int d = 0; d < 13; ++d)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) acc[d][e] = 0;
-            }
             const u32* ab = sA + (bt * 16 + gq) * rw + gi * (KC >> 2) + tq;
             const u32* bb = sB + (size_t)gi * gb + (nt * 8 + gq) * swc + tq;
             const int Kw = KC >> 2;
             int kw = 0;
+            // the first k-step of a group writes each diagonal's first product
+            // with a zero accumulator input (diagonal d = i + j is first met at
+            // i = 0, or at j = 6 for i >= 1 in this loop order)
+            bool first = kc == 0;
             for (; kw + 8 <= Kw; kw += 8) {
                 u32 bf0[7], bf1[7];
 #pragma unroll
@@ -1397,24 +1412,65 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
                     bf0[j] = bb[j * nrow * swc + kw];
                     bf1[j] = bb[j * nrow * swc + kw + 4];
                 }
+                if (first) {
 #pragma unroll
-                for (int i = 0; i < 7; ++i) {
-                    const u32* ap = ab + i * rows * rw + kw;
-                    const u32 a0 = ap[0], a1 = ap[8 * rw], a2 = ap[4], a3 = ap[8 * rw + 4];
+                    for (int i = 0; i < 7; ++i) {
+                        const u32* ap = ab + i * rows * rw + kw;
+                        const u32 a0 = ap[0], a1 = ap[8 * rw], a2 = ap[4], a3 = ap[8 * rw + 4];
 #pragma unroll
-                    for (int j = 0; j < 7; ++j) mma_k32(acc[i + j], a0, a1, a2, a3, bf0[j], bf1[j]);
+                        for (int j = 0; j < 7; ++j) {
+                            if (i == 0 || j == 6) mma_k32_z(acc[i + j], a0, a1, a2, a3, bf0[j], bf1[j]);
+                            else mma_k32(acc[i + j], a0, a1, a2, a3, bf0[j], bf1[j]);
+                        }
+                    }
+                    first = false;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 7; ++i) {
+                        const u32* ap = ab + i * rows * rw + kw;
+                        const u32 a0 = ap[0], a1 = ap[8 * rw], a2 = ap[4], a3 = ap[8 * rw + 4];
+#pragma unroll
+                        for (int j = 0; j < 7; ++j)
+                            mma_k32(acc[i + j], a0, a1, a2, a3, bf0[j], bf1[j]);
+                    }
                 }
             }
             if (kw < Kw) {                                   // one k16 step
-                u32 bf0[7];
+                // Two plane products of the same diagonal share one m16n8k32:
+                // its K halves carry (c_i1, f_d-i1) and (c_i2, f_d-i2), so the
+                // 49 k16 products take 28 k32 instructions (the k16 form
+                // costs a k32 issue slot for half the work) and each
+                // diagonal's dependency chain is at most 4 long.  Round r
+                // issues the r-th pair of every diagonal (independent
+                // accumulators back to back).
+                u32 bf0[7], xa[7], xb[7];
 #pragma unroll
                 for (int j = 0; j < 7; ++j) bf0[j] = bb[j * nrow * swc + kw];
 #pragma unroll
                 for (int i = 0; i < 7; ++i) {
                     const u32* ap = ab + i * rows * rw + kw;
-                    const u32 a0 = ap[0], a1 = ap[8 * rw];
+                    xa[i] = ap[0];
+                    xb[i] = ap[8 * rw];
+                }
 #pragma unroll
-                    for (int j = 0; j < 7; ++j) mma_k16(acc[i + j], a0, a1, bf0[j]);
+                for (int r = 0; r < 4; ++r) {
+#pragma unroll
+                    for (int d = 0; d < 13; ++d) {
+                        const int lo = d > 6 ? d - 6 : 0, hi = d < 6 ? d : 6;
+                        const int i1 = lo + 2 * r, i2 = i1 + 1;
+                        if (i1 > hi) continue;
+                        if (i2 <= hi) {
+                            if (first && r == 0)
+                                mma_k32_z(acc[d], xa[i1], xb[i1], xa[i2], xb[i2], bf0[d - i1],
+                                          bf0[d - i2]);
+                            else
+                                mma_k32(acc[d], xa[i1], xb[i1], xa[i2], xb[i2], bf0[d - i1],
+                                        bf0[d - i2]);
+                        } else {
+                            if (first && r == 0) mma_k16_z(acc[d], xa[i1], xb[i1], bf0[d - i1]);
+                            else mma_k16(acc[d], xa[i1], xb[i1], bf0[d - i1]);
+                        }
+                    }
                 }
             }
             if (kc == nkc - 1) {
