@@ -431,11 +431,17 @@ __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr,
                            (blk << (K - 1 - v));
             load_tw_run(tws + o, tw, tb, 1 << (K - 1 - v));
         }
+        // element c sits at PAD(base + c 2^lt0); for lt0 >= 4 that is
+        // PAD(base) + c (2^lt0 + 2^(lt0-4)) (base's low lt0 bits are off < 2^lt0):
+        // linear addresses, no per-element padding arithmetic (the forward
+        // passes keep PAD(): their 64-register cap spills otherwise)
+        const int pbo = PAD(base);
+        const int pst = lt0 >= 4 ? (1 << lt0) + (1 << (lt0 - 4)) : 0;
+        auto ai = [&](int c) { return lt0 >= 4 ? pbo + c * pst : PAD(base + (c << lt0)); };
         double x[1 << K];
 #pragma unroll
         for (int c = 0; c < (1 << K); ++c) {
-            const double v = RAW ? u2d(reinterpret_cast<const u64*>(s)[PAD(base + (c << lt0))])
-                                 : s[PAD(base + (c << lt0))];
+            const double v = RAW ? u2d(reinterpret_cast<const u64*>(s)[ai(c)]) : s[ai(c)];
             // raw inputs are lazy residues in [0, 4q) (the MAC's output):
             // stage 0 multiplies X - Y (|.| < 4q) directly and reduces only
             // its sums, after which the bounds below hold as for reduced
@@ -456,7 +462,7 @@ __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr,
             }
         }
 #pragma unroll
-        for (int c = 0; c < (1 << K); ++c) s[PAD(base + (c << lt0))] = x[c];
+        for (int c = 0; c < (1 << K); ++c) s[ai(c)] = x[c];
     }
 }
 
