@@ -39,6 +39,12 @@ namespace cg = cooperative_groups;
 #ifndef HE_NTT_MINB
 #define HE_NTT_MINB 2        // forward NTT (cluster kernels): CTAs per SM (register cap)
 #endif
+#ifndef HE_INV_RADIX
+#define HE_INV_RADIX 3       // inverse cluster kernel: log2 of the pass radix
+#endif
+#ifndef HE_INV_CL
+#define HE_INV_CL 1          // full inverse NTT at N >= 16384: FP64 cluster kernel
+#endif
 #ifndef HE_NTT_SPEC
 #define HE_NTT_SPEC 1        // forward NTT: compile-time instances for plain-20 layers
 #endif
@@ -644,10 +650,75 @@ k_ntt_inv_split(const u64* in, u64* out, int logN,
     cl.sync();                          // keep smem alive for the partner
 }
 
+// FP64 inverse for N >= 2048 (N = 16384 / 32768: a cluster of 2^S CTAs per limb, the
+// mirror of the forward cluster kernels): each CTA runs the first log2 N - S
+// Gentleman-Sande stages on its own 8192-word segment in shared memory, then
+// the S stages whose span crosses segments read the partner's segment over
+// DSMEM (values in registers across the cluster barrier), then N^{-1} and the
+// canonical store.  Replaces one 1024-thread CTA with 139 KB of shared memory
+// (one per SM) at N = 16384 and the integer split kernel at N = 32768.
+template <int S>
+__global__ void __cluster_dims__(1 << S, 1, 1) __launch_bounds__(256, 3)
+k_ntt_inv_dp_cl(const u64* __restrict__ in, u64* __restrict__ out, int logN, int L,
+                const he_limb* __restrict__ limbs, const double* __restrict__ twid_all) {
+    extern __shared__ u64 sm_raw[];
+    double* sm = reinterpret_cast<double*>(sm_raw);
+    const int N = 1 << logN, NS = N >> S;
+    const int li = blockIdx.x >> S, seg = blockIdx.x & ((1 << S) - 1), l = li % L;
+    const he_limb& Lm = limbs[l];
+    const double q = Lm.qd, qi = Lm.qinvd;
+    const double* tw = twid_all + (size_t)l * N;
+    const u64* src = in + (size_t)li * N + (size_t)seg * NS;
+    for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src + i);
+        sm[PAD(i)] = u2d(v.x);
+        sm[PAD(i + 1)] = u2d(v.y);
+    }
+    __syncthreads();
+    gs_all_dp<HE_INV_RADIX>(sm, 0, 1, logN - S, seg, logN, tw, q, qi);   // in-segment stages
+    cg::cluster_group cl = cg::this_cluster();
+    for (int t = 0; t < S; ++t) {                                 // span NS << t
+        // pair (lower segment a, upper segment a + 2^t): the lower CTA
+        // takes indices i < NS/2, the upper one i >= NS/2, and each reads
+        // both inputs and writes both outputs of its indices (one of them
+        // over DSMEM), so no value is overwritten before its last read
+        cl.sync();
+        const int partner = seg ^ (1 << t);
+        const bool upper = (seg >> t) & 1;
+        const double w = tw[(1 << (S - 1 - t)) + (seg >> (t + 1))];
+        double* lo = upper ? cl.map_shared_rank(sm, partner) : sm;
+        double* hi = upper ? sm : cl.map_shared_rank(sm, partner);
+        const int i0 = upper ? NS / 2 : 0;
+        for (int i = i0 + threadIdx.x; i < i0 + NS / 2; i += blockDim.x) {
+            const double X = dp_reduce(lo[PAD(i)], q, qi), Y = dp_reduce(hi[PAD(i)], q, qi);
+            lo[PAD(i)] = X + Y;
+            hi[PAD(i)] = dp_mulmod(X - Y, w, q, qi);
+        }
+    }
+    if (S) cl.sync();
+    const double nid = (double)Lm.ninv;
+    u64* dst = out + (size_t)li * N + (size_t)seg * NS;
+    for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
+        const u64 x = d2canon(dp_mulmod(dp_reduce(sm[PAD(i)], q, qi), nid, q, qi), q, qi);
+        const u64 y = d2canon(dp_mulmod(dp_reduce(sm[PAD(i + 1)], q, qi), nid, q, qi), q, qi);
+        *reinterpret_cast<ulonglong2*>(dst + i) = make_ulonglong2(x, y);
+    }
+}
+
 static he_status launch_ntt_inv(const he_ctx* c, const u64* in, u64* out,
                                 long nlimbs, cudaStream_t st) {
     if (nlimbs <= 0) return HE_OK;
     const int N = c->N;
+    if (c->ntt_mode == 0 && c->logN >= 11 && HE_INV_CL) {
+        const int S = c->logN > 13 ? c->logN - 13 : 0;
+        const size_t smem = sizeof(u64) * padded_words(N >> S);
+        auto k = S == 0 ? k_ntt_inv_dp_cl<0> : (S == 1 ? k_ntt_inv_dp_cl<1> : k_ntt_inv_dp_cl<2>);
+        if (!set_smem(k, smem)) return HE_ECUDA;
+        k<<<(unsigned)(nlimbs << S), 256, smem, st>>>(in, out, c->logN, c->L, c->d_limb,
+                                                     c->d_twd_inv);
+        HE_CHECK_LAUNCH();
+        return HE_OK;
+    }
     if (c->logN <= 14) {
         const size_t smem = sizeof(u64) * padded_words(N);
         auto k = c->ntt_mode == 0 ? k_ntt_inv<true> : k_ntt_inv<false>;
