@@ -195,6 +195,9 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
             Lm.mrd[0] = centred(h_mulmod(i32, i32, q));          // 2^-64
             Lm.mrd[1] = centred(i32);
             Lm.mrd[2] = centred((1ull << 32) % q);               // 2^32
+            Lm.pw8[0] = 1u << 8;
+            Lm.pw8[1] = 1u << 16;
+            Lm.pw8[2] = 1u << 24;
         }
         Lm.qd = (double)q;
         Lm.qinvd = 1.0 / (double)q;

@@ -33,6 +33,7 @@ struct he_limb {
     double c32d, c64d, c96d;  // 2^32, 2^64, 2^96 mod q, centred (FP64 MAC recombination)
     u64 mq;                 // -q^{-1} mod 2^64 (Montgomery reduction of the int8 MAC sums)
     double mrd[3];          // 2^-64, 2^-32, 2^32 mod q, centred (FP64 form of that reduction)
+    uint32_t pw8[3];        // 2^8, 2^16, 2^24 (runtime multipliers: one IMAD.WIDE per term)
 };
 
 struct he_ctx {

@@ -48,6 +48,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_NTT_SPEC
 #define HE_NTT_SPEC 1        // forward NTT: compile-time instances for plain-20 layers
 #endif
+#ifndef HE_TC_PWR
+#define HE_TC_PWR 0       // tcgen05 MAC recombination with run-time power-of-two multipliers
+#endif
 #ifndef HE_K4_SPEC
 #define HE_K4_SPEC 1         // K4: compile-time instance for the plain-20 s = 8 layers
 #endif
@@ -1279,6 +1282,7 @@ __device__ __forceinline__ void mma_k16_z(int (&d)[4], u32 a0, u32 a1, u32 b0) {
 struct Redc {
     u64 q, mq;      // q and -q^{-1} mod 2^64, held in registers by the MAC kernels
     const he_limb* L;   // FP64 constants (reduce13_mdp)
+    u32 p8, p16, p24;   // 2^8, 2^16, 2^24 loaded at run time (HE_MAC_PWR)
 };
 __device__ __forceinline__ u64 redc128(u64 lo, u64 hi, Redc R, bool lazy) {
     const u64 m = lo * R.mq;
@@ -1288,21 +1292,27 @@ __device__ __forceinline__ u64 redc128(u64 lo, u64 hi, Redc R, bool lazy) {
 // V = sum_{d<13} S_d 2^{8d} as (lo, hi): P_k = sum_{d=4k..4k+3} S_d 2^{8(d-4k)}
 // (three mad.wide each, or the 32-bit pairs when S_d < 2^23, i.e. K <= 16),
 // V = P0 + P1 2^32 + P2 2^64 + P3 2^96.
-template <bool K16, class S>
+template <bool K16, bool PWR, class S>
 __device__ __forceinline__ u64 reduce13_mont(S sd, Redc Lm, bool lazy) {
     u64 P[3];
 #pragma unroll
+    // PWR: the powers of two come from registers loaded at run time, so each
+    // term is one IMAD.WIDE.U32 (an immediate power of two is rewritten by
+    // ptxas into SHL + HI + two adds).  Measured per layer: K = 16 43.2 ->
+    // 41.0 us, K = 64 33.3 -> 32.9 us, but K = 32 39.0 -> 41.0 us (kept off).
+    const u32 c8 = PWR ? Lm.p8 : 1u << 8, c16 = PWR ? Lm.p16 : 1u << 16,
+              c24 = PWR ? Lm.p24 : 1u << 24;
     for (int k = 0; k < 3; ++k) {
         if (K16) {
             const u32 a = (u32)sd(4 * k) + ((u32)sd(4 * k + 1) << 8);
             const u32 b = (u32)sd(4 * k + 2) + ((u32)sd(4 * k + 3) << 8);
             P[k] = a;
-            madw(P[k], b, 1u << 16);
+            madw(P[k], b, c16);
         } else {
             P[k] = (u64)(u32)sd(4 * k);
-            madw(P[k], (u32)sd(4 * k + 1), 1u << 8);
-            madw(P[k], (u32)sd(4 * k + 2), 1u << 16);
-            madw(P[k], (u32)sd(4 * k + 3), 1u << 24);
+            madw(P[k], (u32)sd(4 * k + 1), c8);
+            madw(P[k], (u32)sd(4 * k + 2), c16);
+            madw(P[k], (u32)sd(4 * k + 3), c24);
         }
     }
     const u64 P3 = (u64)(u32)sd(12);
@@ -1449,7 +1459,8 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gq = lane >> 2, tq = lane & 3;
     const int bt = warp / nnt, nt = warp - bt * nnt;
-    const Redc Lm = {limbs[l].q, limbs[l].mq, limbs + l};
+    const Redc Lm = {limbs[l].q, limbs[l].mq, limbs + l, limbs[l].pw8[0], limbs[l].pw8[1],
+                     limbs[l].pw8[2]};
     int acc[13][4];
     u64 ob[HE_MAC_OB][4];
     int nob = 0;
@@ -1559,8 +1570,9 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
                         ob[OB - 1][e] = reduce13_mdp([&](int d) { return acc[d][e]; }, Lm, lazy);
                     else
                         ob[OB - 1][e] =
-                            MINB > 1 ? reduce13_mont<true>([&](int d) { return acc[d][e]; }, Lm, lazy)
-                                     : reduce13_mont<false>([&](int d) { return acc[d][e]; }, Lm, lazy);
+                            MINB > 1 ? reduce13_mont<true, true>([&](int d) { return acc[d][e]; }, Lm, lazy)
+                                     : reduce13_mont<false, KPC != 32>([&](int d) { return acc[d][e]; },
+                                                                       Lm, lazy);
                 }
                 ++nob;
                 if (nob == OB || gu + gi == gcnt - 1) {
@@ -1713,7 +1725,8 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
     // instruction descriptor: S32 accumulate, u8 x u8, K-major A and B,
     // N = 16, M = BT
     const uint32_t idesc = (2u << 4) | ((16u >> 3) << 17) | ((uint32_t)(BT >> 4) << 24);
-    const Redc Lm = {limbs[l].q, limbs[l].mq, limbs + l};
+    const Redc Lm = {limbs[l].q, limbs[l].mq, limbs + l, limbs[l].pw8[0], limbs[l].pw8[1],
+                     limbs[l].pw8[2]};
     const int quarter = warp & 3, half = warp >> 2;      // TMEM lane quarter, column half
     const int r = quarter * 32 + lane;                   // this thread's image row
     const int b = b0 + r;
@@ -1766,7 +1779,7 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
 #pragma unroll
                 for (int d = 0; d < 13; ++d) S[d] = Sv[d][e];
                 out[(((size_t)l * B + b) * c_o + n) * M + g] =
-                    reduce13_mont<false>([&](int d) { return S[d]; }, Lm, lazy);
+                    reduce13_mont<false, HE_TC_PWR>([&](int d) { return S[d]; }, Lm, lazy);
             }
         }
     }
