@@ -199,6 +199,9 @@ extern "C" he_status he_ctx_create(const he_ring_desc* r, int device,
             Lm.pw8[1] = 1u << 16;
             Lm.pw8[2] = 1u << 24;
         }
+        Lm.td = (double)r->t;
+        Lm.t_invd = 1.0 / (double)r->t;
+        Lm.rtd = (double)rt;
         Lm.qd = (double)q;
         Lm.qinvd = 1.0 / (double)q;
         {

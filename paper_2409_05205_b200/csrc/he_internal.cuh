@@ -34,6 +34,7 @@ struct he_limb {
     u64 mq;                 // -q^{-1} mod 2^64 (Montgomery reduction of the int8 MAC sums)
     double mrd[3];          // 2^-64, 2^-32, 2^32 mod q, centred (FP64 form of that reduction)
     uint32_t pw8[3];        // 2^8, 2^16, 2^24 (runtime multipliers: one IMAD.WIDE per term)
+    double td, t_invd, rtd; // t, fl(1/t), r_t as doubles (context-wide; K4 mask encoding)
 };
 
 struct he_ctx {

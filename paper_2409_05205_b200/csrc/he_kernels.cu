@@ -51,6 +51,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_TC_PWR
 #define HE_TC_PWR 0       // tcgen05 MAC recombination with run-time power-of-two multipliers
 #endif
+#ifndef HE_K4_PF
+#define HE_K4_PF 1        // K4 scatter writer: phi1 loads one batch ahead
+#endif
 #ifndef HE_K4_SPEC
 #define HE_K4_SPEC 1         // K4: compile-time instance for the plain-20 s = 8 layers
 #endif
@@ -2012,11 +2015,56 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         // FP64 mask encoding (enc_dp) when the context has a table (t <= 2^20):
         // no random table gathers in the writer
         const bool encd = DP && enc_tab != nullptr;
-        const double td = (double)t, t_inv_d = 1.0 / (double)t, rtd = (double)r_t;
+        const double td = Lm.td, t_inv_d = Lm.t_invd, rtd = Lm.rtd;   // host-computed
         // transform outputs < 8q + 16 when the last pass is radix-16: reduce
         // before adding the encoding (|sum| must stay below 2^52)
         const bool xred = (logM & 3) == 0;
-        for (int j0 = jt; j0 < M; j0 += EB * jstep) {
+        if (HE_K4_PF && encd) {
+            // software-pipelined phi1 loads: batch k + 1 is in flight while
+            // batch k is encoded, added and stored
+            u32 mn[EB];
+            int vn[EB];
+            auto fetch = [&](int j0) {
+#pragma unroll
+                for (int e = 0; e < EB; ++e) {
+                    const int j = j0 + e * jstep;
+                    vn[e] = -1;
+                    if (want_c && j < M) {
+                        const int K_ = kr >> lstr, L_ = lc >> lstr;
+                        if (((kr | lc) & (cstr - 1)) == 0 && K_ < w_o && L_ < h_o)
+                            vn[e] = (K_ * h_o + L_) * c_ob + nl;
+                    }
+                    mn[e] = (ph && j < M && (orow || vn[e] >= 0)) ? ph[(j << logs) + u] : 0u;
+                    kr += dk;
+                    lc += dl;
+                    if (lc >= h_p) { lc -= h_p; ++kr; }
+                }
+            };
+            fetch(jt);
+            for (int j0 = jt; j0 < M; j0 += EB * jstep) {
+                u32 m[EB];
+                int vi[EB];
+#pragma unroll
+                for (int e = 0; e < EB; ++e) { m[e] = mn[e]; vi[e] = vn[e]; }
+                if (j0 + EB * jstep < M) fetch(j0 + EB * jstep);
+#pragma unroll
+                for (int e = 0; e < EB; ++e) {
+                    const int j = j0 + e * jstep;
+                    if (j >= M || (!orow && vi[e] < 0)) continue;
+                    double y = ph ? enc_dp(u2d(m[e]), rtd, td, t_inv_d, Lm.tinvd, Lm.qd, Lm.qinvd)
+                                  : 0.0;
+                    if (owned) {
+                        double x = reinterpret_cast<const double*>(sm)[abase + PAD(j)];
+                        if (xred) x = dp_reduce(x, Lm.qd, Lm.qinvd);
+                        y += x;
+                    }
+                    const u64 v = d2canon(y, Lm.qd, Lm.qinvd);
+                    if (orow) orow[(j << logs) + u] = v;
+                    if (vi[e] >= 0) crow[vi[e]] = v;
+                }
+            }
+        }
+        for (int j0 = jt; j0 < M && !(HE_K4_PF && encd); j0 += EB * jstep) {
             u32 m[EB];
             int vi[EB];
 #pragma unroll
@@ -2139,10 +2187,16 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     int* jv = reinterpret_cast<int*>(sm + (size_t)cc * stride);
     u64* crow = comp ? comp + (((size_t)b * P.n_ob + ob) * L + l) * P.n_valid : nullptr;
     if (crow) {
+        // j = kr h_p + lc without integer division: kr = floor((j + 1/2) / h_p)
+        // in float is exact for j < 2^22 ((j + 1/2) / h_p is >= 1/(2 h_p) away
+        // from an integer, the float error below that); the conv stride is a
+        // power of two (checked by he_conv_plan_make)
+        const float ihp = __frcp_rn((float)P.h_p);
+        const int lstr = __ffs(P.stride) - 1;
         for (int j = threadIdx.x; j < M; j += blockDim.x) {
-            const int kr = j / P.h_p, lc = j - kr * P.h_p;
-            const int K_ = kr / P.stride, L_ = lc / P.stride;
-            jv[j] = (kr == K_ * P.stride && lc == L_ * P.stride && K_ < P.w_o && L_ < P.h_o)
+            const int kr = (int)(((float)j + 0.5f) * ihp), lc = j - kr * P.h_p;
+            const int K_ = kr >> lstr, L_ = lc >> lstr;
+            jv[j] = (((kr | lc) & (P.stride - 1)) == 0 && K_ < P.w_o && L_ < P.h_o)
                         ? (K_ * P.h_o + L_) * c_ob : -1;
         }
     }
