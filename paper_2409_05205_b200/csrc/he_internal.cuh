@@ -17,6 +17,10 @@ typedef unsigned long long u64;
 typedef unsigned int u32;
 
 // Per-limb constants (device copy in he_ctx::d_limb).
+#ifndef HE_QDIV
+#define HE_QDIV 1
+#endif
+
 struct he_limb {
     u64 q;          // prime q_j
     u64 q2;         // 2 q_j
@@ -144,6 +148,21 @@ __device__ __forceinline__ u64 enc_plain(u64 m, const he_limb& L, u64 t,
 
 // acc += a * b (32 x 32 -> 64, 64-bit accumulate): one IMAD.WIDE.U32.
 // (Plain C `acc += (u64)a * b` makes nvcc add the zero high words too.)
+// x / d for 0 <= x < 2^20, 1 <= d < 2^20 without an integer division (the
+// kernels' block-index decompositions): floor((x + 1/2) r) with r the
+// hardware reciprocal of d (relative error < 2^-22) is exact there --
+// (x + 1/2)/d is at least 1/(2d) away from an integer and the float error is
+// below (x + 1/2)/d 1.25 2^-22 < 1/(2d); larger x take the integer division.
+__device__ __forceinline__ int qdiv(int x, int d) {
+#if HE_QDIV
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)d));
+    return x < (1 << 20) ? (int)(((float)x + 0.5f) * r) : x / d;
+#else
+    return x / d;
+#endif
+}
+
 __device__ __forceinline__ void madw(u64& acc, u32 a, u32 b) {
     asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
 }

@@ -174,7 +174,7 @@ __device__ __forceinline__ void ntt_store(u64* out, int li, int seg, int NS, int
                                           int l, const TileLay& T, F val) {
     if (OUT_FMT == 2) {
         unsigned char* A = reinterpret_cast<unsigned char*>(out);
-        const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
+        const int bb = qdiv(li, L), b = bb / T.n_ib, beta = bb - b * T.n_ib;
         const int s = 1 << T.logs, M = N >> T.logs, K = T.n_ib * T.Ku;
         const int lgt = __ffs(T.Gt) - 1;
         for (int i = 4 * threadIdx.x; i < NS; i += 4 * blockDim.x) {
@@ -228,7 +228,7 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
     double* sm = reinterpret_cast<double*>(sm_raw);
     const int N = 1 << logN, NS = N >> S;
     const int li = blockIdx.x >> S, seg = blockIdx.x & ((1 << S) - 1);
-    const int l = li % L;
+    const int l = li - qdiv(li, L) * L;
     const double q = limbs[l].qd, qinv = limbs[l].qinvd;
     const double* tw = twd_all + (size_t)l * N;
     const u64* src = in + (size_t)li * N;
@@ -1298,13 +1298,14 @@ __device__ __forceinline__ u64 redc128(u64 lo, u64 hi, Redc R, bool lazy) {
 template <bool K16, bool PWR, class S>
 __device__ __forceinline__ u64 reduce13_mont(S sd, Redc Lm, bool lazy) {
     u64 P[3];
-#pragma unroll
     // PWR: the powers of two come from registers loaded at run time, so each
     // term is one IMAD.WIDE.U32 (an immediate power of two is rewritten by
     // ptxas into SHL + HI + two adds).  Measured per layer: K = 16 43.2 ->
     // 41.0 us, K = 64 33.3 -> 32.9 us, but K = 32 39.0 -> 41.0 us (kept off).
     const u32 c8 = PWR ? Lm.p8 : 1u << 8, c16 = PWR ? Lm.p16 : 1u << 16,
               c24 = PWR ? Lm.p24 : 1u << 24;
+    // (no unroll pragma: the compiler's choice measured faster than forcing
+    // it -- K = 16 MAC 41.0 vs 43.0 us -- and `unroll 1` puts P in local memory)
     for (int k = 0; k < 3; ++k) {
         if (K16) {
             const u32 a = (u32)sd(4 * k) + ((u32)sd(4 * k + 1) << 8);
@@ -1396,7 +1397,7 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
     const int rw = imma_sw_dev(GS * KC);                  // A row: GS groups x KC bytes
     const int gb = 7 * nrow * swc;                        // B words per group
     const int buf_words = 7 * rows * rw + GS * gb;        // one staging buffer
-    const int nGc = (M + G - 1) / G;
+    const int nGc = (M + G - 1) / G;   // (qdiv here measured slower: 0.806 -> 0.817 ms MAC)
     const int l = blockIdx.x / nGc, g0 = (blockIdx.x - l * nGc) * G;
     const int b0 = blockIdx.y * rows;
     const int gcnt = min(G, M - g0);
@@ -1936,12 +1937,11 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     // (HP, WO, CST: padded row length h_p, output side w_o = h_o, conv stride)
     const int h_p = HP ? HP : P.h_p, w_o = WO ? WO : P.w_o, h_o = WO ? WO : P.h_o;
     const int cstr = CST ? CST : P.stride;
-    int r = blockIdx.x;
-    const int ch = r % nchunk;
-    r /= nchunk;
-    const int l = r % L;
-    r /= L;
-    const int ob = r % P.n_ob, b = r / P.n_ob;
+    int r = NCH ? (int)blockIdx.x / NCH : qdiv(blockIdx.x, nchunk);
+    const int ch = blockIdx.x - r * nchunk;
+    const int rl = qdiv(r, L);
+    const int l = r - rl * L;
+    const int b = qdiv(rl, P.n_ob), ob = rl - b * P.n_ob;
     const he_limb Lm = limbs[l];
     const u64 q = Lm.q, q2 = 2 * q;
     const ulonglong2* twi = twi_all + (size_t)l * N;
@@ -2169,12 +2169,11 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     const int cc = CCC ? CCC : cc_, nchunk = NCH ? NCH : nchunk_, stride = STC ? STC : stride_;
     const int c_ob = COB ? COB : P.c_ob, s_ = 1 << logs, step = COB ? s_ / COB : P.step;
     const int N = 1 << logN, M = N >> logs, logM = logN - logs;
-    int r = blockIdx.x;
-    const int ch = r % nchunk;
-    r /= nchunk;
-    const int l = r % L;
-    r /= L;
-    const int ob = r % P.n_ob, b = r / P.n_ob;
+    int r = NCH ? (int)blockIdx.x / NCH : qdiv(blockIdx.x, nchunk);
+    const int ch = blockIdx.x - r * nchunk;
+    const int rl = qdiv(r, L);
+    const int l = r - rl * L;
+    const int b = qdiv(rl, P.n_ob), ob = rl - b * P.n_ob;
     const double qd = limbs[l].qd, qi = limbs[l].qinvd, tinvq = limbs[l].tinvd;
     const int ch0 = ch * cc, ncc = min(cc, c_ob - ch0);
     const u64* fb = fold + (((size_t)l * B + b) * P.c_o + ob * c_ob + ch0) * M;
