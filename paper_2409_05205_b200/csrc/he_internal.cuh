@@ -20,6 +20,9 @@ typedef unsigned int u32;
 #ifndef HE_QDIV
 #define HE_QDIV 1
 #endif
+#ifndef HE_TW_LAZY
+#define HE_TW_LAZY 1      // radix-16 CT passes: the last stage's twiddles loaded at that stage
+#endif
 
 struct he_limb {
     u64 q;          // prime q_j
@@ -285,7 +288,7 @@ __device__ __forceinline__ void ct_bfly_dp(double& X, double& Y, double w, doubl
 // to |x| <= q/2 + 1 at the start of the pass; stage r inputs are then below
 // (0.5 + r) q + 1 (|T| <= q), so for K <= 4 every stage multiplies directly
 // (multiplicand < 3.5 q + 1 < 4 q).  Outputs < 4.5 q + 1.
-template <int K, bool NORED = false>
+template <int K, bool NORED = false, bool LZ = false>
 __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0, int seg,
                                            int split, const double* __restrict__ tw,
                                            double q, double qinv) {
@@ -297,8 +300,13 @@ __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0
         const int blk = g >> ltk, off = g & (tk - 1);
         const int base = (blk << (lt0 + 1)) + off;
         double tws[(1 << K) - 1];
+        // LZ (the 64-register conv-path kernels): the last HE_TW_LAZY stages'
+        // twiddles are loaded when each stage starts -- fewer live registers
+        // in radix-16 passes, spills 72 -> 40 bytes, s = 8 forward NTT 62.4 ->
+        // 60.2 us; the 80-register full transforms keep loading them up front
+        constexpr int RUP = (LZ && HE_TW_LAZY && K == 4) ? K - HE_TW_LAZY : K;
 #pragma unroll
-        for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
+        for (int r = 0, o = 0; r < RUP; o += (1 << r), ++r) {
             const int twb = (1 << (st0 + r)) + (seg << (st0 + r - split)) + (blk << r);
             load_tw_run(tws + o, tw, twb, 1 << r);
         }
@@ -309,6 +317,10 @@ __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0
                          : dp_reduce(sm[PAD(base + (c << ltk))], q, qinv);
 #pragma unroll
         for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
+            if (r >= RUP) {
+                const int twb = (1 << (st0 + r)) + (seg << (st0 + r - split)) + (blk << r);
+                load_tw_run(tws + o, tw, twb, 1 << r);
+            }
             const int half = 1 << (K - 1 - r);
 #pragma unroll
             for (int c = 0; c < (1 << K); ++c) {
@@ -322,7 +334,7 @@ __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0
     }
 }
 
-template <int RMAX>
+template <int RMAX, bool LZ = false>
 __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg, int split,
                                           const double* tw, double q, double qinv,
                                           int end) {
@@ -343,12 +355,12 @@ __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg,
         st += rem;
         __syncthreads();
     } else if (split + RMAX <= 4) {
-        ct_pass_dp<RMAX, true>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        ct_pass_dp<RMAX, true, LZ>(sm, logN, NS, st, seg, split, tw, q, qinv);
         st += RMAX;
         __syncthreads();
     }
     for (; st < end; st += RMAX) {
-        ct_pass_dp<RMAX>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        ct_pass_dp<RMAX, false, LZ>(sm, logN, NS, st, seg, split, tw, q, qinv);
         __syncthreads();
     }
 }

@@ -283,7 +283,7 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
     }
     if (S) cg::this_cluster().sync();
     else __syncthreads();
-    ct_all_dp<RM>(sm, logN, NS, seg, S, tw, q, qinv, end);    // outputs < 4 q
+    ct_all_dp<RM, OUT_FMT == 2>(sm, logN, NS, seg, S, tw, q, qinv, end);    // outputs < 4 q
     ntt_store<OUT_FMT>(out, li, seg, NS, N, L, l, T,
                        [&](int i) {
                            return OUT_FMT == 2 ? d2lazy(sm[PAD(i)], q, qinv)
