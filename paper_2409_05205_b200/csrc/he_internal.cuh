@@ -334,7 +334,7 @@ __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0
     }
 }
 
-template <int RMAX, bool LZ = false>
+template <int RMAX, bool LZ = false, bool UNR = false>
 __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg, int split,
                                           const double* tw, double q, double qinv,
                                           int end) {
@@ -358,6 +358,17 @@ __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg,
         ct_pass_dp<RMAX, true, LZ>(sm, logN, NS, st, seg, split, tw, q, qinv);
         st += RMAX;
         __syncthreads();
+    }
+    if (UNR) {
+        // compile-time geometry (the plain-20 instances): unrolled, so every
+        // pass's stage offset and strides are immediates
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            if (st + p * RMAX >= end) break;
+            ct_pass_dp<RMAX, false, LZ>(sm, logN, NS, st + p * RMAX, seg, split, tw, q, qinv);
+            __syncthreads();
+        }
+        return;
     }
     for (; st < end; st += RMAX) {
         ct_pass_dp<RMAX, false, LZ>(sm, logN, NS, st, seg, split, tw, q, qinv);
