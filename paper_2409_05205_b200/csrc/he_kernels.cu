@@ -58,6 +58,9 @@ namespace cg = cooperative_groups;
 #define HE_NTT_UNR 1      // s = 8 forward-NTT instances: pass loop unrolled (59.3 vs 60.1 us;
                           // the s = 32 instance measured slower, 34.1 vs 31.1 us)
 #endif
+#ifndef HE_FOLD_GN
+#define HE_FOLD_GN 1      // s = 32 / s = 128 plain-20 layers: fold in [l][b][g][n] layout
+#endif
 #ifndef HE_K4_SPEC
 #define HE_K4_SPEC 1         // K4: compile-time instance for the plain-20 s = 8 layers
 #endif
@@ -1382,7 +1385,8 @@ struct FastDiv {
 // fixed; LZ 1/0: lazy fixed, -1 runtime) turn the shared-memory strides into
 // immediates (the generic form spends about a fifth of its instructions on
 // address arithmetic); 0 / -1 keep the runtime arguments.
-template <int TB16, int MINB = 1, int KPC = 0, int KCC = 0, int COC = 0, int GSC = 0, int LZ = -1>
+template <int TB16, int MINB = 1, int KPC = 0, int KCC = 0, int COC = 0, int GSC = 0, int LZ = -1,
+          int FL = 0>
 __global__ void __launch_bounds__(MINB > 1 ? 128 : 512, MINB)
 k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
            u64* __restrict__ out, int B, int L, int M, int c_o_, int Kp_, int G, int GS_,
@@ -1563,7 +1567,26 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
                     }
                 }
             }
-            if (kc == nkc - 1) {
+            if (FL && kc == nkc - 1) {
+                // fold layout [l][b][g][n] (FL = 1): the 4 outputs of a lane are
+                // two channel pairs, each one 16-byte store; the 4 lanes of a
+                // quad cover 8 consecutive channels (64 contiguous bytes)
+                const int g = g0 + gu + gi;
+                u64 v[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    v[e] = reduce13_mont<false, KPC != 32>([&](int d) { return acc[d][e]; }, Lm,
+                                                           lazy);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int b = b0 + bt * 16 + gq + 8 * h;
+                    const int n = nt * 8 + 2 * tq;
+                    if (b < B && n < c_o)
+                        *reinterpret_cast<ulonglong2*>(
+                            out + (((size_t)l * B + b) * M + g) * c_full + n0 + n) =
+                            make_ulonglong2(v[2 * h], v[2 * h + 1]);
+                }
+            } else if (kc == nkc - 1) {
                 // outputs of HE_MAC_OB consecutive groups are kept (shift
                 // register ob, newest last) and leave as one run of HE_MAC_OB
                 // words per (b, n) row of the fold, instead of 8-byte writes
@@ -1812,7 +1835,8 @@ static he_status launch_mac_tc(const unsigned char* A, const unsigned char* Fpl,
 static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fpl, u64* out,
                                  int B, int n_ib, int L, int logN, int logs, int c_o,
                                  const he_limb* limbs, cudaStream_t st, int Ku, int lazy,
-                                 int mac_tc) {
+                                 int mac_tc, int fl_req = 0, int* fl_used = nullptr) {
+    if (fl_used) *fl_used = 0;
     const int M = (1 << logN) >> logs, K = n_ib * Ku;
     const int Kp = imma_kp(K);
     if (c_o > 256) return HE_ESHAPE;
@@ -1902,6 +1926,21 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
             k = k_mac_imma<2, 1, 64, 64, 64, 1, 1>;
         else if (!k16 && Kp == 64 && KC == 32 && c_o == 64 && GS == 1)
             k = k_mac_imma<2, 1, 64, 32, 64, 1, 1>;
+    }
+    // fold layout [l][b][g][n] for the instances K4's row writer reads it from
+    // (plain-20 s = 32 / s = 128 layers; the caller asks only then)
+    if (HE_MAC_SPEC && fl_req && lazy && !k16 && nct == 1) {
+        auto kf = k;
+        if (TB16 == 2 && Kp == 32 && KC == 32 && c_o == 32 && GS == 2)
+            kf = k_mac_imma<2, 1, 32, 32, 32, 2, 1, 1>;
+        else if (TB16 == 1 && Kp == 32 && KC == 32 && c_o == 64 && GS == 1)
+            kf = k_mac_imma<1, 1, 32, 32, 64, 1, 1, 1>;
+        else if (TB16 == 1 && Kp == 64 && KC == 64 && c_o == 64 && GS == 1)
+            kf = k_mac_imma<1, 1, 64, 64, 64, 1, 1, 1>;
+        if (kf != k) {
+            k = kf;
+            if (fl_used) *fl_used = 1;
+        }
     }
     if (!set_smem(k, smem)) return HE_ECUDA;
     dim3 grid(L * ((M + G - 1) / G), (B + rows - 1) / rows, nct);
@@ -2160,8 +2199,10 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
 // leave as one 16-byte store and their phi1 as one 8-byte load, a warp
 // covers whole runs of the row, and the valid-slot payload index comes from
 // a per-CTA table jv[j] = K w_o' + L (or -1), built while the fold rows load,
-// instead of per-element row/column tracking.
-template <int V, int LN = 0, int LS = 0, int CCC = 0, int STC = 0, int NCH = 0, int COB = 0>
+// instead of per-element row/column tracking.  FL = 1: the fold arrives in
+// the [l][b][g][n] layout (k_mac_imma FL = 1; CCC, COB fixed).
+template <int V, int LN = 0, int LS = 0, int CCC = 0, int STC = 0, int NCH = 0, int COB = 0,
+          int FL = 0>
 __global__ void __launch_bounds__(256, HE_K4_ROWS_MINB)
 k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
             u64* __restrict__ out, u64* __restrict__ comp, PlanDev P, int B, int L, int logN_,
@@ -2182,9 +2223,22 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     const int ch0 = ch * cc, ncc = min(cc, c_ob - ch0);
     const u64* fb = fold + (((size_t)l * B + b) * P.c_o + ob * c_ob + ch0) * M;
     const int tot = ncc * M, nvalid_a = min(ncc, P.c_o - (ob * c_ob + ch0));
-    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-        const bool ok = (idx >> logM) < nvalid_a;
-        cp_async_n<8>(sm + (idx >> logM) * stride + PAD(idx & (M - 1)), ok ? fb + idx : fb, ok);
+    if (FL) {
+        // [l][b][g][n]: consecutive threads take consecutive channels of one group
+        static_assert(!FL || (CCC > 0 && COB > 0), "FL needs the compile-time chunk");
+        constexpr int LCC = FL ? __builtin_ctz(CCC > 0 ? CCC : 1) : 0;
+        const u64* fg = fold + ((size_t)l * B + b) * M * P.c_o + ob * c_ob + ch0;
+        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+            const int chn = idx & (CCC - 1), g = idx >> LCC;
+            const bool ok = chn < nvalid_a;
+            cp_async_n<8>(sm + chn * stride + PAD(g), ok ? fg + (size_t)g * P.c_o + chn : fold, ok);
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+            const bool ok = (idx >> logM) < nvalid_a;
+            cp_async_n<8>(sm + (idx >> logM) * stride + PAD(idx & (M - 1)), ok ? fb + idx : fb,
+                          ok);
+        }
     }
     cp_async_commit();
     int* jv = reinterpret_cast<int*>(sm + (size_t)cc * stride);
@@ -2316,10 +2370,17 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
                                          tile_gt(c->N >> P.logs), P.logs, P.Ku});
     if (s != HE_OK) return s;
     rec(ev, 1, st);
+    // K4 row-writer instances that read the [l][b][g][n] fold (see below)
+    const int Mq = c->N >> P.logs;
+    const bool rows_path = c->ntt_mode == 0 && c->d_enc != nullptr && Mq >= 2 &&
+                           Mq <= HE_K4_ROWS_MAXM && HE_K4_ROWS;
+    const bool fl_req = HE_FOLD_GN && HE_K4_SPEC && rows_path && c->logN == 14 &&
+                        ((P.logs == 5 && P.c_ob == 32) || (P.logs == 7 && P.c_ob == 64));
+    int fl_used = 0;
     if (imma)
         s = launch_mac_imma((const unsigned char*)spec, (const unsigned char*)d_fspec, fold, B,
                             P.n_ib, c->L, c->logN, P.logs, P.c_o, c->d_limb, st, P.Ku,
-                            c->ntt_mode == 0, c->mac_tc);
+                            c->ntt_mode == 0, c->mac_tc, fl_req, &fl_used);
     else
         s = launch_mac(spec, (const u64*)d_fspec, fold, B, P.n_ib, c->L, c->logN, P.logs,
                        P.c_o, c->d_limb, st, P.Ku);
@@ -2347,10 +2408,17 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
         auto k4 = v2 ? k_intt_rows<2> : k_intt_rows<1>;
         if (HE_K4_SPEC && v2 && c->logN == 14) {       // plain-20 s = 32 and s = 128 layers
             if (P.logs == 5 && cc == 8 && stride == 546 && nchunk == 4 && P.c_ob == 32)
-                k4 = k_intt_rows<2, 14, 5, 8, 546, 4, 32>;
+                k4 = fl_used ? k_intt_rows<2, 14, 5, 8, 546, 4, 32, 1>
+                             : k_intt_rows<2, 14, 5, 8, 546, 4, 32>;
             else if (P.logs == 7 && cc == 32 && stride == 137 && nchunk == 2 && P.c_ob == 64)
-                k4 = k_intt_rows<2, 14, 7, 32, 137, 2, 64>;
+                k4 = fl_used ? k_intt_rows<2, 14, 7, 32, 137, 2, 64, 1>
+                             : k_intt_rows<2, 14, 7, 32, 137, 2, 64>;
         }
+        // (fl_req is set exactly for these two instances' shapes, so a fold in
+        //  the [l][b][g][n] layout always meets its reader; guard regardless)
+        if (fl_used && k4 != k_intt_rows<2, 14, 5, 8, 546, 4, 32, 1> &&
+            k4 != k_intt_rows<2, 14, 7, 32, 137, 2, 64, 1>)
+            return HE_ESHAPE;
         if (!set_smem(k4, smem)) return HE_ECUDA;
         rec(ev, 2, st);
         const double td = (double)c->t;
