@@ -61,6 +61,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_FOLD_GN
 #define HE_FOLD_GN 1      // s = 32 / s = 128 plain-20 layers: fold in [l][b][g][n] layout
 #endif
+#ifndef HE_FOLD_GN8
+#define HE_FOLD_GN8 3     // s = 8 layers (scatter K4, cc = 2): fold [l][b][n/2][g][2] (3), [l][b][g][n] (1), off (0)
+#endif
 #ifndef HE_K4_SPEC
 #define HE_K4_SPEC 1         // K4: compile-time instance for the plain-20 s = 8 layers
 #endif
@@ -1567,7 +1570,7 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
                     }
                 }
             }
-            if (FL && kc == nkc - 1) {
+            if (FL == 1 && kc == nkc - 1) {
                 // fold layout [l][b][g][n] (FL = 1): the 4 outputs of a lane are
                 // two channel pairs, each one 16-byte store; the 4 lanes of a
                 // quad cover 8 consecutive channels (64 contiguous bytes)
@@ -1575,8 +1578,10 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
                 u64 v[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    v[e] = reduce13_mont<false, KPC != 32>([&](int d) { return acc[d][e]; }, Lm,
-                                                           lazy);
+                    v[e] = MINB > 1
+                               ? reduce13_mont<true, true>([&](int d) { return acc[d][e]; }, Lm, lazy)
+                               : reduce13_mont<false, KPC != 32>([&](int d) { return acc[d][e]; },
+                                                                 Lm, lazy);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int b = b0 + bt * 16 + gq + 8 * h;
@@ -1606,7 +1611,35 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
                                                                        Lm, lazy);
                 }
                 ++nob;
-                if (nob == OB || gu + gi == gcnt - 1) {
+                if (FL == 3 && (nob == OB || gu + gi == gcnt - 1)) {
+                    // fold layout [l][b][n/2][g][2] (FL = 3): a lane's channel
+                    // pair (2tq, 2tq + 1) over its OB = 2 groups is 32
+                    // contiguous bytes
+                    static_assert(FL != 3 || HE_MAC_OB == 2, "FL = 3 pairs groups");
+                    const int gs0 = g - (OB - 1);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int b = b0 + bt * 16 + gq + 8 * h;
+                        const int n = nt * 8 + 2 * tq;
+                        if (b >= B || n >= c_o) continue;
+                        u64* pr = out + (((size_t)l * B + b) * (c_full >> 1) + ((n0 + n) >> 1)) *
+                                            (2 * (size_t)M);
+                        if (nob == OB && (gs0 & 1) == 0) {
+                            ulonglong2* q2 = reinterpret_cast<ulonglong2*>(pr + 2 * gs0);
+                            q2[0] = make_ulonglong2(ob[0][2 * h], ob[0][2 * h + 1]);
+                            q2[1] = make_ulonglong2(ob[1][2 * h], ob[1][2 * h + 1]);
+                        } else {
+#pragma unroll
+                            for (int z = 0; z < OB; ++z)
+                                if (z >= OB - nob) {
+                                    pr[2 * (gs0 + z)] = ob[z][2 * h];
+                                    pr[2 * (gs0 + z) + 1] = ob[z][2 * h + 1];
+                                }
+                        }
+                    }
+                    nob = 0;
+                }
+                if (FL != 3 && (nob == OB || gu + gi == gcnt - 1)) {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int b = b0 + bt * 16 + gq + 8 * (e >> 1);
@@ -1929,9 +1962,14 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
     }
     // fold layout [l][b][g][n] for the instances K4's row writer reads it from
     // (plain-20 s = 32 / s = 128 layers; the caller asks only then)
-    if (HE_MAC_SPEC && fl_req && lazy && !k16 && nct == 1) {
+    if (HE_MAC_SPEC && fl_req && lazy) {
         auto kf = k;
-        if (TB16 == 2 && Kp == 32 && KC == 32 && c_o == 32 && GS == 2)
+        if (k16 && TB16 == 2 && Kp == 16 && KC == 16 && c_o == 16 && GS == 4)
+            kf = fl_req == 3 ? k_mac_imma<2, HE_MAC_K16_MINB, 16, 16, 16, 4, 1, 3>
+                             : k_mac_imma<2, HE_MAC_K16_MINB, 16, 16, 16, 4, 1, 1>;
+        else if (k16 || nct != 1)
+            ;
+        else if (TB16 == 2 && Kp == 32 && KC == 32 && c_o == 32 && GS == 2)
             kf = k_mac_imma<2, 1, 32, 32, 32, 2, 1, 1>;
         else if (TB16 == 1 && Kp == 32 && KC == 32 && c_o == 64 && GS == 1)
             kf = k_mac_imma<1, 1, 32, 32, 64, 1, 1, 1>;
@@ -1939,7 +1977,7 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
             kf = k_mac_imma<1, 1, 64, 64, 64, 1, 1, 1>;
         if (kf != k) {
             k = kf;
-            if (fl_used) *fl_used = 1;
+            if (fl_used) *fl_used = (k16 && fl_req == 3) ? 3 : 1;
         }
     }
     if (!set_smem(k, smem)) return HE_ECUDA;
@@ -1965,7 +2003,7 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
 // s = 8 instance turns the transform's and the writer's index arithmetic
 // into immediates; 0 keeps the runtime values.
 template <bool DP, int LN = 0, int LS = 0, int CCC = 0, int STC = 0, int NCH = 0, int COB = 0,
-          int HP = 0, int WO = 0, int CST = 0>
+          int HP = 0, int WO = 0, int CST = 0, int FL = 0>
 __global__ void __launch_bounds__(256, 4)
 k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                u64* __restrict__ out, u64* __restrict__ comp, PlanDev P, int B, int L,
@@ -1993,7 +2031,32 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     const u64* fb = fold + (((size_t)l * B + b) * P.c_o + ob * c_ob + ch0) * M;
     const int tot = ncc * M, nvalid_a = min(ncc, P.c_o - (ob * c_ob + ch0));
     const bool raw = DP && logM >= 1;       // cp.async the residues, first pass converts
-    if (raw) {
+    if (raw && FL == 3) {
+        // fold layout [l][b][n/2][g][2] (FL = 3, cc = 2: the chunk is one
+        // channel pair, 2 M contiguous words)
+        static_assert(FL != 3 || CCC == 2, "FL = 3 reads channel pairs");
+        const u64* fg = fold + (((size_t)l * B + b) * (P.c_o >> 1) + ((ob * c_ob + ch0) >> 1)) *
+                                   (2 * (size_t)M);
+        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+            const int chn = idx & 1, g = idx >> 1;
+            const bool ok = chn < nvalid_a;
+            cp_async_n<8>(sm + chn * stride + PAD(g), ok ? fg + idx : fold, ok);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+    } else if (raw && FL) {
+        // fold layout [l][b][g][n] (FL = 1, k_mac_imma FL = 1): consecutive
+        // threads take consecutive channels of one group
+        constexpr int LCC = FL ? __builtin_ctz(CCC > 0 ? CCC : 1) : 0;
+        const u64* fg = fold + ((size_t)l * B + b) * M * P.c_o + ob * c_ob + ch0;
+        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+            const int chn = idx & (CCC - 1), g = idx >> LCC;
+            const bool ok = chn < nvalid_a;
+            cp_async_n<8>(sm + chn * stride + PAD(g), ok ? fg + (size_t)g * P.c_o + chn : fold, ok);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+    } else if (raw) {
         for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
             const bool ok = (idx >> logM) < nvalid_a;
             cp_async_n<8>(sm + (idx >> logM) * stride + PAD(idx & (M - 1)), ok ? fb + idx : fb,
@@ -2374,8 +2437,14 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
     const int Mq = c->N >> P.logs;
     const bool rows_path = c->ntt_mode == 0 && c->d_enc != nullptr && Mq >= 2 &&
                            Mq <= HE_K4_ROWS_MAXM && HE_K4_ROWS;
-    const bool fl_req = HE_FOLD_GN && HE_K4_SPEC && rows_path && c->logN == 14 &&
-                        ((P.logs == 5 && P.c_ob == 32) || (P.logs == 7 && P.c_ob == 64));
+    const bool fl_rows = HE_FOLD_GN && HE_K4_SPEC && rows_path && c->logN == 14 &&
+                         ((P.logs == 5 && P.c_ob == 32) || (P.logs == 7 && P.c_ob == 64));
+    // the s = 8 scatter instances (K4 below: cc = 2, stride 2184, 4 chunks)
+    const bool fl_s8 = HE_FOLD_GN8 && HE_K4_SPEC && c->ntt_mode == 0 && c->logN == 14 &&
+                       P.logs == 3 && P.c_ob == 8 && P.h_p == 34 &&
+                       ((P.w_o == 32 && P.h_o == 32 && P.stride == 1) ||
+                        (P.w_o == 16 && P.h_o == 16 && P.stride == 2));
+    const int fl_req = fl_rows ? 1 : (fl_s8 ? HE_FOLD_GN8 : 0);
     int fl_used = 0;
     if (imma)
         s = launch_mac_imma((const unsigned char*)spec, (const unsigned char*)d_fspec, fold, B,
@@ -2444,10 +2513,19 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
         stride == 2184 && nchunk == 4 && P.c_ob == 8) {
         k4 = k_intt_scatter<true, 14, 3, 2, 2184, 4, 8>;
         if (P.h_p == 34 && P.w_o == 32 && P.h_o == 32 && P.stride == 1)
-            k4 = k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 32, 1>;
+            k4 = fl_used == 3 ? k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 32, 1, 3>
+               : fl_used ? k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 32, 1, 1>
+                         : k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 32, 1>;
         else if (P.h_p == 34 && P.w_o == 16 && P.h_o == 16 && P.stride == 2)
-            k4 = k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 16, 2>;
+            k4 = fl_used == 3 ? k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 16, 2, 3>
+               : fl_used ? k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 16, 2, 1>
+                         : k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 16, 2>;
     }
+    if (fl_used && k4 != k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 32, 1, 1> &&
+        k4 != k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 16, 2, 1> &&
+        k4 != k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 32, 1, 3> &&
+        k4 != k_intt_scatter<true, 14, 3, 2, 2184, 4, 8, 34, 16, 2, 3>)
+        return HE_ESHAPE;                     // (unreachable: fl_req matches these shapes)
     if (!set_smem(k4, smem)) return HE_ECUDA;
     rec(ev, 2, st);
     k4<<<(unsigned)(B * P.n_ob * c->L * nchunk), 256, smem, st>>>(
