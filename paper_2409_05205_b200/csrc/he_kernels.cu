@@ -64,6 +64,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_FOLD_GN8
 #define HE_FOLD_GN8 3     // s = 8 layers (scatter K4, cc = 2): fold [l][b][n/2][g][2] (3), [l][b][g][n] (1), off (0)
 #endif
+#ifndef HE_FOLD_GN5
+#define HE_FOLD_GN5 1     // config 5 (tcgen05 MAC + row writer): fold in [l][b][g][n]
+#endif
 #ifndef HE_K4_SPEC
 #define HE_K4_SPEC 1         // K4: compile-time instance for the plain-20 s = 8 layers
 #endif
@@ -1723,6 +1726,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
 // TMEM budget: 256 columns per CTA, and 128 registers x 256 threads cap the
 // kernel at two CTAs per SM (512 columns, the whole TMEM), so an allocation
 // never waits on another CTA of this kernel; no other kernel uses TMEM.
+template <int FL = 0>
 __global__ void __launch_bounds__(256, 2)
 k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
          u64* __restrict__ out, int B, int L, int M, int c_o, int Kp, int Gt,
@@ -1834,7 +1838,22 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
         __syncthreads();                       // every lane read: TMEM free for chunk ch + 1
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (threadIdx.x == 0 && ch + 1 < nchunks) issue(ch + 1);
-        if (b < B) {
+        if (FL == 1 && b < B && ch * 16 + half * 8 + 8 <= c_o) {
+            // fold layout [l][b][g][n]: the thread's 8 channels are 64
+            // contiguous bytes (four 16-byte stores, not eight rows)
+            u64 v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                int S[13];
+#pragma unroll
+                for (int d = 0; d < 13; ++d) S[d] = Sv[d][e];
+                v[e] = reduce13_mont<false, HE_TC_PWR>([&](int d) { return S[d]; }, Lm, lazy);
+            }
+            ulonglong2* o2 = reinterpret_cast<ulonglong2*>(
+                out + (((size_t)l * B + b) * M + g) * c_o + ch * 16 + half * 8);
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) o2[e / 2] = make_ulonglong2(v[e], v[e + 1]);
+        } else if (b < B) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 const int n = ch * 16 + half * 8 + e;
@@ -1842,8 +1861,9 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
                 int S[13];
 #pragma unroll
                 for (int d = 0; d < 13; ++d) S[d] = Sv[d][e];
-                out[(((size_t)l * B + b) * c_o + n) * M + g] =
-                    reduce13_mont<false, HE_TC_PWR>([&](int d) { return S[d]; }, Lm, lazy);
+                const u64 v = reduce13_mont<false, HE_TC_PWR>([&](int d) { return S[d]; }, Lm, lazy);
+                if (FL == 1) out[(((size_t)l * B + b) * M + g) * c_o + n] = v;
+                else out[(((size_t)l * B + b) * c_o + n) * M + g] = v;
             }
         }
     }
@@ -1853,13 +1873,14 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
 
 static he_status launch_mac_tc(const unsigned char* A, const unsigned char* Fpl, u64* out, int B,
                                int L, int M, int c_o, int Kp, const he_limb* limbs,
-                               cudaStream_t st, int lazy) {
+                               cudaStream_t st, int lazy, int fl = 0) {
     const int Kt = (Kp + 31) & ~31, nrow = (c_o + 15) & ~15;
     const size_t smem = 7 * ((size_t)HE_MAC_TC_BT * Kt + (size_t)nrow * Kt);
     if (smem > 110 * 1024) return HE_ESHAPE;
-    if (!set_smem(k_mac_tc, smem)) return HE_ECUDA;
+    auto k = fl == 1 ? k_mac_tc<1> : k_mac_tc<0>;
+    if (!set_smem(k, smem)) return HE_ECUDA;
     dim3 grid(L * M, (B + HE_MAC_TC_BT - 1) / HE_MAC_TC_BT);
-    k_mac_tc<<<grid, 256, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, tile_gt(M), limbs, lazy);
+    k<<<grid, 256, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, tile_gt(M), limbs, lazy);
     return HE_OK;
 }
 
@@ -1878,8 +1899,12 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
         const int mode = mac_tc;
         const int Kt = (Kp + 31) & ~31, nr16 = (c_o + 15) & ~15;
         const bool fits = 7 * ((size_t)HE_MAC_TC_BT * Kt + (size_t)nr16 * Kt) <= 110 * 1024;
-        if (fits && (mode == 1 || (mode == 2 && B >= HE_MAC_TC_BT)))
-            return launch_mac_tc(A, Fpl, out, B, L, M, c_o, Kp, limbs, st, lazy);
+        if (fits && (mode == 1 || (mode == 2 && B >= HE_MAC_TC_BT))) {
+            // ([l][b][g][n] fold when the caller's K4 instance reads it)
+            const int fl = fl_req == 4 ? 1 : 0;
+            if (fl_used) *fl_used = fl ? 4 : 0;
+            return launch_mac_tc(A, Fpl, out, B, L, M, c_o, Kp, limbs, st, lazy, fl);
+        }
     }
     const int c_full = c_o;
     // K = 16 layers with 32 channels: two 16-channel tiles (grid.z) of the
@@ -1962,7 +1987,7 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
     }
     // fold layout [l][b][g][n] for the instances K4's row writer reads it from
     // (plain-20 s = 32 / s = 128 layers; the caller asks only then)
-    if (HE_MAC_SPEC && fl_req && lazy) {
+    if (HE_MAC_SPEC && (fl_req == 1 || fl_req == 3) && lazy) {
         auto kf = k;
         if (k16 && TB16 == 2 && Kp == 16 && KC == 16 && c_o == 16 && GS == 4)
             kf = fl_req == 3 ? k_mac_imma<2, HE_MAC_K16_MINB, 16, 16, 16, 4, 1, 3>
@@ -2444,7 +2469,11 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
                        P.logs == 3 && P.c_ob == 8 && P.h_p == 34 &&
                        ((P.w_o == 32 && P.h_o == 32 && P.stride == 1) ||
                         (P.w_o == 16 && P.h_o == 16 && P.stride == 2));
-    const int fl_req = fl_rows ? 1 : (fl_s8 ? HE_FOLD_GN8 : 0);
+    // config 5 (N = 32768, s = 256, 64 channels): the tcgen05 MAC writes
+    // [l][b][g][n] for the k_intt_rows<2, 15, 8, 32, 137, 2, 64, 1> instance
+    const bool fl_c5 = HE_FOLD_GN5 && HE_K4_SPEC && rows_path && c->logN == 15 &&
+                       P.logs == 8 && P.c_ob == 64;
+    const int fl_req = fl_rows ? 1 : (fl_s8 ? HE_FOLD_GN8 : (fl_c5 ? 4 : 0));
     int fl_used = 0;
     if (imma)
         s = launch_mac_imma((const unsigned char*)spec, (const unsigned char*)d_fspec, fold, B,
@@ -2485,7 +2514,11 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
         }
         // (fl_req is set exactly for these two instances' shapes, so a fold in
         //  the [l][b][g][n] layout always meets its reader; guard regardless)
+        if (fl_used == 4 && HE_K4_SPEC && v2 && c->logN == 15 && P.logs == 8 && cc == 32 &&
+            stride == 137 && nchunk == 2 && P.c_ob == 64)
+            k4 = k_intt_rows<2, 15, 8, 32, 137, 2, 64, 1>;
         if (fl_used && k4 != k_intt_rows<2, 14, 5, 8, 546, 4, 32, 1> &&
+            k4 != k_intt_rows<2, 15, 8, 32, 137, 2, 64, 1> &&
             k4 != k_intt_rows<2, 14, 7, 32, 137, 2, 64, 1>)
             return HE_ESHAPE;
         if (!set_smem(k4, smem)) return HE_ECUDA;
