@@ -14,24 +14,24 @@ for line in out.splitlines():
     m = re.match(r"\s+/\*[0-9a-f]{4}\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_]*)", line)
     if cur and m:
         funcs[cur][m.group(2)] += 1
-want = [("k_ntt_fwd_dp_s1<2,14,3,2,8,16,16> (forward NTT, s = 8)", "_Z15k_ntt_fwd_dp_s1ILi2ELi14ELi3ELi2ELi8ELi16ELi16EEvPKyPyiiPK7he_limbPKd7TileLay"),
-        ("k_mac_imma<2,5,16,16,16,4,1> (MAC, K = 16)", None),
-        ("k_intt_scatter<1,14,3,2,2184,4,8,34,32,1> (INTT + scatter, s = 8)", None),
-        ("k_intt_rows<2,14,5,8,546,4,32> (INTT + rows, s = 32)", None),
-        ("k_mac_tc (tcgen05 MAC, B >= 128)", "_Z8k_mac_tcPKhS0_PyiiiiiiPK7he_limbi")]
+# the instances the config-4 / config-5 steps launch (profiles/launches_r02.csv)
+want = [("k_ntt_fwd_dp_s1<2,14,3,2,8,16,16> (forward NTT, s = 8)", "_Z15k_ntt_fwd_dp_s1ILi2ELi14ELi3ELi2ELi8ELi16ELi16EE"),
+        ("k_mac_imma<2,5,16,16,16,4,1,3> (MAC, K = 16, s = 8)", "_Z10k_mac_immaILi2ELi5ELi16ELi16ELi16ELi4ELi1ELi3EE"),
+        ("k_intt_scatter<1,14,3,2,2184,4,8,34,32,1,3> (INTT + scatter, s = 8)", "_Z14k_intt_scatterILb1ELi14ELi3ELi2ELi2184ELi4ELi8ELi34ELi32ELi1ELi3EE"),
+        ("k_intt_rows<2,14,5,8,546,4,32,1> (INTT + rows, s = 32)", "_Z11k_intt_rowsILi2ELi14ELi5ELi8ELi546ELi4ELi32ELi1EE"),
+        ("k_ntt_fwd_cols<2> (forward NTT, column form: s = 128, config 5)", "_Z14k_ntt_fwd_colsILi2EE"),
+        ("k_mac_tc<1> (tcgen05 MAC, B >= 128, config 5)", "_Z8k_mac_tcILi1EE")]
 def find(prefix):
     for f in funcs:
         if f.startswith(prefix):
             return f
     return None
-pre = {1: "_Z10k_mac_immaILi2ELi5ELi16ELi16ELi16ELi4ELi1EE", 2: "_Z14k_intt_scatterILb1ELi14ELi3ELi2ELi2184ELi4ELi8ELi34ELi32ELi1EE",
-       3: "_Z11k_intt_rowsILi2ELi14ELi5ELi8ELi546ELi4ELi32EE"}
 lines = ["# Round 2: SASS of the step kernels (sm_100a, `cuobjdump -sass` of libhe_rotfree.so)", "",
          "Static instruction counts per opcode (top 14); the tensor-core and FP64 opcodes show",
          "which pipe each kernel is built on (IMMA = mma.sync int8, UTCMMA / UTC* = tcgen05,",
          "DFMA/DADD/DMUL = the FP64 modular arithmetic, UBLKCP = TMA bulk copy).", ""]
 for i, (title, name) in enumerate(want):
-    name = name or find(pre[i])
+    name = find(name)
     c = funcs.get(name)
     if not c:
         lines.append(f"## {title}\n\n(not found)\n")
