@@ -1305,6 +1305,49 @@ __device__ __forceinline__ u64 redc128(u64 lo, u64 hi, Redc R, bool lazy) {
     const u64 t = hi + __umul64hi(m, R.q) + (lo != 0 ? 1ull : 0ull);
     return lazy ? t : csub(t, R.q);
 }
+// The same REDC done as two 32-bit word steps straight on the partial sums
+// (no 128-bit (lo, hi) assembly, no 64 x 64-bit products): with q' = -q^{-1}
+// mod 2^32 (the low word of R.mq) and V = P0 + P1 2^32 + P2 2^64 + P3 2^96,
+//   m0 = lo32(P0) q' mod 2^32,  A = (V + m0 q) / 2^32
+//      = hi32(P0) + P1 + m0 qhi + hi32(m0 qlo) + [lo32(P0) != 0]
+// (lo32(P0) + lo32(m0 qlo) is 0 mod 2^32, so its carry is that test, taken
+// from the carry flag of one mad.lo.cc), then the same step on A + P2 2^32 +
+// P3 2^64.  Result (V + m q) / 2^64 with m < 2^64: congruent to V R^{-1} and
+// below V / 2^64 + q < 2q (bound as redc128).  The running sums stay below
+// 2^57 (P_k < 2^55, m qhi < 2^50).
+#ifndef HE_REDC_W
+#define HE_REDC_W 1
+#endif
+__device__ __forceinline__ u64 redc_words(u64 P0, u64 P1, u64 P2, u32 P3, Redc R, bool lazy) {
+    const u32 qlo = (u32)R.q, qhi = (u32)(R.q >> 32), qp = (u32)R.mq;
+    u32 lo, hi;
+    asm("{\n\t"
+        ".reg .u32 m, x0, x1, d, p0l, p0h, p1l, p1h, p2l, p2h;\n\t"
+        "mov.b64 {p0l, p0h}, %2;\n\t"
+        "mov.b64 {p1l, p1h}, %3;\n\t"
+        "mov.b64 {p2l, p2h}, %4;\n\t"
+        "mul.lo.u32 m, p0l, %6;\n\t"
+        "add.cc.u32 x0, p1l, p0h;\n\t"
+        "addc.u32 x1, p1h, 0;\n\t"
+        "mad.lo.cc.u32 x0, m, %8, x0;\n\t"
+        "madc.hi.u32 x1, m, %8, x1;\n\t"
+        "mad.lo.cc.u32 d, m, %7, p0l;\n\t"
+        "madc.hi.cc.u32 x0, m, %7, x0;\n\t"
+        "addc.u32 x1, x1, 0;\n\t"
+        "mul.lo.u32 m, x0, %6;\n\t"
+        "add.cc.u32 %0, p2l, x1;\n\t"
+        "addc.u32 %1, p2h, %5;\n\t"
+        "mad.lo.cc.u32 %0, m, %8, %0;\n\t"
+        "madc.hi.u32 %1, m, %8, %1;\n\t"
+        "mad.lo.cc.u32 d, m, %7, x0;\n\t"
+        "madc.hi.cc.u32 %0, m, %7, %0;\n\t"
+        "addc.u32 %1, %1, 0;\n\t"
+        "}"
+        : "=r"(lo), "=r"(hi)
+        : "l"(P0), "l"(P1), "l"(P2), "r"(P3), "r"(qp), "r"(qlo), "r"(qhi));
+    const u64 t = ((u64)hi << 32) | lo;
+    return lazy ? t : csub(t, R.q);
+}
 // V = sum_{d<13} S_d 2^{8d} as (lo, hi): P_k = sum_{d=4k..4k+3} S_d 2^{8(d-4k)}
 // (three mad.wide each, or the 32-bit pairs when S_d < 2^23, i.e. K <= 16),
 // V = P0 + P1 2^32 + P2 2^64 + P3 2^96.
@@ -1332,10 +1375,14 @@ __device__ __forceinline__ u64 reduce13_mont(S sd, Redc Lm, bool lazy) {
             madw(P[k], (u32)sd(4 * k + 3), c24);
         }
     }
+#if HE_REDC_W
+    return redc_words(P[0], P[1], P[2], (u32)sd(12), Lm, lazy);
+#else
     const u64 P3 = (u64)(u32)sd(12);
     const u64 lo = P[0] + (P[1] << 32);
     const u64 hi = P[2] + (P[1] >> 32) + (P3 << 32) + (lo < P[0] ? 1 : 0);
     return redc128(lo, hi, Lm, lazy);
+#endif
 }
 
 // The same Montgomery-domain result on the FP64 pipe (otherwise idle in the
