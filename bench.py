@@ -71,6 +71,12 @@ def parse():
                     help="with --streams > 1: split each layer's batch across the "
                          "streams (batch) or put whole layers on alternating streams "
                          "(layers: independent layer jobs overlap)")
+    ap.add_argument("--schedule", choices=["lpt", "rr"], default="rr",
+                    help="--overlap layers: deal the layer jobs (and the FC job) to "
+                         "the streams longest-first onto the least-loaded stream, by "
+                         "their measured stand-alone times (lpt), or round-robin (rr; "
+                         "default -- lpt measured equal, 1.6995 vs 1.697 ms: the step "
+                         "is throughput-limited, not tail-limited)")
     ap.add_argument("--graph", type=int, default=1,
                     help="1: replay the step as a captured CUDA graph")
     ap.add_argument("--payload-only", type=int, default=0,
@@ -495,6 +501,39 @@ def main():
 
     po_flag = [bool(args.payload_only)]
     order = list(enumerate(layers))     # heavy layers first (reversed: 2.36 vs 2.34 ms)
+    # job -> stream: round-robin (layer i on stream i % nstr, the FC job on the
+    # next one), or LPT: every job timed alone once (after one warm-up call),
+    # then dealt longest first to the stream with the least work so far, so
+    # no stream is left running alone at the end of the step (round-robin put
+    # layers 1, 7, 13 and the FC, the heaviest mix, on one stream)
+    job_stream = {i: i % nstr for i in range(len(layers))}
+    job_stream["fc"] = len(layers) % nstr
+    job_ms = None
+    if nstr > 1 and args.overlap == "layers" and args.schedule == "lpt":
+        def run_job(j):
+            if j == "fc":
+                ctx.fc(fc["n_i"], fc["n_o"], fc["c0_d"], fc["wspec"], fc["benc"],
+                       fc["ph_d"], fc["out"], fc["ws"])
+            else:
+                lw = layers[j]
+                ctx.conv(lw.p, c0_d[j], fspecs[j], phi_d[j], outs[j], ws, compact=comps[j])
+        jobs = list(range(len(layers))) + (["fc"] if fc else [])
+        job_ms = {}
+        for j in jobs:
+            run_job(j)
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            run_job(j)
+            b_.record()
+            b_.synchronize()
+            job_ms[j] = a.elapsed_time(b_)
+        load = [0.0] * nstr
+        lpt = sorted(jobs, key=lambda j: -job_ms[j])
+        for j in lpt:
+            k = min(range(nstr), key=lambda k: load[k])
+            job_stream[j] = k
+            load[k] += job_ms[j]
+        order = [(j, layers[j]) for j in lpt if j != "fc"]
 
     def step():
         po = po_flag[0]
@@ -508,7 +547,7 @@ def main():
                 side[k].wait_event(fork_ev[0])
             for i, lw in order:
                 if args.overlap == "layers":
-                    k = i % nstr
+                    k = job_stream[i]
                     ctx.conv(lw.p, c0_d[i], fspecs[i], phi_d[i], None if po else outs[i],
                              ws_all[k], compact=comps[i], full=not po, stream=side[k])
                     continue
@@ -520,7 +559,7 @@ def main():
                 # the FC job is independent of the conv jobs (R22): it is
                 # the 20th layer job, dealt to the next stream in turn
                 ctx.fc(fc["n_i"], fc["n_o"], fc["c0_d"], fc["wspec"], fc["benc"],
-                       fc["ph_d"], fc["out"], fc["ws"], stream=side[len(layers) % nstr])
+                       fc["ph_d"], fc["out"], fc["ws"], stream=side[job_stream["fc"]])
             for k in range(1, nstr):
                 fork_ev[k].record(side[k])
                 stream.wait_event(fork_ev[k])
@@ -1338,6 +1377,10 @@ def main():
                                        f"collective)"),
                        "partition_axis": axis,
                        "streams": nstr, "overlap": args.overlap,
+                       "schedule": (args.schedule if nstr > 1 and args.overlap == "layers"
+                                    else None),
+                       "job_streams": ({str(j): k for j, k in job_stream.items()}
+                                       if nstr > 1 and args.overlap == "layers" else None),
                        "cuda_graph": graph is not None,
                        "mac": ("tcgen05.mma kind::i8, TMEM accumulators (k_mac_tc)"
                                if (B >= 128 and os.environ.get("HE_MAC_TC", "2") != "0")

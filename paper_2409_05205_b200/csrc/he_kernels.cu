@@ -94,6 +94,22 @@ namespace cg = cooperative_groups;
 #ifndef HE_K4_ROWS_MINB
 #define HE_K4_ROWS_MINB 4    // K4 row writer: CTAs per SM (register cap)
 #endif
+#ifndef HE_K4_W8
+#define HE_K4_W8 1           // K4 s = 8 instances: unrolled writer with immediate offsets
+#endif
+#ifndef HE_K4_CC32
+#define HE_K4_CC32 8         // K4 row writer, plain-20 s = 32 layers: channels per CTA
+#endif
+#ifndef HE_K4_CC128
+#define HE_K4_CC128 32       // K4 row writer, plain-20 s = 128 layers: channels per CTA
+#endif
+// the array strides the host derives for those chunks (16/cc mod 16, or odd)
+constexpr int k4_stride(int M, int cc) {
+    int st = M + (M >> 4);
+    while ((st & 15) != (cc < 16 ? (16 / cc) & 15 : 1) && !(cc >= 16 && (st & 1))) ++st;
+    return st;
+}
+constexpr int K4_ST32 = k4_stride(512, HE_K4_CC32), K4_ST128 = k4_stride(128, HE_K4_CC128);
 #ifndef HE_K4_WORDS
 #define HE_K4_WORDS 6144     // K4: fold-array budget per CTA (words)
 #endif
@@ -1315,6 +1331,9 @@ __device__ __forceinline__ u64 redc128(u64 lo, u64 hi, Redc R, bool lazy) {
 // P3 2^64.  Result (V + m q) / 2^64 with m < 2^64: congruent to V R^{-1} and
 // below V / 2^64 + q < 2q (bound as redc128).  The running sums stay below
 // 2^57 (P_k < 2^55, m qhi < 2^50).
+#ifndef HE_MAC_PWR32
+#define HE_MAC_PWR32 0      // K = 32 MAC: run-time power-of-two multipliers too
+#endif
 #ifndef HE_REDC_W
 #define HE_REDC_W 1
 #endif
@@ -1630,7 +1649,7 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
                 for (int e = 0; e < 4; ++e)
                     v[e] = MINB > 1
                                ? reduce13_mont<true, true>([&](int d) { return acc[d][e]; }, Lm, lazy)
-                               : reduce13_mont<false, KPC != 32>([&](int d) { return acc[d][e]; },
+                               : reduce13_mont<false, (KPC != 32 || HE_MAC_PWR32)>([&](int d) { return acc[d][e]; },
                                                                  Lm, lazy);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -1657,7 +1676,7 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
                     else
                         ob[OB - 1][e] =
                             MINB > 1 ? reduce13_mont<true, true>([&](int d) { return acc[d][e]; }, Lm, lazy)
-                                     : reduce13_mont<false, KPC != 32>([&](int d) { return acc[d][e]; },
+                                     : reduce13_mont<false, (KPC != 32 || HE_MAC_PWR32)>([&](int d) { return acc[d][e]; },
                                                                        Lm, lazy);
                 }
                 ++nob;
@@ -2178,6 +2197,56 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     // per-thread constants, and the (row, column) of j for the payload test
     // are advanced incrementally.  Four phi1 loads in flight; the mask encoding is
     // FP64 arithmetic (enc_dp) when the context has a table-sized t.
+    // Plain-20 s = 8 instances (two 2048-point channels per CTA, step 1, 256
+    // threads, mask on): the writer with every address an immediate offset.
+    // Thread (uo, jt) writes slot u0 + uo of groups j = jt + 128 e, e < 16,
+    // unrolled: phi1, the output row and the channel array advance by
+    // compile-time strides, and the payload index follows (kr, lc) of j
+    // (128 = 3 h_p + 26).  Same values and stores as the generic writer.
+    constexpr bool W8 = FL == 3 && LN == 14 && LS == 3 && CCC == 2 && COB == 8 && HP == 34 &&
+                        WO > 0 && CST > 0;
+    if (W8 && HE_K4_W8 && ph != nullptr && enc_tab != nullptr && blockDim.x == 256) {
+        constexpr int JS = 128, NE = 2048 / JS, EBW = 4;
+        constexpr int LST = CST == 1 ? 0 : (CST == 2 ? 1 : 2);
+        const int uo = threadIdx.x & 1, jt = threadIdx.x >> 1;
+        const int u = u0 + uo;                  // = the channel n of the block (step 1)
+        const double* xs = reinterpret_cast<const double*>(sm) + (u - ch0) * stride + PAD(jt);
+        const u32* pp = ph + (jt << 3) + u;
+        u64* op = orow ? orow + (jt << 3) + u : nullptr;
+        const double td = Lm.td, t_inv_d = Lm.t_invd, rtd = Lm.rtd, tinvq = Lm.tinvd;
+        const double qd = Lm.qd, qi = Lm.qinvd;
+        int kr = (jt * 1928) >> 16;             // jt / 34 for jt < 128
+        int lc = jt - kr * HP;
+        u32 mnext[EBW];
+#pragma unroll
+        for (int z = 0; z < EBW; ++z) mnext[z] = pp[z * (JS << 3)];
+#pragma unroll
+        for (int e0 = 0; e0 < NE; e0 += EBW) {
+            u32 m[EBW];
+#pragma unroll
+            for (int z = 0; z < EBW; ++z) m[z] = mnext[z];
+            if (e0 + EBW < NE) {
+#pragma unroll
+                for (int z = 0; z < EBW; ++z) mnext[z] = pp[(e0 + EBW + z) * (JS << 3)];
+            }
+#pragma unroll
+            for (int z = 0; z < EBW; ++z) {
+                const int e = e0 + z;
+                const int K_ = kr >> LST, L_ = lc >> LST;
+                const bool valid = crow && ((kr | lc) & (CST - 1)) == 0 && K_ < WO && L_ < WO;
+                kr += JS / HP;
+                lc += JS % HP;
+                if (lc >= HP) { lc -= HP; ++kr; }
+                if (!op && !valid) continue;
+                double y = enc_dp(u2d(m[z]), rtd, td, t_inv_d, tinvq, qd, qi);
+                y += xs[e * (JS + JS / 16)];    // PAD(jt + 128 e) = PAD(jt) + 136 e
+                const u64 v = d2canon(y, qd, qi);
+                if (op) op[e * (JS << 3)] = v;
+                if (valid) crow[(K_ * WO + L_) * COB + u] = v;
+            }
+        }
+        return;
+    }
     const int jstep = blockDim.x / w;
     const int uo = threadIdx.x % w, jt = threadIdx.x / w;
     if (jstep > 0 && jt < jstep) {
@@ -2540,6 +2609,8 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
         int cc = std::max(1, std::min(P.c_ob, HE_K4_WORDS / (padded_words(M) + 16)));
         while (cc & (cc - 1)) cc &= cc - 1;
         while (cc < P.c_ob && cc * P.step < HE_K4_MINW) cc *= 2;
+        if (HE_K4_SPEC && c->logN == 14 && P.logs == 5 && P.c_ob == 32) cc = HE_K4_CC32;
+        if (HE_K4_SPEC && c->logN == 14 && P.logs == 7 && P.c_ob == 64) cc = HE_K4_CC128;
         int stride = padded_words(M);
         const int want = cc < 16 ? (16 / cc) & 15 : 1;
         while ((stride & 15) != want && !(cc >= 16 && (stride & 1))) ++stride;
@@ -2552,21 +2623,21 @@ extern "C" he_status he_conv_ex(const he_ctx* c, const he_conv_plan* p, const ui
         const size_t smem = sizeof(u64) * (size_t)cc * stride + sizeof(int) * (size_t)M;
         auto k4 = v2 ? k_intt_rows<2> : k_intt_rows<1>;
         if (HE_K4_SPEC && v2 && c->logN == 14) {       // plain-20 s = 32 and s = 128 layers
-            if (P.logs == 5 && cc == 8 && stride == 546 && nchunk == 4 && P.c_ob == 32)
-                k4 = fl_used ? k_intt_rows<2, 14, 5, 8, 546, 4, 32, 1>
-                             : k_intt_rows<2, 14, 5, 8, 546, 4, 32>;
-            else if (P.logs == 7 && cc == 32 && stride == 137 && nchunk == 2 && P.c_ob == 64)
-                k4 = fl_used ? k_intt_rows<2, 14, 7, 32, 137, 2, 64, 1>
-                             : k_intt_rows<2, 14, 7, 32, 137, 2, 64>;
+            if (P.logs == 5 && cc == HE_K4_CC32 && stride == K4_ST32 && P.c_ob == 32)
+                k4 = fl_used ? k_intt_rows<2, 14, 5, HE_K4_CC32, K4_ST32, 32 / HE_K4_CC32, 32, 1>
+                             : k_intt_rows<2, 14, 5, HE_K4_CC32, K4_ST32, 32 / HE_K4_CC32, 32>;
+            else if (P.logs == 7 && cc == HE_K4_CC128 && stride == K4_ST128 && P.c_ob == 64)
+                k4 = fl_used ? k_intt_rows<2, 14, 7, HE_K4_CC128, K4_ST128, 64 / HE_K4_CC128, 64, 1>
+                             : k_intt_rows<2, 14, 7, HE_K4_CC128, K4_ST128, 64 / HE_K4_CC128, 64>;
         }
         // (fl_req is set exactly for these two instances' shapes, so a fold in
         //  the [l][b][g][n] layout always meets its reader; guard regardless)
         if (fl_used == 4 && HE_K4_SPEC && v2 && c->logN == 15 && P.logs == 8 && cc == 32 &&
             stride == 137 && nchunk == 2 && P.c_ob == 64)
             k4 = k_intt_rows<2, 15, 8, 32, 137, 2, 64, 1>;
-        if (fl_used && k4 != k_intt_rows<2, 14, 5, 8, 546, 4, 32, 1> &&
+        if (fl_used && k4 != k_intt_rows<2, 14, 5, HE_K4_CC32, K4_ST32, 32 / HE_K4_CC32, 32, 1> &&
             k4 != k_intt_rows<2, 15, 8, 32, 137, 2, 64, 1> &&
-            k4 != k_intt_rows<2, 14, 7, 32, 137, 2, 64, 1>)
+            k4 != k_intt_rows<2, 14, 7, HE_K4_CC128, K4_ST128, 64 / HE_K4_CC128, 64, 1>)
             return HE_ESHAPE;
         if (!set_smem(k4, smem)) return HE_ECUDA;
         rec(ev, 2, st);
