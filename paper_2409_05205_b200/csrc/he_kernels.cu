@@ -189,6 +189,14 @@ __device__ __forceinline__ void cp_async_n(void* smem_dst, const void* gsrc, boo
                      "n"(CHUNK), "r"(valid ? CHUNK : 0));
 }
 
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
+    return ok != 0;
+}
 struct TileLay {
     int B, n_ib, logs, Kp, Gt;
     int skip;       // trailing stages not run: log2(s) for the fold (0 = full)
@@ -1779,14 +1787,6 @@ __device__ __forceinline__ void tc_ld8(uint32_t taddr, int (&v)[8]) {
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
                    "=r"(v[6]), "=r"(v[7])
                  : "r"(taddr));
-}
-__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}\n"
-        : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
-    return ok != 0;
 }
 
 // TMEM budget: 256 columns per CTA, and 128 registers x 256 threads cap the
