@@ -1485,8 +1485,10 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
     const int rw = imma_sw_dev(GS * KC);                  // A row: GS groups x KC bytes
     const int gb = 7 * nrow * swc;                        // B words per group
     const int buf_words = 7 * rows * rw + GS * gb;        // one staging buffer
-    const int nGc = (M + G - 1) / G;   // (qdiv here measured slower: 0.806 -> 0.817 ms MAC)
-    const int l = blockIdx.x / nGc, g0 = (blockIdx.x - l * nGc) * G;
+    // M = N / s, G and Gt are powers of two: the block index splits by shifts
+    // (a run-time division here cost ~25 instructions per thread)
+    const int lgG = __ffs(G) - 1, lgN = max(__ffs(M) - 1 - lgG, 0);
+    const int l = blockIdx.x >> lgN, g0 = (blockIdx.x & ((1 << lgN) - 1)) << lgG;
     const int b0 = blockIdx.y * rows;
     const int gcnt = min(G, M - g0);
     const int nkc = Kp / KC;
@@ -1509,22 +1511,25 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
         u32* sA = sm32 + bf * buf_words;
         u32* sB = sA + 7 * rows * rw;
         {   // A: per (plane, image) the unit's gsn groups x KC bytes are contiguous
-            const int gbk = (g0 + gu) / Gt, gi0 = (g0 + gu) - gbk * Gt;
-            const int rcpr = (gsn * KC) >> 4;
+            const int lgt = __ffs(Gt) - 1;
+            const int gbk = (g0 + gu) >> lgt, gi0 = (g0 + gu) & (Gt - 1);
+            const int rcpr = (gsn * KC) >> 4;     // a power of two when KC is (gsn is)
+            const int lrc = __ffs(rcpr) - 1;
             const FastDiv drc(rcpr);
+            constexpr bool KCP2 = KCC > 0 && (KCC & (KCC - 1)) == 0;
             const int per = rows * rcpr;
             const size_t plane_stride = (size_t)B * Gt * Kp;
             const unsigned char* a0 = A + ((((size_t)l * (M / Gt) + gbk) * 7) * B + b0) * Gt * Kp +
                                       (size_t)gi0 * Kp + k0;
             for (int e = threadIdx.x; e < per; e += blockDim.x) {
-                const int bl = drc.div(e), c = e - bl * rcpr;
+                const int bl = KCP2 ? e >> lrc : drc.div(e), c = e - bl * rcpr;
                 const bool ok = b0 + bl < B;
-                const unsigned char* src = a0 + (size_t)bl * Gt * Kp + c * 16;
+                // rows past the batch: zero-fill from a valid address (row 0)
+                const unsigned char* src = a0 + (size_t)(ok ? bl : 0) * Gt * Kp + c * 16;
                 unsigned char* dst = reinterpret_cast<unsigned char*>(sA + (size_t)bl * rw) + c * 16;
 #pragma unroll
                 for (int j = 0; j < 7; ++j)
-                    cp_async_n<16>(dst + (size_t)j * rows * rw * 4, ok ? src + j * plane_stride : A,
-                                   ok);
+                    cp_async_n<16>(dst + (size_t)j * rows * rw * 4, src + j * plane_stride, ok);
             }
         }
         {   // B: per (group, plane) a contiguous c_o x KC block
