@@ -1339,6 +1339,9 @@ __device__ __forceinline__ u64 redc128(u64 lo, u64 hi, Redc R, bool lazy) {
 // P3 2^64.  Result (V + m q) / 2^64 with m < 2^64: congruent to V R^{-1} and
 // below V / 2^64 + q < 2q (bound as redc128).  The running sums stay below
 // 2^57 (P_k < 2^55, m qhi < 2^50).
+#ifndef HE_MAC_GUNR
+#define HE_MAC_GUNR 1       // MAC instances: the unit's group loop unrolled (compile-time GS)
+#endif
 #ifndef HE_MAC_PWR32
 #define HE_MAC_PWR32 0      // K = 32 MAC: run-time power-of-two multipliers too
 #endif
@@ -1575,7 +1578,10 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
         const int gsn = min(GS, gcnt - gu);
         const u32* sA = sm32 + (nbuf == 2 ? (u & 1) : 0) * buf_words;
         const u32* sB = sA + 7 * rows * rw;
-        for (int gi = 0; gi < gsn; ++gi) {
+        // one fold group of the unit (a lambda so the full-unit case below can
+        // run with a compile-time trip count: the HE_MAC_OB output shift
+        // register then needs no register moves)
+        auto group = [&](int gi) {
             const u32* ab = sA + (bt * 16 + gq) * rw + gi * (KC >> 2) + tq;
             const u32* bb = sB + (size_t)gi * gb + (nt * 8 + gq) * swc + tq;
             const int Kw = KC >> 2;
@@ -1742,6 +1748,12 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
                     nob = 0;
                 }
             }
+        };
+        if (GSC > 0 && HE_MAC_GUNR && gsn == GS) {
+#pragma unroll
+            for (int gi = 0; gi < (GSC > 0 ? GSC : 1); ++gi) group(gi);
+        } else {
+            for (int gi = 0; gi < gsn; ++gi) group(gi);
         }
         __syncthreads();                                   // buffer free for refill
     }
