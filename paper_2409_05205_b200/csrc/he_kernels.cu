@@ -45,6 +45,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_INV_CL
 #define HE_INV_CL 1          // full inverse NTT at N >= 16384: FP64 cluster kernel
 #endif
+#ifndef HE_FC_PRUNE
+#define HE_FC_PRUNE 1        // FC inverse: pruned to the tile's output coefficients
+#endif
 #ifndef HE_NTT_SPEC
 #define HE_NTT_SPEC 1        // forward NTT: compile-time instances for plain-20 layers
 #endif
@@ -3078,9 +3081,61 @@ k_fc_inv(const u64* __restrict__ spec, const ulonglong2* __restrict__ wspec,
         else sm[PAD(i)] = acc;
     }
     __syncthreads();
+    const int k0 = tt * P.n_ot, nk = min(P.n_ot, P.n_o - k0);
+    if (DP && HE_FC_PRUNE) {
+        // Pruned inverse: only coefficients k < nk <= 2^kb leave.  A GS stage
+        // v (pair distance 2^v) with v >= kb feeds those outputs only through
+        // its sum outputs X + Y (no twiddle), so the transform runs stages
+        // v < kb in full and each output is the plain sum
+        //   out[k] = sum_m y[k + m 2^kb]   (y: after stage kb - 1),
+        // a column sum instead of logN - kb stages of butterflies (config 4:
+        // 7 of 14 stages' multiplications).
+        int kb = 0;
+        while ((1 << kb) < P.n_ot) ++kb;
+        const double* twd = twid_all + (size_t)l * N;
+        int lt = 0;
+        for (; lt + 4 <= kb; lt += 4) {
+            gs_pass_dp<4>(smd, 0, 1, logN, lt, 0, logN, twd, Lm.qd, Lm.qinvd);
+            __syncthreads();
+        }
+        if (kb - lt == 1) gs_pass_dp<1>(smd, 0, 1, logN, lt, 0, logN, twd, Lm.qd, Lm.qinvd);
+        else if (kb - lt == 2) gs_pass_dp<2>(smd, 0, 1, logN, lt, 0, logN, twd, Lm.qd, Lm.qinvd);
+        else if (kb - lt == 3) gs_pass_dp<3>(smd, 0, 1, logN, lt, 0, logN, twd, Lm.qd, Lm.qinvd);
+        if (kb > lt) __syncthreads();
+        // column sums: thread (k, part) adds terms m = part, part + parts, ...
+        // (each reduced to |.| <= q/2 + 2 first; 8 of them stay below 2^53)
+        const int KN = 1 << kb, T = N >> kb;
+        // (parts * KN <= blockDim <= 1024 words of partial sums; parts = 1
+        //  reduces in place: element k is read only by its own thread)
+        const int parts = min(T, max(1, (int)blockDim.x / KN));
+        double* part_s = parts > 1 ? smd + padded_words(N) : smd;   // [parts][KN]
+        for (int e = threadIdx.x; e < parts * KN; e += blockDim.x) {
+            const int k = e & (KN - 1), pt = e >> kb;
+            double acc = 0.0;
+            int cnt = 0;
+            for (int m = pt; m < T; m += parts) {
+                acc += dp_reduce(smd[PAD(k + (m << kb))], Lm.qd, Lm.qinvd);
+                if (++cnt == 8) { acc = dp_reduce(acc, Lm.qd, Lm.qinvd); cnt = 0; }
+            }
+            part_s[parts > 1 ? e : PAD(e)] = dp_reduce(acc, Lm.qd, Lm.qinvd);
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+            double acc = 0.0;
+            for (int pt = 0; pt < parts; ++pt) {
+                acc += part_s[parts > 1 ? pt * KN + k : PAD(k)];   // |.| <= q/2 + 2 each
+                if ((pt & 7) == 7) acc = dp_reduce(acc, Lm.qd, Lm.qinvd);
+            }
+            u64 v = d2canon(acc, Lm.qd, Lm.qinvd);
+            v = addmod(v, bias_enc[(size_t)l * P.n_o + k0 + k], q);
+            if (phi1)
+                v = addmod(v, enc_plain(phi1[(size_t)b * P.n_o + k0 + k], Lm, t, r_t, t_inv), q);
+            out[((size_t)b * L + l) * P.n_o + k0 + k] = v;
+        }
+        return;
+    }
     if (DP) gs_all_dp<3>(smd, 0, 1, logN, 0, logN, twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
     else gs_all<4>(sm, 0, 1, logN, 0, logN, twi_all + (size_t)l * N, q, q2);
-    const int k0 = tt * P.n_ot, nk = min(P.n_ot, P.n_o - k0);
     for (int k = threadIdx.x; k < nk; k += blockDim.x) {
         u64 v = DP ? d2canon(smd[PAD(k)], Lm.qd, Lm.qinvd) : csub(sm[PAD(k)], q);
         v = addmod(v, bias_enc[(size_t)l * P.n_o + k0 + k], q);
@@ -3164,7 +3219,8 @@ extern "C" he_status he_fc_ex(const he_ctx* c, const he_fc_desc* f, const uint64
     rec(ev, 1, st);
     const unsigned nblk = (unsigned)((long)B * P.n_t * c->L);
     if (c->logN <= 14) {
-        const size_t smem = sizeof(u64) * padded_words(c->N);
+        // (+ the pruned inverse's partial column sums, <= 1024 words)
+        const size_t smem = sizeof(u64) * (padded_words(c->N) + (HE_FC_PRUNE ? 1024 : 0));
         auto kf = c->ntt_mode == 0 ? k_fc_inv<true> : k_fc_inv<false>;
         if (!set_smem(kf, smem)) return HE_ECUDA;
         kf<<<nblk, std::min(1024, std::max(32, (int)(c->N / 16))), smem, st>>>(
