@@ -264,14 +264,16 @@ __device__ __forceinline__ double u2d(u64 x) {
 // (not canonical: for the int8 MAC operand, whose byte split takes any
 // value below 2^56)
 __device__ __forceinline__ u64 d2lazy(double y, double q, double qinv) {
-    const double r = dp_reduce(y, q, qinv) + q;
-    return (u64)(__double_as_longlong(r + 4503599627370496.0) & 0xFFFFFFFFFFFFFull);
+    // r + (q + 2^52) in one rounding: exact, the sum is an integer in [2^52, 2^53)
+    const double r = dp_reduce(y, q, qinv);
+    return (u64)(__double_as_longlong(r + (q + 4503599627370496.0)) & 0xFFFFFFFFFFFFFull);
 }
 // integer-valued |y| < 2^53 -> canonical residue in [0, q)
 __device__ __forceinline__ u64 d2canon(double y, double q, double qinv) {
-    double r = dp_reduce(y, q, qinv);       // |r| <= q/2 + 2 < q
-    r = r < 0.0 ? r + q : r;                // one conditional add suffices
-    return (u64)(__double_as_longlong(r + 4503599627370496.0) & 0xFFFFFFFFFFFFFull);
+    const double r = dp_reduce(y, q, qinv); // |r| <= q/2 + 2 < q
+    // one conditional add suffices; it rides on the 2^52 shift (one DADD)
+    const double off = r < 0.0 ? q + 4503599627370496.0 : 4503599627370496.0;
+    return (u64)(__double_as_longlong(r + off) & 0xFFFFFFFFFFFFFull);
 }
 
 // FP64 Cooley-Tukey butterfly: X' = X + T, Y' = X - T, T = Y w mod q.
