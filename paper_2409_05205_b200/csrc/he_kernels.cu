@@ -715,14 +715,16 @@ k_ntt_inv_dp_cl(const u64* __restrict__ in, u64* __restrict__ out, int logN, int
     const double q = Lm.qd, qi = Lm.qinvd;
     const double* tw = twid_all + (size_t)l * N;
     const u64* src = in + (size_t)li * N + (size_t)seg * NS;
-    for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
-        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src + i);
-        sm[PAD(i)] = u2d(v.x);
-        sm[PAD(i + 1)] = u2d(v.y);
-    }
+    // the whole segment in flight by cp.async (raw canonical residues); the
+    // first pass converts them (RAW)
+    for (int i = threadIdx.x; i < NS; i += blockDim.x)
+        cp_async_n<8>(sm_raw + PAD(i), src + i, true);
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
-    gs_all_dp<HE_INV_RADIX>(sm, 0, 1, logN - S, seg, logN, tw, q, qi);   // in-segment stages
+    gs_all_dp<HE_INV_RADIX, true>(sm, 0, 1, logN - S, seg, logN, tw, q, qi);   // in-segment stages
     cg::cluster_group cl = cg::this_cluster();
+    const double nid = (double)Lm.ninv;
     for (int t = 0; t < S; ++t) {                                 // span NS << t
         // pair (lower segment a, upper segment a + 2^t): the lower CTA
         // takes indices i < NS/2, the upper one i >= NS/2, and each reads
@@ -735,19 +737,33 @@ k_ntt_inv_dp_cl(const u64* __restrict__ in, u64* __restrict__ out, int logN, int
         double* lo = upper ? cl.map_shared_rank(sm, partner) : sm;
         double* hi = upper ? sm : cl.map_shared_rank(sm, partner);
         const int i0 = upper ? NS / 2 : 0;
-        for (int i = i0 + threadIdx.x; i < i0 + NS / 2; i += blockDim.x) {
-            const double X = dp_reduce(lo[PAD(i)], q, qi), Y = dp_reduce(hi[PAD(i)], q, qi);
-            lo[PAD(i)] = X + Y;
-            hi[PAD(i)] = dp_mulmod(X - Y, w, q, qi);
+        if (t == S - 1) {
+            // last stage: N^{-1} rides on it -- X' = (X + Y) n^{-1},
+            // Y' = (X - Y)(w n^{-1}) (|X +- Y| <= q + 4, |w n^{-1}| <= q keep
+            // dp_mulmod's operand bound), so the store only canonicalises
+            const double wn = dp_mulmod(w, nid, q, qi);
+            for (int i = i0 + threadIdx.x; i < i0 + NS / 2; i += blockDim.x) {
+                const double X = dp_reduce(lo[PAD(i)], q, qi), Y = dp_reduce(hi[PAD(i)], q, qi);
+                lo[PAD(i)] = dp_mulmod(X + Y, nid, q, qi);
+                hi[PAD(i)] = dp_mulmod(X - Y, wn, q, qi);
+            }
+        } else {
+            for (int i = i0 + threadIdx.x; i < i0 + NS / 2; i += blockDim.x) {
+                const double X = dp_reduce(lo[PAD(i)], q, qi), Y = dp_reduce(hi[PAD(i)], q, qi);
+                lo[PAD(i)] = X + Y;
+                hi[PAD(i)] = dp_mulmod(X - Y, w, q, qi);
+            }
         }
     }
     if (S) cl.sync();
-    const double nid = (double)Lm.ninv;
     u64* dst = out + (size_t)li * N + (size_t)seg * NS;
     for (int i = 2 * threadIdx.x; i < NS; i += 2 * blockDim.x) {
-        const u64 x = d2canon(dp_mulmod(dp_reduce(sm[PAD(i)], q, qi), nid, q, qi), q, qi);
-        const u64 y = d2canon(dp_mulmod(dp_reduce(sm[PAD(i + 1)], q, qi), nid, q, qi), q, qi);
-        *reinterpret_cast<ulonglong2*>(dst + i) = make_ulonglong2(x, y);
+        // (S >= 1: already scaled and |.| <= q)
+        const double a = S ? sm[PAD(i)] : dp_mulmod(dp_reduce(sm[PAD(i)], q, qi), nid, q, qi);
+        const double b = S ? sm[PAD(i + 1)]
+                           : dp_mulmod(dp_reduce(sm[PAD(i + 1)], q, qi), nid, q, qi);
+        *reinterpret_cast<ulonglong2*>(dst + i) = make_ulonglong2(d2canon(a, q, qi),
+                                                                  d2canon(b, q, qi));
     }
 }
 
