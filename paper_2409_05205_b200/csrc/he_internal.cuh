@@ -290,7 +290,7 @@ __device__ __forceinline__ void ct_bfly_dp(double& X, double& Y, double w, doubl
 // to |x| <= q/2 + 1 at the start of the pass; stage r inputs are then below
 // (0.5 + r) q + 1 (|T| <= q), so for K <= 4 every stage multiplies directly
 // (multiplicand < 3.5 q + 1 < 4 q).  Outputs < 4.5 q + 1.
-template <int K, bool NORED = false, bool LZ = false>
+template <int K, bool NORED = false, bool LZ = false, bool LIN = false>
 __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0, int seg,
                                            int split, const double* __restrict__ tw,
                                            double q, double qinv) {
@@ -312,11 +312,20 @@ __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0
             const int twb = (1 << (st0 + r)) + (seg << (st0 + r - split)) + (blk << r);
             load_tw_run(tws + o, tw, twb, 1 << r);
         }
+        // LIN: PAD(base + (c << ltk)) = PAD(base) + PAD(c << ltk) -- base's
+        // residue mod 16 plus that of c << ltk never reaches 16 (off < 2^ltk,
+        // and base is a multiple of 2^(ltk+K) plus off) -- so with a
+        // compile-time ltk (the unrolled plain-20 instances) every element is
+        // an immediate offset from one base: no per-element address
+        // arithmetic and no addresses kept live (spilled) for the stores.
+        // (With a run-time ltk the 16 offsets would stay live in registers
+        // across the group loop: the full transforms keep the direct form.)
+        const int pb = PAD(base);
+        auto ai = [&](int c) { return LIN ? pb + PAD(c << ltk) : PAD(base + (c << ltk)); };
         double x[1 << K];
 #pragma unroll
         for (int c = 0; c < (1 << K); ++c)
-            x[c] = NORED ? sm[PAD(base + (c << ltk))]
-                         : dp_reduce(sm[PAD(base + (c << ltk))], q, qinv);
+            x[c] = NORED ? sm[ai(c)] : dp_reduce(sm[ai(c)], q, qinv);
 #pragma unroll
         for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
             if (r >= RUP) {
@@ -332,11 +341,11 @@ __device__ __forceinline__ void ct_pass_dp(double* sm, int logN, int NS, int st0
             }
         }
 #pragma unroll
-        for (int c = 0; c < (1 << K); ++c) sm[PAD(base + (c << ltk))] = x[c];
+        for (int c = 0; c < (1 << K); ++c) sm[ai(c)] = x[c];
     }
 }
 
-template <int RMAX, bool LZ = false, bool UNR = false>
+template <int RMAX, bool LZ = false, bool UNR = false, bool LIN = UNR>
 __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg, int split,
                                           const double* tw, double q, double qinv,
                                           int end) {
@@ -349,15 +358,16 @@ __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg,
     // below (1 + split + r) q <= 4q when split + K <= 4 -- no reduction
     if (rem) {
         const bool nr = split + rem <= 4;
-        if (rem == 1) ct_pass_dp<1, true>(sm, logN, NS, st, seg, split, tw, q, qinv);
-        else if (rem == 2 && nr) ct_pass_dp<2, true>(sm, logN, NS, st, seg, split, tw, q, qinv);
-        else if (rem == 2) ct_pass_dp<2>(sm, logN, NS, st, seg, split, tw, q, qinv);
-        else if (nr) ct_pass_dp<3, true>(sm, logN, NS, st, seg, split, tw, q, qinv);
-        else ct_pass_dp<3>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        if (rem == 1) ct_pass_dp<1, true, false, LIN>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        else if (rem == 2 && nr)
+            ct_pass_dp<2, true, false, LIN>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        else if (rem == 2) ct_pass_dp<2, false, false, LIN>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        else if (nr) ct_pass_dp<3, true, false, LIN>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        else ct_pass_dp<3, false, false, LIN>(sm, logN, NS, st, seg, split, tw, q, qinv);
         st += rem;
         __syncthreads();
     } else if (split + RMAX <= 4) {
-        ct_pass_dp<RMAX, true, LZ>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        ct_pass_dp<RMAX, true, LZ, LIN>(sm, logN, NS, st, seg, split, tw, q, qinv);
         st += RMAX;
         __syncthreads();
     }
@@ -367,13 +377,14 @@ __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg,
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
             if (st + p * RMAX >= end) break;
-            ct_pass_dp<RMAX, false, LZ>(sm, logN, NS, st + p * RMAX, seg, split, tw, q, qinv);
+            ct_pass_dp<RMAX, false, LZ, LIN>(sm, logN, NS, st + p * RMAX, seg, split, tw, q,
+                                             qinv);
             __syncthreads();
         }
         return;
     }
     for (; st < end; st += RMAX) {
-        ct_pass_dp<RMAX, false, LZ>(sm, logN, NS, st, seg, split, tw, q, qinv);
+        ct_pass_dp<RMAX, false, LZ, LIN>(sm, logN, NS, st, seg, split, tw, q, qinv);
         __syncthreads();
     }
 }
@@ -481,9 +492,10 @@ __device__ __forceinline__ void gs_pass_dp(double* sm, int arr_stride, int narr,
         // PAD(base) + c (2^lt0 + 2^(lt0-4)) (base's low lt0 bits are off < 2^lt0):
         // linear addresses, no per-element padding arithmetic (the forward
         // passes keep PAD(): their 64-register cap spills otherwise)
+        // (and for any lt0: PAD(base + (c << lt0)) = PAD(base) + PAD(c << lt0),
+        //  as in ct_pass_dp)
         const int pbo = PAD(base);
-        const int pst = lt0 >= 4 ? (1 << lt0) + (1 << (lt0 - 4)) : 0;
-        auto ai = [&](int c) { return lt0 >= 4 ? pbo + c * pst : PAD(base + (c << lt0)); };
+        auto ai = [&](int c) { return pbo + PAD(c << lt0); };
         double x[1 << K];
 #pragma unroll
         for (int c = 0; c < (1 << K); ++c) {

@@ -323,7 +323,9 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
     }
     if (S) cg::this_cluster().sync();
     else __syncthreads();
-    ct_all_dp<RM, OUT_FMT == 2, UNR>(sm, logN, NS, seg, S, tw, q, qinv, end);    // outputs < 4 q
+    // (conv path: immediate-offset pass addressing, LIN; the full transforms
+    //  keep the direct form, measured faster there)
+    ct_all_dp<RM, OUT_FMT == 2, UNR, OUT_FMT == 2>(sm, logN, NS, seg, S, tw, q, qinv, end);
     ntt_store<OUT_FMT>(out, li, seg, NS, N, L, l, T,
                        [&](int i) {
                            return OUT_FMT == 2 ? d2lazy(sm[PAD(i)], q, qinv)
