@@ -395,7 +395,7 @@ __device__ __forceinline__ void ct_all_dp(double* sm, int logN, int NS, int seg,
 // the N-point twiddles of stage st and block k >> (T - st).  One radix-2^K
 // pass over narr column arrays (arr_stride words apart) in shared memory;
 // value bounds as ct_pass_dp.
-template <int K, bool RAW = false>
+template <int K, bool RAW = false, bool LIN = false>
 __device__ __forceinline__ void ct_pass_cols_dp(double* sm, int arr_stride, int narr, int T,
                                                 int st0, const double* __restrict__ tw,
                                                 double q, double qinv) {
@@ -415,13 +415,15 @@ __device__ __forceinline__ void ct_pass_cols_dp(double* sm, int arr_stride, int 
             const int twb = (1 << (st0 + r)) + (blk << r);
             load_tw_run(tws + o, tw, twb, 1 << r);
         }
+        // (LIN: the immediate-offset form of ct_pass_dp's addresses)
+        const int pb = PAD(base);
+        auto ai = [&](int c) { return LIN ? pb + PAD(c << ltk) : PAD(base + (c << ltk)); };
         double x[1 << K];
 #pragma unroll
         for (int c = 0; c < (1 << K); ++c)
             // RAW: canonical u64 residues as copied by cp.async (< q: stage r
             // multiplicands stay below (1 + r) q <= 4q without a reduction)
-            x[c] = RAW ? u2d(reinterpret_cast<const u64*>(s)[PAD(base + (c << ltk))])
-                       : dp_reduce(s[PAD(base + (c << ltk))], q, qinv);
+            x[c] = RAW ? u2d(reinterpret_cast<const u64*>(s)[ai(c)]) : dp_reduce(s[ai(c)], q, qinv);
 #pragma unroll
         for (int r = 0, o = 0; r < K; o += (1 << r), ++r) {
             const int half = 1 << (K - 1 - r);
@@ -433,25 +435,35 @@ __device__ __forceinline__ void ct_pass_cols_dp(double* sm, int arr_stride, int 
             }
         }
 #pragma unroll
-        for (int c = 0; c < (1 << K); ++c) s[PAD(base + (c << ltk))] = x[c];
+        for (int c = 0; c < (1 << K); ++c) s[ai(c)] = x[c];
     }
 }
 
-template <int RMAX, bool RAW = false>
+template <int RMAX, bool RAW = false, bool LIN = false>
 __device__ __forceinline__ void ct_all_cols_dp(double* sm, int arr_stride, int narr, int T,
                                                const double* tw, double q, double qinv) {
     int st = 0;
     const int rem = T % RMAX;
     if (rem) {
-        if (rem == 1) ct_pass_cols_dp<1, RAW>(sm, arr_stride, narr, T, st, tw, q, qinv);
-        else if (rem == 2) ct_pass_cols_dp<2, RAW>(sm, arr_stride, narr, T, st, tw, q, qinv);
-        else ct_pass_cols_dp<3, RAW>(sm, arr_stride, narr, T, st, tw, q, qinv);
+        if (rem == 1) ct_pass_cols_dp<1, RAW, LIN>(sm, arr_stride, narr, T, st, tw, q, qinv);
+        else if (rem == 2) ct_pass_cols_dp<2, RAW, LIN>(sm, arr_stride, narr, T, st, tw, q, qinv);
+        else ct_pass_cols_dp<3, RAW, LIN>(sm, arr_stride, narr, T, st, tw, q, qinv);
         st += rem;
         __syncthreads();
     } else if (RAW && T > 0) {
-        ct_pass_cols_dp<RMAX, true>(sm, arr_stride, narr, T, st, tw, q, qinv);
+        ct_pass_cols_dp<RMAX, true, LIN>(sm, arr_stride, narr, T, st, tw, q, qinv);
         st += RMAX;
         __syncthreads();
+    }
+    if (LIN) {                  // compile-time T: unrolled, strides are immediates
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            if (st >= T) break;
+            ct_pass_cols_dp<RMAX, false, LIN>(sm, arr_stride, narr, T, st, tw, q, qinv);
+            __syncthreads();
+            st += RMAX;
+        }
+        return;
     }
     for (; st < T; st += RMAX) {
         ct_pass_cols_dp<RMAX>(sm, arr_stride, narr, T, st, tw, q, qinv);

@@ -457,14 +457,19 @@ k_ntt_fwd_dp16_s2(const u64* in, u64* out, int logN, int L, const he_limb* __res
 // word stride; coalesced row loads (C consecutive words per row k), and the
 // store writes the same positions p = k s + c in format OUT_FMT.  No
 // cluster, no read amplification: used when skip >= 2 (C >= 4).
-template <int OUT_FMT>
+// TNC, LCC, STC nonzero: log2 M, log2 C and the array stride at compile time
+// (the M = 128, 32-column shape of config 4's s = 128 layers and config 5):
+// the passes' strides become immediates (LIN addressing)
+template <int OUT_FMT, int TNC = 0, int LCC = 0, int STC = 0>
 __global__ void __launch_bounds__(256, 4)
 k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int L,
                const he_limb* __restrict__ limbs, const double* __restrict__ twd_all, TileLay T,
-               int logC, int stride, int nct) {
+               int logC_, int stride_, int nct) {
     extern __shared__ u64 sm_raw[];
     double* sm = reinterpret_cast<double*>(sm_raw);
-    const int N = 1 << logN, logs = T.skip, s = 1 << logs, Tn = logN - logs, M = 1 << Tn;
+    const int logC = LCC ? LCC : logC_, stride = STC ? STC : stride_;
+    const int N = 1 << logN, logs = T.skip, s = 1 << logs, Tn = TNC ? TNC : logN - logs,
+              M = 1 << Tn;
     const int C = 1 << logC;                 // nct column tiles of C columns per limb
     const int li = blockIdx.x / nct, c0 = (blockIdx.x - li * nct) << logC;
     const int l = li % L;
@@ -487,7 +492,7 @@ k_ntt_fwd_cols(const u64* __restrict__ in, u64* __restrict__ out, int logN, int 
         }
         __syncthreads();
     }
-    ct_all_cols_dp<4, true>(sm, stride, C, Tn, tw, q, qinv);
+    ct_all_cols_dp<4, true, TNC != 0>(sm, stride, C, Tn, tw, q, qinv);
     if (OUT_FMT == 2) {
         unsigned char* A = reinterpret_cast<unsigned char*>(out);
         const int bb = li / L, beta = bb % T.n_ib, b = bb / T.n_ib;
@@ -573,6 +578,8 @@ static he_status launch_ntt_fwd(const he_ctx* c, const u64* in, u64* out,
                             int, int, int);
         static kfc const tabc[3] = {k_ntt_fwd_cols<0>, k_ntt_fwd_cols<1>, k_ntt_fwd_cols<2>};
         kfc kc = tabc[out_fmt];
+        if (HE_NTT_SPEC && out_fmt == 2 && logN - T.skip == 7 && logC == 5 && stride == 137)
+            kc = k_ntt_fwd_cols<2, 7, 5, 137>;
         if (!set_smem(kc, smem_c)) return HE_ECUDA;
         kc<<<(unsigned)(nlimbs * nct), 256, smem_c, st>>>(
             in, out, logN, c->L, c->d_limb, c->d_twd_fwd, T, logC, stride, nct);
