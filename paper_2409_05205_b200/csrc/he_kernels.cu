@@ -39,6 +39,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_NTT_MINB
 #define HE_NTT_MINB 2        // forward NTT (cluster kernels): CTAs per SM (register cap)
 #endif
+#ifndef HE_NTT_UNR5
+#define HE_NTT_UNR5 1        // s = 32 forward-NTT instance: pass loop unrolled too
+#endif
 #ifndef HE_INV_RADIX
 #define HE_INV_RADIX 3       // inverse cluster kernel: log2 of the pass radix
 #endif
@@ -424,7 +427,7 @@ k_ntt_fwd_dp_s1(const u64* in, u64* out, int logN, int L, const he_limb* __restr
         T.Gt = GT;
     }
     // conv path (MAC-tile output): radix-16 passes (measured 0.839 -> 0.826 ms per step)
-    ntt_fwd_segment_dp<1, OUT_FMT, (OUT_FMT == 2 ? 4 : 3), (HE_NTT_UNR && LN != 0 && SK == 3)>(
+    ntt_fwd_segment_dp<1, OUT_FMT, (OUT_FMT == 2 ? 4 : 3), (HE_NTT_UNR && LN != 0 && (SK == 3 || (HE_NTT_UNR5 && SK == 5)))>(
         in, out, LN ? LN : logN, L, limbs, tw_all, T);
 }
 template <int OUT_FMT>
