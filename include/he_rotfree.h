@@ -153,7 +153,9 @@ he_status he_pack_filters(const he_ctx* ctx, const he_conv_plan* p,
  * for every k < N/s and channel n of block ob, 0 at every other
  * coefficient, then + enc_j(phi1[b][ob][i]) at every coefficient i.
  * d_out uint64 [B][n_ob][L][N].  d_ws: he_conv_workspace_bytes(B) bytes
- * (HE_ENOMEM if smaller). */
+ * (HE_ENOMEM if smaller); the workspace must not overlap d_c0, d_fspec,
+ * d_phi1 or the outputs (the forward transform reads d_c0 while it writes
+ * the workspace). */
 size_t he_conv_workspace_bytes(const he_ctx* ctx, const he_conv_plan* p,
                                int B);
 he_status he_conv(const he_ctx* ctx, const he_conv_plan* p,

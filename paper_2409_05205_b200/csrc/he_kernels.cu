@@ -42,6 +42,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_NTT_UNR5
 #define HE_NTT_UNR5 1        // s = 32 forward-NTT instance: pass loop unrolled too
 #endif
+#ifndef HE_NTT_NOCL
+#define HE_NTT_NOCL 1        // conv-path forward NTT (N = 16384): no cluster barrier (out != in)
+#endif
 #ifndef HE_INV_RADIX
 #define HE_INV_RADIX 3       // inverse cluster kernel: log2 of the pass radix
 #endif
@@ -324,7 +327,11 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
             sm[PAD(i + 1)] = oy;
         }
     }
-    if (S) cg::this_cluster().sync();
+    // the cluster barrier keeps an in-place transform safe (a CTA must not
+    // overwrite its segment before the partner has read it); the MAC-tile
+    // output (OUT_FMT 2, he_conv_ex only) never aliases the input, so there
+    // the CTAs need no cluster and synchronise only themselves
+    if (S && !(OUT_FMT == 2 && HE_NTT_NOCL)) cg::this_cluster().sync();
     else __syncthreads();
     // (conv path: immediate-offset pass addressing, LIN; the full transforms
     //  keep the direct form, measured faster there)
@@ -415,7 +422,8 @@ k_ntt_fwd_dp_s0(const u64* in, u64* out, int logN, int L, const he_limb* __restr
 // geometry fixed at compile time (the plain-20 conv layers' instances: the
 // index arithmetic of the passes and of the byte-plane store folds away)
 template <int OUT_FMT, int LN = 0, int SK = 0, int NIB = 0, int KU = 0, int KP = 0, int GT = 0>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HE_NTT_T, HE_NTT_MINB)
+__global__ void __cluster_dims__((OUT_FMT == 2 && HE_NTT_NOCL) ? 1 : 2, 1, 1)
+    __launch_bounds__(HE_NTT_T, HE_NTT_MINB)
 k_ntt_fwd_dp_s1(const u64* in, u64* out, int logN, int L, const he_limb* __restrict__ limbs,
                 const double* __restrict__ tw_all, TileLay T) {
     if (LN) {
