@@ -260,7 +260,10 @@ __device__ __forceinline__ void ntt_store(u64* out, int li, int seg, int NS, int
 }
 
 #ifndef HE_NTT_PF
-#define HE_NTT_PF 1
+#define HE_NTT_PF 1   // full forward transforms' register stage: input vectors in flight
+#endif
+#ifndef HE_NTT_PF_CONV
+#define HE_NTT_PF_CONV 2   // conv path (2: 1.606 -> 1.585 ms once it dropped its cluster; 1 was faster with it)
 #endif
 // FP64 variant of ntt_fwd_segment (default; HE_NTT=int selects the integer
 // one): residues as integer-valued doubles, exact FP64 butterflies
@@ -281,7 +284,7 @@ __device__ __forceinline__ void ntt_fwd_segment_dp(const u64* in, u64* out, int 
     const int end = logN - T.skip;
     // software-pipelined loads: the vectors of the next PF iterations are
     // in flight while this one's register stages run
-    constexpr int PF = HE_NTT_PF;
+    constexpr int PF = OUT_FMT == 2 ? HE_NTT_PF_CONV : HE_NTT_PF;
     const int step = 2 * blockDim.x;
     ulonglong2 buf[PF][1 << S];
 #pragma unroll
