@@ -106,6 +106,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_K4_W8
 #define HE_K4_W8 1           // K4 s = 8 instances: unrolled writer with immediate offsets
 #endif
+#ifndef HE_K4_W8_EB
+#define HE_K4_W8_EB 4        // K4 s = 8 writer: phi1 loads per batch (one batch ahead)
+#endif
 #ifndef HE_K4_CC32
 #define HE_K4_CC32 8         // K4 row writer, plain-20 s = 32 layers: channels per CTA
 #endif
@@ -2265,7 +2268,7 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     constexpr bool W8 = FL == 3 && LN == 14 && LS == 3 && CCC == 2 && COB == 8 && HP == 34 &&
                         WO > 0 && CST > 0;
     if (W8 && HE_K4_W8 && ph != nullptr && enc_tab != nullptr && blockDim.x == 256) {
-        constexpr int JS = 128, NE = 2048 / JS, EBW = 4;
+        constexpr int JS = 128, NE = 2048 / JS, EBW = HE_K4_W8_EB;
         constexpr int LST = CST == 1 ? 0 : (CST == 2 ? 1 : 2);
         const int uo = threadIdx.x & 1, jt = threadIdx.x >> 1;
         const int u = u0 + uo;                  // = the channel n of the block (step 1)
