@@ -109,6 +109,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_K4_W8_EB
 #define HE_K4_W8_EB 4        // K4 s = 8 writer: phi1 loads per batch (one batch ahead)
 #endif
+#ifndef HE_K4_RW
+#define HE_K4_RW 1           // K4 row-writer instances: per-thread constant slot columns
+#endif
 #ifndef HE_K4_CC32
 #define HE_K4_CC32 8         // K4 row writer, plain-20 s = 32 layers: channels per CTA
 #endif
@@ -2537,6 +2540,74 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     const bool xred = (logM & 3) == 0;             // radix-16 last pass: outputs < 8q + 16
     const double* smd = reinterpret_cast<const double*>(sm);
     const int lstep = __ffs(step) - 1;           // step = s / c_ob, a power of two
+    // Compile-time instances (LN, LS, CCC, COB fixed; 256 threads): 256 is a
+    // multiple of the threads per group, so every thread keeps the same two
+    // slot columns (ua, ua + 1) for all the groups j = jt + e JSTEP it
+    // visits -- their channels, ownership and array rows are per-thread
+    // constants and phi1 / the output row advance by compile-time strides.
+    // Same values and stores as the generic loop below.
+    constexpr bool RW = HE_K4_RW && V == 2 && LN > 0 && LS > 0 && CCC > 0 && COB > 0;
+    if (RW && blockDim.x == 256 && ph != nullptr && w == CCC * ((1 << LS) / (COB > 0 ? COB : 1))) {
+        constexpr int STEP = (1 << LS) / (COB > 0 ? COB : 1), W = CCC * STEP;
+        constexpr int TPJ = W / 2 > 0 ? W / 2 : 1;
+        constexpr int LSTEP = __builtin_ctz(STEP), LTPJ = __builtin_ctz(TPJ);
+        constexpr int JSTEP = 256 / TPJ, MM = (1 << LN) >> LS, NE = MM / JSTEP > 0 ? MM / JSTEP : 1;
+        constexpr int EB = 4;
+        static_assert(!RW || (TPJ >= 1 && 256 % TPJ == 0 && MM % (JSTEP * EB) == 0),
+                      "row-writer instance geometry");
+        const int uo = (threadIdx.x & (TPJ - 1)) * 2, jt = threadIdx.x >> LTPJ;
+        const int ua = u0 + uo;
+        const int nla = ua >> LSTEP, nlb = (ua + 1) >> LSTEP;
+        const bool owna = (ua & (STEP - 1)) == 0 && nla < ch0 + ncc;
+        const bool ownb = ((ua + 1) & (STEP - 1)) == 0 && nlb < ch0 + ncc;
+        const double* xa = smd + (owna ? nla - ch0 : 0) * STC;
+        const double* xb = smd + (ownb ? nlb - ch0 : 0) * STC;
+        const u32* pp = ph + ((size_t)jt << LS) + ua;
+        u64* op = orow ? orow + ((size_t)jt << LS) + ua : nullptr;
+        uint2 mn[EB];
+#pragma unroll
+        for (int z = 0; z < EB; ++z)
+            mn[z] = *reinterpret_cast<const uint2*>(pp + ((size_t)(z * JSTEP) << LS));
+#pragma unroll 1
+        for (int e0 = 0; e0 < NE; e0 += EB) {
+            uint2 m[EB];
+#pragma unroll
+            for (int z = 0; z < EB; ++z) m[z] = mn[z];
+            if (e0 + EB < NE) {
+#pragma unroll
+                for (int z = 0; z < EB; ++z)
+                    mn[z] = *reinterpret_cast<const uint2*>(
+                        pp + ((size_t)((e0 + EB + z) * JSTEP) << LS));
+            }
+#pragma unroll
+            for (int z = 0; z < EB; ++z) {
+                const int j = jt + (e0 + z) * JSTEP;
+                const int jvj = crow ? jv[j] : -1;
+                if (!op && jvj < 0) continue;
+                double ya = enc_dp(u2d(m[z].x), rtd, td, t_inv_d, tinvq, qd, qi);
+                double yb = enc_dp(u2d(m[z].y), rtd, td, t_inv_d, tinvq, qd, qi);
+                if (owna) {
+                    double x = xa[PAD(j)];
+                    if (xred) x = dp_reduce(x, qd, qi);
+                    ya += x;
+                }
+                if (ownb) {
+                    double x = xb[PAD(j)];
+                    if (xred) x = dp_reduce(x, qd, qi);
+                    yb += x;
+                }
+                const u64 va = d2canon(ya, qd, qi), vb = d2canon(yb, qd, qi);
+                if (op)
+                    *reinterpret_cast<ulonglong2*>(op + ((size_t)((e0 + z) * JSTEP) << LS)) =
+                        make_ulonglong2(va, vb);
+                if (jvj >= 0) {
+                    if (owna) crow[jvj + nla] = va;
+                    if (ownb) crow[jvj + nlb] = vb;
+                }
+            }
+        }
+        return;
+    }
     constexpr int UB = 4;                          // elements per thread in flight
     const int nel = M * tpj;
     for (int e0 = threadIdx.x; e0 < nel; e0 += UB * blockDim.x) {
