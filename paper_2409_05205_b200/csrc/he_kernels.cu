@@ -1894,19 +1894,28 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
         const unsigned char* a0 = A + (((size_t)l * (M / Gt) + gb) * 7 * B) * Gt * Kp +
                                   (size_t)gi * Kp;
         const int cpr = Kt >> 4;                          // chunks per row
+        // (index split without run-time division -- it was a quarter of the
+        //  kernel's instructions -- and padding chunks zero-filled from a
+        //  valid address instead of a pointer select)
+        const FastDiv dcpr(cpr), dnrow(nrow);
+        constexpr int LBT = __builtin_ctz(BT);
         for (int e = threadIdx.x; e < 7 * BT * cpr; e += blockDim.x) {
-            const int c = e % cpr, r = (e / cpr) % BT, j = e / (cpr * BT);
+            const int q1 = dcpr.div(e), c = e - q1 * cpr;
+            const int r = q1 & (BT - 1), j = q1 >> LBT;
             const int b = b0 + r;
             const bool ok = b < B && c * 16 < Kp;
-            const unsigned char* src = ok ? a0 + j * plane_stride + (size_t)b * Gt * Kp + c * 16 : A;
+            const unsigned char* src =
+                a0 + j * plane_stride + (size_t)(ok ? b : b0) * Gt * Kp + (ok ? c * 16 : 0);
             unsigned char* dst = sA + j * a_plane + (r >> 3) * sbo + c * 128 + (r & 7) * 16;
             cp_async_n<16>(dst, src, ok);
         }
         const unsigned char* f0 = Fpl + (((size_t)l * M + g) * 7) * c_o * Kp;
         for (int e = threadIdx.x; e < 7 * nrow * cpr; e += blockDim.x) {
-            const int c = e % cpr, n = (e / cpr) % nrow, j = e / (cpr * nrow);
+            const int q1 = dcpr.div(e), c = e - q1 * cpr;
+            const int j = dnrow.div(q1), n = q1 - j * nrow;
             const bool ok = n < c_o && c * 16 < Kp;
-            const unsigned char* src = ok ? f0 + ((size_t)j * c_o + n) * Kp + c * 16 : Fpl;
+            const unsigned char* src =
+                f0 + ((size_t)j * c_o + (ok ? n : 0)) * Kp + (ok ? c * 16 : 0);
             unsigned char* dst = sB + j * b_plane + (n >> 3) * sbo + c * 128 + (n & 7) * 16;
             cp_async_n<16>(dst, src, ok);
         }
