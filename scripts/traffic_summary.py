@@ -17,7 +17,7 @@ per = {}
 for r in rows[1:]:
     d = per.setdefault(r[ix["ID"]], {"name": r[ix["Kernel Name"]]})
     d[r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", ""))
-classes = {"ntt_fwd": r"k_ntt_fwd_dp_s\d<2>|k_ntt_fwd_s\d<2>|k_ntt_fwd_cols<2>", "mac_fold": r"k_mac_imma|k_mac_fold|k_mac_tc",
+classes = {"ntt_fwd": r"k_ntt_fwd_dp_s\d<2[,>]|k_ntt_fwd_s\d<2[,>]|k_ntt_fwd_cols<2[,>]", "mac_fold": r"k_mac_imma|k_mac_fold|k_mac_tc",
            "intt_scatter": r"k_intt_scatter|k_intt_rows", "fc_inv": r"k_fc_inv"}
 out = {"source": src, "workload": workload, "code": code, "method": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
        "dram__bytes_write.sum, bench.py --profile --steps 1 --warmup 1 (cold-cache, serialised)"}
