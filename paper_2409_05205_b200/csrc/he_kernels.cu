@@ -112,6 +112,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_K4_RW
 #define HE_K4_RW 1           // K4 row-writer instances: per-thread constant slot columns
 #endif
+#ifndef HE_K4_PRE
+#define HE_K4_PRE 1          // K4 s = 8 writer: first phi1 batch loaded before the transform
+#endif
 #ifndef HE_K4_CC32
 #define HE_K4_CC32 8         // K4 row writer, plain-20 s = 32 layers: channels per CTA
 #endif
@@ -2248,6 +2251,21 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         }
     }
     __syncthreads();
+    // Plain-20 s = 8 instances (two 2048-point channels per CTA, step 1, 256
+    // threads, mask on): the writer below with immediate offsets
+    constexpr bool W8 = FL == 3 && LN == 14 && LS == 3 && CCC == 2 && COB == 8 && HP == 34 &&
+                        WO > 0 && CST > 0;
+    const bool w8 = W8 && HE_K4_W8 && phi1 != nullptr && enc_tab != nullptr &&
+                    blockDim.x == 256;
+    // (its first phi1 batch is requested before the transform, so it has
+    //  landed when the writer starts)
+    u32 pre[4] = {0u, 0u, 0u, 0u};
+    if (w8 && HE_K4_PRE) {
+        const u32* pp0 = phi1 + ((size_t)b * P.n_ob + ob) * N + ((threadIdx.x >> 1) << 3) +
+                         ch * CCC + (threadIdx.x & 1);
+#pragma unroll
+        for (int z = 0; z < 4; ++z) pre[z] = pp0[z * (128 << 3)];
+    }
     if (DP && raw)
         gs_all_dp<4, true>(reinterpret_cast<double*>(sm), stride, ncc, logM, 0, logM,
                            twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
@@ -2277,9 +2295,7 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     // unrolled: phi1, the output row and the channel array advance by
     // compile-time strides, and the payload index follows (kr, lc) of j
     // (128 = 3 h_p + 26).  Same values and stores as the generic writer.
-    constexpr bool W8 = FL == 3 && LN == 14 && LS == 3 && CCC == 2 && COB == 8 && HP == 34 &&
-                        WO > 0 && CST > 0;
-    if (W8 && HE_K4_W8 && ph != nullptr && enc_tab != nullptr && blockDim.x == 256) {
+    if (w8) {
         constexpr int JS = 128, NE = 2048 / JS, EBW = HE_K4_W8_EB;
         constexpr int LST = CST == 1 ? 0 : (CST == 2 ? 1 : 2);
         const int uo = threadIdx.x & 1, jt = threadIdx.x >> 1;
@@ -2293,7 +2309,8 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         int lc = jt - kr * HP;
         u32 mnext[EBW];
 #pragma unroll
-        for (int z = 0; z < EBW; ++z) mnext[z] = pp[z * (JS << 3)];
+        for (int z = 0; z < EBW; ++z)
+            mnext[z] = (HE_K4_PRE && EBW == 4) ? pre[z < 4 ? z : 0] : pp[z * (JS << 3)];
 #pragma unroll
         for (int e0 = 0; e0 < NE; e0 += EBW) {
             u32 m[EBW];
