@@ -2552,20 +2552,9 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                         ? (K_ * P.h_o + L_) * c_ob : -1;
         }
     }
-    cp_async_wait<0>();
-    __syncthreads();
-    gs_all_dp<4, true>(reinterpret_cast<double*>(sm), stride, ncc, logM, 0, logM,
-                       twid_all + (size_t)l * N, qd, qi);
     const int u0 = ch0 * step;
     const int u1 = (ch == nchunk - 1) ? s_ : (ch0 + ncc) * step;
     const int w = u1 - u0;                         // a multiple of V (host)
-    const int tpj = w / V;                         // threads per group j (a power of two)
-    const int ltpj = __ffs(tpj) - 1;
-    const u32* ph = phi1 ? phi1 + ((size_t)b * P.n_ob + ob) * N : nullptr;
-    u64* orow = out ? out + (((size_t)b * P.n_ob + ob) * L + l) * N : nullptr;
-    const bool xred = (logM & 3) == 0;             // radix-16 last pass: outputs < 8q + 16
-    const double* smd = reinterpret_cast<const double*>(sm);
-    const int lstep = __ffs(step) - 1;           // step = s / c_ob, a power of two
     // Compile-time instances (LN, LS, CCC, COB fixed; 256 threads): 256 is a
     // multiple of the threads per group, so every thread keeps the same two
     // slot columns (ua, ua + 1) for all the groups j = jt + e JSTEP it
@@ -2573,12 +2562,33 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     // constants and phi1 / the output row advance by compile-time strides.
     // Same values and stores as the generic loop below.
     constexpr bool RW = HE_K4_RW && V == 2 && LN > 0 && LS > 0 && CCC > 0 && COB > 0;
-    if (RW && blockDim.x == 256 && ph != nullptr && w == CCC * ((1 << LS) / (COB > 0 ? COB : 1))) {
-        constexpr int STEP = (1 << LS) / (COB > 0 ? COB : 1), W = CCC * STEP;
-        constexpr int TPJ = W / 2 > 0 ? W / 2 : 1;
-        constexpr int LSTEP = __builtin_ctz(STEP), LTPJ = __builtin_ctz(TPJ);
-        constexpr int JSTEP = 256 / TPJ, MM = (1 << LN) >> LS, NE = MM / JSTEP > 0 ? MM / JSTEP : 1;
-        constexpr int EB = 4;
+    constexpr int STEP = (1 << LS) / (COB > 0 ? COB : 1), W = CCC * STEP;
+    constexpr int TPJ = W / 2 > 0 ? W / 2 : 1;
+    constexpr int LSTEP = __builtin_ctz(STEP), LTPJ = __builtin_ctz(TPJ);
+    constexpr int JSTEP = 256 / TPJ, MM = (1 << LN) >> LS, NE = MM / JSTEP > 0 ? MM / JSTEP : 1;
+    constexpr int EB = 4;
+    const bool rw = RW && blockDim.x == 256 && phi1 != nullptr && w == W;
+    // (its first phi1 batch is requested before the transform)
+    uint2 pre[EB];
+    if (rw && HE_K4_PRE) {
+        const u32* pp0 = phi1 + ((size_t)b * P.n_ob + ob) * N +
+                         ((size_t)(threadIdx.x >> LTPJ) << LS) + u0 + (threadIdx.x & (TPJ - 1)) * 2;
+#pragma unroll
+        for (int z = 0; z < EB; ++z)
+            pre[z] = *reinterpret_cast<const uint2*>(pp0 + ((size_t)(z * JSTEP) << LS));
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    gs_all_dp<4, true>(reinterpret_cast<double*>(sm), stride, ncc, logM, 0, logM,
+                       twid_all + (size_t)l * N, qd, qi);
+    const int tpj = w / V;                         // threads per group j (a power of two)
+    const int ltpj = __ffs(tpj) - 1;
+    const u32* ph = phi1 ? phi1 + ((size_t)b * P.n_ob + ob) * N : nullptr;
+    u64* orow = out ? out + (((size_t)b * P.n_ob + ob) * L + l) * N : nullptr;
+    const bool xred = (logM & 3) == 0;             // radix-16 last pass: outputs < 8q + 16
+    const double* smd = reinterpret_cast<const double*>(sm);
+    const int lstep = __ffs(step) - 1;           // step = s / c_ob, a power of two
+    if (rw) {
         static_assert(!RW || (TPJ >= 1 && 256 % TPJ == 0 && MM % (JSTEP * EB) == 0),
                       "row-writer instance geometry");
         const int uo = (threadIdx.x & (TPJ - 1)) * 2, jt = threadIdx.x >> LTPJ;
@@ -2593,7 +2603,7 @@ k_intt_rows(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         uint2 mn[EB];
 #pragma unroll
         for (int z = 0; z < EB; ++z)
-            mn[z] = *reinterpret_cast<const uint2*>(pp + ((size_t)(z * JSTEP) << LS));
+            mn[z] = HE_K4_PRE ? pre[z] : *reinterpret_cast<const uint2*>(pp + ((size_t)(z * JSTEP) << LS));
 #pragma unroll 1
         for (int e0 = 0; e0 < NE; e0 += EB) {
             uint2 m[EB];
