@@ -16,6 +16,7 @@
 // values are contiguous.  N^{-1} = s^{-1} (N/s)^{-1} is folded into the
 // filter spectra at he_pack_filters time.
 #include <cooperative_groups.h>
+#include <cuda.h>             // CUtensorMap (the TMA descriptors; encoded through the runtime entry point)
 
 #include <string.h>
 
@@ -53,6 +54,9 @@ namespace cg = cooperative_groups;
 #endif
 #ifndef HE_FC_PRUNE
 #define HE_FC_PRUNE 1        // FC inverse: pruned to the tile's output coefficients
+#endif
+#ifndef HE_MAC_TC_TMA
+#define HE_MAC_TC_TMA 1      // tcgen05 MAC: operands staged by two TMA tensor copies
 #endif
 #ifndef HE_NTT_SPEC
 #define HE_NTT_SPEC 1        // forward NTT: compile-time instances for plain-20 layers
@@ -215,6 +219,14 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
         : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
 struct TileLay {
     int B, n_ib, logs, Kp, Gt;
     int skip;       // trailing stages not run: log2(s) for the fold (0 = full)
@@ -1860,11 +1872,12 @@ __device__ __forceinline__ void tc_ld8(uint32_t taddr, int (&v)[8]) {
 // TMEM budget: 256 columns per CTA, and 128 registers x 256 threads cap the
 // kernel at two CTAs per SM (512 columns, the whole TMEM), so an allocation
 // never waits on another CTA of this kernel; no other kernel uses TMEM.
-template <int FL = 0>
+template <int FL = 0, bool TMA = false>
 __global__ void __launch_bounds__(256, 2)
 k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
          u64* __restrict__ out, int B, int L, int M, int c_o, int Kp, int Gt,
-         const he_limb* __restrict__ limbs, int lazy) {
+         const he_limb* __restrict__ limbs, int lazy, const __grid_constant__ CUtensorMap tmA,
+         const __grid_constant__ CUtensorMap tmB) {
     constexpr int BT = HE_MAC_TC_BT;           // images per CTA (= UMMA M)
     extern __shared__ __align__(1024) unsigned char smc[];
     const int Kt = (Kp + 31) & ~31;            // K rounded to the UMMA K step (32 bytes)
@@ -1890,8 +1903,43 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
             (uint32_t)__cvta_generic_to_shared(&s_bar)));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    // ---- stage the operands (16-byte cp.async into the core-matrix layout)
-    {
+    // ---- stage the operands
+    if (TMA) {
+        // two TMA tensor copies (one elected thread): each 5-D box lands
+        // directly in the canonical K-major core-matrix layout -- dims
+        // (16 bytes of k, row mod 8, 16-byte k chunk, row / 8, plane) with the
+        // row / 8 and plane strides of the global MAC-tile layouts, so the
+        // box's dense order is (r & 7) 16 + c 128 + (r >> 3) SBO + j plane.
+        // Out-of-range rows (ragged image tiles, channels past c_o) arrive as
+        // zeros; completion is counted in bytes on an mbarrier.
+        __shared__ __align__(8) uint64_t s_tbar;
+        const uint32_t tb = (uint32_t)__cvta_generic_to_shared(&s_tbar);
+        if (threadIdx.x == 0) {
+            mbar_init(tb, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int gb = g / Gt, gi = g - gb * Gt;
+            mbar_arrive_tx(tb, (uint32_t)(7 * (BT + nrow) * Kt));
+            const uint32_t da = (uint32_t)__cvta_generic_to_shared(sA);
+            const uint32_t db = (uint32_t)__cvta_generic_to_shared(sB);
+            asm volatile(
+                "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(da),
+                "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(0), "r"(0), "r"(gi * (Kp >> 4)),
+                "r"(b0 >> 3), "r"((l * (M / Gt) + gb) * 7), "r"(tb)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(db),
+                "l"(reinterpret_cast<uint64_t>(&tmB)), "r"(0), "r"(0), "r"(0), "r"(0),
+                "r"((l * M + g) * 7), "r"(tb)
+                : "memory");
+        }
+        while (!mbar_try_wait(tb, 0)) {
+        }
+    } else {   // 16-byte cp.async into the core-matrix layout
         const int gb = g / Gt, gi = g - gb * Gt;
         const size_t plane_stride = (size_t)B * Gt * Kp;
         const unsigned char* a0 = A + (((size_t)l * (M / Gt) + gb) * 7 * B) * Gt * Kp +
@@ -2014,6 +2062,23 @@ k_mac_tc(const unsigned char* __restrict__ A, const unsigned char* __restrict__ 
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
 static he_status launch_mac_tc(const unsigned char* A, const unsigned char* Fpl, u64* out, int B,
                                int L, int M, int c_o, int Kp, const he_limb* limbs,
                                cudaStream_t st, int lazy, int fl = 0) {
@@ -2021,9 +2086,38 @@ static he_status launch_mac_tc(const unsigned char* A, const unsigned char* Fpl,
     const size_t smem = 7 * ((size_t)HE_MAC_TC_BT * Kt + (size_t)nrow * Kt);
     if (smem > 110 * 1024) return HE_ESHAPE;
     auto k = fl == 1 ? k_mac_tc<1> : k_mac_tc<0>;
+    const int Gt = tile_gt(M);
+    CUtensorMap tmA, tmB;
+    memset(&tmA, 0, sizeof tmA);
+    memset(&tmB, 0, sizeof tmB);
+    // TMA staging when the boxes tile the operands exactly: whole 32-byte K
+    // steps (Kt = Kp), image and channel counts in rows of 8
+    if (HE_MAC_TC_TMA && Kt == Kp && B % 8 == 0 && c_o % 8 == 0 && encode_tiled() != nullptr) {
+        const cuuint32_t kch = (cuuint32_t)(Kt >> 4), one[5] = {1, 1, 1, 1, 1};
+        const cuuint64_t gA[5] = {16, 8, (cuuint64_t)Gt * Kp / 16, (cuuint64_t)B / 8,
+                                  (cuuint64_t)L * (M / Gt) * 7};
+        const cuuint64_t sAst[4] = {(cuuint64_t)Gt * Kp, 16, (cuuint64_t)8 * Gt * Kp,
+                                    (cuuint64_t)B * Gt * Kp};
+        const cuuint32_t bA[5] = {16, 8, kch, HE_MAC_TC_BT / 8, 7};
+        const cuuint64_t gB[5] = {16, 8, (cuuint64_t)Kp / 16, (cuuint64_t)c_o / 8,
+                                  (cuuint64_t)L * M * 7};
+        const cuuint64_t sBst[4] = {(cuuint64_t)Kp, 16, (cuuint64_t)8 * Kp, (cuuint64_t)c_o * Kp};
+        const cuuint32_t bB[5] = {16, 8, kch, (cuuint32_t)nrow / 8, 7};
+        auto enc = encode_tiled();
+        const bool ok =
+            enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, (void*)A, gA, sAst, bA, one,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                CUDA_SUCCESS &&
+            enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, (void*)Fpl, gB, sBst, bB, one,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                CUDA_SUCCESS;
+        if (ok) k = fl == 1 ? k_mac_tc<1, true> : k_mac_tc<0, true>;
+    }
     if (!set_smem(k, smem)) return HE_ECUDA;
     dim3 grid(L * M, (B + HE_MAC_TC_BT - 1) / HE_MAC_TC_BT);
-    k<<<grid, 256, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, tile_gt(M), limbs, lazy);
+    k<<<grid, 256, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, Gt, limbs, lazy, tmA, tmB);
     return HE_OK;
 }
 

@@ -614,7 +614,10 @@ def test_conv_in_bench_launch_configuration(he):
 
 @pytest.mark.parametrize("case", SMALL + [
     (synth.ConvLayer(16, 24, 5, 5), 1024, 0, 130),        # two 128-image tiles, ragged
-    (synth.ConvLayer(64, 64, 8, 8), 8192, 0, 129)],        # K = 64, c_o = 64
+    (synth.ConvLayer(64, 64, 8, 8), 8192, 0, 129),         # K = 64, c_o = 64
+    # TMA-staged operands (B % 8 == 0, K a multiple of 32, c_o % 8 == 0):
+    (synth.ConvLayer(64, 64, 8, 8), 8192, 0, 136),         # second tile: 8 images
+    (synth.ConvLayer(32, 40, 8, 8), 8192, 0, 16)],         # c_o = 40: 8 zero channel rows
     ids=lambda c: f"{c[0]}-N{c[1]}-B{c[3]}")
 def test_conv_tcgen05_mac_path(he, case, monkeypatch):
     """The tcgen05 MAC (k_mac_tc, the default for >= 128 images) forced on
