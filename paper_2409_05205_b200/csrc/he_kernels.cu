@@ -58,6 +58,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_MAC_TC_TMA
 #define HE_MAC_TC_TMA 1      // tcgen05 MAC: operands staged by two TMA tensor copies
 #endif
+#ifndef HE_MAC_TMA16
+#define HE_MAC_TMA16 1       // K = 16 mma.sync MAC instance: operands staged by TMA tensor copies
+#endif
 #ifndef HE_NTT_SPEC
 #define HE_NTT_SPEC 1        // forward NTT: compile-time instances for plain-20 layers
 #endif
@@ -1537,8 +1540,17 @@ __global__ void __launch_bounds__(MINB > 1 ? 128 : 512, MINB)
 k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict__ Fpl,
            u64* __restrict__ out, int B, int L, int M, int c_o_, int Kp_, int G, int GS_,
            int KC_, int Gt, int nbuf, const he_limb* __restrict__ limbs, int lazy_,
-           int c_full) {
-    extern __shared__ u32 sm32[];
+           int c_full, int use_tma, const __grid_constant__ CUtensorMap tmA,
+           const __grid_constant__ CUtensorMap tmF) {
+    extern __shared__ __align__(1024) u32 sm32[];
+    // K = 16 instance (config 4's s = 8 layers): with use_tma the unit's A tile
+    // arrives by one 3-D TMA copy (64-byte rows, SWIZZLE_64B: the 16-byte
+    // chunk of row r sits at chunk ^ ((r >> 1) & 3), conflict-free fragment
+    // loads without padding) and its F tile by one 2-D copy, instead of
+    // 10.5 cp.async (and their address arithmetic) per thread
+    constexpr bool TK16 = HE_MAC_TMA16 && KPC == 16 && KCC == 16 && COC == 16 && GSC == 4 &&
+                          TB16 == 2 && MINB == 5;
+    const bool tma = TK16 && use_tma;
     constexpr int rows = 16 * TB16;
     // channel tile: channels [n0, n0 + c_o) of the c_full output channels
     // (blockIdx.z; c_o = c_full when the layer is not tiled)
@@ -1548,7 +1560,7 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
     const bool lazy = LZ >= 0 ? (LZ == 1) : (lazy_ != 0);
     const int nrow = (c_o + 7) & ~7, nnt = nrow >> 3;
     const int swc = imma_sw_dev(KC);
-    const int rw = imma_sw_dev(GS * KC);                  // A row: GS groups x KC bytes
+    const int rw = tma ? (GS * KC) >> 2 : imma_sw_dev(GS * KC);   // A row: GS groups x KC bytes
     const int gb = 7 * nrow * swc;                        // B words per group
     const int buf_words = 7 * rows * rw + GS * gb;        // one staging buffer
     // M = N / s, G and Gt are powers of two: the block index splits by shifts
@@ -1627,7 +1639,38 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
     int acc[13][4];
     u64 ob[HE_MAC_OB][4];
     int nob = 0;
-    issue(0, 0);
+    if (tma) {
+        __shared__ __align__(8) uint64_t s_tbar;
+        const uint32_t tb = (uint32_t)__cvta_generic_to_shared(&s_tbar);
+        if (threadIdx.x == 0) {
+            mbar_init(tb, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int lgt = __ffs(Gt) - 1;
+            const int gbk = g0 >> lgt, gi0 = g0 & (Gt - 1);
+            mbar_arrive_tx(tb, (uint32_t)(7 * rows * GS * KC + GS * 7 * c_o * Kp));
+            const uint32_t da = (uint32_t)__cvta_generic_to_shared(sm32);
+            const uint32_t df = da + (uint32_t)(7 * rows * rw * 4);
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(da),
+                "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(gi0 * Kp), "r"(b0),
+                "r"((l * (M >> lgt) + gbk) * 7), "r"(tb)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(df),
+                "l"(reinterpret_cast<uint64_t>(&tmF)), "r"(n0 * Kp), "r"((l * M + g0) * 7),
+                "r"(tb)
+                : "memory");
+        }
+        while (!mbar_try_wait(tb, 0)) {
+        }
+    } else {
+        issue(0, 0);
+    }
     for (int u = 0; u < nunits; ++u) {
         if (nbuf == 2 && u + 1 < nunits) {                 // prefetch the next unit
             issue(u + 1, (u + 1) & 1);
@@ -1645,7 +1688,9 @@ k_mac_imma(const unsigned char* __restrict__ A, const unsigned char* __restrict_
         // run with a compile-time trip count: the HE_MAC_OB output shift
         // register then needs no register moves)
         auto group = [&](int gi) {
-            const u32* ab = sA + (bt * 16 + gq) * rw + gi * (KC >> 2) + tq;
+            // (TMA tile: 16-byte chunk gi of row bt 16 + gq at gi ^ (gq >> 1))
+            const u32* ab = tma ? sA + (bt * 16 + gq) * rw + ((gi ^ (gq >> 1)) << 2) + tq
+                                : sA + (bt * 16 + gq) * rw + gi * (KC >> 2) + tq;
             const u32* bb = sB + (size_t)gi * gb + (nt * 8 + gq) * swc + tq;
             const int Kw = KC >> 2;
             int kw = 0;
@@ -2243,9 +2288,34 @@ static he_status launch_mac_imma(const unsigned char* A, const unsigned char* Fp
         }
     }
     if (!set_smem(k, smem)) return HE_ECUDA;
+    // TMA staging for the K = 16 instance (one unit per CTA, whole groups)
+    CUtensorMap tmA, tmF;
+    memset(&tmA, 0, sizeof tmA);
+    memset(&tmF, 0, sizeof tmF);
+    int use_tma = 0;
+    if (HE_MAC_TMA16 && k16 && TB16 == 2 && Kp == 16 && KC == 16 && c_o == 16 && GS == 4 &&
+        G == GS && M % G == 0 && Gt % GS == 0 && encode_tiled() != nullptr) {
+        const cuuint32_t one[3] = {1, 1, 1};
+        const cuuint64_t gA[3] = {(cuuint64_t)Gt * Kp, (cuuint64_t)B, (cuuint64_t)L * (M / Gt) * 7};
+        const cuuint64_t sA_[2] = {(cuuint64_t)Gt * Kp, (cuuint64_t)B * Gt * Kp};
+        const cuuint32_t bA[3] = {(cuuint32_t)(GS * KC), (cuuint32_t)rows, 7};
+        const cuuint64_t gF[2] = {(cuuint64_t)c_full * Kp, (cuuint64_t)L * M * 7};
+        const cuuint64_t sF_[1] = {(cuuint64_t)c_full * Kp};
+        const cuuint32_t bF[2] = {(cuuint32_t)(c_o * Kp), (cuuint32_t)(GS * 7)};
+        auto enc = encode_tiled();
+        if (enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)A, gA, sA_, bA, one,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                CUDA_SUCCESS &&
+            enc(&tmF, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)Fpl, gF, sF_, bF, one,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                CUDA_SUCCESS)
+            use_tma = 1;
+    }
     dim3 grid(L * ((M + G - 1) / G), (B + rows - 1) / rows, nct);
     k<<<grid, 32 * warps, smem, st>>>(A, Fpl, out, B, L, M, c_o, Kp, G, GS, KC, Gt, nbuf, limbs,
-                                      lazy, c_full);
+                                      lazy, c_full, use_tma, tmA, tmF);
     return HE_OK;
 }
 
