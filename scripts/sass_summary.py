@@ -19,8 +19,8 @@ want = [("k_ntt_fwd_dp_s1<2,14,3,2,8,16,16> (forward NTT, s = 8)", "_Z15k_ntt_fw
         ("k_mac_imma<2,5,16,16,16,4,1,3> (MAC, K = 16, s = 8)", "_Z10k_mac_immaILi2ELi5ELi16ELi16ELi16ELi4ELi1ELi3EE"),
         ("k_intt_scatter<1,14,3,2,2184,4,8,34,32,1,3> (INTT + scatter, s = 8)", "_Z14k_intt_scatterILb1ELi14ELi3ELi2ELi2184ELi4ELi8ELi34ELi32ELi1ELi3EE"),
         ("k_intt_rows<2,14,5,8,546,4,32,1> (INTT + rows, s = 32)", "_Z11k_intt_rowsILi2ELi14ELi5ELi8ELi546ELi4ELi32ELi1EE"),
-        ("k_ntt_fwd_cols<2> (forward NTT, column form: s = 128, config 5)", "_Z14k_ntt_fwd_colsILi2EE"),
-        ("k_mac_tc<1> (tcgen05 MAC, B >= 128, config 5)", "_Z8k_mac_tcILi1EE")]
+        ("k_ntt_fwd_cols<2,7,5,137> (forward NTT, column form: s = 128, config 5)", "_Z14k_ntt_fwd_colsILi2ELi7ELi5ELi137EE"),
+        ("k_mac_tc<1,true> (tcgen05 MAC with TMA staging, B >= 128, config 5)", "_Z8k_mac_tcILi1ELb1EE")]
 def find(prefix):
     for f in funcs:
         if f.startswith(prefix):
@@ -41,6 +41,10 @@ for i, (title, name) in enumerate(want):
     lines.append("| opcode | count |\n|---|---|")
     for op, n in c.most_common(14):
         lines.append(f"| {op} | {n} |")
+    key = {op: c[op] for op in ("IMMA", "UTCIMMA", "UTMALDG", "UBLKCP", "LDGSTS", "DFMA", "SYNCS")
+           if c.get(op)}
+    lines.append("")
+    lines.append("pipe-defining opcodes: " + ", ".join(f"{k} {v}" for k, v in key.items()))
     lines.append("")
 open("/root/repo/profiles/r02_sass.md", "w").write("\n".join(lines) + "\n")
 print("\n".join(lines)[:1500])
