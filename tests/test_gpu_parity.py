@@ -630,6 +630,18 @@ def test_conv_tcgen05_mac_path(he, case, monkeypatch):
     run_conv(he, ctx, ring, Ly, B, seed=B + N, s_override=so, check_b=check)
 
 
+@pytest.mark.parametrize("B", [20, 32, 45])
+def test_conv_k16_mac_tma_path(he, B):
+    """The K = 16 int8 MAC instance (16 channels, four groups per CTA, 32-image
+    tiles) with its operands staged by TMA tensor copies: a ragged last tile
+    (images past B arrive as TMA out-of-bounds zeros), every image checked."""
+    N = 8192
+    primes = synth.PRIMES_N8192[:2]
+    ctx = he.Context(primes, N.bit_length() - 1, 65537)
+    ring = R.Ring(N, tuple(primes), 65537)
+    run_conv(he, ctx, ring, synth.ConvLayer(8, 16, 16, 16), B, seed=B + 16)
+
+
 def test_conv_wide_layer_over_256_channels(he):
     """c_o > 256: the IMAD MAC path (the tensor-core kernel keeps all of a
     group's output channels in one CTA); n_ob > 1 blocks, bit-exact."""
