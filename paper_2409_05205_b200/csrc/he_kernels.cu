@@ -122,6 +122,12 @@ namespace cg = cooperative_groups;
 #ifndef HE_K4_PRE
 #define HE_K4_PRE 1          // K4 s = 8 writer: first phi1 batch loaded before the transform
 #endif
+#ifndef HE_K4_FUSE
+#define HE_K4_FUSE 1         // K4 s = 8 instances: last radix-8 GS pass in the writer's registers
+#endif
+#ifndef HE_K4_FUSE_PU
+#define HE_K4_FUSE_PU 1      // (its two radix-8 groups per thread: loop unroll factor)
+#endif
 #ifndef HE_K4_CC32
 #define HE_K4_CC32 8         // K4 row writer, plain-20 s = 32 layers: channels per CTA
 #endif
@@ -2424,13 +2430,24 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     // (its first phi1 batch is requested before the transform, so it has
     //  landed when the writer starts)
     u32 pre[4] = {0u, 0u, 0u, 0u};
+    // (HE_K4_FUSE: the writer visits e = 0, 2, ..., 14 first, see below)
+    constexpr int PSTEP = HE_K4_FUSE ? 2 : 1;
     if (w8 && HE_K4_PRE) {
         const u32* pp0 = phi1 + ((size_t)b * P.n_ob + ob) * N + ((threadIdx.x >> 1) << 3) +
                          ch * CCC + (threadIdx.x & 1);
 #pragma unroll
-        for (int z = 0; z < 4; ++z) pre[z] = pp0[z * (128 << 3)];
+        for (int z = 0; z < 4; ++z) pre[z] = pp0[z * PSTEP * (128 << 3)];
     }
-    if (DP && raw)
+    if (W8 && HE_K4_FUSE && w8) {
+        // stages 0-7 as two radix-16 passes; stages 8-10 (the last radix-8
+        // pass) run in the writer's registers below
+        gs_pass_dp<4, true>(reinterpret_cast<double*>(sm), stride, ncc, logM, 0, 0, logM,
+                            twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
+        __syncthreads();
+        gs_pass_dp<4>(reinterpret_cast<double*>(sm), stride, ncc, logM, 4, 0, logM,
+                      twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
+        __syncthreads();
+    } else if (DP && raw)
         gs_all_dp<4, true>(reinterpret_cast<double*>(sm), stride, ncc, logM, 0, logM,
                            twid_all + (size_t)l * N, Lm.qd, Lm.qinvd);
     else if (DP)
@@ -2469,6 +2486,73 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
         u64* op = orow ? orow + (jt << 3) + u : nullptr;
         const double td = Lm.td, t_inv_d = Lm.t_invd, rtd = Lm.rtd, tinvq = Lm.tinvd;
         const double qd = Lm.qd, qi = Lm.qinvd;
+        if (HE_K4_FUSE) {
+            // The last GS pass (stages 8-10, radix 8) fused into the writer:
+            // its group at offset off = jt + 128 p holds the elements
+            // j = off + 256 c (c < 8), i.e. e = 2 c + p -- exactly this
+            // thread's column u -- so the pass's outputs go from registers
+            // to the mask add and the store (no shared-memory round trip,
+            // one barrier fewer).  Block 0 of stages 8, 9, 10 for every
+            // group: twiddles tw[4..7], tw[2..3], tw[1] (gs_pass_dp's
+            // indexing with lt0 = 8, K = 3, seg = 0).  Same values as the
+            // unfused pass + writer.
+            static_assert(!W8 || EBW == 4, "fused s = 8 writer: phi1 batches of 4");
+            const double* tw = twid_all + (size_t)l * N;
+            u32 mn[4];
+#pragma unroll
+            for (int z = 0; z < 4; ++z) mn[z] = HE_K4_PRE ? pre[z] : pp[(2 * z) * (JS << 3)];
+            constexpr int PU = HE_K4_FUSE_PU;
+#pragma unroll PU
+            for (int p = 0; p < 2; ++p) {
+                double x[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    x[c] = dp_reduce(xs[(2 * c + p) * (JS + JS / 16)], qd, qi);
+#pragma unroll
+                for (int v = 0; v < 3; ++v) {
+                    // (twiddles loaded per stage: L1 hits, fewer live registers)
+                    double tws[4];
+                    load_tw_run(tws, tw, 4 >> v, 4 >> v);
+                    const int half = 1 << v;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        if (c & half) continue;
+                        const double X = x[c], Y = x[c + half];
+                        x[c] = X + Y;
+                        x[c + half] = dp_mulmod(X - Y, tws[c >> (v + 1)], qd, qi);
+                    }
+                }
+                const int j0 = jt + 128 * p;    // < 256: (j0 1928) >> 16 = j0 / 34
+                int kr = (j0 * 1928) >> 16;
+                int lc = j0 - kr * HP;
+#pragma unroll
+                for (int c0 = 0; c0 < 8; c0 += 4) {
+                    u32 m[4];
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) m[z] = mn[z];
+                    if (p == 0 || c0 == 0) {    // next batch: (p, 4) or (1, 0)
+                        const int np = c0 == 4 ? 1 : p, nc = c0 == 4 ? 0 : 4;
+#pragma unroll
+                        for (int z = 0; z < 4; ++z) mn[z] = pp[(2 * (nc + z) + np) * (JS << 3)];
+                    }
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) {
+                        const int c = c0 + z, e = 2 * c + p;
+                        const int K_ = kr >> LST, L_ = lc >> LST;
+                        const bool valid = crow && ((kr | lc) & (CST - 1)) == 0 && K_ < WO && L_ < WO;
+                        kr += 256 / HP;
+                        lc += 256 % HP;
+                        if (lc >= HP) { lc -= HP; ++kr; }
+                        if (!op && !valid) continue;
+                        const double y = enc_dp(u2d(m[z]), rtd, td, t_inv_d, tinvq, qd, qi) + x[c];
+                        const u64 v = d2canon(y, qd, qi);
+                        if (op) op[e * (JS << 3)] = v;
+                        if (valid) crow[(K_ * WO + L_) * COB + u] = v;
+                    }
+                }
+            }
+            return;
+        }
         int kr = (jt * 1928) >> 16;             // jt / 34 for jt < 128
         int lc = jt - kr * HP;
         u32 mnext[EBW];
