@@ -49,6 +49,9 @@ namespace cg = cooperative_groups;
 #ifndef HE_INV_RADIX
 #define HE_INV_RADIX 3       // inverse cluster kernel: log2 of the pass radix
 #endif
+#ifndef HE_INV_FUSE
+#define HE_INV_FUSE 1        // inverse cluster kernel: last stages in registers, fused with the store
+#endif
 #ifndef HE_INV_CL
 #define HE_INV_CL 1          // full inverse NTT at N >= 16384: FP64 cluster kernel
 #endif
@@ -775,9 +778,78 @@ k_ntt_inv_dp_cl(const u64* __restrict__ in, u64* __restrict__ out, int logN, int
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    gs_all_dp<HE_INV_RADIX, true>(sm, 0, 1, logN - S, seg, logN, tw, q, qi);   // in-segment stages
     cg::cluster_group cl = cg::this_cluster();
     const double nid = (double)Lm.ninv;
+    if (HE_INV_FUSE) {
+        // In-segment stages 0 .. logM - 2 as radix-8 passes in shared memory
+        // (the same passes gs_all_dp runs), then one register step per index
+        // i < NS/2 for the last in-segment stage (span NS/2) and the S
+        // cross-segment stages: its 2^(S+1) elements i + h NS/2 of every
+        // segment a are read (the partners' over DSMEM), transformed, scaled
+        // by N^{-1} and stored to global memory directly -- no radix-2 pass,
+        // no DSMEM writes, no separate store pass, one cluster barrier fewer.
+        // The CTAs split the indices (no redundant work).  Same operations
+        // in the same order as the unfused path.
+        static_assert(HE_INV_RADIX == 3, "fused inverse: radix-8 passes");
+        const int logM = logN - S, end = logM - 1;
+        gs_pass_dp<3, true>(sm, 0, 1, logM, 0, seg, logN, tw, q, qi);
+        __syncthreads();
+        int lt = 3;
+        for (; lt + 3 <= end; lt += 3) {
+            gs_pass_dp<3>(sm, 0, 1, logM, lt, seg, logN, tw, q, qi);
+            __syncthreads();
+        }
+        if (end - lt == 1) gs_pass_dp<1>(sm, 0, 1, logM, lt, seg, logN, tw, q, qi);
+        else if (end - lt == 2) gs_pass_dp<2>(sm, 0, 1, logM, lt, seg, logN, tw, q, qi);
+        if (S) cl.sync();
+        else __syncthreads();
+        constexpr int NSG = 1 << S;
+        const int H = NS >> 1, per = H >> S;
+        const double* sg[NSG];
+        double wl[NSG];                      // stage logM - 1: block a of the N-point table
+#pragma unroll
+        for (int a = 0; a < NSG; ++a) {
+            sg[a] = (a == seg) ? sm : cl.map_shared_rank(sm, a);
+            wl[a] = __ldg(tw + NSG + a);
+        }
+        u64* dst = out + (size_t)li * N;
+        for (int i = seg * per + threadIdx.x; i < (seg + 1) * per; i += blockDim.x) {
+            double x[2 * NSG];
+#pragma unroll
+            for (int a = 0; a < NSG; ++a) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) x[2 * a + h] = dp_reduce(sg[a][PAD(i + h * H)], q, qi);
+                const double X = x[2 * a], Y = x[2 * a + 1];
+                x[2 * a] = X + Y;
+                x[2 * a + 1] = dp_mulmod(X - Y, wl[a], q, qi);
+            }
+#pragma unroll
+            for (int t = 0; t < S; ++t) {
+#pragma unroll
+                for (int a = 0; a < NSG; ++a) {
+                    if (a & (1 << t)) continue;
+                    const double w = __ldg(tw + (1 << (S - 1 - t)) + (a >> (t + 1)));
+                    const double wn = t == S - 1 ? dp_mulmod(w, nid, q, qi) : w;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        double& lo = x[2 * a + h];
+                        double& hi = x[2 * (a + (1 << t)) + h];
+                        const double X = dp_reduce(lo, q, qi), Y = dp_reduce(hi, q, qi);
+                        lo = t == S - 1 ? dp_mulmod(X + Y, nid, q, qi) : X + Y;
+                        hi = dp_mulmod(X - Y, wn, q, qi);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 2 * NSG; ++k) {
+                const double v = S ? x[k] : dp_mulmod(dp_reduce(x[k], q, qi), nid, q, qi);
+                dst[(size_t)(k >> 1) * NS + (k & 1) * H + i] = d2canon(v, q, qi);
+            }
+        }
+        if (S) cl.sync();                    // partners may still read this segment
+        return;
+    }
+    gs_all_dp<HE_INV_RADIX, true>(sm, 0, 1, logN - S, seg, logN, tw, q, qi);   // in-segment stages
     for (int t = 0; t < S; ++t) {                                 // span NS << t
         // pair (lower segment a, upper segment a + 2^t): the lower CTA
         // takes indices i < NS/2, the upper one i >= NS/2, and each reads

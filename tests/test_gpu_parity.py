@@ -94,6 +94,26 @@ def test_ntt_roundtrip(he, N):
     assert np.array_equal(u64(d), x)
 
 
+@pytest.mark.parametrize("N", [2048, 4096])
+def test_ntt_roundtrip_cluster_sizes(he, N):
+    """The FP64 inverse kernel's other single-CTA sizes (log2 N - 1 = 10, 11
+    in-segment stages before its fused register step), forward pinned to the
+    definition on sampled outputs, inverse by the round trip."""
+    primes = tuple(R.find_primes(N, 50, 2))
+    ctx = ctx_for(he, N, primes)
+    logN = N.bit_length() - 1
+    x = synth.uniform_residues((3, len(primes), N), primes, 4, "misc", N)
+    d = dev(x)
+    ctx.ntt_forward(d)
+    got = u64(d)
+    pos = np.array([0, 1, 5, N // 2, N - 1])
+    ks = np.array([brv(int(p), logN) for p in pos], np.int32)
+    for j, q in enumerate(primes):
+        assert np.array_equal(got[2, j, pos], R.ntt_def(x[2, j], q, ctx.psi(j), ks))
+    ctx.ntt_inverse(d)
+    assert np.array_equal(u64(d), x)
+
+
 def test_ntt_inverse_matches_definition(he):
     N, primes = 256, RINGS[256]
     ctx = ctx_for(he, N, primes)
