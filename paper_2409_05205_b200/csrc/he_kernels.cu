@@ -2497,6 +2497,7 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
     // threads, mask on): the writer below with immediate offsets
     constexpr bool W8 = FL == 3 && LN == 14 && LS == 3 && CCC == 2 && COB == 8 && HP == 34 &&
                         WO > 0 && CST > 0;
+    constexpr int HPD = HP ? HP : 1;         // (divisor of the W8-only index steps; W8 implies HP = 34)
     const bool w8 = W8 && HE_K4_W8 && phi1 != nullptr && enc_tab != nullptr &&
                     blockDim.x == 256;
     // (its first phi1 batch is requested before the transform, so it has
@@ -2612,8 +2613,8 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                         const int c = c0 + z, e = 2 * c + p;
                         const int K_ = kr >> LST, L_ = lc >> LST;
                         const bool valid = crow && ((kr | lc) & (CST - 1)) == 0 && K_ < WO && L_ < WO;
-                        kr += 256 / HP;
-                        lc += 256 % HP;
+                        kr += 256 / HPD;
+                        lc += 256 % HPD;
                         if (lc >= HP) { lc -= HP; ++kr; }
                         if (!op && !valid) continue;
                         const double y = enc_dp(u2d(m[z]), rtd, td, t_inv_d, tinvq, qd, qi) + x[c];
@@ -2645,8 +2646,8 @@ k_intt_scatter(const u64* __restrict__ fold, const u32* __restrict__ phi1,
                 const int e = e0 + z;
                 const int K_ = kr >> LST, L_ = lc >> LST;
                 const bool valid = crow && ((kr | lc) & (CST - 1)) == 0 && K_ < WO && L_ < WO;
-                kr += JS / HP;
-                lc += JS % HP;
+                kr += JS / HPD;
+                lc += JS % HPD;
                 if (lc >= HP) { lc -= HP; ++kr; }
                 if (!op && !valid) continue;
                 double y = enc_dp(u2d(m[z]), rtd, td, t_inv_d, tinvq, qd, qi);
